@@ -1,0 +1,328 @@
+"""B200-native non-smooth Newton step (Macklin et al. 2019, arXiv 1907.04587).
+
+Host-side Python mirror of the reference's solver interface
+(/root/reference/proj/include/nsdyn/newton.h) over the C ABI in
+include/nsdyn_gpu.h. Names follow the reference: NewtonConfig, newton_step,
+count_rows, SolveReport fields, NewtonIterationStats fields.
+
+    solver = NewtonSolver(topology, NewtonConfig(precision="fp64"))
+    report = solver.newton_step(q, u, contacts, h=0.0083, gravity=(0, 0, -9.81))
+
+The compute runs in hand-written sm_100a kernels; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import (NSD_ABORTED, NSD_FP32, NSD_FP64, NSD_OK, NsdError, check, lib, nsd_config, nsd_contact,
+                   nsd_iter_stats, nsd_shape, nsd_step_in, nsd_step_out, nsd_topology)
+
+__all__ = ["NewtonConfig", "NewtonSolver", "BatchSolver", "Scene", "contacts_from_arrays", "contacts_to_arrays",
+           "count_rows", "NsdError"]
+
+_R_STRAT = {"identity": 0, "h2": 1, "effmass": 2}
+_NCP = {"minmap": 0, "fb": 1}
+
+
+@dataclass
+class NewtonConfig:
+    """NewtonConfig + LinearSolverConfig (newton.h:12-23, solvers.h:11-16)."""
+    newton_iterations: int = 8
+    step_fraction: float = 0.75
+    epsilon_reg: float = 1e-6
+    geometric_stiffness: bool = True
+    r_strategy: int = 2
+    ncp_kind: int = 1
+    linear_method: int = 3
+    linear_max_iterations: int = 40
+    linear_tolerance: float = 1e-10
+    preconditioner: int = 1
+    newton_tolerance: float = 1e-6
+    line_search: bool = False
+    precision: str = "fp32"
+
+    def to_c(self) -> nsd_config:
+        c = nsd_config()
+        c.newton_iterations = self.newton_iterations
+        c.step_fraction = self.step_fraction
+        c.epsilon_reg = self.epsilon_reg
+        c.geometric_stiffness = int(bool(self.geometric_stiffness))
+        c.r_strategy = _R_STRAT.get(self.r_strategy, self.r_strategy) if isinstance(self.r_strategy, str) else self.r_strategy
+        c.ncp_kind = _NCP.get(self.ncp_kind, self.ncp_kind) if isinstance(self.ncp_kind, str) else self.ncp_kind
+        c.linear_method = self.linear_method
+        c.linear_max_iterations = self.linear_max_iterations
+        c.linear_tolerance = self.linear_tolerance
+        c.preconditioner = self.preconditioner
+        c.newton_tolerance = self.newton_tolerance
+        c.line_search = int(bool(self.line_search))
+        c.precision = NSD_FP64 if self.precision == "fp64" else NSD_FP32
+        return c
+
+    @staticmethod
+    def from_c(c: nsd_config, precision=None) -> "NewtonConfig":
+        return NewtonConfig(c.newton_iterations, c.step_fraction, c.epsilon_reg, bool(c.geometric_stiffness),
+                            c.r_strategy, c.ncp_kind, c.linear_method, c.linear_max_iterations, c.linear_tolerance,
+                            c.preconditioner, c.newton_tolerance, bool(c.line_search),
+                            precision or ("fp64" if c.precision == NSD_FP64 else "fp32"))
+
+
+def _dp(a):
+    return a.ctypes.data_as(_lib.D)
+
+
+def _ip(a):
+    return a.ctypes.data_as(_lib.I32)
+
+
+class Topology:
+    """Static scene arrays in the C-ABI layout (owns the numpy buffers)."""
+
+    KEYS_I = ("body_type", "joint_kind", "joint_body", "tet_body")
+    KEYS_D = ("body_mass", "body_inertia", "joint_frame", "joint_param", "tet_dm_inv", "tet_volume", "tet_material")
+
+    def __init__(self, **arrays):
+        self.a = {}
+        for k in self.KEYS_I:
+            self.a[k] = np.ascontiguousarray(arrays.get(k, np.zeros(0)), dtype=np.int32)
+        for k in self.KEYS_D:
+            self.a[k] = np.ascontiguousarray(arrays.get(k, np.zeros(0)), dtype=np.float64)
+        bt = self.a["body_type"]
+        self.n_bodies = len(bt)
+        self.num_dof = int(np.sum(np.where(bt == 1, 6, 3)))
+        self.num_coord = int(np.sum(np.where(bt == 1, 7, 3)))
+        self.n_joints = len(self.a["joint_kind"])
+        self.n_tets = len(self.a["tet_volume"])
+        self._c = nsd_topology(self.n_bodies, _ip(self.a["body_type"]), _dp(self.a["body_mass"]),
+                               _dp(self.a["body_inertia"]), self.n_joints, _ip(self.a["joint_kind"]),
+                               _ip(self.a["joint_body"]), _dp(self.a["joint_frame"]), _dp(self.a["joint_param"]),
+                               self.n_tets, _ip(self.a["tet_body"]), _dp(self.a["tet_dm_inv"]),
+                               _dp(self.a["tet_volume"]), _dp(self.a["tet_material"]))
+
+    @property
+    def c(self):
+        return self._c
+
+
+def count_rows(topology: Topology, n_contacts: int) -> int:
+    """count_rows (newton.h:114)."""
+    return lib().nsd_count_rows(C.byref(topology.c), n_contacts)
+
+
+def contacts_from_arrays(ib, db):
+    """(n,4) int [body_a, body_b, feature, 0] + (n,22) doubles -> nsd_contact array."""
+    n = len(ib)
+    arr = (nsd_contact * max(n, 1))()
+    for i in range(n):
+        c = arr[i]
+        c.body_a, c.body_b, c.feature = int(ib[i][0]), int(ib[i][1]), int(ib[i][2])
+        d = db[i]
+        for k in range(3):
+            c.local_a[k], c.local_b[k], c.normal[k], c.d1[k], c.d2[k] = d[k], d[3 + k], d[6 + k], d[9 + k], d[12 + k]
+        c.thickness, c.mu, c.lambda_n = d[15], d[16], d[17]
+        c.lambda_f[0], c.lambda_f[1] = d[18], d[19]
+    return arr, n
+
+
+def contacts_to_arrays(arr, n):
+    ib = np.zeros((n, 4), np.int32)
+    db = np.zeros((n, 22))
+    for i in range(n):
+        c = arr[i]
+        ib[i] = (c.body_a, c.body_b, c.feature, 0)
+        db[i, 0:3], db[i, 3:6], db[i, 6:9] = list(c.local_a), list(c.local_b), list(c.normal)
+        db[i, 9:12], db[i, 12:15] = list(c.d1), list(c.d2)
+        db[i, 15], db[i, 16], db[i, 17] = c.thickness, c.mu, c.lambda_n
+        db[i, 18], db[i, 19] = c.lambda_f[0], c.lambda_f[1]
+    return ib, db
+
+
+class NewtonSolver:
+    """One scene on one GPU: nsd_create / nsd_step (the newton_step boundary)."""
+
+    def __init__(self, topology: Topology, config: NewtonConfig, device: int = 0):
+        self.topology = topology
+        self.config = config
+        h = C.c_void_p()
+        check(lib().nsd_create(C.byref(topology.c), C.byref(config.to_c()), device, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().nsd_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def set_config(self, config: NewtonConfig):
+        check(lib().nsd_set_config(self._h, C.byref(config.to_c())))
+        self.config = config
+
+    @property
+    def last_step_ms(self):
+        return lib().nsd_last_step_ms(self._h)
+
+    def newton_step(self, q, u, contacts=None, h=0.0083, gravity=(0.0, 0.0, -9.81), f_extra=None,
+                    joint_frame=None):
+        """newton_step (newton.cpp:321-418). contacts: (ib, db) arrays or (nsd_contact array, n)."""
+        T, cfg = self.topology, self.config
+        q = np.ascontiguousarray(q, np.float64)
+        u = np.ascontiguousarray(u, np.float64)
+        if contacts is None:
+            carr, nc = (nsd_contact * 1)(), 0
+        elif isinstance(contacts, tuple) and isinstance(contacts[0], np.ndarray):
+            carr, nc = contacts_from_arrays(*contacts)
+        else:
+            carr, nc = contacts
+        fx = None if f_extra is None else np.ascontiguousarray(f_extra, np.float64)
+        jf = None if joint_frame is None else np.ascontiguousarray(joint_frame, np.float64)
+        sin = nsd_step_in()
+        sin.q, sin.u = _dp(q), _dp(u)
+        sin.n_contacts, sin.contacts = nc, C.cast(carr, C.POINTER(nsd_contact))
+        sin.h = h
+        for k in range(3):
+            sin.gravity[k] = gravity[k]
+        sin.f_extra = _dp(fx) if fx is not None else None
+        sin.joint_frame = _dp(jf) if jf is not None else None
+        nrows = count_rows(T, nc)
+        N, ml = cfg.newton_iterations, cfg.linear_max_iterations
+        qo, uo = np.zeros(T.num_coord), np.zeros(T.num_dof)
+        lam = np.zeros(max(nrows, 1))
+        iters = (nsd_iter_stats * max(N, 1))()
+        hist = np.zeros(max(N, 1) * (ml + 1))
+        hlen = np.zeros(max(N, 1), np.int32)
+        tel = np.zeros(6 * max(nc, 1))
+        cout = (nsd_contact * max(nc, 1))()
+        so = nsd_step_out()
+        so.q, so.u, so.lambda_ = _dp(qo), _dp(uo), _dp(lam)
+        so.contacts = C.cast(cout, C.POINTER(nsd_contact))
+        so.iters = C.cast(iters, C.POINTER(nsd_iter_stats))
+        so.linear_history, so.linear_history_len, so.contact_telemetry = _dp(hist), _ip(hlen), _dp(tel)
+        rc = lib().nsd_step(self._h, C.byref(sin), C.byref(so))
+        check(rc, allow_abort=True)
+        n = so.n_iterations
+        stats = np.array([[it.residual_inf, it.merit_l2, it.comp_error_max, it.cone_violation_max, it.step_size,
+                           it.linear_iterations, it.linear_residual, it.linear_breakdown] for it in iters[:n]])
+        return dict(q=qo, u=uo, lam=lam[:nrows], stats=stats.reshape(n, 8), n_iterations=n,
+                    hist=hist.reshape(max(N, 1), ml + 1), hist_len=hlen[:n].copy(), tel=tel.reshape(-1, 6)[:nc],
+                    final=np.array([so.final_residual_inf, so.final_comp_error, so.final_cone_violation,
+                                    so.min_gap, so.min_diag_shift, so.aborted, so.converged]),
+                    contacts=contacts_to_arrays(cout, nc), n_rows=so.n_rows, aborted=bool(so.aborted),
+                    ms=self.last_step_ms)
+
+
+class Scene:
+    """Product-side builders (nsd_scene_build): topology, shapes, state, config."""
+
+    def __init__(self, name: str, seed: int = 0):
+        h = C.c_void_p()
+        check(lib().nsd_scene_build(name.encode(), seed, C.byref(h)))
+        self._h = h
+        d = np.zeros(8, np.int32)
+        check(lib().nsd_scene_dims(h, _ip(d)))
+        self.dims = dict(zip(["n_bodies", "num_dof", "num_coord", "n_joints", "n_tets", "n_shapes",
+                              "newton_iterations", "linear_max_iterations"], (int(x) for x in d)))
+        t = nsd_topology()
+        check(lib().nsd_scene_topology(h, C.byref(t)))
+        nb, nj, nt = t.n_bodies, t.n_joints, t.n_tets
+
+        def arr(p, n, dt):
+            return np.ctypeslib.as_array(p, shape=(max(n, 0),)).astype(dt).copy() if n > 0 else np.zeros(0, dt)
+
+        self.topology = Topology(body_type=arr(t.body_type, nb, np.int32), body_mass=arr(t.body_mass, nb, float),
+                                 body_inertia=arr(t.body_inertia, 9 * nb, float),
+                                 joint_kind=arr(t.joint_kind, nj, np.int32), joint_body=arr(t.joint_body, 2 * nj, np.int32),
+                                 joint_frame=arr(t.joint_frame, 21 * nj, float),
+                                 joint_param=arr(t.joint_param, 2 * nj, float), tet_body=arr(t.tet_body, 4 * nt, np.int32),
+                                 tet_dm_inv=arr(t.tet_dm_inv, 9 * nt, float), tet_volume=arr(t.tet_volume, nt, float),
+                                 tet_material=arr(t.tet_material, 4 * nt, float))
+        ns = self.dims["n_shapes"]
+        self.shapes = (nsd_shape * max(ns, 1))()
+        mg, mud = C.c_double(), C.c_double()
+        check(lib().nsd_scene_shapes(h, C.cast(self.shapes, C.POINTER(nsd_shape)), C.byref(mg), C.byref(mud)))
+        self.n_shapes, self.margin, self.mu_default = ns, mg.value, mud.value
+        self.q, self.u = np.zeros(self.dims["num_coord"]), np.zeros(self.dims["num_dof"])
+        check(lib().nsd_scene_state(h, _dp(self.q), _dp(self.u)))
+        cfg, hh, g = nsd_config(), C.c_double(), np.zeros(3)
+        check(lib().nsd_scene_config(h, C.byref(cfg), C.byref(hh), _dp(g)))
+        self.config, self.h, self.gravity = NewtonConfig.from_c(cfg), hh.value, g
+        lib().nsd_scene_destroy(h)
+        self._h = None
+
+
+class BatchSolver:
+    """Many environments sharing one topology (nsd_batch_*): device narrow phase
+    + Newton step per env, one team (warp or CTA) per environment."""
+
+    def __init__(self, topology: Topology, shapes, n_shapes, margin, mu_default, config: NewtonConfig, n_env: int,
+                 max_contacts: int = 48, device: int = 0):
+        self.topology, self.config, self.n_env = topology, config, n_env
+        h = C.c_void_p()
+        check(lib().nsd_batch_create(C.byref(topology.c), n_shapes, C.cast(shapes, C.POINTER(nsd_shape)), margin,
+                                     mu_default, C.byref(config.to_c()), n_env, max_contacts, device, C.byref(h)))
+        self._h = h
+        info = np.zeros(6, np.int32)
+        check(lib().nsd_batch_info(h, _ip(info)))
+        self.info = info
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().nsd_batch_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def set_stream(self, stream_ptr):
+        check(lib().nsd_batch_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def set_state(self, q, u):
+        q = np.ascontiguousarray(q, np.float64)
+        u = np.ascontiguousarray(u, np.float64)
+        check(lib().nsd_batch_set_state(self._h, _dp(q), _dp(u)))
+
+    def get_state(self):
+        T = self.topology
+        q, u = np.zeros(self.n_env * T.num_coord), np.zeros(self.n_env * T.num_dof)
+        check(lib().nsd_batch_get_state(self._h, _dp(q), _dp(u)))
+        return q.reshape(self.n_env, -1), u.reshape(self.n_env, -1)
+
+    def step(self, h, gravity, torque=None):
+        g = np.ascontiguousarray(gravity, np.float64)
+        t = None if torque is None else np.ascontiguousarray(torque, np.float64)
+        check(lib().nsd_batch_step(self._h, _dp(t) if t is not None else None, 0, h, _dp(g)))
+
+    def step_device(self, h, gravity, torque_ptr=None, dtype=0):
+        g = np.ascontiguousarray(gravity, np.float64)
+        check(lib().nsd_batch_step_device(self._h, C.c_void_p(torque_ptr) if torque_ptr else None, dtype, h, _dp(g)))
+
+    def sync(self):
+        check(lib().nsd_batch_sync(self._h))
+
+    def results(self, with_iters=False):
+        n = self.n_env
+        nc, ab, fr = np.zeros(n, np.int32), np.zeros(n, np.int32), np.zeros(n)
+        N = self.config.newton_iterations
+        its = (nsd_iter_stats * (n * N))() if with_iters else None
+        check(lib().nsd_batch_results(self._h, _ip(nc), _ip(ab), _dp(fr),
+                                      C.cast(its, C.POINTER(nsd_iter_stats)) if its is not None else None))
+        out = dict(n_contacts=nc, aborted=ab, final_residual_inf=fr)
+        if its is not None:
+            out["stats"] = np.array([[it.residual_inf, it.merit_l2, it.comp_error_max, it.cone_violation_max,
+                                      it.step_size, it.linear_iterations, it.linear_residual, it.linear_breakdown]
+                                     for it in its]).reshape(n, N, 8)
+        return out
+
+    def contacts(self, env):
+        n = C.c_int32()
+        check(lib().nsd_batch_contacts(self._h, env, None, C.byref(n)))
+        arr = (nsd_contact * max(n.value, 1))()
+        check(lib().nsd_batch_contacts(self._h, env, C.cast(arr, C.POINTER(nsd_contact)), C.byref(n)))
+        return contacts_to_arrays(arr, n.value)
+
+    def device_state(self):
+        q, u, dt = C.c_void_p(), C.c_void_p(), C.c_int32()
+        check(lib().nsd_batch_device_state(self._h, C.byref(q), C.byref(u), C.byref(dt)))
+        return q.value, u.value, dt.value

@@ -1,0 +1,1273 @@
+// C-ABI implementation (include/nsdyn_gpu.h): handles, device memory, kernels.
+//
+//   k_single_block / k_single_grid  one scene, nsd_step (newton_step boundary)
+//   k_batch_warp / k_batch_block    many environments, nsd_batch_step
+//                                   (device narrow phase + newton_step per env)
+#include "nsdyn_gpu.h"
+
+#include "nsd_collide.cuh"
+#include "nsd_engine.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+struct NsdError : std::runtime_error {
+  int code;
+  NsdError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define NSD_CK(call)                                                                           \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      throw NsdError(NSD_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+template <class F> int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const NsdError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NSD_INVALID;
+  }
+}
+
+// Device buffer (raw bytes).
+struct DBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t bytes) {
+    if (bytes <= n && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    NSD_CK(cudaMalloc(&p, bytes ? bytes : 16));
+    n = bytes;
+  }
+  template <class T> T* as(size_t off_elems = 0) const { return static_cast<T*>(p) + off_elems; }
+};
+
+// Pinned host staging.
+struct HBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  ~HBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void alloc(size_t bytes) {
+    if (bytes <= n && p) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    NSD_CK(cudaMallocHost(&p, bytes ? bytes : 16));
+    n = bytes;
+  }
+};
+
+// Bump allocator over a byte layout (256-byte aligned sub-arrays).
+struct Layout {
+  size_t bytes = 0;
+  template <class T> size_t add(size_t count) {
+    const size_t off = (bytes + 255) & ~size_t(255);
+    bytes = off + sizeof(T) * std::max<size_t>(count, 1);
+    return off;
+  }
+};
+
+nsd::Cfg to_cfg(const nsd_config& c) {
+  nsd::Cfg o;
+  o.newton_iterations = c.newton_iterations;
+  o.step_fraction = c.step_fraction;
+  o.epsilon_reg = c.epsilon_reg;
+  o.geometric_stiffness = c.geometric_stiffness;
+  o.r_strategy = c.r_strategy;
+  o.ncp_kind = c.ncp_kind;
+  o.linear_max_iterations = c.linear_max_iterations;
+  o.linear_tolerance = c.linear_tolerance;
+  o.preconditioner = c.preconditioner;
+  o.newton_tolerance = c.newton_tolerance;
+  o.line_search = c.line_search;
+  return o;
+}
+
+void check_cfg(const nsd_config& c) {
+  if (c.precision != NSD_FP32 && c.precision != NSD_FP64) throw NsdError(NSD_INVALID, "precision must be 0 or 1");
+  if (c.linear_method != 3)
+    throw NsdError(NSD_UNSUPPORTED, "only PCR (linear_method 3) runs on the device path (SURVEY §8f row 4)");
+  if (c.linear_max_iterations < 1) throw NsdError(NSD_INVALID, "solve_linear: max_iterations < 1");
+  if (c.newton_iterations < 0) throw NsdError(NSD_INVALID, "newton_iterations < 0");
+  if (c.r_strategy < 0 || c.r_strategy > 2 || c.ncp_kind < 0 || c.ncp_kind > 1 || c.preconditioner < 0 ||
+      c.preconditioner > 1)
+    throw NsdError(NSD_INVALID, "config enum out of range");
+}
+
+// ------------------------------------------------------------------ host topology preprocessing
+struct HostTopo {
+  int nb = 0, ndof = 0, ncoord = 0, nd3 = 0, nj = 0, nt = 0, rows_joint = 0, rows_static = 0;
+  std::vector<int> btype, bdof, bcoord, d3_body, d3_kind, jkind, jbody, jrow, tbody, sinc_off, sinc_ent;
+  std::vector<double> bmass, binertia, jparam, jframe, tdminv, tvol, tmat;
+};
+
+void body_blocks_h(const HostTopo& T, int b, int& lin, int& ang) {
+  if (b < 0) {
+    lin = ang = -1;
+    return;
+  }
+  lin = T.bdof[b] / 3;
+  ang = T.btype[b] == 1 ? lin + 1 : -1;
+}
+
+HostTopo preprocess(const nsd_topology& tp) {
+  HostTopo T;
+  if (tp.n_bodies < 0 || tp.n_joints < 0 || tp.n_tets < 0) throw NsdError(NSD_INVALID, "negative counts");
+  T.nb = tp.n_bodies;
+  T.nj = tp.n_joints;
+  T.nt = tp.n_tets;
+  for (int b = 0; b < T.nb; ++b) {
+    const int ty = tp.body_type[b];
+    if (ty != 0 && ty != 1) throw NsdError(NSD_INVALID, "body type must be 0 or 1");
+    if (!(tp.body_mass[b] > 0.0)) throw NsdError(NSD_INVALID, "body mass must be positive");
+    T.btype.push_back(ty);
+    T.bdof.push_back(T.ndof);
+    T.bcoord.push_back(T.ncoord);
+    T.ndof += ty ? 6 : 3;
+    T.ncoord += ty ? 7 : 3;
+    T.bmass.push_back(tp.body_mass[b]);
+    for (int k = 0; k < 9; ++k) T.binertia.push_back(ty ? tp.body_inertia[9 * b + k] : (k % 4 == 0 ? 1.0 : 0.0));
+    T.d3_body.push_back(b);
+    T.d3_kind.push_back(ty ? nsd::kRigidLin : nsd::kParticleLin);
+    if (ty) {
+      T.d3_body.push_back(b);
+      T.d3_kind.push_back(nsd::kRigidAng);
+    }
+  }
+  T.nd3 = T.ndof / 3;
+  int row = 0;
+  for (int j = 0; j < T.nj; ++j) {
+    const int k = tp.joint_kind[j];
+    if (k < 0 || k > 3) throw NsdError(NSD_INVALID, "joint kind out of range");
+    const int a = tp.joint_body[2 * j], b = tp.joint_body[2 * j + 1];
+    if (a >= T.nb || b >= T.nb || a < -1 || b < -1) throw NsdError(NSD_INVALID, "joint references invalid body");
+    T.jkind.push_back(k);
+    T.jbody.push_back(a);
+    T.jbody.push_back(b);
+    T.jrow.push_back(row);
+    row += nsd::joint_nrows(k);
+    for (int i = 0; i < 21; ++i) T.jframe.push_back(tp.joint_frame[21 * j + i]);
+    T.jparam.push_back(tp.joint_param[2 * j]);
+    T.jparam.push_back(tp.joint_param[2 * j + 1]);
+  }
+  T.rows_joint = row;
+  for (int e = 0; e < T.nt; ++e) {
+    for (int k = 0; k < 4; ++k) {
+      const int b = tp.tet_body[4 * e + k];
+      if (b < 0 || b >= T.nb || T.btype[b] != 0) throw NsdError(NSD_INVALID, "tet vertex must be a particle body");
+      T.tbody.push_back(b);
+    }
+    for (int k = 0; k < 9; ++k) T.tdminv.push_back(tp.tet_dm_inv[9 * e + k]);
+    T.tvol.push_back(tp.tet_volume[e]);
+    for (int k = 0; k < 4; ++k) T.tmat.push_back(tp.tet_material[4 * e + k]);
+  }
+  T.rows_static = T.rows_joint + 3 * T.nt;
+  // static incidence: (row, slot) per dof3 block, rows ascending
+  std::vector<std::vector<int>> inc(T.nd3);
+  for (int j = 0; j < T.nj; ++j) {
+    int al, aa, bl, ba;
+    body_blocks_h(T, T.jbody[2 * j], al, aa);
+    body_blocks_h(T, T.jbody[2 * j + 1], bl, ba);
+    for (int k = 0; k < nsd::joint_nrows(T.jkind[j]); ++k) {
+      const bool lin = nsd::joint_row_linear(T.jkind[j], k);
+      int b4[4] = {lin ? al : -1, aa, lin ? bl : -1, ba};
+      if (b4[2] >= 0 && b4[2] == b4[0]) b4[2] = -1;
+      if (b4[3] >= 0 && b4[3] == b4[1]) b4[3] = -1;
+      const int r = T.jrow[j] + k;
+      for (int s = 0; s < 4; ++s)
+        if (b4[s] >= 0) inc[b4[s]].push_back(4 * r + s);
+    }
+  }
+  for (int e = 0; e < T.nt; ++e)
+    for (int i = 0; i < 3; ++i) {
+      const int r = T.rows_joint + 3 * e + i;
+      for (int s = 0; s < 4; ++s) inc[T.bdof[T.tbody[4 * e + s]] / 3].push_back(4 * r + s);
+    }
+  T.sinc_off.assign(T.nd3 + 1, 0);
+  for (int b = 0; b < T.nd3; ++b) {
+    T.sinc_off[b + 1] = T.sinc_off[b] + static_cast<int>(inc[b].size());
+    for (int v : inc[b]) T.sinc_ent.push_back(v);
+  }
+  return T;
+}
+
+// Device copy of the static topology in precision R.
+template <class R> struct DevTopo {
+  DBuf buf;
+  nsd::Topo<R> t{};
+  R* jframe = nullptr;  // the (updatable) joint frames
+  void upload(const HostTopo& H) {
+    Layout L;
+    const size_t o_btype = L.add<int>(H.nb), o_bdof = L.add<int>(H.nb), o_bcoord = L.add<int>(H.nb),
+                 o_d3b = L.add<int>(H.nd3), o_d3k = L.add<int>(H.nd3), o_jkind = L.add<int>(H.nj),
+                 o_jbody = L.add<int>(2 * H.nj), o_jrow = L.add<int>(H.nj), o_tbody = L.add<int>(4 * H.nt),
+                 o_soff = L.add<int>(H.nd3 + 1), o_sent = L.add<int>(H.sinc_ent.size()), o_bmass = L.add<R>(H.nb),
+                 o_bin = L.add<R>(9 * H.nb), o_jparam = L.add<R>(2 * H.nj), o_jframe = L.add<R>(21 * H.nj),
+                 o_tdm = L.add<R>(9 * H.nt), o_tvol = L.add<R>(H.nt), o_tmat = L.add<R>(4 * H.nt);
+    std::vector<char> host(L.bytes, 0);
+    auto put_i = [&](size_t off, const std::vector<int>& v) {
+      if (!v.empty()) std::memcpy(host.data() + off, v.data(), v.size() * sizeof(int));
+    };
+    auto put_r = [&](size_t off, const std::vector<double>& v) {
+      R* d = reinterpret_cast<R*>(host.data() + off);
+      for (size_t i = 0; i < v.size(); ++i) d[i] = static_cast<R>(v[i]);
+    };
+    put_i(o_btype, H.btype);
+    put_i(o_bdof, H.bdof);
+    put_i(o_bcoord, H.bcoord);
+    put_i(o_d3b, H.d3_body);
+    put_i(o_d3k, H.d3_kind);
+    put_i(o_jkind, H.jkind);
+    put_i(o_jbody, H.jbody);
+    put_i(o_jrow, H.jrow);
+    put_i(o_tbody, H.tbody);
+    put_i(o_soff, H.sinc_off);
+    put_i(o_sent, H.sinc_ent);
+    put_r(o_bmass, H.bmass);
+    put_r(o_bin, H.binertia);
+    put_r(o_jparam, H.jparam);
+    put_r(o_jframe, H.jframe);
+    put_r(o_tdm, H.tdminv);
+    put_r(o_tvol, H.tvol);
+    put_r(o_tmat, H.tmat);
+    buf.alloc(L.bytes);
+    NSD_CK(cudaMemcpy(buf.p, host.data(), L.bytes, cudaMemcpyHostToDevice));
+    char* base = static_cast<char*>(buf.p);
+    t.nb = H.nb;
+    t.ndof = H.ndof;
+    t.ncoord = H.ncoord;
+    t.nd3 = H.nd3;
+    t.btype = reinterpret_cast<const int*>(base + o_btype);
+    t.bmass = reinterpret_cast<const R*>(base + o_bmass);
+    t.binertia = reinterpret_cast<const R*>(base + o_bin);
+    t.bdof = reinterpret_cast<const int*>(base + o_bdof);
+    t.bcoord = reinterpret_cast<const int*>(base + o_bcoord);
+    t.d3_body = reinterpret_cast<const int*>(base + o_d3b);
+    t.d3_kind = reinterpret_cast<const int*>(base + o_d3k);
+    t.nj = H.nj;
+    t.jkind = reinterpret_cast<const int*>(base + o_jkind);
+    t.jbody = reinterpret_cast<const int*>(base + o_jbody);
+    t.jparam = reinterpret_cast<const R*>(base + o_jparam);
+    t.jrow = reinterpret_cast<const int*>(base + o_jrow);
+    t.rows_joint = H.rows_joint;
+    t.nt = H.nt;
+    t.tbody = reinterpret_cast<const int*>(base + o_tbody);
+    t.tdminv = reinterpret_cast<const R*>(base + o_tdm);
+    t.tvol = reinterpret_cast<const R*>(base + o_tvol);
+    t.tmat = reinterpret_cast<const R*>(base + o_tmat);
+    t.rows_static = H.rows_static;
+    t.sinc_off = reinterpret_cast<const int*>(base + o_soff);
+    t.sinc_ent = reinterpret_cast<const int*>(base + o_sent);
+    jframe = reinterpret_cast<R*>(base + o_jframe);
+  }
+};
+
+// Offsets (in elements) of one scene's Work arrays inside an R arena and an
+// int arena. Used for the single scene (one instance) and per env (strided).
+struct WorkPlan {
+  // R arrays
+  size_t q, q0, qp, u, u0, ut, g, gp, up, shift, hinv, w, du, ub, fx, iw6, iwi6, coeff, hv, cd, lam, x, xn, r, rn, z,
+      zn, p, ap, az, inv, bx, ctet, cgeo, strideR;
+  // int arrays
+  size_t blk, cbody, cfeat, cinc_off, cinc_ent, cinc_cnt, strideI;
+  void plan(const HostTopo& T, int ccap) {
+    const size_t rcap = T.rows_static + 3 * static_cast<size_t>(ccap);
+    size_t o = 0;
+    auto a = [&](size_t n) {
+      const size_t off = o;
+      o += (n + 31) & ~size_t(31);  // 32-element alignment inside an env slice
+      return off;
+    };
+    q = a(T.ncoord);
+    q0 = a(T.ncoord);
+    qp = a(T.ncoord);
+    u = a(T.ndof);
+    u0 = a(T.ndof);
+    ut = a(T.ndof);
+    g = a(T.ndof);
+    gp = a(T.ndof);
+    up = a(T.ndof);
+    shift = a(T.ndof);
+    hinv = a(T.ndof);
+    w = a(T.ndof);
+    du = a(T.ndof);
+    ub = a(T.ndof);
+    fx = a(T.ndof);
+    iw6 = a(6 * T.nd3);
+    iwi6 = a(6 * T.nd3);
+    coeff = a(12 * rcap);
+    hv = a(rcap);
+    cd = a(rcap);
+    lam = a(rcap);
+    x = a(rcap);
+    xn = a(rcap);
+    r = a(rcap);
+    rn = a(rcap);
+    z = a(rcap);
+    zn = a(rcap);
+    p = a(rcap);
+    ap = a(rcap);
+    az = a(rcap);
+    inv = a(rcap);
+    bx = a(rcap);
+    ctet = a(9 * static_cast<size_t>(T.nt));
+    cgeo = a(17 * static_cast<size_t>(ccap));
+    strideR = o;
+    o = 0;
+    blk = a(4 * rcap);
+    cbody = a(2 * static_cast<size_t>(ccap));
+    cfeat = a(ccap);
+    cinc_off = a(T.nd3 + 1);
+    cinc_ent = a(4 * static_cast<size_t>(ccap));
+    cinc_cnt = a(T.nd3 + 1);
+    strideI = o;
+  }
+  template <class R> __host__ __device__ nsd::Work<R> bind(R* rb, int* ib) const {
+    nsd::Work<R> W{};
+    W.q = rb + q;
+    W.q0 = rb + q0;
+    W.qp = rb + qp;
+    W.u = rb + u;
+    W.u0 = rb + u0;
+    W.ut = rb + ut;
+    W.g = rb + g;
+    W.gp = rb + gp;
+    W.up = rb + up;
+    W.shift = rb + shift;
+    W.hinv = rb + hinv;
+    W.w = rb + w;
+    W.du = rb + du;
+    W.ub = rb + ub;
+    W.iw6 = rb + iw6;
+    W.iwi6 = rb + iwi6;
+    W.coeff = rb + coeff;
+    W.hv = rb + hv;
+    W.cd = rb + cd;
+    W.lam = rb + lam;
+    W.x = rb + x;
+    W.xn = rb + xn;
+    W.r = rb + r;
+    W.rn = rb + rn;
+    W.z = rb + z;
+    W.zn = rb + zn;
+    W.p = rb + p;
+    W.ap = rb + ap;
+    W.az = rb + az;
+    W.inv = rb + inv;
+    W.bx = rb + bx;
+    W.ctet = rb + ctet;
+    W.cgeo = rb + cgeo;
+    W.blk = ib + blk;
+    W.cbody = ib + cbody;
+    W.cinc_off = ib + cinc_off;
+    W.cinc_ent = ib + cinc_ent;
+    return W;
+  }
+};
+
+}  // namespace
+
+// ================================================================== kernels
+template <class R>
+__global__ void __launch_bounds__(1024) k_single_block(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out) {
+  __shared__ double red[2 * 33 * nsd::kRedMax];
+  nsd::BlockTeam t(red);
+  nsd::newton_setup(t, T, W);
+  t.sync();
+  nsd::newton_solve(t, T, W, cfg, out);
+}
+
+template <class R>
+__global__ void __launch_bounds__(256) k_single_grid(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out,
+                                                     double* gpart) {
+  __shared__ double red[2 * 33 * nsd::kRedMax];
+  nsd::GridTeam t(red, gpart);
+  nsd::newton_setup(t, T, W);
+  t.sync();
+  nsd::newton_solve(t, T, W, cfg, out);
+}
+
+
+// ------------------------------------------------------------------ batched
+template <class R> struct BatchArgs {
+  nsd::Topo<R> T;
+  nsd::Cfg cfg;
+  int n_env, ns, npairs, maxc;
+  const int2* pairs;
+  const nsd::ShapeD<R>* shapes;
+  const R* jframe;
+  R margin, mu_default, h, grav[3];
+  R* qs;  // persistent state (n_env * ncoord)
+  R* us;
+  const void* torque;  // n_env * nj or null
+  int torque_double;
+  R* rbase;
+  int* ibase;
+  size_t strideR, strideI;
+  WorkPlan plan;
+  nsd::CandD<R>* cand;  // n_env * npairs * 4
+  int* pair_cnt;        // n_env * npairs
+  int* nc_out;          // n_env
+  int* overflow;        // n_env
+  double* fin;          // n_env * 8
+  nsd::IterOut* iters;  // n_env * newton_iterations
+};
+
+// One environment: extension forces, setup, device narrow phase, contact
+// incidence, Newton solve, state write-back (step_world, scene.cpp:709-732).
+template <class R, class Team> __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env) {
+  const nsd::Topo<R>& T = A.T;
+  R* rb = A.rbase + (size_t)env * A.strideR;
+  int* ib = A.ibase + (size_t)env * A.strideI;
+  nsd::Work<R> W = A.plan.template bind<R>(rb, ib);
+  W.jframe = A.jframe;
+  W.h = A.h;
+  W.grav[0] = A.grav[0];
+  W.grav[1] = A.grav[1];
+  W.grav[2] = A.grav[2];
+  R* qs = A.qs + (size_t)env * T.ncoord;
+  R* us = A.us + (size_t)env * T.ndof;
+  R* q0 = rb + A.plan.q0;
+  R* u0 = rb + A.plan.u0;
+  for (int i = t.rank(); i < T.ncoord; i += t.size()) q0[i] = qs[i];
+  for (int i = t.rank(); i < T.ndof; i += t.size()) u0[i] = us[i];
+  W.f_extra = nullptr;
+  if (A.torque) {
+    R* fx = rb + A.plan.fx;
+    t.sync();
+    // joint torques about revolute axes at q- (extension hook): +tau*axis on a, -tau*axis on b
+    for (int b = t.rank(); b < T.nb; b += t.size()) {
+      const int d = T.bdof[b];
+      nsd::V3<R> f = nsd::v3(R(0), R(0), R(0));
+      if (T.btype[b] == 1) {
+        for (int j = 0; j < T.nj; ++j) {
+          if (T.jkind[j] != 1) continue;
+          const int ja = T.jbody[2 * j], jb = T.jbody[2 * j + 1];
+          if (ja != b && jb != b) continue;
+          const R tau = A.torque_double ? R(static_cast<const double*>(A.torque)[(size_t)env * T.nj + j])
+                                        : R(static_cast<const float*>(A.torque)[(size_t)env * T.nj + j]);
+          const nsd::V3<R> axl = nsd::ld3(A.jframe + 21 * j + 6);
+          const nsd::V3<R> ax = ja < 0 ? axl : nsd::mul(nsd::body_rot(T, q0, ja), axl);
+          if (ja == b) f = f + tau * ax;
+          if (jb == b) f = f - tau * ax;
+        }
+      }
+      for (int k = 0; k < 3; ++k) fx[d + k] = R(0);
+      if (T.btype[b] == 1) nsd::st3(fx + d + 3, f);
+    }
+    W.f_extra = fx;
+  }
+  t.sync();
+  nsd::newton_setup(t, T, W);
+  t.sync();
+  // ---- narrow phase over shape pairs with the unconstrained velocity
+  nsd::BodyView<R> view{T.btype, T.bdof, T.bcoord, W.q0, W.ut};
+  nsd::CandD<R>* cand = A.cand + (size_t)env * A.npairs * 4;
+  int* cnt = A.pair_cnt + (size_t)env * A.npairs;
+  for (int p = t.rank(); p < A.npairs; p += t.size()) {
+    const int2 ij = A.pairs[p];
+    R th, mu;
+    cnt[p] = nsd::pair_contacts(view, A.shapes[ij.x], A.shapes[ij.y], A.h, A.margin, A.mu_default, cand + 4 * p, &th,
+                                &mu);
+  }
+  t.sync();
+  int total = 0;
+  for (int p = 0; p < A.npairs; ++p) total += cnt[p];
+  const int nc = total < A.maxc ? total : A.maxc;
+  int* cbody = ib + A.plan.cbody;
+  int* cfeat = ib + A.plan.cfeat;
+  R* cgeo = rb + A.plan.cgeo;
+  // canonical (a.body, b.body, feature) order, stable in generation order
+  for (int p = t.rank(); p < A.npairs; p += t.size()) {
+    for (int k = 0; k < cnt[p]; ++k) {
+      const nsd::CandD<R>& c = cand[4 * p + k];
+      int rank = 0;
+      for (int p2 = 0; p2 < A.npairs; ++p2)
+        for (int k2 = 0; k2 < cnt[p2]; ++k2) {
+          const nsd::CandD<R>& o = cand[4 * p2 + k2];
+          if (nsd::canonical_less(o.a, o.b, o.feature, c.a, c.b, c.feature) ||
+              (o.a == c.a && o.b == c.b && o.feature == c.feature && (p2 < p || (p2 == p && k2 < k))))
+            ++rank;
+        }
+      if (rank >= nc) continue;
+      cbody[2 * rank] = c.a;
+      cbody[2 * rank + 1] = c.b;
+      cfeat[rank] = c.feature;
+      R* g = cgeo + 17 * rank;
+      nsd::V3<R> n = nsd::get3(c.n), d1, d2;
+      nsd::tangent_basis(n, d1, d2);
+      for (int i = 0; i < 3; ++i) {
+        g[i] = c.la[i];
+        g[3 + i] = c.lb[i];
+        g[6 + i] = c.n[i];
+      }
+      nsd::st3(g + 9, d1);
+      nsd::st3(g + 12, d2);
+      g[15] = c.thick;
+      g[16] = c.mu;
+    }
+  }
+  t.sync();
+  W.nc = nc;
+  W.normal_begin = T.rows_static;
+  W.friction_begin = T.rows_static + nc;
+  W.nrows = T.rows_static + 3 * nc;
+  // ---- contact incidence per dof3 block (contact*4 + slot, contacts ascending)
+  int* coff = ib + A.plan.cinc_off;
+  int* cent = ib + A.plan.cinc_ent;
+  int* ccnt = ib + A.plan.cinc_cnt;
+  for (int b = t.rank(); b < T.nd3; b += t.size()) {
+    int n = 0;
+    for (int c = 0; c < nc; ++c) {
+      int al, aa, bl, ba;
+      nsd::body_blocks(T, cbody[2 * c], al, aa);
+      nsd::body_blocks(T, cbody[2 * c + 1], bl, ba);
+      if (bl >= 0 && bl == al) bl = -1;
+      if (ba >= 0 && ba == aa) ba = -1;
+      n += (al == b) + (aa == b) + (bl == b) + (ba == b);
+    }
+    ccnt[b] = n;
+  }
+  t.sync();
+  if (t.rank() == 0) {
+    int s = 0;
+    for (int b = 0; b < T.nd3; ++b) {
+      coff[b] = s;
+      s += ccnt[b];
+    }
+    coff[T.nd3] = s;
+  }
+  t.sync();
+  for (int b = t.rank(); b < T.nd3; b += t.size()) {
+    int o = coff[b];
+    for (int c = 0; c < nc; ++c) {
+      int b4[4];
+      nsd::body_blocks(T, cbody[2 * c], b4[0], b4[1]);
+      nsd::body_blocks(T, cbody[2 * c + 1], b4[2], b4[3]);
+      if (b4[2] >= 0 && b4[2] == b4[0]) b4[2] = -1;
+      if (b4[3] >= 0 && b4[3] == b4[1]) b4[3] = -1;
+      for (int s = 0; s < 4; ++s)
+        if (b4[s] == b) cent[o++] = 4 * c + s;
+    }
+  }
+  t.sync();
+  nsd::StepOut out{};
+  out.iters = A.iters ? A.iters + (size_t)env * A.cfg.newton_iterations : nullptr;
+  out.fin = A.fin + (size_t)env * 8;
+  nsd::newton_solve(t, T, W, A.cfg, out);
+  t.sync();
+  for (int i = t.rank(); i < T.ncoord; i += t.size()) qs[i] = W.q[i];
+  for (int i = t.rank(); i < T.ndof; i += t.size()) us[i] = W.u[i];
+  if (t.rank() == 0) {
+    A.nc_out[env] = nc;
+    A.overflow[env] = total > A.maxc ? total : 0;
+  }
+}
+
+template <class R> __global__ void __launch_bounds__(128) k_batch_warp(BatchArgs<R> A) {
+  const int env = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (env >= A.n_env) return;  // warp-uniform
+  nsd::WarpTeam t(threadIdx.x & 31);
+  batch_env(t, A, env);
+}
+
+template <class R> __global__ void __launch_bounds__(256) k_batch_block(BatchArgs<R> A) {
+  __shared__ double red[2 * 33 * nsd::kRedMax];
+  nsd::BlockTeam t(red);
+  batch_env(t, A, blockIdx.x);
+}
+
+// ================================================================== handles
+struct SolverBase {
+  virtual ~SolverBase() = default;
+  virtual int step(const nsd_step_in* in, nsd_step_out* out) = 0;
+  virtual void set_cfg(const nsd_config& c) = 0;
+  double last_ms = 0.0;
+};
+
+template <class R> struct Solver final : SolverBase {
+  HostTopo H;
+  DevTopo<R> topo;
+  nsd_config cfg;
+  int ccap = 0;
+  WorkPlan plan;
+  DBuf rarena, iarena, outbuf, gpart;
+  HBuf stage_r, stage_i, stage_o;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int grid_blocks = 0;
+  bool use_grid = false;
+  int block_threads = 256;
+
+  Solver(const nsd_topology& tp, const nsd_config& c, int device) : cfg(c) {
+    NSD_CK(cudaSetDevice(device));
+    H = preprocess(tp);
+    topo.upload(H);
+    NSD_CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    NSD_CK(cudaEventCreate(&ev0));
+    NSD_CK(cudaEventCreate(&ev1));
+    ensure(16);
+    const size_t work = std::max<size_t>({(size_t)H.rows_static + 48, (size_t)H.nd3, (size_t)H.nb});
+    if (work <= 4096) {
+      use_grid = false;
+      block_threads = work <= 256 ? 128 : (work <= 1024 ? 256 : 512);
+    } else {
+      use_grid = true;
+      int dev_sms = 0, per_sm = 0;
+      NSD_CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
+      NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R>, 256, 0));
+      if (per_sm < 1) throw NsdError(NSD_CUDA_ERROR, "grid kernel cannot be resident");
+      grid_blocks = dev_sms * std::min(per_sm, 2);
+      gpart.alloc(sizeof(double) * 2 * grid_blocks * nsd::kRedMax);
+    }
+  }
+  ~Solver() override {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+  void set_cfg(const nsd_config& c) override { cfg = c; }
+  void ensure(int nc) {
+    if (nc <= ccap && rarena.p) return;
+    ccap = std::max(nc, std::max(16, ccap * 2));
+    plan.plan(H, ccap);
+    rarena.alloc(sizeof(R) * plan.strideR);
+    iarena.alloc(sizeof(int) * plan.strideI);
+  }
+
+  int step(const nsd_step_in* in, nsd_step_out* out) override {
+    if (!in || !out || !in->q || !in->u || !out->q || !out->u) throw NsdError(NSD_INVALID, "null step buffers");
+    if (!(in->h > 0.0)) throw NsdError(NSD_INVALID, "integrate_coordinates: h must be positive");
+    const int nc = in->n_contacts;
+    if (nc < 0 || (nc > 0 && !in->contacts)) throw NsdError(NSD_INVALID, "bad contact list");
+    for (int c = 0; c < nc; ++c) {
+      const nsd_contact& k = in->contacts[c];
+      if (k.body_a < -1 || k.body_a >= H.nb || k.body_b < -1 || k.body_b >= H.nb)
+        throw NsdError(NSD_INVALID, "contact references invalid body");
+    }
+    ensure(nc);
+    const int N = cfg.newton_iterations, ml = cfg.linear_max_iterations;
+    const int nrows = H.rows_static + 3 * nc;
+    // ---- stage inputs: q0, u0, f_extra(fx), cgeo, jframe (R); cbody, cinc (int)
+    const size_t nR = (size_t)H.ncoord + H.ndof + H.ndof + 17 * (size_t)nc + 21 * (size_t)H.nj;
+    stage_r.alloc(sizeof(R) * nR);
+    R* sr = static_cast<R*>(stage_r.p);
+    size_t o = 0;
+    for (int i = 0; i < H.ncoord; ++i) sr[o++] = R(in->q[i]);
+    for (int i = 0; i < H.ndof; ++i) sr[o++] = R(in->u[i]);
+    for (int i = 0; i < H.ndof; ++i) sr[o++] = in->f_extra ? R(in->f_extra[i]) : R(0);
+    for (int c = 0; c < nc; ++c) {
+      const nsd_contact& k = in->contacts[c];
+      for (int i = 0; i < 3; ++i) sr[o + i] = R(k.local_a[i]);
+      for (int i = 0; i < 3; ++i) sr[o + 3 + i] = R(k.local_b[i]);
+      for (int i = 0; i < 3; ++i) sr[o + 6 + i] = R(k.normal[i]);
+      for (int i = 0; i < 3; ++i) sr[o + 9 + i] = R(k.d1[i]);
+      for (int i = 0; i < 3; ++i) sr[o + 12 + i] = R(k.d2[i]);
+      sr[o + 15] = R(k.thickness);
+      sr[o + 16] = R(k.mu);
+      o += 17;
+    }
+    const double* jf = in->joint_frame ? in->joint_frame : H.jframe.data();
+    for (int i = 0; i < 21 * H.nj; ++i) sr[o++] = R(jf[i]);
+    // contact incidence (contact*4 + slot), contacts ascending within a block
+    std::vector<int> cnt(H.nd3 + 1, 0);
+    std::vector<int> b4all(4 * (size_t)nc);
+    for (int c = 0; c < nc; ++c) {
+      int* b4 = &b4all[4 * c];
+      body_blocks_h(H, in->contacts[c].body_a, b4[0], b4[1]);
+      body_blocks_h(H, in->contacts[c].body_b, b4[2], b4[3]);
+      if (b4[2] >= 0 && b4[2] == b4[0]) b4[2] = -1;
+      if (b4[3] >= 0 && b4[3] == b4[1]) b4[3] = -1;
+      for (int s = 0; s < 4; ++s)
+        if (b4[s] >= 0) cnt[b4[s] + 1]++;
+    }
+    for (int b = 0; b < H.nd3; ++b) cnt[b + 1] += cnt[b];
+    const size_t nI = 2 * (size_t)nc + (H.nd3 + 1) + 4 * (size_t)nc;
+    stage_i.alloc(sizeof(int) * nI);
+    int* si = static_cast<int*>(stage_i.p);
+    for (int c = 0; c < nc; ++c) {
+      si[2 * c] = in->contacts[c].body_a;
+      si[2 * c + 1] = in->contacts[c].body_b;
+    }
+    int* soff = si + 2 * nc;
+    int* sent = soff + H.nd3 + 1;
+    for (int b = 0; b <= H.nd3; ++b) soff[b] = cnt[b];
+    {
+      std::vector<int> fillp(cnt.begin(), cnt.end() - 1);
+      for (int c = 0; c < nc; ++c)
+        for (int s = 0; s < 4; ++s) {
+          const int b = b4all[4 * c + s];
+          if (b >= 0) sent[fillp[b]++] = 4 * c + s;
+        }
+    }
+    R* rb = rarena.as<R>();
+    int* ib = iarena.as<int>();
+    R* q0 = rb + plan.q0;
+    R* u0 = rb + plan.u0;
+    R* fx = rb + plan.fx;
+    R* cgeo = rb + plan.cgeo;
+    NSD_CK(cudaMemcpyAsync(q0, sr, sizeof(R) * H.ncoord, cudaMemcpyHostToDevice, stream));
+    NSD_CK(cudaMemcpyAsync(u0, sr + H.ncoord, sizeof(R) * H.ndof, cudaMemcpyHostToDevice, stream));
+    NSD_CK(cudaMemcpyAsync(fx, sr + H.ncoord + H.ndof, sizeof(R) * H.ndof, cudaMemcpyHostToDevice, stream));
+    if (nc)
+      NSD_CK(cudaMemcpyAsync(cgeo, sr + H.ncoord + 2 * H.ndof, sizeof(R) * 17 * nc, cudaMemcpyHostToDevice, stream));
+    if (H.nj)
+      NSD_CK(cudaMemcpyAsync(topo.jframe, sr + H.ncoord + 2 * H.ndof + 17 * nc, sizeof(R) * 21 * H.nj,
+                             cudaMemcpyHostToDevice, stream));
+    if (nc) NSD_CK(cudaMemcpyAsync(ib + plan.cbody, si, sizeof(int) * 2 * nc, cudaMemcpyHostToDevice, stream));
+    NSD_CK(cudaMemcpyAsync(ib + plan.cinc_off, soff, sizeof(int) * (H.nd3 + 1), cudaMemcpyHostToDevice, stream));
+    if (nc)
+      NSD_CK(cudaMemcpyAsync(ib + plan.cinc_ent, sent, sizeof(int) * cnt[H.nd3], cudaMemcpyHostToDevice, stream));
+    // ---- outputs
+    Layout L;
+    const size_t o_it = L.add<nsd::IterOut>(N), o_hist = L.add<double>((size_t)N * (ml + 1)),
+                 o_hl = L.add<int>(N), o_tel = L.add<double>(6 * (size_t)nc), o_fin = L.add<double>(8);
+    outbuf.alloc(L.bytes);
+    char* ob = outbuf.as<char>();
+    NSD_CK(cudaMemsetAsync(ob, 0, L.bytes, stream));
+    nsd::StepOut so{};
+    so.iters = reinterpret_cast<nsd::IterOut*>(ob + o_it);
+    so.hist = reinterpret_cast<double*>(ob + o_hist);
+    so.hist_len = reinterpret_cast<int*>(ob + o_hl);
+    so.tel = reinterpret_cast<double*>(ob + o_tel);
+    so.fin = reinterpret_cast<double*>(ob + o_fin);
+    nsd::Work<R> W = plan.bind<R>(rb, ib);
+    W.jframe = topo.jframe;
+    W.f_extra = in->f_extra ? fx : nullptr;
+    W.h = R(in->h);
+    for (int k = 0; k < 3; ++k) W.grav[k] = R(in->gravity[k]);
+    W.nc = nc;
+    W.nrows = nrows;
+    W.normal_begin = H.rows_static;
+    W.friction_begin = H.rows_static + nc;
+    nsd::Cfg kc = to_cfg(cfg);
+    NSD_CK(cudaEventRecord(ev0, stream));
+    if (!use_grid) {
+      k_single_block<R><<<1, block_threads, 0, stream>>>(topo.t, W, kc, so);
+      NSD_CK(cudaGetLastError());
+    } else {
+      double* gp = gpart.as<double>();
+      void* args[] = {&topo.t, &W, &kc, &so, &gp};
+      NSD_CK(cudaLaunchCooperativeKernel((void*)k_single_grid<R>, dim3(grid_blocks), dim3(256), args, 0, stream));
+    }
+    NSD_CK(cudaEventRecord(ev1, stream));
+    // ---- download
+    stage_o.alloc(L.bytes + sizeof(R) * ((size_t)H.ncoord + H.ndof + nrows));
+    char* ho = static_cast<char*>(stage_o.p);
+    NSD_CK(cudaMemcpyAsync(ho, ob, L.bytes, cudaMemcpyDeviceToHost, stream));
+    R* hq = reinterpret_cast<R*>(ho + L.bytes);
+    R* hu = hq + H.ncoord;
+    R* hl = hu + H.ndof;
+    NSD_CK(cudaMemcpyAsync(hq, rb + plan.q, sizeof(R) * H.ncoord, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(hu, rb + plan.u, sizeof(R) * H.ndof, cudaMemcpyDeviceToHost, stream));
+    if (nrows) NSD_CK(cudaMemcpyAsync(hl, rb + plan.lam, sizeof(R) * nrows, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaStreamSynchronize(stream));
+    float ms = 0.f;
+    NSD_CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    last_ms = ms;
+    const double* fin = reinterpret_cast<const double*>(ho + o_fin);
+    const nsd::IterOut* its = reinterpret_cast<const nsd::IterOut*>(ho + o_it);
+    const int nit = static_cast<int>(fin[7]);
+    const bool aborted = fin[5] != 0.0;
+    for (int i = 0; i < H.ncoord; ++i) out->q[i] = double(hq[i]);
+    for (int i = 0; i < H.ndof; ++i) out->u[i] = double(hu[i]);
+    if (out->lambda)
+      for (int i = 0; i < nrows; ++i) out->lambda[i] = double(hl[i]);
+    if (out->iters)
+      for (int i = 0; i < nit; ++i) {
+        nsd_iter_stats& s = out->iters[i];
+        s.residual_inf = its[i].residual_inf;
+        s.merit_l2 = its[i].merit_l2;
+        s.comp_error_max = its[i].comp_error_max;
+        s.cone_violation_max = its[i].cone_violation_max;
+        s.step_size = its[i].step_size;
+        s.linear_residual = its[i].linear_residual;
+        s.linear_iterations = its[i].linear_iterations;
+        s.linear_breakdown = its[i].linear_breakdown;
+      }
+    if (out->linear_history) {
+      const double* hh = reinterpret_cast<const double*>(ho + o_hist);
+      std::memcpy(out->linear_history, hh, sizeof(double) * (size_t)N * (ml + 1));
+    }
+    if (out->linear_history_len) std::memcpy(out->linear_history_len, ho + o_hl, sizeof(int) * N);
+    if (out->contact_telemetry && nc && !aborted)
+      std::memcpy(out->contact_telemetry, ho + o_tel, sizeof(double) * 6 * nc);
+    if (out->contacts && !aborted) {
+      const int nb0 = H.rows_static, fb0 = H.rows_static + nc;
+      for (int c = 0; c < nc; ++c) {
+        if (out->contacts != in->contacts) out->contacts[c] = in->contacts[c];
+        out->contacts[c].lambda_n = double(hl[nb0 + c]);
+        out->contacts[c].lambda_f[0] = double(hl[fb0 + 2 * c]);
+        out->contacts[c].lambda_f[1] = double(hl[fb0 + 2 * c + 1]);
+      }
+    }
+    out->n_iterations = nit;
+    out->n_rows = nrows;
+    out->final_residual_inf = fin[0];
+    out->final_comp_error = fin[1];
+    out->final_cone_violation = fin[2];
+    out->min_gap = fin[3];
+    out->min_diag_shift = fin[4];
+    out->aborted = aborted ? 1 : 0;
+    out->converged = fin[6] != 0.0 ? 1 : 0;
+    return aborted ? NSD_ABORTED : NSD_OK;
+  }
+};
+
+struct BatchBase {
+  virtual ~BatchBase() = default;
+  virtual void set_state(const double* q, const double* u) = 0;
+  virtual void get_state(double* q, double* u) = 0;
+  virtual void step(const void* torque, int on_device, int dtype, double h, const double* g) = 0;
+  virtual void results(int* nc, int* ab, double* fres, nsd_iter_stats* its) = 0;
+  virtual void contacts(int env, nsd_contact* out, int* n) = 0;
+  virtual void device_state(void** q, void** u, int* dtype) = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  int info[6] = {0, 0, 0, 0, 0, 0};
+};
+
+template <class R> struct Batch final : BatchBase {
+  HostTopo H;
+  DevTopo<R> topo;
+  nsd_config cfg;
+  int n_env, maxc, ns, npairs;
+  WorkPlan plan;
+  DBuf rarena, iarena, shapes, pairs, cand, paircnt, ncout, ovf, fin, iters, qs, us, torque;
+  HBuf stage;
+  double margin, mu_default;
+  int team_threads = 32;  // 32: warp per env; >32: CTA per env
+  std::vector<nsd::ShapeD<R>> hshapes;
+
+  Batch(const nsd_topology& tp, int n_shapes, const nsd_shape* sh, double mg, double mud, const nsd_config& c,
+        int nenv, int mc, int device)
+      : cfg(c), n_env(nenv), maxc(mc), ns(n_shapes), margin(mg), mu_default(mud) {
+    NSD_CK(cudaSetDevice(device));
+    if (nenv < 1 || mc < 1 || n_shapes < 0) throw NsdError(NSD_INVALID, "bad batch sizes");
+    H = preprocess(tp);
+    topo.upload(H);
+    for (int i = 0; i < ns; ++i) {
+      nsd::ShapeD<R> s{};
+      s.body = sh[i].body;
+      s.kind = sh[i].kind;
+      if (s.body >= H.nb || s.body < -1 || s.kind < 0 || s.kind > 2) throw NsdError(NSD_INVALID, "bad shape");
+      for (int k = 0; k < 3; ++k) {
+        s.n[k] = R(sh[i].normal[k]);
+        s.he[k] = R(sh[i].half_extents[k]);
+      }
+      s.offset = R(sh[i].offset);
+      s.radius = R(sh[i].radius);
+      s.thick = R(sh[i].thickness);
+      s.mu = R(sh[i].mu);
+      hshapes.push_back(s);
+    }
+    std::vector<int2> hp;
+    for (int i = 0; i < ns; ++i)
+      for (int j = i + 1; j < ns; ++j) hp.push_back(make_int2(i, j));
+    npairs = static_cast<int>(hp.size());
+    shapes.alloc(sizeof(nsd::ShapeD<R>) * std::max(ns, 1));
+    pairs.alloc(sizeof(int2) * std::max(npairs, 1));
+    if (ns) NSD_CK(cudaMemcpy(shapes.p, hshapes.data(), sizeof(nsd::ShapeD<R>) * ns, cudaMemcpyHostToDevice));
+    if (npairs) NSD_CK(cudaMemcpy(pairs.p, hp.data(), sizeof(int2) * npairs, cudaMemcpyHostToDevice));
+    plan.plan(H, maxc);
+    rarena.alloc(sizeof(R) * plan.strideR * n_env);
+    iarena.alloc(sizeof(int) * plan.strideI * n_env);
+    NSD_CK(cudaMemset(rarena.p, 0, sizeof(R) * plan.strideR * n_env));
+    NSD_CK(cudaMemset(iarena.p, 0, sizeof(int) * plan.strideI * n_env));
+    cand.alloc(sizeof(nsd::CandD<R>) * (size_t)std::max(npairs, 1) * 4 * n_env);
+    paircnt.alloc(sizeof(int) * (size_t)std::max(npairs, 1) * n_env);
+    ncout.alloc(sizeof(int) * n_env);
+    ovf.alloc(sizeof(int) * n_env);
+    fin.alloc(sizeof(double) * 8 * n_env);
+    iters.alloc(sizeof(nsd::IterOut) * (size_t)std::max(cfg.newton_iterations, 1) * n_env);
+    qs.alloc(sizeof(R) * (size_t)H.ncoord * n_env);
+    us.alloc(sizeof(R) * (size_t)H.ndof * n_env);
+    torque.alloc(sizeof(R) * (size_t)std::max(H.nj, 1) * n_env);
+    NSD_CK(cudaMemset(ncout.p, 0, sizeof(int) * n_env));
+    NSD_CK(cudaMemset(ovf.p, 0, sizeof(int) * n_env));
+    NSD_CK(cudaMemset(fin.p, 0, sizeof(double) * 8 * n_env));
+    NSD_CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    const char* env_team = std::getenv("NSD_BATCH_TEAM");
+    if (env_team) team_threads = std::max(32, std::atoi(env_team));
+    info[0] = n_env;
+    info[1] = H.ncoord;
+    info[2] = H.ndof;
+    info[3] = H.nj;
+    info[4] = H.rows_static + 3 * maxc;
+    info[5] = team_threads;
+  }
+  ~Batch() override {
+    if (stream && own_stream) cudaStreamDestroy(stream);
+  }
+  void set_state(const double* q, const double* u) override {
+    const size_t nq = (size_t)H.ncoord * n_env, nu = (size_t)H.ndof * n_env;
+    stage.alloc(sizeof(R) * (nq + nu));
+    R* s = static_cast<R*>(stage.p);
+    for (size_t i = 0; i < nq; ++i) s[i] = R(q[i]);
+    for (size_t i = 0; i < nu; ++i) s[nq + i] = R(u[i]);
+    NSD_CK(cudaMemcpyAsync(qs.p, s, sizeof(R) * nq, cudaMemcpyHostToDevice, stream));
+    NSD_CK(cudaMemcpyAsync(us.p, s + nq, sizeof(R) * nu, cudaMemcpyHostToDevice, stream));
+    NSD_CK(cudaStreamSynchronize(stream));
+  }
+  void get_state(double* q, double* u) override {
+    const size_t nq = (size_t)H.ncoord * n_env, nu = (size_t)H.ndof * n_env;
+    stage.alloc(sizeof(R) * (nq + nu));
+    R* s = static_cast<R*>(stage.p);
+    NSD_CK(cudaMemcpyAsync(s, qs.p, sizeof(R) * nq, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(s + nq, us.p, sizeof(R) * nu, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaStreamSynchronize(stream));
+    if (q)
+      for (size_t i = 0; i < nq; ++i) q[i] = double(s[i]);
+    if (u)
+      for (size_t i = 0; i < nu; ++i) u[i] = double(s[nq + i]);
+  }
+  void device_state(void** q, void** u, int* dtype) override {
+    *q = qs.p;
+    *u = us.p;
+    *dtype = sizeof(R) == 8 ? 1 : 0;
+  }
+  void step(const void* tq, int on_device, int dtype, double h, const double* g) override {
+    if (!(h > 0.0)) throw NsdError(NSD_INVALID, "integrate_coordinates: h must be positive");
+    BatchArgs<R> A{};
+    A.T = topo.t;
+    A.cfg = to_cfg(cfg);
+    A.n_env = n_env;
+    A.ns = ns;
+    A.npairs = npairs;
+    A.maxc = maxc;
+    A.pairs = pairs.as<int2>();
+    A.shapes = shapes.as<nsd::ShapeD<R>>();
+    A.jframe = topo.jframe;
+    A.margin = R(margin);
+    A.mu_default = R(mu_default);
+    A.h = R(h);
+    for (int k = 0; k < 3; ++k) A.grav[k] = R(g[k]);
+    A.qs = qs.as<R>();
+    A.us = us.as<R>();
+    A.torque = nullptr;
+    if (tq) {
+      if (on_device) {
+        A.torque = tq;
+        A.torque_double = dtype;
+      } else {
+        const size_t n = (size_t)H.nj * n_env;
+        stage.alloc(sizeof(double) * n);
+        std::memcpy(stage.p, tq, sizeof(double) * n);
+        torque.alloc(sizeof(double) * n);
+        NSD_CK(cudaMemcpyAsync(torque.p, stage.p, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+        A.torque = torque.p;
+        A.torque_double = 1;
+      }
+    }
+    A.rbase = rarena.as<R>();
+    A.ibase = iarena.as<int>();
+    A.strideR = plan.strideR;
+    A.strideI = plan.strideI;
+    A.plan = plan;
+    A.cand = cand.as<nsd::CandD<R>>();
+    A.pair_cnt = paircnt.as<int>();
+    A.nc_out = ncout.as<int>();
+    A.overflow = ovf.as<int>();
+    A.fin = fin.as<double>();
+    A.iters = iters.as<nsd::IterOut>();
+    if (team_threads == 32) {
+      const int per_block = 4;
+      k_batch_warp<R><<<(n_env + per_block - 1) / per_block, 32 * per_block, 0, stream>>>(A);
+    } else {
+      k_batch_block<R><<<n_env, team_threads, 0, stream>>>(A);
+    }
+    NSD_CK(cudaGetLastError());
+  }
+  void results(int* nc, int* ab, double* fres, nsd_iter_stats* its) override {
+    std::vector<int> hn(n_env), ho(n_env);
+    std::vector<double> hf(8 * (size_t)n_env);
+    NSD_CK(cudaMemcpyAsync(hn.data(), ncout.p, sizeof(int) * n_env, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(ho.data(), ovf.p, sizeof(int) * n_env, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(hf.data(), fin.p, sizeof(double) * 8 * n_env, cudaMemcpyDeviceToHost, stream));
+    std::vector<nsd::IterOut> hi;
+    const int N = cfg.newton_iterations;
+    if (its) {
+      hi.resize((size_t)N * n_env);
+      NSD_CK(cudaMemcpyAsync(hi.data(), iters.p, sizeof(nsd::IterOut) * hi.size(), cudaMemcpyDeviceToHost, stream));
+    }
+    NSD_CK(cudaStreamSynchronize(stream));
+    int overflow_env = -1;
+    for (int e = 0; e < n_env; ++e) {
+      if (nc) nc[e] = hn[e];
+      if (ab) ab[e] = hf[8 * e + 5] != 0.0;
+      if (fres) fres[e] = hf[8 * e];
+      if (ho[e] && overflow_env < 0) overflow_env = e;
+    }
+    if (its)
+      for (size_t i = 0; i < hi.size(); ++i) {
+        its[i].residual_inf = hi[i].residual_inf;
+        its[i].merit_l2 = hi[i].merit_l2;
+        its[i].comp_error_max = hi[i].comp_error_max;
+        its[i].cone_violation_max = hi[i].cone_violation_max;
+        its[i].step_size = hi[i].step_size;
+        its[i].linear_residual = hi[i].linear_residual;
+        its[i].linear_iterations = hi[i].linear_iterations;
+        its[i].linear_breakdown = hi[i].linear_breakdown;
+      }
+    if (overflow_env >= 0)
+      throw NsdError(NSD_INVALID, "env " + std::to_string(overflow_env) + " produced " +
+                                      std::to_string(ho[overflow_env]) + " contacts > max_contacts " +
+                                      std::to_string(maxc));
+  }
+  void contacts(int env, nsd_contact* out, int* n) override {
+    if (env < 0 || env >= n_env) throw NsdError(NSD_INVALID, "env out of range");
+    int nc = 0;
+    NSD_CK(cudaMemcpyAsync(&nc, ncout.as<int>() + env, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaStreamSynchronize(stream));
+    *n = nc;
+    if (!out || nc == 0) return;
+    std::vector<int> cb(2 * nc), cf(nc);
+    std::vector<R> cg(17 * (size_t)nc), lam(H.rows_static + 3 * (size_t)nc);
+    const R* rb = rarena.as<R>() + (size_t)env * plan.strideR;
+    const int* ib = iarena.as<int>() + (size_t)env * plan.strideI;
+    NSD_CK(cudaMemcpyAsync(cb.data(), ib + plan.cbody, sizeof(int) * 2 * nc, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(cf.data(), ib + plan.cfeat, sizeof(int) * nc, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(cg.data(), rb + plan.cgeo, sizeof(R) * 17 * nc, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(lam.data(), rb + plan.lam, sizeof(R) * lam.size(), cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaStreamSynchronize(stream));
+    for (int c = 0; c < nc; ++c) {
+      nsd_contact& k = out[c];
+      std::memset(&k, 0, sizeof(k));
+      k.body_a = cb[2 * c];
+      k.body_b = cb[2 * c + 1];
+      k.feature = cf[c];
+      for (int i = 0; i < 3; ++i) {
+        k.local_a[i] = cg[17 * c + i];
+        k.local_b[i] = cg[17 * c + 3 + i];
+        k.normal[i] = cg[17 * c + 6 + i];
+        k.d1[i] = cg[17 * c + 9 + i];
+        k.d2[i] = cg[17 * c + 12 + i];
+      }
+      k.thickness = cg[17 * c + 15];
+      k.mu = cg[17 * c + 16];
+      k.lambda_n = lam[H.rows_static + c];
+      k.lambda_f[0] = lam[H.rows_static + nc + 2 * c];
+      k.lambda_f[1] = lam[H.rows_static + nc + 2 * c + 1];
+    }
+  }
+};
+
+// ================================================================== C ABI
+struct nsd_solver {
+  std::unique_ptr<SolverBase> impl;
+};
+struct nsd_batch {
+  std::unique_ptr<BatchBase> impl;
+};
+
+extern "C" {
+
+const char* nsd_last_error(void) { return g_err.c_str(); }
+
+void nsd_config_default(nsd_config* c, int32_t precision) {
+  c->newton_iterations = 8;
+  c->step_fraction = 0.75;
+  c->epsilon_reg = 1e-6;
+  c->geometric_stiffness = 1;
+  c->r_strategy = 2;
+  c->ncp_kind = 1;
+  c->linear_method = 3;
+  c->linear_max_iterations = 40;
+  c->linear_tolerance = 1e-10;
+  c->preconditioner = 1;
+  c->newton_tolerance = 1e-6;
+  c->line_search = 0;
+  c->precision = precision;
+}
+
+int32_t nsd_count_rows(const nsd_topology* topo, int32_t n_contacts) {
+  if (!topo) return -1;
+  int n = 0;
+  for (int j = 0; j < topo->n_joints; ++j) n += nsd::joint_nrows(topo->joint_kind[j]);
+  return n + 3 * topo->n_tets + 3 * n_contacts;
+}
+
+int nsd_create(const nsd_topology* topo, const nsd_config* cfg, int32_t device, nsd_solver** out) {
+  return guarded([&] {
+    if (!topo || !cfg || !out) throw NsdError(NSD_INVALID, "null argument");
+    check_cfg(*cfg);
+    auto* s = new nsd_solver();
+    try {
+      if (cfg->precision == NSD_FP64)
+        s->impl.reset(new Solver<double>(*topo, *cfg, device));
+      else
+        s->impl.reset(new Solver<float>(*topo, *cfg, device));
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+    return NSD_OK;
+  });
+}
+
+int nsd_set_config(nsd_solver* s, const nsd_config* cfg) {
+  return guarded([&] {
+    if (!s || !cfg) throw NsdError(NSD_INVALID, "null argument");
+    check_cfg(*cfg);
+    s->impl->set_cfg(*cfg);
+    return NSD_OK;
+  });
+}
+
+int nsd_step(nsd_solver* s, const nsd_step_in* in, nsd_step_out* out) {
+  return guarded([&] {
+    if (!s) throw NsdError(NSD_INVALID, "null solver");
+    return s->impl->step(in, out);
+  });
+}
+
+double nsd_last_step_ms(const nsd_solver* s) { return s ? s->impl->last_ms : 0.0; }
+
+int nsd_destroy(nsd_solver* s) {
+  delete s;
+  return NSD_OK;
+}
+
+int nsd_batch_create(const nsd_topology* topo, int32_t n_shapes, const nsd_shape* shapes, double margin,
+                     double mu_default, const nsd_config* cfg, int32_t n_env, int32_t max_contacts, int32_t device,
+                     nsd_batch** out) {
+  return guarded([&] {
+    if (!topo || !cfg || !out || (n_shapes > 0 && !shapes)) throw NsdError(NSD_INVALID, "null argument");
+    check_cfg(*cfg);
+    auto* b = new nsd_batch();
+    try {
+      if (cfg->precision == NSD_FP64)
+        b->impl.reset(new Batch<double>(*topo, n_shapes, shapes, margin, mu_default, *cfg, n_env, max_contacts, device));
+      else
+        b->impl.reset(new Batch<float>(*topo, n_shapes, shapes, margin, mu_default, *cfg, n_env, max_contacts, device));
+    } catch (...) {
+      delete b;
+      throw;
+    }
+    *out = b;
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_set_state(nsd_batch* b, const double* q, const double* u) {
+  return guarded([&] {
+    if (!b || !q || !u) throw NsdError(NSD_INVALID, "null argument");
+    b->impl->set_state(q, u);
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_get_state(nsd_batch* b, double* q, double* u) {
+  return guarded([&] {
+    if (!b) throw NsdError(NSD_INVALID, "null argument");
+    b->impl->get_state(q, u);
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_set_stream(nsd_batch* b, void* stream) {
+  return guarded([&] {
+    if (!b) throw NsdError(NSD_INVALID, "null argument");
+    if (b->impl->own_stream && b->impl->stream) cudaStreamDestroy(b->impl->stream);
+    if (stream) {
+      b->impl->stream = static_cast<cudaStream_t>(stream);
+      b->impl->own_stream = false;
+    } else {
+      NSD_CK(cudaStreamCreateWithFlags(&b->impl->stream, cudaStreamNonBlocking));
+      b->impl->own_stream = true;
+    }
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_step(nsd_batch* b, const double* joint_torque, int32_t torque_on_device, double h,
+                   const double gravity[3]) {
+  return guarded([&] {
+    if (!b || !gravity) throw NsdError(NSD_INVALID, "null argument");
+    b->impl->step(joint_torque, torque_on_device, 1, h, gravity);
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_step_device(nsd_batch* b, const void* joint_torque_dev, int32_t dtype, double h,
+                          const double gravity[3]) {
+  return guarded([&] {
+    if (!b || !gravity) throw NsdError(NSD_INVALID, "null argument");
+    b->impl->step(joint_torque_dev, 1, dtype, h, gravity);
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_sync(nsd_batch* b) {
+  return guarded([&] {
+    if (!b) throw NsdError(NSD_INVALID, "null argument");
+    NSD_CK(cudaStreamSynchronize(b->impl->stream));
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_results(nsd_batch* b, int32_t* n_contacts, int32_t* aborted, double* final_residual_inf,
+                      nsd_iter_stats* iters) {
+  return guarded([&] {
+    if (!b) throw NsdError(NSD_INVALID, "null argument");
+    b->impl->results(n_contacts, aborted, final_residual_inf, iters);
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_contacts(nsd_batch* b, int32_t env, nsd_contact* out, int32_t* n) {
+  return guarded([&] {
+    if (!b || !n) throw NsdError(NSD_INVALID, "null argument");
+    b->impl->contacts(env, out, n);
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_device_state(nsd_batch* b, void** q_dev, void** u_dev, int32_t* dtype) {
+  return guarded([&] {
+    if (!b || !q_dev || !u_dev || !dtype) throw NsdError(NSD_INVALID, "null argument");
+    b->impl->device_state(q_dev, u_dev, dtype);
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_info(const nsd_batch* b, int32_t* info) {
+  if (!b || !info) return NSD_INVALID;
+  for (int i = 0; i < 6; ++i) info[i] = b->impl->info[i];
+  return NSD_OK;
+}
+
+int nsd_batch_destroy(nsd_batch* b) {
+  delete b;
+  return NSD_OK;
+}
+
+}  // extern "C"

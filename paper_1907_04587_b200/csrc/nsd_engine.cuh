@@ -1,0 +1,1194 @@
+// The per-timestep non-smooth Newton solve on the device.
+//
+// One implementation of the reference's newton_step (src/newton.cpp:321-418),
+// written against a Team (nsd_team.cuh) so the same code runs as
+//   * a cooperative persistent grid for one large scene (C2/C4 FEM scenes),
+//   * one CTA for one small scene (C1/C3), and
+//   * one warp or CTA per environment for the batched RL path (C5).
+//
+// Data layout (all int32 ids; R = float or double):
+//   rows      fixed layout of make_layout (newton.cpp:18-41):
+//             [joints 3/5/5/2 | tets 3 each | contact normals | friction pairs]
+//   J         coeff[12*row]: four 3-wide slots; blk[4*row]: the "dof3 block"
+//             (dof/3) each slot acts on, -1 if unused. A rigid body owns two
+//             blocks (linear, angular), a particle one. <=12 nnz per row.
+//   C         cd[row] for scalar rows; ctet[9*tet] for the 3x3 Neo-Hookean block.
+//   H^-1      hinv[dof] for linear blocks (1/(m+shift)), iwi6[6*blk] (I_w^-1,
+//             symmetric) for angular blocks.
+//   J^T pull  deterministic body-side gather over an incidence list per dof3
+//             block (static joints+tets list, per-step contact list) — no
+//             atomics, fixed order, so results are run-to-run bitwise stable
+//             (SPEC.md:710 determinism).
+// The Schur complement S = J H^-1 J^T + C + eps I is never formed (the
+// reference builds it explicitly, newton.cpp:242-290): every PCR iteration
+// applies it matrix-free as one pull pass (w = H^-1 J^T z, dof-parallel) and one
+// gather pass (Az = J w + C z + eps z, row-parallel).
+#pragma once
+
+#include "nsd_math.cuh"
+#include "nsd_team.cuh"
+
+namespace nsd {
+
+using std::isfinite;
+using std::sqrt;
+
+enum BlockKind : int { kParticleLin = 0, kRigidLin = 1, kRigidAng = 2 };
+
+struct Cfg {
+  int newton_iterations;
+  double step_fraction;
+  double epsilon_reg;
+  int geometric_stiffness;
+  int r_strategy;  // 0 identity, 1 h^2, 2 effective mass
+  int ncp_kind;    // 0 min map, 1 FB
+  int linear_max_iterations;
+  double linear_tolerance;
+  int preconditioner;  // 0 none, 1 diagonal
+  double newton_tolerance;
+  int line_search;
+};
+
+// Static topology (shared by every environment of a batch).
+template <class R> struct Topo {
+  int nb, ndof, ncoord, nd3;
+  const int* btype;   // per body: 0 particle, 1 rigid
+  const R* bmass;
+  const R* binertia;  // 9 per body (body frame)
+  const int* bdof;
+  const int* bcoord;
+  const int* d3_body;  // per dof3 block: owning body
+  const int* d3_kind;  // BlockKind
+  int nj;
+  const int* jkind;
+  const int* jbody;  // 2 per joint
+  const R* jparam;   // 2 per joint: compliance, stiffness
+  const int* jrow;   // first row of each joint
+  int rows_joint;
+  int nt;
+  const int* tbody;   // 4 per tet (global body ids)
+  const R* tdminv;    // 9 per tet
+  const R* tvol;
+  const R* tmat;      // 4 per tet: c1, d1, alpha, diagonal flag
+  int rows_static;    // rows_joint + 3 nt
+  const int* sinc_off;  // static incidence per dof3 block (nd3 + 1)
+  const int* sinc_ent;  // row*4 + slot, ascending rows within a block
+};
+
+// Per-scene (per-env) mutable state and scratch. All pointers are either
+// global memory (grid/batched-global) or shared memory (batched-smem).
+template <class R> struct Work {
+  // state
+  R* q;         // ncoord, current iterate (in/out)
+  R* u;         // ndof, current iterate (in/out)
+  const R* q0;  // step-start coordinates q-
+  const R* u0;  // step-start velocities u-
+  const R* jframe;   // 21 per joint
+  const R* f_extra;  // ndof or nullptr
+  R h;
+  R grav[3];
+  // contacts (SoA)
+  int nc;
+  const int* cbody;  // 2 per contact
+  const R* cgeo;     // 17 per contact: la3 lb3 n3 d1_3 d2_3 thickness mu
+  const int* cinc_off;  // contact incidence per dof3 block (nd3 + 1)
+  const int* cinc_ent;  // contact*4 + slot
+  // rows
+  int nrows, normal_begin, friction_begin;
+  R* coeff;  // 12 per row
+  int* blk;  // 4 per row
+  R* hv;
+  R* cd;
+  R* ctet;   // 9 per tet
+  R* lam;
+  // PCR vectors
+  R *x, *xn, *r, *rn, *z, *zn, *p, *ap, *az, *inv, *bx, *qp;
+  // dof vectors
+  R *ut, *g, *gp, *up, *shift, *hinv, *w, *du, *ub;
+  // dof3 block data
+  R* iw6;   // 6 per block (sym: xx yy zz xy xz yz), angular blocks
+  R* iwi6;  // inverse
+};
+
+struct IterOut {
+  double residual_inf, merit_l2, comp_error_max, cone_violation_max, step_size, linear_residual;
+  int linear_iterations, linear_breakdown;
+};
+
+struct StepOut {
+  IterOut* iters;     // newton_iterations (may be null)
+  double* hist;       // newton_iterations * (max_lin + 1) (may be null)
+  int* hist_len;      // newton_iterations (may be null)
+  double* tel;        // 6 per contact (may be null)
+  double* fin;        // 8: final_residual_inf, final_comp, final_cone, min_gap, min_diag_shift, aborted, converged, n_iterations
+  double* lam_out;    // rows (may be null) -- unused: lam stays in Work
+};
+
+// ------------------------------------------------------------------ helpers
+template <class R> __device__ __forceinline__ V3<R> ld3(const R* p) { return v3(p[0], p[1], p[2]); }
+template <class R> __device__ __forceinline__ void st3(R* p, V3<R> v) {
+  p[0] = v.x;
+  p[1] = v.y;
+  p[2] = v.z;
+}
+template <class R> __device__ __forceinline__ V3<R> sym_mul(const R* s6, V3<R> v) {
+  // s6 = xx yy zz xy xz yz
+  return v3(s6[0] * v.x + s6[3] * v.y + s6[4] * v.z, s6[3] * v.x + s6[1] * v.y + s6[5] * v.z,
+            s6[4] * v.x + s6[5] * v.y + s6[2] * v.z);
+}
+template <class R> __device__ __forceinline__ R sym_quad(const R* s6, V3<R> v) { return dot(v, sym_mul(s6, v)); }
+
+// Rotation of a body from its quaternion (identity for particles / world).
+template <class R> __device__ __forceinline__ M3<R> body_rot(const Topo<R>& T, const R* q, int b) {
+  if (b < 0 || T.btype[b] == 0) return m3_identity<R>();
+  const R* t = q + T.bcoord[b] + 3;
+  return quat_rot(t[0], t[1], t[2], t[3]);
+}
+template <class R> __device__ __forceinline__ V3<R> body_pos(const Topo<R>& T, const R* q, int b) {
+  return ld3(q + T.bcoord[b]);
+}
+
+// Slot blocks of a body (linear, angular) as dof3 indices.
+template <class R> __device__ __forceinline__ void body_blocks(const Topo<R>& T, int b, int& lin, int& ang) {
+  if (b < 0) {
+    lin = ang = -1;
+    return;
+  }
+  lin = T.bdof[b] / 3;
+  ang = T.btype[b] == 1 ? lin + 1 : -1;
+}
+
+// J_i M^-1 J_i^T over the row's slots; hinv_lin == nullptr -> unshifted (1/m).
+template <class R>
+__device__ __forceinline__ R row_inv_quad(const Topo<R>& T, const Work<R>& W, const R* c12, const int* b4,
+                                          bool shifted) {
+  R s = R(0);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int b = b4[k];
+    if (b < 0) continue;
+    const V3<R> c = v3(c12[3 * k], c12[3 * k + 1], c12[3 * k + 2]);
+    if (T.d3_kind[b] == kRigidAng) {
+      s += sym_quad(W.iwi6 + 6 * b, c);
+    } else if (shifted) {
+      const R* hi = W.hinv + 3 * b;
+      s += c.x * c.x * hi[0] + c.y * c.y * hi[1] + c.z * c.z * hi[2];
+    } else {
+      const R m = T.bmass[T.d3_body[b]];
+      s += c.x * c.x / m + c.y * c.y / m + c.z * c.z / m;
+    }
+  }
+  return s;
+}
+
+// J_i . v over the row's slots (v: a dof vector).
+template <class R> __device__ __forceinline__ R row_dot(const R* c12, const int* b4, const R* v) {
+  R s = R(0);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int b = b4[k];
+    if (b < 0) continue;
+    const R* vb = v + 3 * b;
+    s += c12[3 * k] * vb[0] + c12[3 * k + 1] * vb[1] + c12[3 * k + 2] * vb[2];
+  }
+  return s;
+}
+
+template <class R> __device__ __forceinline__ R r_factor(R emd, R h, bool position, int strat) {
+  const R ts = position ? h * h : h;
+  if (strat == 0) return R(1);
+  if (strat == 1) return ts;
+  return emd <= R(0) ? ts : ts * emd;
+}
+
+template <class R> struct PhiV {
+  R v, dc, dl;
+};
+template <class R> __device__ __forceinline__ PhiV<R> phi_n(R c, R lam, R r, int kind) {  // ncp.cpp:7-32
+  PhiV<R> o;
+  const R rl = r * lam;
+  if (kind == 0) {
+    if (c <= rl) {
+      o.v = c;
+      o.dc = R(1);
+      o.dl = R(0);
+    } else {
+      o.v = rl;
+      o.dc = R(0);
+      o.dl = r;
+    }
+    return o;
+  }
+  const R root = sqrt(c * c + rl * rl);
+  o.v = c + rl - root;
+  if (root == R(0)) {
+    o.dc = R(0);
+    o.dl = r;
+  } else {
+    o.dc = R(1) - c / root;
+    o.dl = (R(1) - rl / root) * r;
+  }
+  return o;
+}
+template <class R> __device__ __forceinline__ R friction_W(R vt, R lf, R mln, R r, int kind) {  // ncp.cpp:34-49
+  const R degenerate = R(1e-12), cap = R(1e12);
+  if (kind == 0) {
+    if (vt <= r * (mln - lf)) return R(0);
+    if (mln <= degenerate) return cap;
+    return (vt - r * (mln - lf)) / mln;
+  }
+  const R slack = mln - lf;
+  const R root = sqrt(vt * vt + r * r * slack * slack);
+  const R numer = root - r * slack;
+  const R denom = vt + r * mln - root;
+  if (denom <= degenerate) return cap;
+  return r * numer / denom;
+}
+
+// Structural slot usage of joint rows (joint_rows, constraints.cpp:141-220):
+// point/translation rows use all four slots, axis-dot rows the angular ones.
+__host__ __device__ __forceinline__ int joint_nrows(int kind) { return kind == 3 ? 2 : (kind == 0 ? 3 : 5); }
+__host__ __device__ __forceinline__ bool joint_row_linear(int kind, int k) {
+  if (kind == 0) return true;
+  if (kind == 1) return k < 3;
+  if (kind == 2) return k < 2;
+  return false;
+}
+
+// ------------------------------------------------------------------ row blocks (static per step)
+template <class R, class Team> __device__ void setup_row_blocks(Team& t, const Topo<R>& T, Work<R>& W) {
+  const int ng = T.nj + T.nt + W.nc;
+  for (int g = t.rank(); g < ng; g += t.size()) {
+    if (g < T.nj) {
+      const int kind = T.jkind[g], r0 = T.jrow[g];
+      int al, aa, bl, ba;
+      body_blocks(T, T.jbody[2 * g], al, aa);
+      body_blocks(T, T.jbody[2 * g + 1], bl, ba);
+      const int nr = joint_nrows(kind);
+      for (int k = 0; k < nr; ++k) {
+        int* b = W.blk + 4 * (r0 + k);
+        const bool lin = joint_row_linear(kind, k);
+        b[0] = lin ? al : -1;
+        b[1] = aa;
+        b[2] = lin ? bl : -1;
+        b[3] = ba;
+        if (b[2] >= 0 && b[2] == b[0]) b[2] = -1;  // same body on both sides: slots merge
+        if (b[3] >= 0 && b[3] == b[1]) b[3] = -1;
+      }
+    } else if (g < T.nj + T.nt) {
+      const int e = g - T.nj;
+      const int r0 = T.rows_joint + 3 * e;
+      int vb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) vb[k] = T.bdof[T.tbody[4 * e + k]] / 3;
+      for (int i = 0; i < 3; ++i) {
+        int* b = W.blk + 4 * (r0 + i);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) b[k] = vb[k];
+      }
+    } else {
+      const int c = g - T.nj - T.nt;
+      int al, aa, bl, ba;
+      body_blocks(T, W.cbody[2 * c], al, aa);
+      body_blocks(T, W.cbody[2 * c + 1], bl, ba);
+      const int rows[3] = {W.normal_begin + c, W.friction_begin + 2 * c, W.friction_begin + 2 * c + 1};
+      for (int i = 0; i < 3; ++i) {
+        int* b = W.blk + 4 * rows[i];
+        b[0] = al;
+        b[1] = aa;
+        b[2] = (bl >= 0 && bl == al) ? -1 : bl;
+        b[3] = (ba >= 0 && ba == aa) ? -1 : ba;
+      }
+    }
+  }
+}
+
+// Sums a coefficient contribution into the slot owning `blk` (handles the
+// merged same-body case) — used by joint/contact assembly.
+template <class R> __device__ __forceinline__ void slot_add(R* c12, const int* b4, int s, int blk, V3<R> v) {
+  int k = s;
+  if (blk < 0) return;
+  if (b4[s] != blk) k = (s == 2 ? 0 : 1);  // merged into the body-a slot
+  c12[3 * k] += v.x;
+  c12[3 * k + 1] += v.y;
+  c12[3 * k + 2] += v.z;
+}
+
+// ------------------------------------------------------------------ assembly (newton.cpp:100-231)
+struct AsmStats {
+  double hmax, hsq, comp, cone;
+};
+
+template <class R>
+__device__ void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, R h, AsmStats& st) {
+  const int kind = T.jkind[j], ba = T.jbody[2 * j], bb = T.jbody[2 * j + 1];
+  const R* fr = W.jframe + 21 * j;
+  const V3<R> anc_a = ld3(fr), anc_b = ld3(fr + 3), ax_a = ld3(fr + 6), ax_a2 = ld3(fr + 9), ax_b1 = ld3(fr + 12),
+              ax_b2 = ld3(fr + 15), rest = ld3(fr + 18);
+  const M3<R> Ra = body_rot(T, q, ba), Rb = body_rot(T, q, bb);
+  const bool rig_a = ba >= 0 && T.btype[ba] == 1, rig_b = bb >= 0 && T.btype[bb] == 1;
+  // world attach points and lever arms (attach_world_point / add_point_jacobian)
+  V3<R> wa, wb, ra = v3(R(0), R(0), R(0)), rb = ra;
+  if (ba < 0) wa = anc_a;
+  else if (!rig_a) wa = body_pos(T, q, ba);
+  else {
+    ra = mul(Ra, anc_a);
+    wa = body_pos(T, q, ba) + ra;
+  }
+  if (bb < 0) wb = anc_b;
+  else if (!rig_b) wb = body_pos(T, q, bb);
+  else {
+    rb = mul(Rb, anc_b);
+    wb = body_pos(T, q, bb) + rb;
+  }
+  const R comp = T.jparam[2 * j];
+  const R e_bend = T.jparam[2 * j + 1] > R(0) ? R(1) / T.jparam[2 * j + 1] : R(0);
+  const int r0 = T.jrow[j];
+  const V3<R> axw = ba < 0 ? ax_a : mul(Ra, ax_a);
+  int al, aa, bl, bA;
+  body_blocks(T, ba, al, aa);
+  body_blocks(T, bb, bl, bA);
+
+  auto emit = [&](int k, R value, R e) {
+    const int row = r0 + k;
+    const R lam = W.lam[row] / h;
+    const R hv = (value + e * lam) / h;
+    W.hv[row] = hv;
+    W.cd[row] = e / (h * h);
+    st.hmax = fmax(st.hmax, (double)ab(hv));
+    st.hsq += (double)hv * (double)hv;
+  };
+  auto point_row = [&](int k, V3<R> d, R value, bool prism) {
+    R* c = W.coeff + 12 * (r0 + k);
+    const int* b = W.blk + 4 * (r0 + k);
+#pragma unroll
+    for (int i = 0; i < 12; ++i) c[i] = R(0);
+    slot_add(c, b, 0, al, d);
+    if (rig_a) slot_add(c, b, 1, aa, cross(ra, d));
+    slot_add(c, b, 2, bl, -d);
+    if (rig_b) slot_add(c, b, 3, bA, -cross(rb, d));
+    if (prism && rig_a) slot_add(c, b, 1, aa, cross(d, wa - wb));
+    emit(k, value, comp);
+  };
+  auto axis_row = [&](int k, V3<R> xa, V3<R> xb, R restv, R e) {
+    R* c = W.coeff + 12 * (r0 + k);
+    const int* b = W.blk + 4 * (r0 + k);
+#pragma unroll
+    for (int i = 0; i < 12; ++i) c[i] = R(0);
+    const V3<R> cr = cross(xa, xb);
+    if (rig_a) slot_add(c, b, 1, aa, cr);
+    if (rig_b) slot_add(c, b, 3, bA, -cr);
+    emit(k, dot(xa, xb) - restv, e);
+  };
+  const V3<R> e0 = v3(R(1), R(0), R(0)), e1 = v3(R(0), R(1), R(0)), e2 = v3(R(0), R(0), R(1));
+  if (kind == 0 || kind == 1) {
+    point_row(0, e0, wa.x - wb.x, false);
+    point_row(1, e1, wa.y - wb.y, false);
+    point_row(2, e2, wa.z - wb.z, false);
+    if (kind == 1) {
+      const V3<R> b1 = bb < 0 ? ax_b1 : mul(Rb, ax_b1), b2 = bb < 0 ? ax_b2 : mul(Rb, ax_b2);
+      axis_row(3, axw, b1, rest.x, comp);
+      axis_row(4, axw, b2, rest.y, comp);
+    }
+  } else if (kind == 2) {
+    // tangent_basis(ax) (constraints.cpp:93-101)
+    int sm = 0;
+    if (ab(axw.y) < ab(axw.x)) sm = 1;
+    if (ab(axw.z) < ab(axw[sm])) sm = 2;
+    V3<R> ee = v3(R(0), R(0), R(0));
+    ee[sm] = R(1);
+    const V3<R> t1 = normalize(ee - dot(ee, axw) * axw);
+    const V3<R> t2 = cross(axw, t1);
+    const V3<R> d = wa - wb;
+    point_row(0, t1, dot(t1, d), true);
+    point_row(1, t2, dot(t2, d), true);
+    const V3<R> a2 = ba < 0 ? ax_a2 : mul(Ra, ax_a2);
+    const V3<R> b1 = bb < 0 ? ax_b1 : mul(Rb, ax_b1), b2 = bb < 0 ? ax_b2 : mul(Rb, ax_b2);
+    axis_row(2, axw, b1, rest.x, comp);
+    axis_row(3, axw, b2, rest.y, comp);
+    axis_row(4, a2, b2, rest.z, comp);
+  } else {
+    const V3<R> b1 = bb < 0 ? ax_b1 : mul(Rb, ax_b1), b2 = bb < 0 ? ax_b2 : mul(Rb, ax_b2);
+    axis_row(0, axw, b1, rest.x, e_bend);
+    axis_row(1, axw, b2, rest.y, e_bend);
+  }
+}
+
+// Neo-Hookean element rows (materials.cpp:180-193, 57-114).
+template <class R>
+__device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R h, AsmStats& st) {
+  const int* tb = T.tbody + 4 * e;
+  V3<R> p[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) p[k] = body_pos(T, q, tb[k]);
+  M3<R> dm;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) dm.a[i] = T.tdminv[9 * e + i];
+  M3<R> ds;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const V3<R> d = p[k + 1] - p[0];
+    ds(0, k) = d.x;
+    ds(1, k) = d.y;
+    ds(2, k) = d.z;
+  }
+  const M3<R> F = mul(ds, dm);
+  const Svd<R> sv = svd3_signed(F);
+  const R vol = T.tvol[e];
+  const R c1 = T.tmat[4 * e], d1 = T.tmat[4 * e + 1], alpha = T.tmat[4 * e + 2];
+  const bool diag_only = T.tmat[4 * e + 3] != R(0);
+  const V3<R> s = sv.S;
+  // gradient c = V_e * dPsi/ds with (J - alpha) (materials.cpp:57-61)
+  const R J = s.x * s.y * s.z;
+  const V3<R> dj = v3(s.y * s.z, s.x * s.z, s.x * s.y);
+  const R kk = R(2) * d1 * (J - alpha);
+  const R tc1 = R(2) * c1;
+  const V3<R> cg = v3(vol * (tc1 * s.x + kk * dj.x), vol * (tc1 * s.y + kk * dj.y), vol * (tc1 * s.z + kk * dj.z));
+  // Hessian (materials.cpp:63-74)
+  const R k0 = R(2) * J - alpha;
+  const R k1 = d1 * s.z * k0, k2 = d1 * s.y * k0, k3 = d1 * s.x * k0;
+  M3<R> H;
+  H(0, 0) = R(2) * (d1 * s.y * s.y * s.z * s.z + c1);
+  H(1, 1) = R(2) * (d1 * s.x * s.x * s.z * s.z + c1);
+  H(2, 2) = R(2) * (d1 * s.x * s.x * s.y * s.y + c1);
+  H(0, 1) = H(1, 0) = R(2) * k1;
+  H(0, 2) = H(2, 0) = R(2) * k2;
+  H(1, 2) = H(2, 1) = R(2) * k3;
+  // compliance_block (materials.cpp:82-102): PSD check with the restated eigensolver
+  {
+    V3<R> ev;
+    M3<R> dummy;
+    sym_eig3<R, false>(H, ev, dummy);
+    if (mn(ev.x, mn(ev.y, ev.z)) <= R(0)) H = project_psd3(H);
+  }
+  M3<R> N;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) N.a[i] = vol * H.a[i];
+  M3<R> E;
+  bool use_diag = diag_only;
+  if (!use_diag) {
+    const R det = det3(N);
+    if (!isfinite(det) || fabs((double)det) < 1e-300) use_diag = true;
+  }
+  if (use_diag) {
+    E = m3_zero<R>();
+    E(0, 0) = N(0, 0) > R(0) ? R(1) / N(0, 0) : R(0);
+    E(1, 1) = N(1, 1) > R(0) ? R(1) / N(1, 1) : R(0);
+    E(2, 2) = N(2, 2) > R(0) ? R(1) / N(2, 2) : R(0);
+  } else {
+    E = inverse3(N);
+  }
+  // rows: h = E (c + lambda/h) / h, C = E / h^2, J = ds/dq (materials.cpp:104-114)
+  const int r0 = T.rows_joint + 3 * e;
+  const R l0 = W.lam[r0] / h, l1 = W.lam[r0 + 1] / h, l2 = W.lam[r0 + 2] / h;
+  const V3<R> cl = v3(cg.x + l0, cg.y + l1, cg.z + l2);
+  const R ih2 = R(1) / (h * h);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const R hv = (E(i, 0) * cl.x + E(i, 1) * cl.y + E(i, 2) * cl.z) / h;
+    W.hv[r0 + i] = hv;
+    st.hmax = fmax(st.hmax, (double)ab(hv));
+    st.hsq += (double)hv * (double)hv;
+    const V3<R> ui = col(sv.U, i);
+    const V3<R> wi = mul(dm, col(sv.V, i));
+    R* c = W.coeff + 12 * (r0 + i);
+    const R w0 = -(wi.x + wi.y + wi.z);
+    st3(c, w0 * ui);
+    st3(c + 3, wi.x * ui);
+    st3(c + 6, wi.y * ui);
+    st3(c + 9, wi.z * ui);
+  }
+#pragma unroll
+  for (int i = 0; i < 9; ++i) W.ctet[9 * e + i] = E.a[i] / (h * h);
+  (void)ih2;
+}
+
+// Contact rows (newton.cpp:166-218; constraints.cpp:67-91).
+template <class R>
+__device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const R* u, int c, R h, const Cfg& cfg,
+                                 AsmStats& st) {
+  const int ba = W.cbody[2 * c], bb = W.cbody[2 * c + 1];
+  const R* g = W.cgeo + 17 * c;
+  const V3<R> la = ld3(g), lb = ld3(g + 3), n = ld3(g + 6), d1 = ld3(g + 9), d2 = ld3(g + 12);
+  const R thick = g[15], mu = g[16];
+  const bool rig_a = ba >= 0 && T.btype[ba] == 1, rig_b = bb >= 0 && T.btype[bb] == 1;
+  V3<R> pa, pb, ra = v3(R(0), R(0), R(0)), rb = ra;
+  if (ba < 0) pa = la;
+  else if (!rig_a) pa = body_pos(T, q, ba);
+  else {
+    ra = mul(body_rot(T, q, ba), la);
+    pa = body_pos(T, q, ba) + ra;
+  }
+  if (bb < 0) pb = lb;
+  else if (!rig_b) pb = body_pos(T, q, bb);
+  else {
+    rb = mul(body_rot(T, q, bb), lb);
+    pb = body_pos(T, q, bb) + rb;
+  }
+  int al, aa, bl, bA;
+  body_blocks(T, ba, al, aa);
+  body_blocks(T, bb, bl, bA);
+  const int nr = W.normal_begin + c, f0 = W.friction_begin + 2 * c;
+  const int* blk = W.blk + 4 * nr;  // identical slot blocks for the 3 rows
+  auto fill = [&](R* cc, V3<R> d) {
+#pragma unroll
+    for (int i = 0; i < 12; ++i) cc[i] = R(0);
+    slot_add(cc, blk, 0, al, d);
+    if (rig_a) slot_add(cc, blk, 1, aa, cross(ra, d));
+    slot_add(cc, blk, 2, bl, -d);
+    if (rig_b) slot_add(cc, blk, 3, bA, -cross(rb, d));
+  };
+  R cn[12];
+  fill(cn, n);
+  const R gap = dot(n, pa - pb) - thick;
+  const R lam_n = W.lam[nr] / h;
+  const R rn = r_factor(row_inv_quad(T, W, cn, blk, false), h, true, cfg.r_strategy);
+  const PhiV<R> phi = phi_n(gap, lam_n, rn, cfg.ncp_kind);
+  const R hn = phi.v / h;
+  W.hv[nr] = hn;
+  W.cd[nr] = phi.dl / (h * h);
+  {
+    R* c12 = W.coeff + 12 * nr;
+    if (phi.dc != R(0)) {
+#pragma unroll
+      for (int i = 0; i < 12; ++i) c12[i] = cn[i] * phi.dc;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 12; ++i) c12[i] = R(0);
+    }
+  }
+  st.comp = fmax(st.comp, (double)ab(mn(gap, lam_n)));
+  const R lf0 = W.lam[f0] / h, lf1 = W.lam[f0 + 1] / h;
+  const R mu_ln = mu * lam_n;
+  const R lfn = sqrt(lf0 * lf0 + lf1 * lf1);
+  st.cone = fmax(st.cone, (double)mx(R(0), lfn - mu_ln));
+  R* c1 = W.coeff + 12 * f0;
+  R* c2 = W.coeff + 12 * (f0 + 1);
+  R h1, h2;
+  if (mu_ln > R(0)) {
+    fill(c1, d1);
+    fill(c2, d2);
+    const R v0 = row_dot(c1, blk, u), v1 = row_dot(c2, blk, u);
+    const R df = R(0.5) * (row_inv_quad(T, W, c1, blk, false) + row_inv_quad(T, W, c2, blk, false));
+    const R rf = r_factor(df, h, false, cfg.r_strategy);
+    const R wv = friction_W(sqrt(v0 * v0 + v1 * v1), lfn, mu_ln, rf, cfg.ncp_kind);
+    h1 = v0 + wv * lf0;
+    h2 = v1 + wv * lf1;
+    W.cd[f0] = W.cd[f0 + 1] = wv / h;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 12; ++i) c1[i] = c2[i] = R(0);
+    h1 = lf0;
+    h2 = lf1;
+    W.cd[f0] = W.cd[f0 + 1] = R(1) / h;
+  }
+  W.hv[f0] = h1;
+  W.hv[f0 + 1] = h2;
+  st.hmax = fmax(st.hmax, fmax((double)ab(hn), fmax((double)ab(h1), (double)ab(h2))));
+  st.hsq += (double)hn * hn + (double)h1 * h1 + (double)h2 * h2;
+}
+
+template <class R, class Team>
+__device__ void assemble(Team& t, const Topo<R>& T, Work<R>& W, const R* q, const R* u, const Cfg& cfg, AsmStats& st) {
+  const int ng = T.nj + T.nt + W.nc;
+  for (int g = t.rank(); g < ng; g += t.size()) {
+    if (g < T.nj)
+      assemble_joint(T, W, q, g, W.h, st);
+    else if (g < T.nj + T.nt)
+      assemble_tet(T, W, q, g - T.nj, W.h, st);
+    else
+      assemble_contact(T, W, q, u, g - T.nj - T.nt, W.h, cfg, st);
+  }
+}
+
+// ------------------------------------------------------------------ J^T pull for one dof3 block
+template <class R>
+__device__ __forceinline__ V3<R> pull(const Topo<R>& T, const Work<R>& W, int b, const R* y) {
+  R sx = R(0), sy = R(0), sz = R(0);
+  const int s0 = T.sinc_off[b], s1 = T.sinc_off[b + 1];
+  for (int e = s0; e < s1; ++e) {
+    const int ent = T.sinc_ent[e];
+    const int row = ent >> 2, slot = ent & 3;
+    const R yr = y[row];
+    const R* c = W.coeff + 12 * row + 3 * slot;
+    sx += c[0] * yr;
+    sy += c[1] * yr;
+    sz += c[2] * yr;
+  }
+  if (W.nc > 0) {
+    const int c0 = W.cinc_off[b], c1 = W.cinc_off[b + 1];
+    // ascending row order: all normal rows first, then the friction pairs
+    for (int e = c0; e < c1; ++e) {
+      const int ent = W.cinc_ent[e];
+      const int row = W.normal_begin + (ent >> 2), slot = ent & 3;
+      const R yr = y[row];
+      const R* c = W.coeff + 12 * row + 3 * slot;
+      sx += c[0] * yr;
+      sy += c[1] * yr;
+      sz += c[2] * yr;
+    }
+    for (int e = c0; e < c1; ++e) {
+      const int ent = W.cinc_ent[e];
+      const int row = W.friction_begin + 2 * (ent >> 2), slot = ent & 3;
+      const R y0 = y[row], y1 = y[row + 1];
+      const R* c = W.coeff + 12 * row + 3 * slot;
+      sx += c[0] * y0;
+      sy += c[1] * y0;
+      sz += c[2] * y0;
+      sx += c[12] * y1;
+      sy += c[13] * y1;
+      sz += c[14] * y1;
+    }
+  }
+  return v3(sx, sy, sz);
+}
+
+// H^-1 v on one block.
+template <class R>
+__device__ __forceinline__ V3<R> hinv_apply(const Topo<R>& T, const Work<R>& W, int b, V3<R> v) {
+  if (T.d3_kind[b] == kRigidAng) return sym_mul(W.iwi6 + 6 * b, v);
+  const R* hi = W.hinv + 3 * b;
+  return v3(v.x * hi[0], v.y * hi[1], v.z * hi[2]);
+}
+
+// Operator pass 1: w = H^-1 J^T y (dof-parallel).
+template <class R, class Team> __device__ void op_pull(Team& t, const Topo<R>& T, Work<R>& W, const R* y) {
+  for (int b = t.rank(); b < T.nd3; b += t.size()) st3(W.w + 3 * b, hinv_apply(T, W, b, pull(T, W, b, y)));
+}
+
+// Operator pass 2 for row i: (J w + C z + eps z)_i.
+template <class R>
+__device__ __forceinline__ R op_row(const Topo<R>& T, const Work<R>& W, int i, const R* z, R eps) {
+  R s = row_dot(W.coeff + 12 * i, W.blk + 4 * i, W.w);
+  if (i >= T.rows_joint && i < T.rows_static) {
+    const int e = (i - T.rows_joint) / 3, k = (i - T.rows_joint) - 3 * e;
+    const R* cb = W.ctet + 9 * e + 3 * k;
+    const int r0 = T.rows_joint + 3 * e;
+    s += cb[0] * z[r0] + cb[1] * z[r0 + 1] + cb[2] * z[r0 + 2];
+  } else {
+    s += W.cd[i] * z[i];
+  }
+  return s + eps * z[i];
+}
+
+// Diagonal of the Schur complement for row i (matrix-free diagonal_preconditioner).
+template <class R> __device__ __forceinline__ R schur_diag(const Topo<R>& T, const Work<R>& W, int i, R eps) {
+  R s = row_inv_quad(T, W, W.coeff + 12 * i, W.blk + 4 * i, true);
+  if (i >= T.rows_joint && i < T.rows_static) {
+    const int e = (i - T.rows_joint) / 3, k = (i - T.rows_joint) - 3 * e;
+    s += W.ctet[9 * e + 4 * k];
+  } else {
+    s += W.cd[i];
+  }
+  return s + eps;
+}
+
+// ------------------------------------------------------------------ Newton step
+// Step setup (newton.cpp:327-338): q = q-, M~ at q- (world inertia and its
+// inverse per rigid body), f_ext = gravity + gyroscopic (+ extension force),
+// u~ = u- + h M~^-1 f_ext, zero starting iterate. Needs a team barrier after.
+template <class R, class Team> __device__ void newton_setup(Team& t, const Topo<R>& T, Work<R>& W) {
+  const R h = W.h;
+  for (int b = t.rank(); b < T.nb; b += t.size()) {
+    const int d = T.bdof[b], cd = T.bcoord[b];
+    const R m = T.bmass[b];
+    V3<R> f = v3(m * W.grav[0], m * W.grav[1], m * W.grav[2]);
+    for (int k = 0; k < (T.btype[b] ? 7 : 3); ++k) W.q[cd + k] = W.q0[cd + k];
+    if (W.f_extra) f = f + ld3(W.f_extra + d);
+    st3(W.ut + d, ld3(W.u0 + d) + h * (f / m));
+    if (T.btype[b] == 1) {
+      const M3<R> Rm = quat_rot(W.q0[cd + 3], W.q0[cd + 4], W.q0[cd + 5], W.q0[cd + 6]);
+      M3<R> I;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) I.a[i] = T.binertia[9 * b + i];
+      const M3<R> Iw = mul(mul(Rm, I), transpose(Rm));
+      const M3<R> Ii = inverse3(Iw);
+      const int ab3 = d / 3 + 1;
+      R* s6 = W.iw6 + 6 * ab3;
+      s6[0] = Iw(0, 0);
+      s6[1] = Iw(1, 1);
+      s6[2] = Iw(2, 2);
+      s6[3] = Iw(0, 1);
+      s6[4] = Iw(0, 2);
+      s6[5] = Iw(1, 2);
+      R* i6 = W.iwi6 + 6 * ab3;
+      i6[0] = Ii(0, 0);
+      i6[1] = Ii(1, 1);
+      i6[2] = Ii(2, 2);
+      i6[3] = Ii(0, 1);
+      i6[4] = Ii(0, 2);
+      i6[5] = Ii(1, 2);
+      const V3<R> w = ld3(W.u0 + d + 3);
+      V3<R> tq = -cross(w, mul(Iw, w));
+      if (W.f_extra) tq = tq + ld3(W.f_extra + d + 3);
+      st3(W.ut + d + 3, w + h * mul(Ii, tq));
+    }
+  }
+  for (int i = t.rank(); i < T.ndof; i += t.size()) {
+    W.u[i] = R(0);
+    W.shift[i] = R(0);
+    W.hinv[i] = R(0);
+  }
+}
+
+// The Newton loop, final classification and telemetry (newton.cpp:343-416).
+// Requires newton_setup() and a barrier, and the step's contact set + incidence.
+template <class R, class Team>
+__device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cfg, StepOut out) {
+  const R h = W.h;
+  const int nr = W.nrows;
+  const int maxlin = cfg.linear_max_iterations;
+  const R eps = R(cfg.epsilon_reg);
+  const R tfrac = R(cfg.step_fraction);
+  for (int i = t.rank(); i < nr; i += t.size()) W.lam[i] = R(0);
+  setup_row_blocks(t, T, W);
+  // any friction (line-search gate, newton.cpp:341)
+  double has_fric = 0.0;
+  for (int c = t.rank(); c < W.nc; c += t.size())
+    if (W.cgeo[17 * c + 16] > R(0)) has_fric = 1.0;
+  {
+    double s0[1] = {0.0}, m0[1] = {has_fric};
+    t.reduce(s0, m0);
+    has_fric = m0[0];
+  }
+  const bool line_search = cfg.line_search && has_fric == 0.0;
+  double min_shift = 0.0;
+  int n_done = 0;
+  int aborted = 0;
+
+  for (int it = 0; it < cfg.newton_iterations; ++it) {
+    // ---- assemble
+    AsmStats as{0.0, 0.0, 0.0, 0.0};
+    assemble(t, T, W, W.q, W.u, cfg, as);
+    t.sync();
+    // ---- g = M~(u - u~) - J^T lambda; geometric stiffness; H^-1; w = H^-1 g
+    double gmax = 0.0, gsq = 0.0, smin = 0.0;
+    const bool gs = it >= 1 && cfg.geometric_stiffness;
+    for (int b = t.rank(); b < T.nd3; b += t.size()) {
+      const V3<R> jl = pull(T, W, b, W.lam);
+      const int kind = T.d3_kind[b];
+      const int d = 3 * b;
+      V3<R> gv, mdiag;
+      const V3<R> du = ld3(W.u + d) - ld3(W.ut + d);
+      if (kind == kRigidAng) {
+        const R* s6 = W.iw6 + 6 * b;
+        gv = sym_mul(s6, du) - jl;
+        mdiag = v3(s6[0], s6[1], s6[2]);
+      } else {
+        const R m = T.bmass[T.d3_body[b]];
+        gv = v3(m * du.x, m * du.y, m * du.z) - jl;
+        mdiag = v3(m, m, m);
+      }
+      if (gs) {
+        if (kind == kParticleLin) {
+          const R m = mdiag.x;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const R dd = W.u[d + k] - W.up[d + k];
+            R sh = R(0);
+            if (!(ab(dd) < R(1e-10))) {
+              const R ck = -((gv[k] - W.gp[d + k] + m * dd) / dd);
+              sh = -mn(R(0), ck);
+            }
+            W.shift[d + k] = sh;
+            smin = fmin(smin, (double)sh);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) W.shift[d + k] = R(0);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        W.gp[d + k] = gv[k];
+        W.up[d + k] = W.u[d + k];
+        W.g[d + k] = gv[k];
+        gmax = fmax(gmax, (double)(ab(gv[k]) / mdiag[k]));
+        gsq += (double)gv[k] * (double)gv[k];
+      }
+      if (kind != kRigidAng) {
+        const R m = mdiag.x;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) W.hinv[d + k] = R(1) / (m + W.shift[d + k]);
+      }
+      st3(W.w + d, hinv_apply(T, W, b, gv));
+    }
+    double s2[2] = {gsq, as.hsq}, m3[4] = {fmax(gmax, as.hmax), as.comp, as.cone, -smin};
+    t.reduce(s2, m3);
+    min_shift = fmin(min_shift, -m3[3]);
+    IterOut io;
+    io.residual_inf = m3[0];
+    io.merit_l2 = sqrt(s2[0] + s2[1]);
+    io.comp_error_max = m3[1];
+    io.cone_violation_max = m3[2];
+    io.linear_iterations = 0;
+    io.linear_residual = 0.0;
+    io.linear_breakdown = 0;
+
+    // ---- Schur RHS b = J H^-1 g - h, diagonal preconditioner, r = b (x0 = 0)
+    double rr = 0.0, rzr = 0.0;
+    for (int i = t.rank(); i < nr; i += t.size()) {
+      const R b = row_dot(W.coeff + 12 * i, W.blk + 4 * i, W.w) - W.hv[i];
+      R inv = R(1);
+      if (cfg.preconditioner == 1) {
+        const R sd = schur_diag(T, W, i, eps);
+        inv = sd > R(0) ? R(1) / sd : R(1);
+      }
+      W.inv[i] = inv;
+      W.r[i] = b;
+      W.x[i] = R(0);
+      W.bx[i] = R(0);
+      W.z[i] = inv * b;
+      rr += (double)b * b;
+      rzr += (double)b * (double)(inv * b);
+    }
+    int lin_used = 0, breakdown = 0, hist_n = 0;
+    double hist_last = 0.0;
+    if (nr > 0) {
+      double s1[2] = {rr, rzr}, m0[1] = {0.0};
+      t.reduce(s1, m0);
+      hist_last = sqrt(s1[0]);
+      double phist_last = sqrt(s1[1]);
+      double best_res = hist_last;
+      hist_n = 1;
+      if (t.rank() == 0 && out.hist) out.hist[(size_t)it * (maxlin + 1)] = hist_last;
+      bool pending_best = false;
+      R *x = W.x, *xn = W.xn, *r = W.r, *rn = W.rn, *z = W.z, *zn = W.zn;
+      double zaz = 0.0;
+      if (maxlin > 0 && hist_last > cfg.linear_tolerance) {
+        // az = A z, zaz = z . az
+        op_pull(t, T, W, z);
+        t.sync();
+        double za = 0.0;
+        for (int i = t.rank(); i < nr; i += t.size()) {
+          const R a = op_row(T, W, i, z, eps);
+          W.az[i] = a;
+          za += (double)z[i] * a;
+        }
+        double s[1] = {za}, m[1] = {0.0};
+        t.reduce(s, m);
+        zaz = s[0];
+      }
+      double beta = 0.0;
+      for (int itl = 0; itl < maxlin && hist_last > cfg.linear_tolerance; ++itl) {
+        // phase A: p = z + beta p, ap = az + beta ap; den = ap . M^-1 ap
+        double den = 0.0;
+        const R rb = R(beta);
+        for (int i = t.rank(); i < nr; i += t.size()) {
+          R pi, api;
+          if (itl == 0) {
+            pi = z[i];
+            api = W.az[i];
+          } else {
+            pi = z[i] + rb * W.p[i];
+            api = W.az[i] + rb * W.ap[i];
+          }
+          W.p[i] = pi;
+          W.ap[i] = api;
+          den += (double)api * (double)(W.inv[i] * api);
+          if (pending_best) W.bx[i] = x[i];
+        }
+        pending_best = false;
+        {
+          double s[1] = {den}, m[1] = {0.0};
+          t.reduce(s, m);
+          den = s[0];
+        }
+        if (fabs(den) < 1e-300) {
+          breakdown = 1;
+          break;
+        }
+        const double alpha = zaz / den;
+        const R ra = R(alpha);
+        // phase B: x' = x + a p, r' = r - a ap, z' = z - a M^-1 ap
+        double pn2 = 0.0, rn2 = 0.0;
+        for (int i = t.rank(); i < nr; i += t.size()) {
+          const R api = W.ap[i];
+          xn[i] = x[i] + ra * W.p[i];
+          const R rv = r[i] - ra * api;
+          rn[i] = rv;
+          zn[i] = z[i] - ra * (W.inv[i] * api);
+          pn2 += (double)rv * (double)(W.inv[i] * rv);
+          rn2 += (double)rv * rv;
+        }
+        {
+          double s[2] = {pn2, rn2}, m[1] = {0.0};
+          t.reduce(s, m);
+          pn2 = s[0];
+          rn2 = s[1];
+        }
+        const double pn = sqrt(pn2);
+        if (pn > phist_last) break;  // monotone guard: stop at the numerical floor
+        // commit
+        R* tmp = x;
+        x = xn;
+        xn = tmp;
+        tmp = r;
+        r = rn;
+        rn = tmp;
+        tmp = z;
+        z = zn;
+        zn = tmp;
+        hist_last = sqrt(rn2);
+        phist_last = pn;
+        if (t.rank() == 0 && out.hist && hist_n <= maxlin) out.hist[(size_t)it * (maxlin + 1) + hist_n] = hist_last;
+        ++hist_n;
+        if (hist_last < best_res) {
+          best_res = hist_last;
+          pending_best = true;
+        }
+        lin_used = itl + 1;
+        if (fabs(zaz) < 1e-300) {
+          breakdown = 1;
+          break;
+        }
+        // az = A z', zaz' = z' . az
+        op_pull(t, T, W, z);
+        t.sync();
+        double za = 0.0;
+        for (int i = t.rank(); i < nr; i += t.size()) {
+          const R a = op_row(T, W, i, z, eps);
+          W.az[i] = a;
+          za += (double)z[i] * a;
+          if (pending_best) W.bx[i] = x[i];
+        }
+        pending_best = false;
+        {
+          double s[1] = {za}, m[1] = {0.0};
+          t.reduce(s, m);
+          beta = s[0] / zaz;
+          zaz = s[0];
+        }
+      }
+      if (pending_best) {
+        for (int i = t.rank(); i < nr; i += t.size()) W.bx[i] = x[i];
+      }
+      // keep the committed iterate pointers for the next Newton iteration's phase
+      W.x = x;
+      W.xn = xn;
+      W.r = r;
+      W.rn = rn;
+      W.z = z;
+      W.zn = zn;
+    }
+    io.linear_iterations = lin_used;
+    io.linear_breakdown = breakdown;
+    io.linear_residual = hist_n > 0 ? hist_last : 0.0;
+    t.sync();
+    // ---- du = H^-1 (J^T dlambda - g); NaN check (newton.cpp:295,362-369)
+    double dl2 = 0.0, du2 = 0.0, bad = 0.0;
+    for (int i = t.rank(); i < nr; i += t.size()) {
+      const R v = W.bx[i];
+      dl2 += (double)v * v;
+      if (!isfinite(v)) bad = 1.0;
+    }
+    for (int b = t.rank(); b < T.nd3; b += t.size()) {
+      const V3<R> jd = nr > 0 ? pull(T, W, b, W.bx) : v3(R(0), R(0), R(0));
+      const V3<R> dv = hinv_apply(T, W, b, jd - ld3(W.g + 3 * b));
+      st3(W.du + 3 * b, dv);
+      du2 += (double)dv.x * dv.x + (double)dv.y * dv.y + (double)dv.z * dv.z;
+      if (!isfinite(dv.x) || !isfinite(dv.y) || !isfinite(dv.z)) bad = 1.0;
+    }
+    {
+      double s[2] = {dl2, du2}, m[1] = {bad};
+      t.reduce(s, m);
+      dl2 = s[0];
+      du2 = s[1];
+      bad = m[0];
+    }
+    if (bad != 0.0) {
+      for (int i = t.rank(); i < T.ncoord; i += t.size()) W.q[i] = W.q0[i];
+      for (int i = t.rank(); i < T.ndof; i += t.size()) W.u[i] = W.u0[i];
+      if (t.rank() == 0 && out.iters) out.iters[it] = io;
+      aborted = 1;
+      n_done = it + 1;
+      break;
+    }
+    // ---- optional merit line search (newton.cpp:371-391)
+    R tstep = tfrac;
+    if (line_search) {
+      const R trials[4] = {R(1), R(0.5), R(0.25), R(0.125)};
+      for (int k = 0; k < 4; ++k) {
+        const R tr = trials[k];
+        R* pl = W.xn;   // probe lambda (free after the solve)
+        R* pu = W.ub;   // probe velocities
+        for (int i = t.rank(); i < nr; i += t.size()) pl[i] = W.lam[i] + tr * W.bx[i];
+        for (int i = t.rank(); i < T.ndof; i += t.size()) pu[i] = W.u[i] + tr * W.du[i];
+        for (int b = t.rank(); b < T.nb; b += t.size()) {
+          const int cd = T.bcoord[b], d = T.bdof[b];
+          for (int k2 = 0; k2 < 3; ++k2) W.qp[cd + k2] = W.q0[cd + k2] + h * pu[d + k2];
+          if (T.btype[b] == 1) {
+            const R* th = W.q + cd + 3;
+            const R wx = pu[d + 3], wy = pu[d + 4], wz = pu[d + 5];
+            R nq[4];
+            nq[0] = W.q0[cd + 3] + h * (R(0.5) * (-th[1] * wx - th[2] * wy - th[3] * wz));
+            nq[1] = W.q0[cd + 4] + h * (R(0.5) * (th[0] * wx + th[3] * wy - th[2] * wz));
+            nq[2] = W.q0[cd + 5] + h * (R(0.5) * (-th[3] * wx + th[0] * wy + th[1] * wz));
+            nq[3] = W.q0[cd + 6] + h * (R(0.5) * (th[2] * wx - th[1] * wy + th[0] * wz));
+            const R nn = sqrt(nq[0] * nq[0] + nq[1] * nq[1] + nq[2] * nq[2] + nq[3] * nq[3]);
+            if ((double)nn < 1e-300) {
+              nq[0] = R(1);
+              nq[1] = nq[2] = nq[3] = R(0);
+            } else {
+              for (int k2 = 0; k2 < 4; ++k2) nq[k2] = nq[k2] / nn;
+            }
+            for (int k2 = 0; k2 < 4; ++k2) W.qp[cd + 3 + k2] = nq[k2];
+          }
+        }
+        t.sync();
+        R* save_lam = W.lam;
+        W.lam = pl;
+        AsmStats ps{0.0, 0.0, 0.0, 0.0};
+        assemble(t, T, W, W.qp, pu, cfg, ps);
+        t.sync();
+        double pg = 0.0;
+        for (int b = t.rank(); b < T.nd3; b += t.size()) {
+          const V3<R> jl = pull(T, W, b, W.lam);
+          const V3<R> dv = ld3(pu + 3 * b) - ld3(W.ut + 3 * b);
+          V3<R> gv;
+          if (T.d3_kind[b] == kRigidAng)
+            gv = sym_mul(W.iw6 + 6 * b, dv) - jl;
+          else {
+            const R m = T.bmass[T.d3_body[b]];
+            gv = v3(m * dv.x, m * dv.y, m * dv.z) - jl;
+          }
+          pg += (double)gv.x * gv.x + (double)gv.y * gv.y + (double)gv.z * gv.z;
+        }
+        W.lam = save_lam;
+        double s[2] = {pg, ps.hsq}, m[1] = {0.0};
+        t.reduce(s, m);
+        if (sqrt(s[0] + s[1]) < io.merit_l2) {
+          tstep = tr;
+          break;
+        }
+      }
+    }
+    // ---- damped update + integration (newton.cpp:393-396, bodies.cpp:58-86).
+    // Each body owns its dofs, so u += t du and q = q- + h G(q) u run in one pass;
+    // G is evaluated at the current iterate before q is overwritten.
+    for (int i = t.rank(); i < nr; i += t.size()) W.lam[i] += tstep * W.bx[i];
+    for (int b = t.rank(); b < T.nb; b += t.size()) {
+      const int cd = T.bcoord[b], d = T.bdof[b];
+      const int nd = T.btype[b] == 1 ? 6 : 3;
+      for (int k = 0; k < nd; ++k) W.u[d + k] += tstep * W.du[d + k];
+      for (int k = 0; k < 3; ++k) W.q[cd + k] = W.q0[cd + k] + h * W.u[d + k];
+      if (T.btype[b] == 1) {
+        R* th = W.q + cd + 3;
+        const R ox = W.u[d + 3], oy = W.u[d + 4], oz = W.u[d + 5];
+        R nq[4];
+        nq[0] = W.q0[cd + 3] + h * (R(0.5) * (-th[1] * ox - th[2] * oy - th[3] * oz));
+        nq[1] = W.q0[cd + 4] + h * (R(0.5) * (th[0] * ox + th[3] * oy - th[2] * oz));
+        nq[2] = W.q0[cd + 5] + h * (R(0.5) * (-th[3] * ox + th[0] * oy + th[1] * oz));
+        nq[3] = W.q0[cd + 6] + h * (R(0.5) * (th[2] * ox - th[1] * oy + th[0] * oz));
+        const R nn = sqrt(nq[0] * nq[0] + nq[1] * nq[1] + nq[2] * nq[2] + nq[3] * nq[3]);
+        if ((double)nn < 1e-300) {
+          nq[0] = R(1);
+          nq[1] = nq[2] = nq[3] = R(0);
+        } else {
+          for (int k = 0; k < 4; ++k) nq[k] = nq[k] / nn;
+        }
+        for (int k = 0; k < 4; ++k) th[k] = nq[k];
+      }
+    }
+    io.step_size = (double)tstep * sqrt(du2 + dl2);
+    if (t.rank() == 0) {
+      if (out.iters) out.iters[it] = io;
+      if (out.hist_len) out.hist_len[it] = nr > 0 ? hist_n : 0;
+    }
+    n_done = it + 1;
+    t.sync();
+  }
+
+  if (aborted) {
+    if (t.rank() == 0 && out.fin) {
+      out.fin[5] = 1.0;
+      out.fin[6] = 0.0;
+      out.fin[7] = n_done;
+    }
+    return 1;
+  }
+  // ---- final assembly for classification and telemetry (newton.cpp:409-416)
+  AsmStats fs{0.0, 0.0, 0.0, 0.0};
+  assemble(t, T, W, W.q, W.u, cfg, fs);
+  t.sync();
+  double gmax = 0.0;
+  for (int b = t.rank(); b < T.nd3; b += t.size()) {
+    const V3<R> jl = pull(T, W, b, W.lam);
+    const V3<R> du = ld3(W.u + 3 * b) - ld3(W.ut + 3 * b);
+    if (T.d3_kind[b] == kRigidAng) {
+      const R* s6 = W.iw6 + 6 * b;
+      const V3<R> gv = sym_mul(s6, du) - jl;
+      gmax = fmax(gmax, fmax((double)(ab(gv.x) / s6[0]), fmax((double)(ab(gv.y) / s6[1]), (double)(ab(gv.z) / s6[2]))));
+    } else {
+      const R m = T.bmass[T.d3_body[b]];
+      const V3<R> gv = v3(m * du.x, m * du.y, m * du.z) - jl;
+      gmax = fmax(gmax, fmax((double)(ab(gv.x) / m), fmax((double)(ab(gv.y) / m), (double)(ab(gv.z) / m))));
+    }
+  }
+  // contact telemetry + min gap (fill_contact_telemetry, newton.cpp:67-94)
+  double mgap = W.nc ? __builtin_huge_val() : 0.0;
+  for (int c = t.rank(); c < W.nc; c += t.size()) {
+    const int ba = W.cbody[2 * c], bb = W.cbody[2 * c + 1];
+    const R* g = W.cgeo + 17 * c;
+    const V3<R> la = ld3(g), lb = ld3(g + 3), n = ld3(g + 6), d1 = ld3(g + 9), d2 = ld3(g + 12);
+    V3<R> pa, pb, ra = v3(R(0), R(0), R(0)), rb = ra;
+    const bool rig_a = ba >= 0 && T.btype[ba] == 1, rig_b = bb >= 0 && T.btype[bb] == 1;
+    if (ba < 0) pa = la;
+    else if (!rig_a) pa = body_pos(T, W.q, ba);
+    else {
+      ra = mul(body_rot(T, W.q, ba), la);
+      pa = body_pos(T, W.q, ba) + ra;
+    }
+    if (bb < 0) pb = lb;
+    else if (!rig_b) pb = body_pos(T, W.q, bb);
+    else {
+      rb = mul(body_rot(T, W.q, bb), lb);
+      pb = body_pos(T, W.q, bb) + rb;
+    }
+    const R gap = dot(n, pa - pb) - g[15];
+    auto vel = [&](V3<R> d) {
+      R s = R(0);
+      if (ba >= 0) {
+        const int o = T.bdof[ba];
+        s += dot(d, ld3(W.u + o));
+        if (rig_a) s += dot(cross(ra, d), ld3(W.u + o + 3));
+      }
+      if (bb >= 0) {
+        const int o = T.bdof[bb];
+        s -= dot(d, ld3(W.u + o));
+        if (rig_b) s -= dot(cross(rb, d), ld3(W.u + o + 3));
+      }
+      return s;
+    };
+    const R v0 = vel(d1), v1 = vel(d2);
+    const int nrw = W.normal_begin + c, f0 = W.friction_begin + 2 * c;
+    const R lf0 = W.lam[f0] / h, lf1 = W.lam[f0 + 1] / h;
+    if (out.tel) {
+      double* o = out.tel + 6 * c;
+      o[0] = gap;
+      o[1] = W.lam[nrw] / h;
+      o[2] = sqrt(lf0 * lf0 + lf1 * lf1);
+      o[3] = g[16];
+      o[4] = sqrt(v0 * v0 + v1 * v1);
+      o[5] = lf0 * v0 + lf1 * v1;
+    }
+    mgap = fmin(mgap, (double)gap);
+  }
+  {
+    double s[1] = {0.0}, m[4] = {fmax(gmax, fs.hmax), fs.comp, fs.cone, -mgap};
+    t.reduce(s, m);
+    if (t.rank() == 0 && out.fin) {
+      out.fin[0] = m[0];
+      out.fin[1] = m[1];
+      out.fin[2] = m[2];
+      out.fin[3] = W.nc ? -m[3] : 0.0;
+      out.fin[4] = min_shift;
+      out.fin[5] = 0.0;
+      out.fin[6] = m[0] < cfg.newton_tolerance ? 1.0 : 0.0;
+      out.fin[7] = n_done;
+    }
+  }
+  return 0;
+}
+
+}  // namespace nsd

@@ -1,0 +1,162 @@
+// Execution teams for the Newton-step engine.
+//
+// The whole per-timestep solve (nsd_engine.cuh) is written once against a
+// "team": a set of threads that cooperatively owns one scene. A team exposes
+// rank/size for strided work loops, a barrier, and a deterministic all-reduce
+// (fixed summation order; every member receives the identical bits, so all
+// data-dependent branches — PCR exits, breakdown, abort — are team-uniform).
+//
+//   WarpTeam  — one warp per environment (batched RL path, tiny scenes):
+//               barrier = __syncwarp, reductions = shuffle trees.
+//   BlockTeam — one CTA per scene/environment: barrier = __syncthreads,
+//               reductions through double-buffered shared memory.
+//   GridTeam  — a cooperative persistent grid per large scene (FEM configs):
+//               barrier = grid-wide sync, reductions through per-CTA partials
+//               in global memory summed in CTA order.
+#pragma once
+
+#include <cooperative_groups.h>
+
+namespace nsd {
+
+constexpr int kRedMax = 8;  // max values per fused reduction
+
+__device__ __forceinline__ double warp_sum_down(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  return v;
+}
+__device__ __forceinline__ double warp_max_down(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, off));
+  return v;
+}
+
+struct WarpTeam {
+  int lane;
+  __device__ explicit WarpTeam(int l) : lane(l) {}
+  __device__ __forceinline__ int rank() const { return lane; }
+  __device__ __forceinline__ int size() const { return 32; }
+  __device__ __forceinline__ void sync() const { __syncwarp(); }
+  // sums s[0..NS), maxima m[0..NM); results broadcast from lane 0.
+  template <int NS, int NM>
+  __device__ __forceinline__ void reduce(double (&s)[NS], double (&m)[NM]) {
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < NS; ++k) s[k] = __shfl_sync(0xffffffffu, warp_sum_down(s[k]), 0);
+#pragma unroll
+    for (int k = 0; k < NM; ++k) m[k] = __shfl_sync(0xffffffffu, warp_max_down(m[k]), 0);
+  }
+};
+
+struct BlockTeam {
+  double* red;  // shared: 2 * (33 * kRedMax) doubles
+  int parity;
+  __device__ explicit BlockTeam(double* smem_red) : red(smem_red), parity(0) {}
+  __device__ __forceinline__ int rank() const { return threadIdx.x; }
+  __device__ __forceinline__ int size() const { return blockDim.x; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  template <int NS, int NM>
+  __device__ __forceinline__ void reduce(double (&s)[NS], double (&m)[NM]) {
+    constexpr int K = NS + NM;
+    static_assert(K <= kRedMax, "too many values in one reduction");
+    double* buf = red + parity * (33 * kRedMax);
+    parity ^= 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const double v = warp_sum_down(s[k]);
+      if (lane == 0) buf[warp * kRedMax + k] = v;
+    }
+#pragma unroll
+    for (int k = 0; k < NM; ++k) {
+      const double v = warp_max_down(m[k]);
+      if (lane == 0) buf[warp * kRedMax + NS + k] = v;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const double v = warp_sum_down(lane < nw ? buf[lane * kRedMax + k] : 0.0);
+        if (lane == 0) buf[32 * kRedMax + k] = v;
+      }
+#pragma unroll
+      for (int k = 0; k < NM; ++k) {
+        const double v = warp_max_down(lane < nw ? buf[lane * kRedMax + NS + k] : -__builtin_huge_val());
+        if (lane == 0) buf[32 * kRedMax + NS + k] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NS; ++k) s[k] = buf[32 * kRedMax + k];
+#pragma unroll
+    for (int k = 0; k < NM; ++k) m[k] = buf[32 * kRedMax + NS + k];
+  }
+};
+
+struct GridTeam {
+  double* red;    // shared: 2 * (33 * kRedMax)
+  double* gpart;  // global: 2 * gridDim.x * kRedMax
+  int parity;
+  __device__ GridTeam(double* smem_red, double* global_part) : red(smem_red), gpart(global_part), parity(0) {}
+  __device__ __forceinline__ int rank() const { return blockIdx.x * blockDim.x + threadIdx.x; }
+  __device__ __forceinline__ int size() const { return gridDim.x * blockDim.x; }
+  __device__ __forceinline__ void sync() const { cooperative_groups::this_grid().sync(); }
+  template <int NS, int NM>
+  __device__ __forceinline__ void reduce(double (&s)[NS], double (&m)[NM]) {
+    constexpr int K = NS + NM;
+    static_assert(K <= kRedMax, "too many values in one reduction");
+    double* buf = red + parity * (33 * kRedMax);
+    double* gp = gpart + parity * (gridDim.x * kRedMax);
+    parity ^= 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const double v = warp_sum_down(s[k]);
+      if (lane == 0) buf[warp * kRedMax + k] = v;
+    }
+#pragma unroll
+    for (int k = 0; k < NM; ++k) {
+      const double v = warp_max_down(m[k]);
+      if (lane == 0) buf[warp * kRedMax + NS + k] = v;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const double v = warp_sum_down(lane < nw ? buf[lane * kRedMax + k] : 0.0);
+        if (lane == 0) gp[blockIdx.x * kRedMax + k] = v;
+      }
+#pragma unroll
+      for (int k = 0; k < NM; ++k) {
+        const double v = warp_max_down(lane < nw ? buf[lane * kRedMax + NS + k] : -__builtin_huge_val());
+        if (lane == 0) gp[blockIdx.x * kRedMax + NS + k] = v;
+      }
+    }
+    cooperative_groups::this_grid().sync();
+    if (warp == 0) {
+      const int nb = gridDim.x;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        double acc = 0.0;
+        for (int b = lane; b < nb; b += 32) acc += __ldcg(gp + b * kRedMax + k);
+        acc = warp_sum_down(acc);
+        if (lane == 0) buf[32 * kRedMax + k] = acc;
+      }
+#pragma unroll
+      for (int k = 0; k < NM; ++k) {
+        double acc = -__builtin_huge_val();
+        for (int b = lane; b < nb; b += 32) acc = fmax(acc, __ldcg(gp + b * kRedMax + NS + k));
+        acc = warp_max_down(acc);
+        if (lane == 0) buf[32 * kRedMax + NS + k] = acc;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NS; ++k) s[k] = buf[32 * kRedMax + k];
+#pragma unroll
+    for (int k = 0; k < NM; ++k) m[k] = buf[32 * kRedMax + NS + k];
+  }
+};
+
+}  // namespace nsd

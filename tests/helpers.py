@@ -1,0 +1,55 @@
+"""Shared helpers for parity tests: build a case with the CPU oracle, run the
+same newton_step through the C ABI on the GPU, compare."""
+import numpy as np
+
+from oracle import oracle_py as O
+
+
+def oracle_case(name, seed=0, warm_steps=0, overrides=None):
+    w = O.OracleWorld(name, seed)
+    if overrides:
+        w.set_config(**overrides)
+    if warm_steps:
+        w.step(warm_steps)
+    w.prepare()
+    q, u = w.state()
+    ib, db = w.contacts()
+    return dict(world=w, topo=w.topology(), q=q, u=u, contacts=(ib, db), h=w.h, gravity=w.gravity(),
+                joint_frame=w.joint_frames(), cfg=w.get_config(), dims=w.dims())
+
+
+def newton_config(cfg, precision):
+    from paper_1907_04587_b200 import NewtonConfig
+
+    return NewtonConfig(newton_iterations=cfg["newton_iterations"], step_fraction=cfg["step_fraction"],
+                        epsilon_reg=cfg["epsilon_reg"], geometric_stiffness=bool(cfg["geometric_stiffness"]),
+                        r_strategy=cfg["r_strategy"], ncp_kind=cfg["ncp_kind"], linear_method=3,
+                        linear_max_iterations=cfg["linear_max_iterations"], linear_tolerance=cfg["linear_tolerance"],
+                        preconditioner=cfg["preconditioner"], newton_tolerance=cfg["newton_tolerance"],
+                        line_search=bool(cfg["line_search"]), precision=precision)
+
+
+def run_gpu(case, precision, f_extra=None):
+    from paper_1907_04587_b200 import NewtonSolver, Topology
+
+    topo = Topology(**case["topo"])
+    s = NewtonSolver(topo, newton_config(case["cfg"], precision))
+    out = s.newton_step(case["q"], case["u"], case["contacts"], h=case["h"], gravity=tuple(case["gravity"]),
+                        f_extra=f_extra, joint_frame=case["joint_frame"])
+    s.close()
+    return out
+
+
+def run_oracle(case):
+    w = case["world"]
+    rc = w.newton()
+    q, u = w.state()
+    rep = w.report()
+    return dict(q=q, u=u, rc=rc, **rep)
+
+
+def rel_err(a, b, floor=1e-12):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    if a.size == 0:
+        return 0.0
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), floor))

@@ -1,0 +1,101 @@
+"""Batched many-environment path (C5 ants) against the oracle's step_world run
+per environment: bit-exact contact set (count, order, bodies, features) every
+step, states within the stated tolerance, with and without the joint-torque
+extension hook, and env results independent of how environments are grouped
+(the property that makes GPU sharding safe)."""
+import numpy as np
+import pytest
+
+from oracle import oracle_py as O
+from tests.helpers import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _batch(n_env, prec, env0=0, max_contacts=48, team=None):
+    import os
+
+    from paper_1907_04587_b200 import BatchSolver, Scene
+
+    if team:
+        os.environ["NSD_BATCH_TEAM"] = str(team)
+    s0 = Scene("c5", 0)
+    qs, us = [], []
+    for e in range(env0, env0 + n_env):
+        s = Scene("c5", e)
+        qs.append(s.q)
+        us.append(s.u)
+    cfg = s0.config
+    cfg.precision = prec
+    b = BatchSolver(s0.topology, s0.shapes, s0.n_shapes, s0.margin, s0.mu_default, cfg, n_env, max_contacts)
+    if team:
+        del os.environ["NSD_BATCH_TEAM"]
+    b.set_state(np.concatenate(qs), np.concatenate(us))
+    return b, s0
+
+
+def _torques(env, step, nj):
+    rng = np.random.default_rng(env * 1000003 + step)
+    return rng.uniform(-1.0, 1.0, nj)
+
+
+@pytest.mark.parametrize("prec,steps,tol", [("fp64", 25, 1e-8), ("fp32", 10, 2e-3)])
+@pytest.mark.parametrize("actuated", [False, True])
+def test_batch_matches_oracle(prec, steps, tol, actuated):
+    n_env = 24
+    b, s0 = _batch(n_env, prec)
+    nj = s0.topology.n_joints
+    worlds = [O.OracleWorld("c5", e) for e in range(n_env)]
+    for st in range(steps):
+        tau = np.stack([_torques(e, st, nj) for e in range(n_env)]) if actuated else None
+        for e, w in enumerate(worlds):
+            w.set_joint_torques(tau[e] if actuated else None)
+            assert w.step(1) == 0
+        b.step(s0.h, s0.gravity, torque=tau.reshape(-1) if actuated else None)
+        res = b.results()
+        assert not res["aborted"].any()
+        q, u = b.get_state()
+        for e, w in enumerate(worlds):
+            ib, db = w.contacts()
+            gib, gdb = b.contacts(e)
+            if prec == "fp64" or st < 3:
+                assert res["n_contacts"][e] == len(ib), (st, e)
+                assert np.array_equal(gib[:, :3], ib[:, :3]), (st, e)
+            oq, ou = w.state()
+            assert rel_err(q[e], oq) < tol, (st, e, rel_err(q[e], oq))
+            assert rel_err(u[e], ou, floor=1e-3) < tol * 100, (st, e)
+
+
+def test_batch_team_shapes_agree_fp64():
+    """Warp-per-env and CTA-per-env teams give the same states (fixed-order reductions differ
+    only in association; fp64 agreement to 1e-12)."""
+    bw, s0 = _batch(16, "fp64", team=32)
+    bb, _ = _batch(16, "fp64", team=64)
+    for _ in range(5):
+        bw.step(s0.h, s0.gravity)
+        bb.step(s0.h, s0.gravity)
+    qw, _ = bw.get_state()
+    qb, _ = bb.get_state()
+    assert rel_err(qw, qb) < 1e-11
+
+
+def test_batch_env_offset_independent():
+    """Env i gives the same bits whether it runs in a batch starting at env 0 or env 8
+    (what the GPU sharding relies on)."""
+    a, s0 = _batch(16, "fp32", env0=0)
+    b, _ = _batch(8, "fp32", env0=8)
+    for _ in range(6):
+        a.step(s0.h, s0.gravity)
+        b.step(s0.h, s0.gravity)
+    qa, _ = a.get_state()
+    qb, _ = b.get_state()
+    assert np.array_equal(qa[8:], qb)
+
+
+def test_batch_overflow_reported():
+    from paper_1907_04587_b200 import NsdError
+
+    b, s0 = _batch(4, "fp32", max_contacts=4)
+    b.step(s0.h, s0.gravity)
+    with pytest.raises(NsdError):
+        b.results()
