@@ -1,0 +1,301 @@
+#!/usr/bin/env python3
+"""Benchmark: batched non-smooth Newton step, C5 workload (ant environments).
+
+One "step" = one step_world for every environment on the GPU: device narrow
+phase (sphere/box vs half-space and body pairs) + the full non-smooth Newton
+solve (4 Newton x 10 PCR, Fischer-Burmeister, effective-mass r, friction) +
+integration — a single kernel launch (k_batch_warp / k_batch_block).
+
+  value   env-steps/s, actions pre-staged in HBM, L2 flushed between steps,
+          device time (CUDA events) summed over exactly K steps, max over ranks
+  e2e     same metric through the C ABI with host actions: per step H2D of the
+          joint torques from pinned memory + step + D2H of (q, u) to pinned memory
+  --impl reference   the reference's CPU path: the oracle restatement of
+          nsdyn::step_world (oracle/, the reference itself does not build here),
+          OpenMP over environments on all host cores.
+
+Multi-GPU: one process per GPU (torchrun), each rank owns envs
+[rank*E, (rank+1)*E) with global-env-id seeds; no collective on the data path
+(SURVEY §8e); "scaling": "weak".
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--envs", type=int, default=4096, help="environments per GPU")
+    p.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    p.add_argument("--passive", action="store_true", help="no joint torques (pure reference semantics)")
+    p.add_argument("--team", type=int, default=0, help="threads per env team (32 = warp, 64/128 = CTA)")
+    p.add_argument("--max-contacts", type=int, default=48)
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU baseline sample length")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device):
+        self.device, self.samples, self.proc, self.thread = device, [], None, None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i] and "Not" not in s[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+def b_cr_bytes(n_contacts, nj_rows=40, n_joint_nnz=384, n_joints=8, dof=54, rigid=9, value_bytes=4):
+    """SURVEY §8(d) algorithmic bytes of one CR iteration for one env:
+    B_CR = 2(vZ + 4X) + v n_C + 2vD + v D_particle + 7v B_rigid + 13 v R
+    (fp32: v = 4 -> 2(4Z+4X) + 4n_C + 8D + 4D_p + 28B_rigid + 52R)."""
+    nc = np.asarray(n_contacts, dtype=np.float64)
+    R = nj_rows + 3 * nc
+    Z = n_joint_nnz + 18 * nc
+    X = 2 * n_joints + 2 * nc
+    n_C = R
+    v = value_bytes
+    return 2 * (v * Z + 4 * X) + v * n_C + 2 * v * dof + 7 * v * rigid + 13 * v * R
+
+
+def cpu_baseline(args, n_env_total):
+    from oracle import oracle_py as O
+
+    # calibrate on 2 steps, then size the sample to ~cpu_seconds
+    n_env = min(n_env_total, 4096)
+    t, used, _ = O.c5_bench(0, n_env, 1, not args.passive)
+    steps = max(1, min(50, int(args.cpu_seconds / max(t, 1e-3))))
+    t, used, _ = O.c5_bench(0, n_env, steps, not args.passive)
+    return {"value": n_env * steps / t, "unit": "env-steps/s", "cores": used, "kind": "port",
+            "sample": f"{n_env} C5 ant envs x {steps} steps (oracle step_world, 4 Newton x 10 PCR, "
+                      f"OpenMP over envs), {t:.2f} s"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_info()
+    if rank != 0:
+        return
+    cb = cpu_baseline(args, args.envs)
+    # each bench "step" = one bounded sample step over the workload; report the rate
+    line = {"impl": "reference", "metric": "env-steps/sec at fixed Newton/CR iters", "value": cb["value"],
+            "unit": "env-steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * args.envs / cb["value"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, ws),
+            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "env-steps/s", "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, ws):
+    return {"workload": "C5 batched RL: ant environments (torso sphere + 8 box links, 8 revolute joints, "
+                        "ground contact, mu=1), one step_world per env per step",
+            "envs_per_gpu": args.envs, "global_envs": args.envs * ws, "newton_iterations": 4,
+            "linear_iterations": 10, "linear_tolerance": 1e-10, "ncp": "fischer-burmeister",
+            "r_strategy": "effective-mass", "actuated": not args.passive, "parallelism": f"env-shard x{ws}",
+            "l2": "flushed (256 MiB memset) between timed steps"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    ws, rank, local = dist_info()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1907_04587_b200 import BatchSolver, Scene, batch_states
+
+    if args.team:
+        os.environ["NSD_BATCH_TEAM"] = str(args.team)
+    E = args.envs
+    env0 = rank * E
+    tmpl = Scene("c5", env0)
+    T = tmpl.topology
+    q0, u0 = batch_states("c5", env0, E, T.num_coord, T.num_dof)
+    cfg = tmpl.config
+    cfg.precision = args.precision
+    b = BatchSolver(T, tmpl.shapes, tmpl.n_shapes, tmpl.margin, tmpl.mu_default, cfg, E, args.max_contacts,
+                    device=local)
+    stream = torch.cuda.Stream(device=local)  # non-default stream: the C ABI reads handle 0 as "own stream"
+    torch.cuda.set_stream(stream)
+    b.set_stream(stream.cuda_stream)
+    b.set_state(q0, u0)
+    nj = T.n_joints
+    K, W = args.steps, args.warmup
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    torques = (torch.rand((K + W, E, nj), generator=gen, device="cuda", dtype=torch.float32) * 2 - 1)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step(i):
+        ptr = None if args.passive else torques[i].data_ptr()
+        b.step_device(tmpl.h, tmpl.gravity, ptr, 0)
+
+    for i in range(W):
+        step(i)
+    torch.cuda.synchronize()
+    b.results()  # raises on contact overflow / errors
+
+    # ---- value: device-resident inputs, L2 flushed between steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    sampler = ClockSampler(local)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for k in range(K):
+        flush.zero_()
+        ev[k][0].record(stream)
+        step(W + k)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if ws > 1:
+        torch.distributed.barrier()
+    dev_ms = sum(a.elapsed_time(bb) for a, bb in ev)
+    res = b.results()
+    nc = res["n_contacts"].astype(np.float64)
+    aborted = int(res["aborted"].sum())
+
+    # ---- e2e: host actions -> H2D, step, D2H of the state, through the C ABI
+    dt = torch.float32 if args.precision == "fp32" else torch.float64
+    h_tq = torch.empty((K, E, nj), dtype=torch.float32, pin_memory=True)
+    h_tq.copy_(torques[W:W + K].cpu())
+    d_tq = torch.empty((E, nj), dtype=torch.float32, device="cuda")
+    h_q = torch.empty((K, E * T.num_coord), dtype=dt, pin_memory=True)
+    h_u = torch.empty((K, E * T.num_dof), dtype=dt, pin_memory=True)
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for k in range(K):
+        flush.zero_()
+        ev2[k][0].record(stream)
+        if not args.passive:
+            d_tq.copy_(h_tq[k], non_blocking=True)
+        b.step_device(tmpl.h, tmpl.gravity, None if args.passive else d_tq.data_ptr(), 0)
+        b.copy_state_async(h_q[k].data_ptr(), h_u[k].data_ptr())
+        ev2[k][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = sum(a.elapsed_time(bb) for a, bb in ev2)
+    h2d = 0 if args.passive else E * nj * 4
+    d2h = E * (T.num_coord + T.num_dof) * (4 if args.precision == "fp32" else 8)
+
+    if ws > 1:
+        t = torch.tensor([dev_ms, e2e_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev_ms, e2e_ms = float(t[0]), float(t[1])
+    total_envs = E * ws
+    value = total_envs * K / (dev_ms / 1000.0)
+    e2e = total_envs * K / (e2e_ms / 1000.0)
+
+    # ---- roofline of the (single) step kernel: SURVEY §8(d) algorithmic bytes
+    vb = 4 if args.precision == "fp32" else 8
+    per_env_cr = b_cr_bytes(nc, value_bytes=vb)
+    bytes_per_launch = float(np.sum(per_env_cr)) * cfg.newton_iterations * cfg.linear_max_iterations
+    launch_s = dev_ms / 1000.0 / K
+    peak, peak_kind = hbm_peak()
+    achieved = bytes_per_launch / launch_s / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.precision)
+        except Exception:
+            traffic = None
+
+    if rank != 0:
+        return
+    line = {"metric": "env-steps/sec at fixed Newton/CR iters", "value": value, "unit": "env-steps/s",
+            "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": dev_ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+            "data": "synthetic", "config": workload_config(args, ws),
+            "us_per_cr_iter": 1000.0 * (dev_ms / K) / (cfg.newton_iterations * cfg.linear_max_iterations),
+            "mean_contacts_per_env": float(nc.mean()), "aborted_envs": aborted,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "bytes_per_launch": bytes_per_launch,
+                         "model": "SURVEY 8(d) B_CR per env per CR iteration x 40 CR iterations x envs"},
+            "e2e": {"value": e2e, "unit": "env-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": K, "clocks": clocks}
+    if ws == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args, E)
+        except Exception as e:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -173,6 +173,10 @@ int nsd_batch_results(nsd_batch* b, int32_t* n_contacts, int32_t* aborted, doubl
 int nsd_batch_contacts(nsd_batch* b, int32_t env, nsd_contact* out, int32_t* n);
 /* Device pointers of the packed state (for zero-copy consumers). */
 int nsd_batch_device_state(nsd_batch* b, void** q_dev, void** u_dev, int32_t* dtype);
+/* Enqueues (no sync) a copy of the packed state in the batch precision
+ * (float or double, see nsd_batch_device_state) to q_dst / u_dst (pinned host
+ * or device memory); either may be NULL. */
+int nsd_batch_copy_state_async(nsd_batch* b, void* q_dst, void* u_dst);
 int nsd_batch_info(const nsd_batch* b, int32_t* info /* [n_env, num_coord, num_dof, n_joints, max_rows, team_threads] */);
 int nsd_batch_destroy(nsd_batch* b);
 
@@ -187,6 +191,9 @@ int nsd_scene_shapes(const nsd_scene* s, nsd_shape* shapes, double* margin, doub
 int nsd_scene_state(const nsd_scene* s, double* q, double* u);
 int nsd_scene_config(const nsd_scene* s, nsd_config* cfg, double* h, double* gravity);
 int nsd_scene_destroy(nsd_scene* s);
+/* Initial states of n copies of a seeded builder (seed0 .. seed0+n-1), e.g. the
+ * per-environment C5 ants: q n*num_coord, u n*num_dof. */
+int nsd_scene_batch_state(const char* name, uint32_t seed0, int32_t n, double* q, double* u);
 
 #ifdef __cplusplus
 }

@@ -253,6 +253,13 @@ class Scene:
         self._h = None
 
 
+def batch_states(name: str, seed0: int, n: int, num_coord: int, num_dof: int):
+    """Initial states of n seeded copies of a builder (one C call)."""
+    q, u = np.zeros(n * num_coord), np.zeros(n * num_dof)
+    check(lib().nsd_scene_batch_state(name.encode(), seed0, n, _dp(q), _dp(u)))
+    return q, u
+
+
 class BatchSolver:
     """Many environments sharing one topology (nsd_batch_*): device narrow phase
     + Newton step per env, one team (warp or CTA) per environment."""
@@ -321,6 +328,10 @@ class BatchSolver:
         arr = (nsd_contact * max(n.value, 1))()
         check(lib().nsd_batch_contacts(self._h, env, C.cast(arr, C.POINTER(nsd_contact)), C.byref(n)))
         return contacts_to_arrays(arr, n.value)
+
+    def copy_state_async(self, q_ptr, u_ptr):
+        check(lib().nsd_batch_copy_state_async(self._h, C.c_void_p(q_ptr) if q_ptr else None,
+                                               C.c_void_p(u_ptr) if u_ptr else None))
 
     def device_state(self):
         q, u, dt = C.c_void_p(), C.c_void_p(), C.c_int32()

@@ -396,7 +396,7 @@ struct WorkPlan {
 
 // ================================================================== kernels
 template <class R>
-__global__ void __launch_bounds__(1024) k_single_block(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out) {
+__global__ void __launch_bounds__(512) k_single_block(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out) {
   __shared__ double red[2 * 33 * nsd::kRedMax];
   nsd::BlockTeam t(red);
   nsd::newton_setup(t, T, W);
@@ -849,6 +849,7 @@ struct BatchBase {
   virtual void results(int* nc, int* ab, double* fres, nsd_iter_stats* its) = 0;
   virtual void contacts(int env, nsd_contact* out, int* n) = 0;
   virtual void device_state(void** q, void** u, int* dtype) = 0;
+  virtual void copy_state_async(void* q, void* u) = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   int info[6] = {0, 0, 0, 0, 0, 0};
@@ -953,6 +954,10 @@ template <class R> struct Batch final : BatchBase {
     *u = us.p;
     *dtype = sizeof(R) == 8 ? 1 : 0;
   }
+  void copy_state_async(void* q, void* u) override {
+    if (q) NSD_CK(cudaMemcpyAsync(q, qs.p, sizeof(R) * (size_t)H.ncoord * n_env, cudaMemcpyDefault, stream));
+    if (u) NSD_CK(cudaMemcpyAsync(u, us.p, sizeof(R) * (size_t)H.ndof * n_env, cudaMemcpyDefault, stream));
+  }
   void step(const void* tq, int on_device, int dtype, double h, const double* g) override {
     if (!(h > 0.0)) throw NsdError(NSD_INVALID, "integrate_coordinates: h must be positive");
     BatchArgs<R> A{};
@@ -978,6 +983,7 @@ template <class R> struct Batch final : BatchBase {
         A.torque_double = dtype;
       } else {
         const size_t n = (size_t)H.nj * n_env;
+        NSD_CK(cudaStreamSynchronize(stream));  // staging buffer may still feed the previous copy
         stage.alloc(sizeof(double) * n);
         std::memcpy(stage.p, tq, sizeof(double) * n);
         torque.alloc(sizeof(double) * n);
@@ -1255,6 +1261,14 @@ int nsd_batch_device_state(nsd_batch* b, void** q_dev, void** u_dev, int32_t* dt
   return guarded([&] {
     if (!b || !q_dev || !u_dev || !dtype) throw NsdError(NSD_INVALID, "null argument");
     b->impl->device_state(q_dev, u_dev, dtype);
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_copy_state_async(nsd_batch* b, void* q_dst, void* u_dst) {
+  return guarded([&] {
+    if (!b) throw NsdError(NSD_INVALID, "null argument");
+    b->impl->copy_state_async(q_dst, u_dst);
     return NSD_OK;
   });
 }

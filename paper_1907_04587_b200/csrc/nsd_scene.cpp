@@ -705,4 +705,24 @@ int nsd_scene_destroy(nsd_scene* s) {
   return NSD_OK;
 }
 
+int nsd_scene_batch_state(const char* name, uint32_t seed0, int32_t n, double* q, double* u) {
+  if (!name || n < 0 || !q || !u) return NSD_INVALID;
+  try {
+    size_t oq = 0, ou = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      bool ok = false;
+      nsdw::Scene s = nsdw::build(name, seed0 + static_cast<uint32_t>(i), &ok);
+      if (!ok) return NSD_INVALID;
+      const nsdw::World w = nsdw::build_world(s);
+      std::memcpy(q + oq, w.q.data(), sizeof(double) * w.q.size());
+      std::memcpy(u + ou, w.u.data(), sizeof(double) * w.u.size());
+      oq += w.q.size();
+      ou += w.u.size();
+    }
+    return NSD_OK;
+  } catch (...) {
+    return NSD_INVALID;
+  }
+}
+
 }  // extern "C"
