@@ -289,105 +289,134 @@ template <class R> struct DevTopo {
   }
 };
 
-// Offsets (in elements) of one scene's Work arrays inside an R arena and an
-// int arena. Used for the single scene (one instance) and per env (strided).
+// Offsets (in elements) of one scene's Work arrays. "Hot" arrays are touched
+// every PCR iteration and live in shared memory for the warp-per-env batched
+// kernel (global memory otherwise); "cold" arrays stay in global memory.
 struct WorkPlan {
-  // R arrays
-  size_t q, q0, qp, u, u0, ut, g, gp, up, shift, hinv, w, du, ub, fx, iw6, iwi6, coeff, hv, cd, lam, x, xn, r, rn, z,
-      zn, p, ap, az, inv, bx, ctet, cgeo, strideR;
-  // int arrays
-  size_t blk, cbody, cfeat, cinc_off, cinc_ent, cinc_cnt, strideI;
-  void plan(const HostTopo& T, int ccap) {
-    const size_t rcap = T.rows_static + 3 * static_cast<size_t>(ccap);
+  // hot R
+  size_t q, u, g, w, du, hinv, iwi6, coeff, hv, cd, lam, x, r, z, p, ap, az, inv, bx, cdir, carm, cscale, hotR;
+  // hot int
+  size_t blk, cbody, cinc_off, cinc_ent, hotI;
+  // cold R
+  size_t q0, u0, qp, ut, iw6, gp, up, shift, ub, fx, ctet, xn, rn, zn, cgeo, xlam, coldR;
+  // cold int
+  size_t cfeat, cinc_cnt, xcbody, coldI;
+  size_t hot_bytes_f, hot_bytes_d;  // bytes of the hot set per env for float / double
+  int rcap = 0, ccap = 0;
+
+  void plan(const HostTopo& T, int cc) {
+    ccap = cc;
+    rcap = T.rows_static + 3 * cc;
+    const size_t rs = T.rows_static, rc = rcap, c = cc;
     size_t o = 0;
     auto a = [&](size_t n) {
       const size_t off = o;
-      o += (n + 31) & ~size_t(31);  // 32-element alignment inside an env slice
+      o += (n + 1) & ~size_t(1);  // keep 8-byte alignment for doubles
       return off;
     };
     q = a(T.ncoord);
-    q0 = a(T.ncoord);
-    qp = a(T.ncoord);
     u = a(T.ndof);
-    u0 = a(T.ndof);
-    ut = a(T.ndof);
     g = a(T.ndof);
+    w = a(T.ndof);
+    du = a(T.ndof);
+    hinv = a(T.ndof);
+    iwi6 = a(6 * T.nd3);
+    coeff = a(12 * rs);
+    hv = a(rc);
+    cd = a(rc);
+    lam = a(rc);
+    x = a(rc);
+    r = a(rc);
+    z = a(rc);
+    p = a(rc);
+    ap = a(rc);
+    az = a(rc);
+    inv = a(rc);
+    bx = a(rc);
+    cdir = a(9 * c);
+    carm = a(6 * c);
+    cscale = a(2 * c);
+    hotR = o;
+    o = 0;
+    blk = a(4 * rs);
+    cbody = a(2 * c);
+    cinc_off = a(T.nd3 + 1);
+    cinc_ent = a(4 * c);
+    hotI = o;
+    o = 0;
+    q0 = a(T.ncoord);
+    u0 = a(T.ndof);
+    qp = a(T.ncoord);
+    ut = a(T.ndof);
+    iw6 = a(6 * T.nd3);
     gp = a(T.ndof);
     up = a(T.ndof);
     shift = a(T.ndof);
-    hinv = a(T.ndof);
-    w = a(T.ndof);
-    du = a(T.ndof);
     ub = a(T.ndof);
     fx = a(T.ndof);
-    iw6 = a(6 * T.nd3);
-    iwi6 = a(6 * T.nd3);
-    coeff = a(12 * rcap);
-    hv = a(rcap);
-    cd = a(rcap);
-    lam = a(rcap);
-    x = a(rcap);
-    xn = a(rcap);
-    r = a(rcap);
-    rn = a(rcap);
-    z = a(rcap);
-    zn = a(rcap);
-    p = a(rcap);
-    ap = a(rcap);
-    az = a(rcap);
-    inv = a(rcap);
-    bx = a(rcap);
     ctet = a(9 * static_cast<size_t>(T.nt));
-    cgeo = a(17 * static_cast<size_t>(ccap));
-    strideR = o;
+    xn = a(rc);
+    rn = a(rc);
+    zn = a(rc);
+    cgeo = a(17 * c);
+    xlam = a(rc);
+    coldR = o;
     o = 0;
-    blk = a(4 * rcap);
-    cbody = a(2 * static_cast<size_t>(ccap));
-    cfeat = a(ccap);
-    cinc_off = a(T.nd3 + 1);
-    cinc_ent = a(4 * static_cast<size_t>(ccap));
+    cfeat = a(c);
     cinc_cnt = a(T.nd3 + 1);
-    strideI = o;
+    xcbody = a(2 * c);
+    coldI = o;
+    hot_bytes_f = ((hotR * 4 + 15) & ~size_t(15)) + hotI * 4;
+    hot_bytes_d = ((hotR * 8 + 15) & ~size_t(15)) + hotI * 4;
+    hot_bytes_f = (hot_bytes_f + 15) & ~size_t(15);
+    hot_bytes_d = (hot_bytes_d + 15) & ~size_t(15);
   }
-  template <class R> __host__ __device__ nsd::Work<R> bind(R* rb, int* ib) const {
+  template <class R> size_t hot_bytes() const { return sizeof(R) == 8 ? hot_bytes_d : hot_bytes_f; }
+  template <class R> __host__ __device__ int* hot_ints(R* hr) const {
+    return reinterpret_cast<int*>(reinterpret_cast<char*>(hr) + ((hotR * sizeof(R) + 15) & ~size_t(15)));
+  }
+  template <class R> __host__ __device__ nsd::Work<R> bind(R* hr, int* hi, R* cr, int* ci) const {
     nsd::Work<R> W{};
-    W.q = rb + q;
-    W.q0 = rb + q0;
-    W.qp = rb + qp;
-    W.u = rb + u;
-    W.u0 = rb + u0;
-    W.ut = rb + ut;
-    W.g = rb + g;
-    W.gp = rb + gp;
-    W.up = rb + up;
-    W.shift = rb + shift;
-    W.hinv = rb + hinv;
-    W.w = rb + w;
-    W.du = rb + du;
-    W.ub = rb + ub;
-    W.iw6 = rb + iw6;
-    W.iwi6 = rb + iwi6;
-    W.coeff = rb + coeff;
-    W.hv = rb + hv;
-    W.cd = rb + cd;
-    W.lam = rb + lam;
-    W.x = rb + x;
-    W.xn = rb + xn;
-    W.r = rb + r;
-    W.rn = rb + rn;
-    W.z = rb + z;
-    W.zn = rb + zn;
-    W.p = rb + p;
-    W.ap = rb + ap;
-    W.az = rb + az;
-    W.inv = rb + inv;
-    W.bx = rb + bx;
-    W.ctet = rb + ctet;
-    W.cgeo = rb + cgeo;
-    W.blk = ib + blk;
-    W.cbody = ib + cbody;
-    W.cinc_off = ib + cinc_off;
-    W.cinc_ent = ib + cinc_ent;
+    W.q = hr + q;
+    W.u = hr + u;
+    W.ut = cr + ut;
+    W.g = hr + g;
+    W.w = hr + w;
+    W.du = hr + du;
+    W.hinv = hr + hinv;
+    W.iw6 = cr + iw6;
+    W.iwi6 = hr + iwi6;
+    W.coeff = hr + coeff;
+    W.hv = hr + hv;
+    W.cd = hr + cd;
+    W.lam = hr + lam;
+    W.x = hr + x;
+    W.xn = cr + xn;
+    W.r = hr + r;
+    W.rn = cr + rn;
+    W.z = hr + z;
+    W.zn = cr + zn;
+    W.p = hr + p;
+    W.ap = hr + ap;
+    W.az = hr + az;
+    W.inv = hr + inv;
+    W.bx = hr + bx;
+    W.cgeo = cr + cgeo;
+    W.cdir = hr + cdir;
+    W.carm = hr + carm;
+    W.cscale = hr + cscale;
+    W.blk = hi + blk;
+    W.cbody = hi + cbody;
+    W.cinc_off = hi + cinc_off;
+    W.cinc_ent = hi + cinc_ent;
+    W.q0 = cr + q0;
+    W.u0 = cr + u0;
+    W.qp = cr + qp;
+    W.gp = cr + gp;
+    W.up = cr + up;
+    W.shift = cr + shift;
+    W.ub = cr + ub;
+    W.ctet = cr + ctet;
     return W;
   }
 };
@@ -395,31 +424,30 @@ struct WorkPlan {
 }  // namespace
 
 // ================================================================== kernels
-template <class R>
+template <class R, bool kTets>
 __global__ void __launch_bounds__(512) k_single_block(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out) {
   __shared__ double red[2 * 33 * nsd::kRedMax];
   nsd::BlockTeam t(red);
   nsd::newton_setup(t, T, W);
   t.sync();
-  nsd::newton_solve(t, T, W, cfg, out);
+  nsd::newton_solve<R, kTets>(t, T, W, cfg, out);
 }
 
-template <class R>
+template <class R, bool kTets>
 __global__ void __launch_bounds__(256) k_single_grid(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out,
                                                      double* gpart) {
   __shared__ double red[2 * 33 * nsd::kRedMax];
   nsd::GridTeam t(red, gpart);
   nsd::newton_setup(t, T, W);
   t.sync();
-  nsd::newton_solve(t, T, W, cfg, out);
+  nsd::newton_solve<R, kTets>(t, T, W, cfg, out);
 }
-
 
 // ------------------------------------------------------------------ batched
 template <class R> struct BatchArgs {
   nsd::Topo<R> T;
   nsd::Cfg cfg;
-  int n_env, ns, npairs, maxc;
+  int n_env, ns, npairs, maxc, envs_per_block, hot_in_smem;
   const int2* pairs;
   const nsd::ShapeD<R>* shapes;
   const R* jframe;
@@ -428,9 +456,10 @@ template <class R> struct BatchArgs {
   R* us;
   const void* torque;  // n_env * nj or null
   int torque_double;
-  R* rbase;
-  int* ibase;
-  size_t strideR, strideI;
+  char* hot_global;  // per-env hot slices when not in shared memory
+  size_t hot_bytes;
+  R* cold_r;
+  int* cold_i;
   WorkPlan plan;
   nsd::CandD<R>* cand;  // n_env * npairs * 4
   int* pair_cnt;        // n_env * npairs
@@ -442,11 +471,14 @@ template <class R> struct BatchArgs {
 
 // One environment: extension forces, setup, device narrow phase, contact
 // incidence, Newton solve, state write-back (step_world, scene.cpp:709-732).
-template <class R, class Team> __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env) {
+template <class R, class Team>
+__device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr) {
   const nsd::Topo<R>& T = A.T;
-  R* rb = A.rbase + (size_t)env * A.strideR;
-  int* ib = A.ibase + (size_t)env * A.strideI;
-  nsd::Work<R> W = A.plan.template bind<R>(rb, ib);
+  const WorkPlan& P = A.plan;
+  int* hi = P.hot_ints(hr);
+  R* cr = A.cold_r + (size_t)env * P.coldR;
+  int* ci = A.cold_i + (size_t)env * P.coldI;
+  nsd::Work<R> W = P.template bind<R>(hr, hi, cr, ci);
   W.jframe = A.jframe;
   W.h = A.h;
   W.grav[0] = A.grav[0];
@@ -454,13 +486,13 @@ template <class R, class Team> __device__ void batch_env(Team& t, const BatchArg
   W.grav[2] = A.grav[2];
   R* qs = A.qs + (size_t)env * T.ncoord;
   R* us = A.us + (size_t)env * T.ndof;
-  R* q0 = rb + A.plan.q0;
-  R* u0 = rb + A.plan.u0;
+  R* q0 = cr + P.q0;
+  R* u0 = cr + P.u0;
   for (int i = t.rank(); i < T.ncoord; i += t.size()) q0[i] = qs[i];
   for (int i = t.rank(); i < T.ndof; i += t.size()) u0[i] = us[i];
   W.f_extra = nullptr;
   if (A.torque) {
-    R* fx = rb + A.plan.fx;
+    R* fx = cr + P.fx;
     t.sync();
     // joint torques about revolute axes at q- (extension hook): +tau*axis on a, -tau*axis on b
     for (int b = t.rank(); b < T.nb; b += t.size()) {
@@ -501,21 +533,23 @@ template <class R, class Team> __device__ void batch_env(Team& t, const BatchArg
   int total = 0;
   for (int p = 0; p < A.npairs; ++p) total += cnt[p];
   const int nc = total < A.maxc ? total : A.maxc;
-  int* cbody = ib + A.plan.cbody;
-  int* cfeat = ib + A.plan.cfeat;
-  R* cgeo = rb + A.plan.cgeo;
+  int* cbody = hi + P.cbody;
+  int* cfeat = ci + P.cfeat;
+  R* cgeo = cr + P.cgeo;
   // canonical (a.body, b.body, feature) order, stable in generation order
   for (int p = t.rank(); p < A.npairs; p += t.size()) {
     for (int k = 0; k < cnt[p]; ++k) {
-      const nsd::CandD<R>& c = cand[4 * p + k];
+      const nsd::CandD<R> c = cand[4 * p + k];
       int rank = 0;
-      for (int p2 = 0; p2 < A.npairs; ++p2)
-        for (int k2 = 0; k2 < cnt[p2]; ++k2) {
+      for (int p2 = 0; p2 < A.npairs; ++p2) {
+        const int n2 = cnt[p2];
+        for (int k2 = 0; k2 < n2; ++k2) {
           const nsd::CandD<R>& o = cand[4 * p2 + k2];
           if (nsd::canonical_less(o.a, o.b, o.feature, c.a, c.b, c.feature) ||
               (o.a == c.a && o.b == c.b && o.feature == c.feature && (p2 < p || (p2 == p && k2 < k))))
             ++rank;
         }
+      }
       if (rank >= nc) continue;
       cbody[2 * rank] = c.a;
       cbody[2 * rank + 1] = c.b;
@@ -540,17 +574,15 @@ template <class R, class Team> __device__ void batch_env(Team& t, const BatchArg
   W.friction_begin = T.rows_static + nc;
   W.nrows = T.rows_static + 3 * nc;
   // ---- contact incidence per dof3 block (contact*4 + slot, contacts ascending)
-  int* coff = ib + A.plan.cinc_off;
-  int* cent = ib + A.plan.cinc_ent;
-  int* ccnt = ib + A.plan.cinc_cnt;
+  int* coff = hi + P.cinc_off;
+  int* cent = hi + P.cinc_ent;
+  int* ccnt = ci + P.cinc_cnt;
   for (int b = t.rank(); b < T.nd3; b += t.size()) {
     int n = 0;
     for (int c = 0; c < nc; ++c) {
       int al, aa, bl, ba;
       nsd::body_blocks(T, cbody[2 * c], al, aa);
       nsd::body_blocks(T, cbody[2 * c + 1], bl, ba);
-      if (bl >= 0 && bl == al) bl = -1;
-      if (ba >= 0 && ba == aa) ba = -1;
       n += (al == b) + (aa == b) + (bl == b) + (ba == b);
     }
     ccnt[b] = n;
@@ -571,8 +603,6 @@ template <class R, class Team> __device__ void batch_env(Team& t, const BatchArg
       int b4[4];
       nsd::body_blocks(T, cbody[2 * c], b4[0], b4[1]);
       nsd::body_blocks(T, cbody[2 * c + 1], b4[2], b4[3]);
-      if (b4[2] >= 0 && b4[2] == b4[0]) b4[2] = -1;
-      if (b4[3] >= 0 && b4[3] == b4[1]) b4[3] = -1;
       for (int s = 0; s < 4; ++s)
         if (b4[s] == b) cent[o++] = 4 * c + s;
     }
@@ -581,27 +611,41 @@ template <class R, class Team> __device__ void batch_env(Team& t, const BatchArg
   nsd::StepOut out{};
   out.iters = A.iters ? A.iters + (size_t)env * A.cfg.newton_iterations : nullptr;
   out.fin = A.fin + (size_t)env * 8;
-  nsd::newton_solve(t, T, W, A.cfg, out);
+  nsd::newton_solve<R, false>(t, T, W, A.cfg, out);
   t.sync();
   for (int i = t.rank(); i < T.ncoord; i += t.size()) qs[i] = W.q[i];
   for (int i = t.rank(); i < T.ndof; i += t.size()) us[i] = W.u[i];
+  // export the step's contact set and multipliers (nsd_batch_contacts)
+  R* xl = cr + P.xlam;
+  int* xb = ci + P.xcbody;
+  for (int i = t.rank(); i < W.nrows; i += t.size()) xl[i] = W.lam[i];
+  for (int i = t.rank(); i < 2 * nc; i += t.size()) xb[i] = cbody[i];
   if (t.rank() == 0) {
     A.nc_out[env] = nc;
     A.overflow[env] = total > A.maxc ? total : 0;
   }
 }
 
+// Warp per environment; the env's hot working set in shared memory.
 template <class R> __global__ void __launch_bounds__(128) k_batch_warp(BatchArgs<R> A) {
-  const int env = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int wib = threadIdx.x >> 5;
+  const int env = blockIdx.x * A.envs_per_block + wib;
   if (env >= A.n_env) return;  // warp-uniform
+  R* hr = A.hot_in_smem ? reinterpret_cast<R*>(smem + (size_t)wib * A.hot_bytes)
+                        : reinterpret_cast<R*>(A.hot_global + (size_t)env * A.hot_bytes);
   nsd::WarpTeam t(threadIdx.x & 31);
-  batch_env(t, A, env);
+  batch_env(t, A, env, hr);
 }
 
+// CTA per environment.
 template <class R> __global__ void __launch_bounds__(256) k_batch_block(BatchArgs<R> A) {
+  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[2 * 33 * nsd::kRedMax];
   nsd::BlockTeam t(red);
-  batch_env(t, A, blockIdx.x);
+  R* hr = A.hot_in_smem ? reinterpret_cast<R*>(smem)
+                        : reinterpret_cast<R*>(A.hot_global + (size_t)blockIdx.x * A.hot_bytes);
+  batch_env(t, A, blockIdx.x, hr);
 }
 
 // ================================================================== handles
@@ -618,18 +662,20 @@ template <class R> struct Solver final : SolverBase {
   nsd_config cfg;
   int ccap = 0;
   WorkPlan plan;
-  DBuf rarena, iarena, outbuf, gpart;
+  DBuf hotr, hoti, coldr, coldi, outbuf, gpart;
   HBuf stage_r, stage_i, stage_o;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int grid_blocks = 0;
   bool use_grid = false;
+  bool tets = false;
   int block_threads = 256;
 
   Solver(const nsd_topology& tp, const nsd_config& c, int device) : cfg(c) {
     NSD_CK(cudaSetDevice(device));
     H = preprocess(tp);
     topo.upload(H);
+    tets = H.nt > 0;
     NSD_CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     NSD_CK(cudaEventCreate(&ev0));
     NSD_CK(cudaEventCreate(&ev1));
@@ -642,7 +688,10 @@ template <class R> struct Solver final : SolverBase {
       use_grid = true;
       int dev_sms = 0, per_sm = 0;
       NSD_CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
-      NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R>, 256, 0));
+      if (tets)
+        NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, true>, 256, 0));
+      else
+        NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, false>, 256, 0));
       if (per_sm < 1) throw NsdError(NSD_CUDA_ERROR, "grid kernel cannot be resident");
       grid_blocks = dev_sms * std::min(per_sm, 2);
       gpart.alloc(sizeof(double) * 2 * grid_blocks * nsd::kRedMax);
@@ -655,11 +704,12 @@ template <class R> struct Solver final : SolverBase {
   }
   void set_cfg(const nsd_config& c) override { cfg = c; }
   void ensure(int nc) {
-    if (nc <= ccap && rarena.p) return;
+    if (nc <= ccap && hotr.p) return;
     ccap = std::max(nc, std::max(16, ccap * 2));
     plan.plan(H, ccap);
-    rarena.alloc(sizeof(R) * plan.strideR);
-    iarena.alloc(sizeof(int) * plan.strideI);
+    hotr.alloc(plan.hot_bytes<R>());
+    coldr.alloc(sizeof(R) * plan.coldR);
+    coldi.alloc(sizeof(int) * plan.coldI);
   }
 
   int step(const nsd_step_in* in, nsd_step_out* out) override {
@@ -675,7 +725,7 @@ template <class R> struct Solver final : SolverBase {
     ensure(nc);
     const int N = cfg.newton_iterations, ml = cfg.linear_max_iterations;
     const int nrows = H.rows_static + 3 * nc;
-    // ---- stage inputs: q0, u0, f_extra(fx), cgeo, jframe (R); cbody, cinc (int)
+    // ---- stage inputs: q0, u0, f_extra (cold); cgeo (hot); joint frames (topology)
     const size_t nR = (size_t)H.ncoord + H.ndof + H.ndof + 17 * (size_t)nc + 21 * (size_t)H.nj;
     stage_r.alloc(sizeof(R) * nR);
     R* sr = static_cast<R*>(stage_r.p);
@@ -703,8 +753,6 @@ template <class R> struct Solver final : SolverBase {
       int* b4 = &b4all[4 * c];
       body_blocks_h(H, in->contacts[c].body_a, b4[0], b4[1]);
       body_blocks_h(H, in->contacts[c].body_b, b4[2], b4[3]);
-      if (b4[2] >= 0 && b4[2] == b4[0]) b4[2] = -1;
-      if (b4[3] >= 0 && b4[3] == b4[1]) b4[3] = -1;
       for (int s = 0; s < 4; ++s)
         if (b4[s] >= 0) cnt[b4[s] + 1]++;
     }
@@ -727,24 +775,23 @@ template <class R> struct Solver final : SolverBase {
           if (b >= 0) sent[fillp[b]++] = 4 * c + s;
         }
     }
-    R* rb = rarena.as<R>();
-    int* ib = iarena.as<int>();
-    R* q0 = rb + plan.q0;
-    R* u0 = rb + plan.u0;
-    R* fx = rb + plan.fx;
-    R* cgeo = rb + plan.cgeo;
-    NSD_CK(cudaMemcpyAsync(q0, sr, sizeof(R) * H.ncoord, cudaMemcpyHostToDevice, stream));
-    NSD_CK(cudaMemcpyAsync(u0, sr + H.ncoord, sizeof(R) * H.ndof, cudaMemcpyHostToDevice, stream));
-    NSD_CK(cudaMemcpyAsync(fx, sr + H.ncoord + H.ndof, sizeof(R) * H.ndof, cudaMemcpyHostToDevice, stream));
+    R* hr = hotr.as<R>();
+    int* hi = plan.hot_ints(hr);
+    R* cr = coldr.as<R>();
+    int* ci = coldi.as<int>();
+    NSD_CK(cudaMemcpyAsync(cr + plan.q0, sr, sizeof(R) * H.ncoord, cudaMemcpyHostToDevice, stream));
+    NSD_CK(cudaMemcpyAsync(cr + plan.u0, sr + H.ncoord, sizeof(R) * H.ndof, cudaMemcpyHostToDevice, stream));
+    NSD_CK(cudaMemcpyAsync(cr + plan.fx, sr + H.ncoord + H.ndof, sizeof(R) * H.ndof, cudaMemcpyHostToDevice, stream));
     if (nc)
-      NSD_CK(cudaMemcpyAsync(cgeo, sr + H.ncoord + 2 * H.ndof, sizeof(R) * 17 * nc, cudaMemcpyHostToDevice, stream));
+      NSD_CK(cudaMemcpyAsync(cr + plan.cgeo, sr + H.ncoord + 2 * H.ndof, sizeof(R) * 17 * nc, cudaMemcpyHostToDevice,
+                             stream));
     if (H.nj)
       NSD_CK(cudaMemcpyAsync(topo.jframe, sr + H.ncoord + 2 * H.ndof + 17 * nc, sizeof(R) * 21 * H.nj,
                              cudaMemcpyHostToDevice, stream));
-    if (nc) NSD_CK(cudaMemcpyAsync(ib + plan.cbody, si, sizeof(int) * 2 * nc, cudaMemcpyHostToDevice, stream));
-    NSD_CK(cudaMemcpyAsync(ib + plan.cinc_off, soff, sizeof(int) * (H.nd3 + 1), cudaMemcpyHostToDevice, stream));
+    if (nc) NSD_CK(cudaMemcpyAsync(hi + plan.cbody, si, sizeof(int) * 2 * nc, cudaMemcpyHostToDevice, stream));
+    NSD_CK(cudaMemcpyAsync(hi + plan.cinc_off, soff, sizeof(int) * (H.nd3 + 1), cudaMemcpyHostToDevice, stream));
     if (nc)
-      NSD_CK(cudaMemcpyAsync(ib + plan.cinc_ent, sent, sizeof(int) * cnt[H.nd3], cudaMemcpyHostToDevice, stream));
+      NSD_CK(cudaMemcpyAsync(hi + plan.cinc_ent, sent, sizeof(int) * cnt[H.nd3], cudaMemcpyHostToDevice, stream));
     // ---- outputs
     Layout L;
     const size_t o_it = L.add<nsd::IterOut>(N), o_hist = L.add<double>((size_t)N * (ml + 1)),
@@ -758,9 +805,9 @@ template <class R> struct Solver final : SolverBase {
     so.hist_len = reinterpret_cast<int*>(ob + o_hl);
     so.tel = reinterpret_cast<double*>(ob + o_tel);
     so.fin = reinterpret_cast<double*>(ob + o_fin);
-    nsd::Work<R> W = plan.bind<R>(rb, ib);
+    nsd::Work<R> W = plan.bind<R>(hr, hi, cr, ci);
     W.jframe = topo.jframe;
-    W.f_extra = in->f_extra ? fx : nullptr;
+    W.f_extra = in->f_extra ? cr + plan.fx : nullptr;
     W.h = R(in->h);
     for (int k = 0; k < 3; ++k) W.grav[k] = R(in->gravity[k]);
     W.nc = nc;
@@ -770,12 +817,16 @@ template <class R> struct Solver final : SolverBase {
     nsd::Cfg kc = to_cfg(cfg);
     NSD_CK(cudaEventRecord(ev0, stream));
     if (!use_grid) {
-      k_single_block<R><<<1, block_threads, 0, stream>>>(topo.t, W, kc, so);
+      if (tets)
+        k_single_block<R, true><<<1, block_threads, 0, stream>>>(topo.t, W, kc, so);
+      else
+        k_single_block<R, false><<<1, block_threads, 0, stream>>>(topo.t, W, kc, so);
       NSD_CK(cudaGetLastError());
     } else {
       double* gp = gpart.as<double>();
       void* args[] = {&topo.t, &W, &kc, &so, &gp};
-      NSD_CK(cudaLaunchCooperativeKernel((void*)k_single_grid<R>, dim3(grid_blocks), dim3(256), args, 0, stream));
+      void* fn = tets ? (void*)k_single_grid<R, true> : (void*)k_single_grid<R, false>;
+      NSD_CK(cudaLaunchCooperativeKernel(fn, dim3(grid_blocks), dim3(256), args, 0, stream));
     }
     NSD_CK(cudaEventRecord(ev1, stream));
     // ---- download
@@ -785,9 +836,9 @@ template <class R> struct Solver final : SolverBase {
     R* hq = reinterpret_cast<R*>(ho + L.bytes);
     R* hu = hq + H.ncoord;
     R* hl = hu + H.ndof;
-    NSD_CK(cudaMemcpyAsync(hq, rb + plan.q, sizeof(R) * H.ncoord, cudaMemcpyDeviceToHost, stream));
-    NSD_CK(cudaMemcpyAsync(hu, rb + plan.u, sizeof(R) * H.ndof, cudaMemcpyDeviceToHost, stream));
-    if (nrows) NSD_CK(cudaMemcpyAsync(hl, rb + plan.lam, sizeof(R) * nrows, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(hq, hr + plan.q, sizeof(R) * H.ncoord, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(hu, hr + plan.u, sizeof(R) * H.ndof, cudaMemcpyDeviceToHost, stream));
+    if (nrows) NSD_CK(cudaMemcpyAsync(hl, hr + plan.lam, sizeof(R) * nrows, cudaMemcpyDeviceToHost, stream));
     NSD_CK(cudaStreamSynchronize(stream));
     float ms = 0.f;
     NSD_CK(cudaEventElapsedTime(&ms, ev0, ev1));
@@ -861,10 +912,13 @@ template <class R> struct Batch final : BatchBase {
   nsd_config cfg;
   int n_env, maxc, ns, npairs;
   WorkPlan plan;
-  DBuf rarena, iarena, shapes, pairs, cand, paircnt, ncout, ovf, fin, iters, qs, us, torque;
+  DBuf hotg, coldr, coldi, shapes, pairs, cand, paircnt, ncout, ovf, fin, iters, qs, us, torque;
   HBuf stage;
   double margin, mu_default;
   int team_threads = 32;  // 32: warp per env; >32: CTA per env
+  int envs_per_block = 4;
+  bool hot_in_smem = true;
+  size_t smem_bytes = 0;
   std::vector<nsd::ShapeD<R>> hshapes;
 
   Batch(const nsd_topology& tp, int n_shapes, const nsd_shape* sh, double mg, double mud, const nsd_config& c,
@@ -873,6 +927,7 @@ template <class R> struct Batch final : BatchBase {
     NSD_CK(cudaSetDevice(device));
     if (nenv < 1 || mc < 1 || n_shapes < 0) throw NsdError(NSD_INVALID, "bad batch sizes");
     H = preprocess(tp);
+    if (H.nt > 0) throw NsdError(NSD_UNSUPPORTED, "batched path: tetrahedral meshes run through nsd_step");
     topo.upload(H);
     for (int i = 0; i < ns; ++i) {
       nsd::ShapeD<R> s{};
@@ -898,10 +953,34 @@ template <class R> struct Batch final : BatchBase {
     if (ns) NSD_CK(cudaMemcpy(shapes.p, hshapes.data(), sizeof(nsd::ShapeD<R>) * ns, cudaMemcpyHostToDevice));
     if (npairs) NSD_CK(cudaMemcpy(pairs.p, hp.data(), sizeof(int2) * npairs, cudaMemcpyHostToDevice));
     plan.plan(H, maxc);
-    rarena.alloc(sizeof(R) * plan.strideR * n_env);
-    iarena.alloc(sizeof(int) * plan.strideI * n_env);
-    NSD_CK(cudaMemset(rarena.p, 0, sizeof(R) * plan.strideR * n_env));
-    NSD_CK(cudaMemset(iarena.p, 0, sizeof(int) * plan.strideI * n_env));
+    const char* env_team = std::getenv("NSD_BATCH_TEAM");
+    if (env_team) team_threads = std::max(32, std::atoi(env_team));
+    const char* env_epb = std::getenv("NSD_ENVS_PER_BLOCK");
+    if (env_epb) envs_per_block = std::max(1, std::atoi(env_epb));
+    const char* env_smem = std::getenv("NSD_HOT_SMEM");
+    if (env_smem) hot_in_smem = std::atoi(env_smem) != 0;
+    const size_t hb = plan.hot_bytes<R>();
+    int max_optin = 0;
+    NSD_CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    if (team_threads == 32) {
+      envs_per_block = std::min(envs_per_block, 4);
+      while (envs_per_block > 1 && hb * envs_per_block > (size_t)max_optin) --envs_per_block;
+      smem_bytes = hb * envs_per_block;
+    } else {
+      smem_bytes = hb;
+    }
+    if (smem_bytes > (size_t)max_optin) hot_in_smem = false;
+    if (!hot_in_smem) {
+      smem_bytes = 0;
+      hotg.alloc(hb * n_env);
+    } else {
+      NSD_CK(cudaFuncSetAttribute(k_batch_warp<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+      NSD_CK(cudaFuncSetAttribute(k_batch_block<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+    }
+    coldr.alloc(sizeof(R) * plan.coldR * n_env);
+    coldi.alloc(sizeof(int) * plan.coldI * n_env);
+    NSD_CK(cudaMemset(coldr.p, 0, sizeof(R) * plan.coldR * n_env));
+    NSD_CK(cudaMemset(coldi.p, 0, sizeof(int) * plan.coldI * n_env));
     cand.alloc(sizeof(nsd::CandD<R>) * (size_t)std::max(npairs, 1) * 4 * n_env);
     paircnt.alloc(sizeof(int) * (size_t)std::max(npairs, 1) * n_env);
     ncout.alloc(sizeof(int) * n_env);
@@ -910,13 +989,11 @@ template <class R> struct Batch final : BatchBase {
     iters.alloc(sizeof(nsd::IterOut) * (size_t)std::max(cfg.newton_iterations, 1) * n_env);
     qs.alloc(sizeof(R) * (size_t)H.ncoord * n_env);
     us.alloc(sizeof(R) * (size_t)H.ndof * n_env);
-    torque.alloc(sizeof(R) * (size_t)std::max(H.nj, 1) * n_env);
+    torque.alloc(sizeof(double) * (size_t)std::max(H.nj, 1) * n_env);
     NSD_CK(cudaMemset(ncout.p, 0, sizeof(int) * n_env));
     NSD_CK(cudaMemset(ovf.p, 0, sizeof(int) * n_env));
     NSD_CK(cudaMemset(fin.p, 0, sizeof(double) * 8 * n_env));
     NSD_CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    const char* env_team = std::getenv("NSD_BATCH_TEAM");
-    if (env_team) team_threads = std::max(32, std::atoi(env_team));
     info[0] = n_env;
     info[1] = H.ncoord;
     info[2] = H.ndof;
@@ -929,6 +1006,7 @@ template <class R> struct Batch final : BatchBase {
   }
   void set_state(const double* q, const double* u) override {
     const size_t nq = (size_t)H.ncoord * n_env, nu = (size_t)H.ndof * n_env;
+    NSD_CK(cudaStreamSynchronize(stream));
     stage.alloc(sizeof(R) * (nq + nu));
     R* s = static_cast<R*>(stage.p);
     for (size_t i = 0; i < nq; ++i) s[i] = R(q[i]);
@@ -939,6 +1017,7 @@ template <class R> struct Batch final : BatchBase {
   }
   void get_state(double* q, double* u) override {
     const size_t nq = (size_t)H.ncoord * n_env, nu = (size_t)H.ndof * n_env;
+    NSD_CK(cudaStreamSynchronize(stream));
     stage.alloc(sizeof(R) * (nq + nu));
     R* s = static_cast<R*>(stage.p);
     NSD_CK(cudaMemcpyAsync(s, qs.p, sizeof(R) * nq, cudaMemcpyDeviceToHost, stream));
@@ -967,6 +1046,8 @@ template <class R> struct Batch final : BatchBase {
     A.ns = ns;
     A.npairs = npairs;
     A.maxc = maxc;
+    A.envs_per_block = team_threads == 32 ? envs_per_block : 1;
+    A.hot_in_smem = hot_in_smem ? 1 : 0;
     A.pairs = pairs.as<int2>();
     A.shapes = shapes.as<nsd::ShapeD<R>>();
     A.jframe = topo.jframe;
@@ -986,16 +1067,15 @@ template <class R> struct Batch final : BatchBase {
         NSD_CK(cudaStreamSynchronize(stream));  // staging buffer may still feed the previous copy
         stage.alloc(sizeof(double) * n);
         std::memcpy(stage.p, tq, sizeof(double) * n);
-        torque.alloc(sizeof(double) * n);
         NSD_CK(cudaMemcpyAsync(torque.p, stage.p, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
         A.torque = torque.p;
         A.torque_double = 1;
       }
     }
-    A.rbase = rarena.as<R>();
-    A.ibase = iarena.as<int>();
-    A.strideR = plan.strideR;
-    A.strideI = plan.strideI;
+    A.hot_global = hotg.as<char>();
+    A.hot_bytes = plan.hot_bytes<R>();
+    A.cold_r = coldr.as<R>();
+    A.cold_i = coldi.as<int>();
     A.plan = plan;
     A.cand = cand.as<nsd::CandD<R>>();
     A.pair_cnt = paircnt.as<int>();
@@ -1004,10 +1084,10 @@ template <class R> struct Batch final : BatchBase {
     A.fin = fin.as<double>();
     A.iters = iters.as<nsd::IterOut>();
     if (team_threads == 32) {
-      const int per_block = 4;
-      k_batch_warp<R><<<(n_env + per_block - 1) / per_block, 32 * per_block, 0, stream>>>(A);
+      const int epb = A.envs_per_block;
+      k_batch_warp<R><<<(n_env + epb - 1) / epb, 32 * epb, smem_bytes, stream>>>(A);
     } else {
-      k_batch_block<R><<<n_env, team_threads, 0, stream>>>(A);
+      k_batch_block<R><<<n_env, team_threads, smem_bytes, stream>>>(A);
     }
     NSD_CK(cudaGetLastError());
   }
@@ -1056,12 +1136,12 @@ template <class R> struct Batch final : BatchBase {
     if (!out || nc == 0) return;
     std::vector<int> cb(2 * nc), cf(nc);
     std::vector<R> cg(17 * (size_t)nc), lam(H.rows_static + 3 * (size_t)nc);
-    const R* rb = rarena.as<R>() + (size_t)env * plan.strideR;
-    const int* ib = iarena.as<int>() + (size_t)env * plan.strideI;
-    NSD_CK(cudaMemcpyAsync(cb.data(), ib + plan.cbody, sizeof(int) * 2 * nc, cudaMemcpyDeviceToHost, stream));
-    NSD_CK(cudaMemcpyAsync(cf.data(), ib + plan.cfeat, sizeof(int) * nc, cudaMemcpyDeviceToHost, stream));
-    NSD_CK(cudaMemcpyAsync(cg.data(), rb + plan.cgeo, sizeof(R) * 17 * nc, cudaMemcpyDeviceToHost, stream));
-    NSD_CK(cudaMemcpyAsync(lam.data(), rb + plan.lam, sizeof(R) * lam.size(), cudaMemcpyDeviceToHost, stream));
+    const R* cr = coldr.as<R>() + (size_t)env * plan.coldR;
+    const int* ci = coldi.as<int>() + (size_t)env * plan.coldI;
+    NSD_CK(cudaMemcpyAsync(cb.data(), ci + plan.xcbody, sizeof(int) * 2 * nc, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(cf.data(), ci + plan.cfeat, sizeof(int) * nc, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(cg.data(), cr + plan.cgeo, sizeof(R) * 17 * nc, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(lam.data(), cr + plan.xlam, sizeof(R) * lam.size(), cudaMemcpyDeviceToHost, stream));
     NSD_CK(cudaStreamSynchronize(stream));
     for (int c = 0; c < nc; ++c) {
       nsd_contact& k = out[c];

@@ -4,25 +4,34 @@
 // written against a Team (nsd_team.cuh) so the same code runs as
 //   * a cooperative persistent grid for one large scene (C2/C4 FEM scenes),
 //   * one CTA for one small scene (C1/C3), and
-//   * one warp or CTA per environment for the batched RL path (C5).
+//   * one warp per environment for the batched RL path (C5), with the
+//     environment's working set in shared memory.
 //
-// Data layout (all int32 ids; R = float or double):
+// Data layout (int32 ids; R = float or double):
 //   rows      fixed layout of make_layout (newton.cpp:18-41):
 //             [joints 3/5/5/2 | tets 3 each | contact normals | friction pairs]
-//   J         coeff[12*row]: four 3-wide slots; blk[4*row]: the "dof3 block"
-//             (dof/3) each slot acts on, -1 if unused. A rigid body owns two
-//             blocks (linear, angular), a particle one. <=12 nnz per row.
+//   J, static rows (joints, tets): coeff[12*row] = four 3-wide slots, blk[4*row]
+//             = the dof3 block (dof/3) of each slot, -1 if unused. A rigid body
+//             owns two blocks (linear, angular), a particle one. <= 12 nnz/row.
+//   J, contact rows: structured. Per contact the world lever arms (carm) and
+//             the NCP scale dc = dphi/dC and friction-active flag (cscale);
+//             the three rows act through the relative contact-point velocity
+//             dv = (v_a + w_a x r_a) - (v_b + w_b x r_b): n.dv*dc, d1.dv, d2.dv.
+//             J^T of a contact is the force f = dc z_n n + z_1 d1 + z_2 d2
+//             applied as (f, r_a x f) / (-f, -r_b x f). Same values as the
+//             reference's 12-coefficient rows (constraints.cpp:56-91) in fewer
+//             loads.
 //   C         cd[row] for scalar rows; ctet[9*tet] for the 3x3 Neo-Hookean block.
 //   H^-1      hinv[dof] for linear blocks (1/(m+shift)), iwi6[6*blk] (I_w^-1,
 //             symmetric) for angular blocks.
-//   J^T pull  deterministic body-side gather over an incidence list per dof3
+//   J^T pull  deterministic body-side gather over incidence lists per dof3
 //             block (static joints+tets list, per-step contact list) — no
 //             atomics, fixed order, so results are run-to-run bitwise stable
 //             (SPEC.md:710 determinism).
 // The Schur complement S = J H^-1 J^T + C + eps I is never formed (the
-// reference builds it explicitly, newton.cpp:242-290): every PCR iteration
-// applies it matrix-free as one pull pass (w = H^-1 J^T z, dof-parallel) and one
-// gather pass (Az = J w + C z + eps z, row-parallel).
+// reference builds it explicitly, newton.cpp:242-290): each PCR iteration
+// applies it matrix-free as one pull pass (w = H^-1 J^T z, dof-parallel) and
+// one gather pass (Az = J w + C z + eps z, row-parallel).
 #pragma once
 
 #include "nsd_math.cuh"
@@ -75,8 +84,7 @@ template <class R> struct Topo {
   const int* sinc_ent;  // row*4 + slot, ascending rows within a block
 };
 
-// Per-scene (per-env) mutable state and scratch. All pointers are either
-// global memory (grid/batched-global) or shared memory (batched-smem).
+// Per-scene (per-env) mutable state and scratch (global or shared memory).
 template <class R> struct Work {
   // state
   R* q;         // ncoord, current iterate (in/out)
@@ -87,16 +95,19 @@ template <class R> struct Work {
   const R* f_extra;  // ndof or nullptr
   R h;
   R grav[3];
-  // contacts (SoA)
+  // contacts
   int nc;
-  const int* cbody;  // 2 per contact
-  const R* cgeo;     // 17 per contact: la3 lb3 n3 d1_3 d2_3 thickness mu
+  const int* cbody;     // 2 per contact
+  const R* cgeo;        // 17 per contact: la3 lb3 n3 d1_3 d2_3 thickness mu
+  R* cdir;              // 9 per contact: n, d1, d2 (hot copy for the operator)
+  R* carm;              // 6 per contact: world lever arms r_a, r_b (per assembly)
+  R* cscale;            // 2 per contact: dc = dphi/dC, friction active (0/1)
   const int* cinc_off;  // contact incidence per dof3 block (nd3 + 1)
   const int* cinc_ent;  // contact*4 + slot
   // rows
   int nrows, normal_begin, friction_begin;
-  R* coeff;  // 12 per row
-  int* blk;  // 4 per row
+  R* coeff;  // 12 per static row
+  int* blk;  // 4 per static row
   R* hv;
   R* cd;
   R* ctet;   // 9 per tet
@@ -116,12 +127,11 @@ struct IterOut {
 };
 
 struct StepOut {
-  IterOut* iters;     // newton_iterations (may be null)
-  double* hist;       // newton_iterations * (max_lin + 1) (may be null)
-  int* hist_len;      // newton_iterations (may be null)
-  double* tel;        // 6 per contact (may be null)
-  double* fin;        // 8: final_residual_inf, final_comp, final_cone, min_gap, min_diag_shift, aborted, converged, n_iterations
-  double* lam_out;    // rows (may be null) -- unused: lam stays in Work
+  IterOut* iters;  // newton_iterations (may be null)
+  double* hist;    // newton_iterations * (max_lin + 1) (may be null)
+  int* hist_len;   // newton_iterations (may be null)
+  double* tel;     // 6 per contact (may be null)
+  double* fin;     // 8: final_residual_inf, final_comp, final_cone, min_gap, min_diag_shift, aborted, converged, n_iterations
 };
 
 // ------------------------------------------------------------------ helpers
@@ -138,7 +148,6 @@ template <class R> __device__ __forceinline__ V3<R> sym_mul(const R* s6, V3<R> v
 }
 template <class R> __device__ __forceinline__ R sym_quad(const R* s6, V3<R> v) { return dot(v, sym_mul(s6, v)); }
 
-// Rotation of a body from its quaternion (identity for particles / world).
 template <class R> __device__ __forceinline__ M3<R> body_rot(const Topo<R>& T, const R* q, int b) {
   if (b < 0 || T.btype[b] == 0) return m3_identity<R>();
   const R* t = q + T.bcoord[b] + 3;
@@ -147,8 +156,6 @@ template <class R> __device__ __forceinline__ M3<R> body_rot(const Topo<R>& T, c
 template <class R> __device__ __forceinline__ V3<R> body_pos(const Topo<R>& T, const R* q, int b) {
   return ld3(q + T.bcoord[b]);
 }
-
-// Slot blocks of a body (linear, angular) as dof3 indices.
 template <class R> __device__ __forceinline__ void body_blocks(const Topo<R>& T, int b, int& lin, int& ang) {
   if (b < 0) {
     lin = ang = -1;
@@ -158,40 +165,16 @@ template <class R> __device__ __forceinline__ void body_blocks(const Topo<R>& T,
   ang = T.btype[b] == 1 ? lin + 1 : -1;
 }
 
-// J_i M^-1 J_i^T over the row's slots; hinv_lin == nullptr -> unshifted (1/m).
+// c^T M^-1 c on one block: unshifted (1/m, I_w^-1) or shifted H^-1.
 template <class R>
-__device__ __forceinline__ R row_inv_quad(const Topo<R>& T, const Work<R>& W, const R* c12, const int* b4,
-                                          bool shifted) {
-  R s = R(0);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int b = b4[k];
-    if (b < 0) continue;
-    const V3<R> c = v3(c12[3 * k], c12[3 * k + 1], c12[3 * k + 2]);
-    if (T.d3_kind[b] == kRigidAng) {
-      s += sym_quad(W.iwi6 + 6 * b, c);
-    } else if (shifted) {
-      const R* hi = W.hinv + 3 * b;
-      s += c.x * c.x * hi[0] + c.y * c.y * hi[1] + c.z * c.z * hi[2];
-    } else {
-      const R m = T.bmass[T.d3_body[b]];
-      s += c.x * c.x / m + c.y * c.y / m + c.z * c.z / m;
-    }
+__device__ __forceinline__ R block_quad(const Topo<R>& T, const Work<R>& W, int b, V3<R> c, bool shifted) {
+  if (T.d3_kind[b] == kRigidAng) return sym_quad(W.iwi6 + 6 * b, c);
+  if (shifted) {
+    const R* hi = W.hinv + 3 * b;
+    return c.x * c.x * hi[0] + c.y * c.y * hi[1] + c.z * c.z * hi[2];
   }
-  return s;
-}
-
-// J_i . v over the row's slots (v: a dof vector).
-template <class R> __device__ __forceinline__ R row_dot(const R* c12, const int* b4, const R* v) {
-  R s = R(0);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int b = b4[k];
-    if (b < 0) continue;
-    const R* vb = v + 3 * b;
-    s += c12[3 * k] * vb[0] + c12[3 * k + 1] * vb[1] + c12[3 * k + 2] * vb[2];
-  }
-  return s;
+  const R m = T.bmass[T.d3_body[b]];
+  return c.x * c.x / m + c.y * c.y / m + c.z * c.z / m;
 }
 
 template <class R> __device__ __forceinline__ R r_factor(R emd, R h, bool position, int strat) {
@@ -255,9 +238,110 @@ __host__ __device__ __forceinline__ bool joint_row_linear(int kind, int k) {
   return false;
 }
 
-// ------------------------------------------------------------------ row blocks (static per step)
-template <class R, class Team> __device__ void setup_row_blocks(Team& t, const Topo<R>& T, Work<R>& W) {
-  const int ng = T.nj + T.nt + W.nc;
+// ------------------------------------------------------------------ contact geometry
+template <class R> struct CView {
+  int ba, bb, al, aa, bl, bA;  // bodies and their lin/ang dof3 blocks (-1 = none)
+  V3<R> n, d1, d2, ra, rb;
+  R dc, act;
+};
+template <class R> __device__ __forceinline__ CView<R> contact_view(const Topo<R>& T, const Work<R>& W, int c) {
+  CView<R> v;
+  v.ba = W.cbody[2 * c];
+  v.bb = W.cbody[2 * c + 1];
+  body_blocks(T, v.ba, v.al, v.aa);
+  body_blocks(T, v.bb, v.bl, v.bA);
+  const R* g = W.cdir + 9 * c;
+  v.n = ld3(g);
+  v.d1 = ld3(g + 3);
+  v.d2 = ld3(g + 6);
+  const R* a = W.carm + 6 * c;
+  v.ra = ld3(a);
+  v.rb = ld3(a + 3);
+  v.dc = W.cscale[2 * c];
+  v.act = W.cscale[2 * c + 1];
+  return v;
+}
+// Relative contact-point velocity of a dof vector: (v_a + w_a x r_a) - (v_b + w_b x r_b).
+template <class R> __device__ __forceinline__ V3<R> contact_dv(const CView<R>& c, const R* v) {
+  V3<R> d = v3(R(0), R(0), R(0));
+  if (c.al >= 0) {
+    d = ld3(v + 3 * c.al);
+    if (c.aa >= 0) d = d + cross(ld3(v + 3 * c.aa), c.ra);
+  }
+  if (c.bl >= 0) {
+    d = d - ld3(v + 3 * c.bl);
+    if (c.bA >= 0) d = d - cross(ld3(v + 3 * c.bA), c.rb);
+  }
+  return d;
+}
+// Direction-row quadratic form d^T J M^-1 J^T d for a contact row along dir.
+template <class R>
+__device__ __forceinline__ R contact_quad(const Topo<R>& T, const Work<R>& W, const CView<R>& c, V3<R> dir,
+                                          bool shifted) {
+  R s = R(0);
+  if (c.al >= 0) {
+    s += block_quad(T, W, c.al, dir, shifted);
+    if (c.aa >= 0) s += block_quad(T, W, c.aa, cross(c.ra, dir), shifted);
+  }
+  if (c.bl >= 0) {
+    s += block_quad(T, W, c.bl, dir, shifted);
+    if (c.bA >= 0) s += block_quad(T, W, c.bA, cross(c.rb, dir), shifted);
+  }
+  return s;
+}
+
+// ------------------------------------------------------------------ row-level J and diag
+// J_i . v for static rows (4 slots x 3).
+template <class R> __device__ __forceinline__ R slot_dot(const R* c12, const int* b4, const R* v) {
+  R s = R(0);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int b = b4[k];
+    if (b < 0) continue;
+    const R* vb = v + 3 * b;
+    s += c12[3 * k] * vb[0] + c12[3 * k + 1] * vb[1] + c12[3 * k + 2] * vb[2];
+  }
+  return s;
+}
+template <class R>
+__device__ __forceinline__ R slot_quad(const Topo<R>& T, const Work<R>& W, const R* c12, const int* b4, bool shifted) {
+  R s = R(0);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int b = b4[k];
+    if (b < 0) continue;
+    s += block_quad(T, W, b, v3(c12[3 * k], c12[3 * k + 1], c12[3 * k + 2]), shifted);
+  }
+  return s;
+}
+// J_i . v for any row.
+template <class R> __device__ __forceinline__ R row_J(const Topo<R>& T, const Work<R>& W, int i, const R* v) {
+  if (i < T.rows_static) return slot_dot(W.coeff + 12 * i, W.blk + 4 * i, v);
+  if (i < W.friction_begin) {
+    const CView<R> c = contact_view(T, W, i - W.normal_begin);
+    return c.dc == R(0) ? R(0) : c.dc * dot(c.n, contact_dv(c, v));
+  }
+  const int k = i - W.friction_begin, c0 = k >> 1;
+  const CView<R> c = contact_view(T, W, c0);
+  if (c.act == R(0)) return R(0);
+  return dot((k & 1) ? c.d2 : c.d1, contact_dv(c, v));
+}
+// J_i H^-1 J_i^T (shifted) for any row.
+template <class R> __device__ __forceinline__ R row_quad(const Topo<R>& T, const Work<R>& W, int i) {
+  if (i < T.rows_static) return slot_quad(T, W, W.coeff + 12 * i, W.blk + 4 * i, true);
+  if (i < W.friction_begin) {
+    const CView<R> c = contact_view(T, W, i - W.normal_begin);
+    return c.dc == R(0) ? R(0) : contact_quad(T, W, c, c.dc * c.n, true);
+  }
+  const int k = i - W.friction_begin;
+  const CView<R> c = contact_view(T, W, k >> 1);
+  if (c.act == R(0)) return R(0);
+  return contact_quad(T, W, c, (k & 1) ? c.d2 : c.d1, true);
+}
+
+// ------------------------------------------------------------------ static row blocks (once per step)
+template <class R, bool kTets, class Team> __device__ void setup_row_blocks(Team& t, const Topo<R>& T, Work<R>& W) {
+  const int ng = T.nj + (kTets ? T.nt : 0);
   for (int g = t.rank(); g < ng; g += t.size()) {
     if (g < T.nj) {
       const int kind = T.jkind[g], r0 = T.jrow[g];
@@ -275,7 +359,7 @@ template <class R, class Team> __device__ void setup_row_blocks(Team& t, const T
         if (b[2] >= 0 && b[2] == b[0]) b[2] = -1;  // same body on both sides: slots merge
         if (b[3] >= 0 && b[3] == b[1]) b[3] = -1;
       }
-    } else if (g < T.nj + T.nt) {
+    } else {
       const int e = g - T.nj;
       const int r0 = T.rows_joint + 3 * e;
       int vb[4];
@@ -286,29 +370,15 @@ template <class R, class Team> __device__ void setup_row_blocks(Team& t, const T
 #pragma unroll
         for (int k = 0; k < 4; ++k) b[k] = vb[k];
       }
-    } else {
-      const int c = g - T.nj - T.nt;
-      int al, aa, bl, ba;
-      body_blocks(T, W.cbody[2 * c], al, aa);
-      body_blocks(T, W.cbody[2 * c + 1], bl, ba);
-      const int rows[3] = {W.normal_begin + c, W.friction_begin + 2 * c, W.friction_begin + 2 * c + 1};
-      for (int i = 0; i < 3; ++i) {
-        int* b = W.blk + 4 * rows[i];
-        b[0] = al;
-        b[1] = aa;
-        b[2] = (bl >= 0 && bl == al) ? -1 : bl;
-        b[3] = (ba >= 0 && ba == aa) ? -1 : ba;
-      }
     }
   }
 }
 
-// Sums a coefficient contribution into the slot owning `blk` (handles the
-// merged same-body case) — used by joint/contact assembly.
+// Adds a coefficient contribution into the slot owning `blk` (merged same-body case).
 template <class R> __device__ __forceinline__ void slot_add(R* c12, const int* b4, int s, int blk, V3<R> v) {
   int k = s;
   if (blk < 0) return;
-  if (b4[s] != blk) k = (s == 2 ? 0 : 1);  // merged into the body-a slot
+  if (b4[s] != blk) k = (s == 2 ? 0 : 1);
   c12[3 * k] += v.x;
   c12[3 * k + 1] += v.y;
   c12[3 * k + 2] += v.z;
@@ -327,7 +397,6 @@ __device__ void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, 
               ax_b2 = ld3(fr + 15), rest = ld3(fr + 18);
   const M3<R> Ra = body_rot(T, q, ba), Rb = body_rot(T, q, bb);
   const bool rig_a = ba >= 0 && T.btype[ba] == 1, rig_b = bb >= 0 && T.btype[bb] == 1;
-  // world attach points and lever arms (attach_world_point / add_point_jacobian)
   V3<R> wa, wb, ra = v3(R(0), R(0), R(0)), rb = ra;
   if (ba < 0) wa = anc_a;
   else if (!rig_a) wa = body_pos(T, q, ba);
@@ -367,7 +436,7 @@ __device__ void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, 
     if (rig_a) slot_add(c, b, 1, aa, cross(ra, d));
     slot_add(c, b, 2, bl, -d);
     if (rig_b) slot_add(c, b, 3, bA, -cross(rb, d));
-    if (prism && rig_a) slot_add(c, b, 1, aa, cross(d, wa - wb));
+    if (prism && rig_a) slot_add(c, b, 1, aa, cross(d, wa - wb));  // t x d (constraints.cpp:195-196)
     emit(k, value, comp);
   };
   auto axis_row = [&](int k, V3<R> xa, V3<R> xb, R restv, R e) {
@@ -391,8 +460,7 @@ __device__ void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, 
       axis_row(4, axw, b2, rest.y, comp);
     }
   } else if (kind == 2) {
-    // tangent_basis(ax) (constraints.cpp:93-101)
-    int sm = 0;
+    int sm = 0;  // tangent_basis(ax) (constraints.cpp:93-101)
     if (ab(axw.y) < ab(axw.x)) sm = 1;
     if (ab(axw.z) < ab(axw[sm])) sm = 2;
     V3<R> ee = v3(R(0), R(0), R(0));
@@ -438,14 +506,12 @@ __device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R 
   const R c1 = T.tmat[4 * e], d1 = T.tmat[4 * e + 1], alpha = T.tmat[4 * e + 2];
   const bool diag_only = T.tmat[4 * e + 3] != R(0);
   const V3<R> s = sv.S;
-  // gradient c = V_e * dPsi/ds with (J - alpha) (materials.cpp:57-61)
-  const R J = s.x * s.y * s.z;
+  const R J = s.x * s.y * s.z;  // gradient with (J - alpha), materials.cpp:57-61
   const V3<R> dj = v3(s.y * s.z, s.x * s.z, s.x * s.y);
   const R kk = R(2) * d1 * (J - alpha);
   const R tc1 = R(2) * c1;
   const V3<R> cg = v3(vol * (tc1 * s.x + kk * dj.x), vol * (tc1 * s.y + kk * dj.y), vol * (tc1 * s.z + kk * dj.z));
-  // Hessian (materials.cpp:63-74)
-  const R k0 = R(2) * J - alpha;
+  const R k0 = R(2) * J - alpha;  // Hessian, materials.cpp:63-74
   const R k1 = d1 * s.z * k0, k2 = d1 * s.y * k0, k3 = d1 * s.x * k0;
   M3<R> H;
   H(0, 0) = R(2) * (d1 * s.y * s.y * s.z * s.z + c1);
@@ -454,8 +520,7 @@ __device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R 
   H(0, 1) = H(1, 0) = R(2) * k1;
   H(0, 2) = H(2, 0) = R(2) * k2;
   H(1, 2) = H(2, 1) = R(2) * k3;
-  // compliance_block (materials.cpp:82-102): PSD check with the restated eigensolver
-  {
+  {  // compliance_block (materials.cpp:82-102): PSD check with the restated eigensolver
     V3<R> ev;
     M3<R> dummy;
     sym_eig3<R, false>(H, ev, dummy);
@@ -478,11 +543,9 @@ __device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R 
   } else {
     E = inverse3(N);
   }
-  // rows: h = E (c + lambda/h) / h, C = E / h^2, J = ds/dq (materials.cpp:104-114)
-  const int r0 = T.rows_joint + 3 * e;
+  const int r0 = T.rows_joint + 3 * e;  // h = E (c + lambda/h) / h, C = E / h^2, J = ds/dq
   const R l0 = W.lam[r0] / h, l1 = W.lam[r0 + 1] / h, l2 = W.lam[r0 + 2] / h;
   const V3<R> cl = v3(cg.x + l0, cg.y + l1, cg.z + l2);
-  const R ih2 = R(1) / (h * h);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const R hv = (E(i, 0) * cl.x + E(i, 1) * cl.y + E(i, 2) * cl.z) / h;
@@ -500,16 +563,16 @@ __device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R 
   }
 #pragma unroll
   for (int i = 0; i < 9; ++i) W.ctet[9 * e + i] = E.a[i] / (h * h);
-  (void)ih2;
 }
 
-// Contact rows (newton.cpp:166-218; constraints.cpp:67-91).
+// Contact rows (newton.cpp:166-218; constraints.cpp:67-91, 103-115) in the
+// structured form: lever arms, NCP scale and friction flag per contact.
 template <class R>
 __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const R* u, int c, R h, const Cfg& cfg,
                                  AsmStats& st) {
   const int ba = W.cbody[2 * c], bb = W.cbody[2 * c + 1];
   const R* g = W.cgeo + 17 * c;
-  const V3<R> la = ld3(g), lb = ld3(g + 3), n = ld3(g + 6), d1 = ld3(g + 9), d2 = ld3(g + 12);
+  const V3<R> la = ld3(g), lb = ld3(g + 3);
   const R thick = g[15], mu = g[16];
   const bool rig_a = ba >= 0 && T.btype[ba] == 1, rig_b = bb >= 0 && T.btype[bb] == 1;
   V3<R> pa, pb, ra = v3(R(0), R(0), R(0)), rb = ra;
@@ -525,62 +588,54 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
     rb = mul(body_rot(T, q, bb), lb);
     pb = body_pos(T, q, bb) + rb;
   }
-  int al, aa, bl, bA;
-  body_blocks(T, ba, al, aa);
-  body_blocks(T, bb, bl, bA);
+  st3(W.carm + 6 * c, ra);
+  st3(W.carm + 6 * c + 3, rb);
+  CView<R> cv;
+  cv.ba = ba;
+  cv.bb = bb;
+  body_blocks(T, ba, cv.al, cv.aa);
+  body_blocks(T, bb, cv.bl, cv.bA);  // a == b needs no merge: both sides enter dv exactly as compress() sums them
+  cv.n = ld3(g + 6);
+  cv.d1 = ld3(g + 9);
+  cv.d2 = ld3(g + 12);
+  {
+    R* cdir = W.cdir + 9 * c;
+    st3(cdir, cv.n);
+    st3(cdir + 3, cv.d1);
+    st3(cdir + 6, cv.d2);
+  }
+  cv.ra = ra;
+  cv.rb = rb;
   const int nr = W.normal_begin + c, f0 = W.friction_begin + 2 * c;
-  const int* blk = W.blk + 4 * nr;  // identical slot blocks for the 3 rows
-  auto fill = [&](R* cc, V3<R> d) {
-#pragma unroll
-    for (int i = 0; i < 12; ++i) cc[i] = R(0);
-    slot_add(cc, blk, 0, al, d);
-    if (rig_a) slot_add(cc, blk, 1, aa, cross(ra, d));
-    slot_add(cc, blk, 2, bl, -d);
-    if (rig_b) slot_add(cc, blk, 3, bA, -cross(rb, d));
-  };
-  R cn[12];
-  fill(cn, n);
-  const R gap = dot(n, pa - pb) - thick;
+  const R gap = dot(cv.n, pa - pb) - thick;
   const R lam_n = W.lam[nr] / h;
-  const R rn = r_factor(row_inv_quad(T, W, cn, blk, false), h, true, cfg.r_strategy);
+  const R rn = r_factor(contact_quad(T, W, cv, cv.n, false), h, true, cfg.r_strategy);
   const PhiV<R> phi = phi_n(gap, lam_n, rn, cfg.ncp_kind);
   const R hn = phi.v / h;
   W.hv[nr] = hn;
   W.cd[nr] = phi.dl / (h * h);
-  {
-    R* c12 = W.coeff + 12 * nr;
-    if (phi.dc != R(0)) {
-#pragma unroll
-      for (int i = 0; i < 12; ++i) c12[i] = cn[i] * phi.dc;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 12; ++i) c12[i] = R(0);
-    }
-  }
+  W.cscale[2 * c] = phi.dc;  // row kept iff dc != 0 (newton.cpp:187)
   st.comp = fmax(st.comp, (double)ab(mn(gap, lam_n)));
   const R lf0 = W.lam[f0] / h, lf1 = W.lam[f0 + 1] / h;
   const R mu_ln = mu * lam_n;
   const R lfn = sqrt(lf0 * lf0 + lf1 * lf1);
   st.cone = fmax(st.cone, (double)mx(R(0), lfn - mu_ln));
-  R* c1 = W.coeff + 12 * f0;
-  R* c2 = W.coeff + 12 * (f0 + 1);
   R h1, h2;
   if (mu_ln > R(0)) {
-    fill(c1, d1);
-    fill(c2, d2);
-    const R v0 = row_dot(c1, blk, u), v1 = row_dot(c2, blk, u);
-    const R df = R(0.5) * (row_inv_quad(T, W, c1, blk, false) + row_inv_quad(T, W, c2, blk, false));
+    const V3<R> dv = contact_dv(cv, u);
+    const R v0 = dot(cv.d1, dv), v1 = dot(cv.d2, dv);
+    const R df = R(0.5) * (contact_quad(T, W, cv, cv.d1, false) + contact_quad(T, W, cv, cv.d2, false));
     const R rf = r_factor(df, h, false, cfg.r_strategy);
     const R wv = friction_W(sqrt(v0 * v0 + v1 * v1), lfn, mu_ln, rf, cfg.ncp_kind);
     h1 = v0 + wv * lf0;
     h2 = v1 + wv * lf1;
     W.cd[f0] = W.cd[f0 + 1] = wv / h;
+    W.cscale[2 * c + 1] = R(1);
   } else {
-#pragma unroll
-    for (int i = 0; i < 12; ++i) c1[i] = c2[i] = R(0);
     h1 = lf0;
     h2 = lf1;
     W.cd[f0] = W.cd[f0 + 1] = R(1) / h;
+    W.cscale[2 * c + 1] = R(0);
   }
   W.hv[f0] = h1;
   W.hv[f0 + 1] = h2;
@@ -588,28 +643,41 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
   st.hsq += (double)hn * hn + (double)h1 * h1 + (double)h2 * h2;
 }
 
-template <class R, class Team>
+template <class R, bool kTets, class Team>
 __device__ void assemble(Team& t, const Topo<R>& T, Work<R>& W, const R* q, const R* u, const Cfg& cfg, AsmStats& st) {
-  const int ng = T.nj + T.nt + W.nc;
+  const int nt = kTets ? T.nt : 0;
+  const int ng = T.nj + nt + W.nc;
   for (int g = t.rank(); g < ng; g += t.size()) {
     if (g < T.nj)
       assemble_joint(T, W, q, g, W.h, st);
-    else if (g < T.nj + T.nt)
+    else if (kTets && g < T.nj + nt)
       assemble_tet(T, W, q, g - T.nj, W.h, st);
     else
-      assemble_contact(T, W, q, u, g - T.nj - T.nt, W.h, cfg, st);
+      assemble_contact(T, W, q, u, g - T.nj - nt, W.h, cfg, st);
   }
 }
 
 // ------------------------------------------------------------------ J^T pull for one dof3 block
-template <class R>
-__device__ __forceinline__ V3<R> pull(const Topo<R>& T, const Work<R>& W, int b, const R* y) {
+// Row vector given by a plain array.
+template <class R> struct RowArr {
+  const R* y;
+  __device__ __forceinline__ R operator()(int i) const { return y[i]; }
+};
+// Row vector z' = z - a * inv .* ap (a PCR update not yet committed in memory).
+template <class R> struct RowPending {
+  const R *z, *inv, *ap;
+  R a;
+  __device__ __forceinline__ R operator()(int i) const { return z[i] - a * (inv[i] * ap[i]); }
+};
+
+template <class R, class YF>
+__device__ __forceinline__ V3<R> pull(const Topo<R>& T, const Work<R>& W, int b, const YF& y) {
   R sx = R(0), sy = R(0), sz = R(0);
   const int s0 = T.sinc_off[b], s1 = T.sinc_off[b + 1];
   for (int e = s0; e < s1; ++e) {
     const int ent = T.sinc_ent[e];
     const int row = ent >> 2, slot = ent & 3;
-    const R yr = y[row];
+    const R yr = y(row);
     const R* c = W.coeff + 12 * row + 3 * slot;
     sx += c[0] * yr;
     sy += c[1] * yr;
@@ -617,33 +685,26 @@ __device__ __forceinline__ V3<R> pull(const Topo<R>& T, const Work<R>& W, int b,
   }
   if (W.nc > 0) {
     const int c0 = W.cinc_off[b], c1 = W.cinc_off[b + 1];
-    // ascending row order: all normal rows first, then the friction pairs
     for (int e = c0; e < c1; ++e) {
       const int ent = W.cinc_ent[e];
-      const int row = W.normal_begin + (ent >> 2), slot = ent & 3;
-      const R yr = y[row];
-      const R* c = W.coeff + 12 * row + 3 * slot;
-      sx += c[0] * yr;
-      sy += c[1] * yr;
-      sz += c[2] * yr;
-    }
-    for (int e = c0; e < c1; ++e) {
-      const int ent = W.cinc_ent[e];
-      const int row = W.friction_begin + 2 * (ent >> 2), slot = ent & 3;
-      const R y0 = y[row], y1 = y[row + 1];
-      const R* c = W.coeff + 12 * row + 3 * slot;
-      sx += c[0] * y0;
-      sy += c[1] * y0;
-      sz += c[2] * y0;
-      sx += c[12] * y1;
-      sy += c[13] * y1;
-      sz += c[14] * y1;
+      const int c = ent >> 2, slot = ent & 3;
+      const R* g = W.cdir + 9 * c;
+      const R dc = W.cscale[2 * c], act = W.cscale[2 * c + 1];
+      const int f0 = W.friction_begin + 2 * c;
+      const R yn = dc * y(W.normal_begin + c), y1 = act * y(f0), y2 = act * y(f0 + 1);
+      // contact force f = dc z_n n + z_1 d1 + z_2 d2
+      V3<R> f = v3(yn * g[0] + y1 * g[3] + y2 * g[6], yn * g[1] + y1 * g[4] + y2 * g[7],
+                   yn * g[2] + y1 * g[5] + y2 * g[8]);
+      if (slot & 1) f = cross(ld3(W.carm + 6 * c + ((slot & 2) ? 3 : 0)), f);
+      if (slot & 2) f = -f;
+      sx += f.x;
+      sy += f.y;
+      sz += f.z;
     }
   }
   return v3(sx, sy, sz);
 }
 
-// H^-1 v on one block.
 template <class R>
 __device__ __forceinline__ V3<R> hinv_apply(const Topo<R>& T, const Work<R>& W, int b, V3<R> v) {
   if (T.d3_kind[b] == kRigidAng) return sym_mul(W.iwi6 + 6 * b, v);
@@ -652,35 +713,27 @@ __device__ __forceinline__ V3<R> hinv_apply(const Topo<R>& T, const Work<R>& W, 
 }
 
 // Operator pass 1: w = H^-1 J^T y (dof-parallel).
-template <class R, class Team> __device__ void op_pull(Team& t, const Topo<R>& T, Work<R>& W, const R* y) {
+template <class R, class Team, class YF> __device__ void op_pull(Team& t, const Topo<R>& T, Work<R>& W, const YF& y) {
   for (int b = t.rank(); b < T.nd3; b += t.size()) st3(W.w + 3 * b, hinv_apply(T, W, b, pull(T, W, b, y)));
 }
 
-// Operator pass 2 for row i: (J w + C z + eps z)_i.
-template <class R>
-__device__ __forceinline__ R op_row(const Topo<R>& T, const Work<R>& W, int i, const R* z, R eps) {
-  R s = row_dot(W.coeff + 12 * i, W.blk + 4 * i, W.w);
-  if (i >= T.rows_joint && i < T.rows_static) {
+// C_i . z for row i (tet block rows or scalar rows).
+template <class R, bool kTets>
+__device__ __forceinline__ R row_C(const Topo<R>& T, const Work<R>& W, int i, const R* z) {
+  if (kTets && i >= T.rows_joint && i < T.rows_static) {
     const int e = (i - T.rows_joint) / 3, k = (i - T.rows_joint) - 3 * e;
     const R* cb = W.ctet + 9 * e + 3 * k;
     const int r0 = T.rows_joint + 3 * e;
-    s += cb[0] * z[r0] + cb[1] * z[r0 + 1] + cb[2] * z[r0 + 2];
-  } else {
-    s += W.cd[i] * z[i];
+    return cb[0] * z[r0] + cb[1] * z[r0 + 1] + cb[2] * z[r0 + 2];
   }
-  return s + eps * z[i];
+  return W.cd[i] * z[i];
 }
-
-// Diagonal of the Schur complement for row i (matrix-free diagonal_preconditioner).
-template <class R> __device__ __forceinline__ R schur_diag(const Topo<R>& T, const Work<R>& W, int i, R eps) {
-  R s = row_inv_quad(T, W, W.coeff + 12 * i, W.blk + 4 * i, true);
-  if (i >= T.rows_joint && i < T.rows_static) {
+template <class R, bool kTets> __device__ __forceinline__ R row_Cdiag(const Topo<R>& T, const Work<R>& W, int i) {
+  if (kTets && i >= T.rows_joint && i < T.rows_static) {
     const int e = (i - T.rows_joint) / 3, k = (i - T.rows_joint) - 3 * e;
-    s += W.ctet[9 * e + 4 * k];
-  } else {
-    s += W.cd[i];
+    return W.ctet[9 * e + 4 * k];
   }
-  return s + eps;
+  return W.cd[i];
 }
 
 // ------------------------------------------------------------------ Newton step
@@ -696,6 +749,11 @@ template <class R, class Team> __device__ void newton_setup(Team& t, const Topo<
     for (int k = 0; k < (T.btype[b] ? 7 : 3); ++k) W.q[cd + k] = W.q0[cd + k];
     if (W.f_extra) f = f + ld3(W.f_extra + d);
     st3(W.ut + d, ld3(W.u0 + d) + h * (f / m));
+    for (int k = 0; k < (T.btype[b] ? 6 : 3); ++k) {
+      W.u[d + k] = R(0);
+      W.shift[d + k] = R(0);
+      W.hinv[d + k] = R(0);
+    }
     if (T.btype[b] == 1) {
       const M3<R> Rm = quat_rot(W.q0[cd + 3], W.q0[cd + 4], W.q0[cd + 5], W.q0[cd + 6]);
       M3<R> I;
@@ -724,16 +782,36 @@ template <class R, class Team> __device__ void newton_setup(Team& t, const Topo<
       st3(W.ut + d + 3, w + h * mul(Ii, tq));
     }
   }
-  for (int i = t.rank(); i < T.ndof; i += t.size()) {
-    W.u[i] = R(0);
-    W.shift[i] = R(0);
-    W.hinv[i] = R(0);
+}
+
+// Integration q = q- + h G(q) u with G at the current iterate (bodies.cpp:58-86).
+template <class R> __device__ __forceinline__ void integrate_body(const Topo<R>& T, const R* q0, R* qdst,
+                                                                 const R* qcur, const R* u, int b, R h) {
+  const int cd = T.bcoord[b], d = T.bdof[b];
+  for (int k = 0; k < 3; ++k) qdst[cd + k] = q0[cd + k] + h * u[d + k];
+  if (T.btype[b] == 1) {
+    const R* th = qcur + cd + 3;
+    const R t0 = th[0], t1 = th[1], t2 = th[2], t3 = th[3];
+    const R ox = u[d + 3], oy = u[d + 4], oz = u[d + 5];
+    R nq[4];
+    nq[0] = q0[cd + 3] + h * (R(0.5) * (-t1 * ox - t2 * oy - t3 * oz));
+    nq[1] = q0[cd + 4] + h * (R(0.5) * (t0 * ox + t3 * oy - t2 * oz));
+    nq[2] = q0[cd + 5] + h * (R(0.5) * (-t3 * ox + t0 * oy + t1 * oz));
+    nq[3] = q0[cd + 6] + h * (R(0.5) * (t2 * ox - t1 * oy + t0 * oz));
+    const R nn = sqrt(nq[0] * nq[0] + nq[1] * nq[1] + nq[2] * nq[2] + nq[3] * nq[3]);
+    if ((double)nn < 1e-300) {
+      nq[0] = R(1);
+      nq[1] = nq[2] = nq[3] = R(0);
+    } else {
+      for (int k = 0; k < 4; ++k) nq[k] = nq[k] / nn;
+    }
+    for (int k = 0; k < 4; ++k) qdst[cd + 3 + k] = nq[k];
   }
 }
 
 // The Newton loop, final classification and telemetry (newton.cpp:343-416).
 // Requires newton_setup() and a barrier, and the step's contact set + incidence.
-template <class R, class Team>
+template <class R, bool kTets, class Team>
 __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cfg, StepOut out) {
   const R h = W.h;
   const int nr = W.nrows;
@@ -741,15 +819,16 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
   const R eps = R(cfg.epsilon_reg);
   const R tfrac = R(cfg.step_fraction);
   for (int i = t.rank(); i < nr; i += t.size()) W.lam[i] = R(0);
-  setup_row_blocks(t, T, W);
-  // any friction (line-search gate, newton.cpp:341)
-  double has_fric = 0.0;
+  setup_row_blocks<R, kTets>(t, T, W);
+  double has_fric = 0.0;  // line-search gate (newton.cpp:341)
   for (int c = t.rank(); c < W.nc; c += t.size())
     if (W.cgeo[17 * c + 16] > R(0)) has_fric = 1.0;
-  {
+  if (cfg.line_search) {
     double s0[1] = {0.0}, m0[1] = {has_fric};
     t.reduce(s0, m0);
     has_fric = m0[0];
+  } else {
+    t.sync();
   }
   const bool line_search = cfg.line_search && has_fric == 0.0;
   double min_shift = 0.0;
@@ -759,13 +838,13 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
   for (int it = 0; it < cfg.newton_iterations; ++it) {
     // ---- assemble
     AsmStats as{0.0, 0.0, 0.0, 0.0};
-    assemble(t, T, W, W.q, W.u, cfg, as);
+    assemble<R, kTets>(t, T, W, W.q, W.u, cfg, as);
     t.sync();
     // ---- g = M~(u - u~) - J^T lambda; geometric stiffness; H^-1; w = H^-1 g
     double gmax = 0.0, gsq = 0.0, smin = 0.0;
     const bool gs = it >= 1 && cfg.geometric_stiffness;
     for (int b = t.rank(); b < T.nd3; b += t.size()) {
-      const V3<R> jl = pull(T, W, b, W.lam);
+      const V3<R> jl = pull(T, W, b, RowArr<R>{W.lam});
       const int kind = T.d3_kind[b];
       const int d = 3 * b;
       V3<R> gv, mdiag;
@@ -779,11 +858,12 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
         gv = v3(m * du.x, m * du.y, m * du.z) - jl;
         mdiag = v3(m, m, m);
       }
-      if (gs) {
-        if (kind == kParticleLin) {
-          const R m = mdiag.x;
+      if (kind == kParticleLin) {
+        // geometric stiffness secant (newton.cpp:299-319); rigid dofs keep shift 0
+        const R m = mdiag.x;
 #pragma unroll
-          for (int k = 0; k < 3; ++k) {
+        for (int k = 0; k < 3; ++k) {
+          if (gs) {
             const R dd = W.u[d + k] - W.up[d + k];
             R sh = R(0);
             if (!(ab(dd) < R(1e-10))) {
@@ -793,15 +873,12 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
             W.shift[d + k] = sh;
             smin = fmin(smin, (double)sh);
           }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 3; ++k) W.shift[d + k] = R(0);
+          W.gp[d + k] = gv[k];
+          W.up[d + k] = W.u[d + k];
         }
       }
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        W.gp[d + k] = gv[k];
-        W.up[d + k] = W.u[d + k];
         W.g[d + k] = gv[k];
         gmax = fmax(gmax, (double)(ab(gv[k]) / mdiag[k]));
         gsq += (double)gv[k] * (double)gv[k];
@@ -813,25 +890,26 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
       }
       st3(W.w + d, hinv_apply(T, W, b, gv));
     }
-    double s2[2] = {gsq, as.hsq}, m3[4] = {fmax(gmax, as.hmax), as.comp, as.cone, -smin};
-    t.reduce(s2, m3);
-    min_shift = fmin(min_shift, -m3[3]);
+    double s2[2] = {gsq, as.hsq}, mm[4] = {fmax(gmax, as.hmax), as.comp, as.cone, -smin};
+    t.reduce(s2, mm);
+    min_shift = fmin(min_shift, -mm[3]);
     IterOut io;
-    io.residual_inf = m3[0];
+    io.residual_inf = mm[0];
     io.merit_l2 = sqrt(s2[0] + s2[1]);
-    io.comp_error_max = m3[1];
-    io.cone_violation_max = m3[2];
+    io.comp_error_max = mm[1];
+    io.cone_violation_max = mm[2];
     io.linear_iterations = 0;
     io.linear_residual = 0.0;
     io.linear_breakdown = 0;
+    io.step_size = 0.0;
 
     // ---- Schur RHS b = J H^-1 g - h, diagonal preconditioner, r = b (x0 = 0)
     double rr = 0.0, rzr = 0.0;
     for (int i = t.rank(); i < nr; i += t.size()) {
-      const R b = row_dot(W.coeff + 12 * i, W.blk + 4 * i, W.w) - W.hv[i];
+      const R b = row_J(T, W, i, W.w) - W.hv[i];
       R inv = R(1);
       if (cfg.preconditioner == 1) {
-        const R sd = schur_diag(T, W, i, eps);
+        const R sd = row_quad(T, W, i) + row_Cdiag<R, kTets>(T, W, i) + eps;
         inv = sd > R(0) ? R(1) / sd : R(1);
       }
       W.inv[i] = inv;
@@ -852,16 +930,20 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
       double best_res = hist_last;
       hist_n = 1;
       if (t.rank() == 0 && out.hist) out.hist[(size_t)it * (maxlin + 1)] = hist_last;
+      // kTets == false (diagonal C): the accepted update x+=a p, r-=a ap, z-=a M^-1 ap
+      // is committed in place during the next row pass (the operator reads the
+      // pending z' on the fly), so no trial buffers xn/rn/zn are needed.
+      constexpr bool kInPlace = !kTets;
       bool pending_best = false;
+      R pend = R(0);  // alpha of an accepted, not yet committed update (kInPlace)
       R *x = W.x, *xn = W.xn, *r = W.r, *rn = W.rn, *z = W.z, *zn = W.zn;
       double zaz = 0.0;
       if (maxlin > 0 && hist_last > cfg.linear_tolerance) {
-        // az = A z, zaz = z . az
-        op_pull(t, T, W, z);
+        op_pull(t, T, W, RowArr<R>{z});  // az = A z, zaz = z . az
         t.sync();
         double za = 0.0;
         for (int i = t.rank(); i < nr; i += t.size()) {
-          const R a = op_row(T, W, i, z, eps);
+          const R a = row_J(T, W, i, W.w) + row_C<R, kTets>(T, W, i, z) + eps * z[i];
           W.az[i] = a;
           za += (double)z[i] * a;
         }
@@ -886,9 +968,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
           W.p[i] = pi;
           W.ap[i] = api;
           den += (double)api * (double)(W.inv[i] * api);
-          if (pending_best) W.bx[i] = x[i];
         }
-        pending_best = false;
         {
           double s[1] = {den}, m[1] = {0.0};
           t.reduce(s, m);
@@ -904,10 +984,12 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
         double pn2 = 0.0, rn2 = 0.0;
         for (int i = t.rank(); i < nr; i += t.size()) {
           const R api = W.ap[i];
-          xn[i] = x[i] + ra * W.p[i];
           const R rv = r[i] - ra * api;
-          rn[i] = rv;
-          zn[i] = z[i] - ra * (W.inv[i] * api);
+          if (!kInPlace) {
+            xn[i] = x[i] + ra * W.p[i];
+            rn[i] = rv;
+            zn[i] = z[i] - ra * (W.inv[i] * api);
+          }
           pn2 += (double)rv * (double)(W.inv[i] * rv);
           rn2 += (double)rv * rv;
         }
@@ -919,16 +1001,19 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
         }
         const double pn = sqrt(pn2);
         if (pn > phist_last) break;  // monotone guard: stop at the numerical floor
-        // commit
-        R* tmp = x;
-        x = xn;
-        xn = tmp;
-        tmp = r;
-        r = rn;
-        rn = tmp;
-        tmp = z;
-        z = zn;
-        zn = tmp;
+        if (kInPlace) {
+          pend = ra;  // commit deferred to the next row pass
+        } else {
+          R* tmp = x;  // commit
+          x = xn;
+          xn = tmp;
+          tmp = r;
+          r = rn;
+          rn = tmp;
+          tmp = z;
+          z = zn;
+          zn = tmp;
+        }
         hist_last = sqrt(rn2);
         phist_last = pn;
         if (t.rank() == 0 && out.hist && hist_n <= maxlin) out.hist[(size_t)it * (maxlin + 1) + hist_n] = hist_last;
@@ -942,15 +1027,32 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
           breakdown = 1;
           break;
         }
-        // az = A z', zaz' = z' . az
-        op_pull(t, T, W, z);
-        t.sync();
         double za = 0.0;
-        for (int i = t.rank(); i < nr; i += t.size()) {
-          const R a = op_row(T, W, i, z, eps);
-          W.az[i] = a;
-          za += (double)z[i] * a;
-          if (pending_best) W.bx[i] = x[i];
+        if (kInPlace) {
+          op_pull(t, T, W, RowPending<R>{z, W.inv, W.ap, pend});  // az = A z', zaz' = z' . az
+          t.sync();
+          for (int i = t.rank(); i < nr; i += t.size()) {
+            const R api = W.ap[i];
+            const R zi = z[i] - pend * (W.inv[i] * api);
+            const R xi = x[i] + pend * W.p[i];
+            z[i] = zi;
+            x[i] = xi;
+            r[i] = r[i] - pend * api;
+            const R a = row_J(T, W, i, W.w) + W.cd[i] * zi + eps * zi;
+            W.az[i] = a;
+            za += (double)zi * a;
+            if (pending_best) W.bx[i] = xi;
+          }
+          pend = R(0);
+        } else {
+          op_pull(t, T, W, RowArr<R>{z});  // az = A z', zaz' = z' . az
+          t.sync();
+          for (int i = t.rank(); i < nr; i += t.size()) {
+            const R a = row_J(T, W, i, W.w) + row_C<R, kTets>(T, W, i, z) + eps * z[i];
+            W.az[i] = a;
+            za += (double)z[i] * a;
+            if (pending_best) W.bx[i] = x[i];
+          }
         }
         pending_best = false;
         {
@@ -960,10 +1062,13 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
           zaz = s[0];
         }
       }
-      if (pending_best) {
-        for (int i = t.rank(); i < nr; i += t.size()) W.bx[i] = x[i];
+      if (pending_best || pend != R(0)) {  // an accepted update whose commit pass never ran
+        for (int i = t.rank(); i < nr; i += t.size()) {
+          const R xi = x[i] + pend * W.p[i];
+          x[i] = xi;
+          if (pending_best) W.bx[i] = xi;
+        }
       }
-      // keep the committed iterate pointers for the next Newton iteration's phase
       W.x = x;
       W.xn = xn;
       W.r = r;
@@ -983,7 +1088,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
       if (!isfinite(v)) bad = 1.0;
     }
     for (int b = t.rank(); b < T.nd3; b += t.size()) {
-      const V3<R> jd = nr > 0 ? pull(T, W, b, W.bx) : v3(R(0), R(0), R(0));
+      const V3<R> jd = nr > 0 ? pull(T, W, b, RowArr<R>{W.bx}) : v3(R(0), R(0), R(0));
       const V3<R> dv = hinv_apply(T, W, b, jd - ld3(W.g + 3 * b));
       st3(W.du + 3 * b, dv);
       du2 += (double)dv.x * dv.x + (double)dv.y * dv.y + (double)dv.z * dv.z;
@@ -1010,40 +1115,21 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
       const R trials[4] = {R(1), R(0.5), R(0.25), R(0.125)};
       for (int k = 0; k < 4; ++k) {
         const R tr = trials[k];
-        R* pl = W.xn;   // probe lambda (free after the solve)
-        R* pu = W.ub;   // probe velocities
+        R* pl = W.xn;  // probe lambda (free after the solve)
+        R* pu = W.ub;  // probe velocities
         for (int i = t.rank(); i < nr; i += t.size()) pl[i] = W.lam[i] + tr * W.bx[i];
         for (int i = t.rank(); i < T.ndof; i += t.size()) pu[i] = W.u[i] + tr * W.du[i];
-        for (int b = t.rank(); b < T.nb; b += t.size()) {
-          const int cd = T.bcoord[b], d = T.bdof[b];
-          for (int k2 = 0; k2 < 3; ++k2) W.qp[cd + k2] = W.q0[cd + k2] + h * pu[d + k2];
-          if (T.btype[b] == 1) {
-            const R* th = W.q + cd + 3;
-            const R wx = pu[d + 3], wy = pu[d + 4], wz = pu[d + 5];
-            R nq[4];
-            nq[0] = W.q0[cd + 3] + h * (R(0.5) * (-th[1] * wx - th[2] * wy - th[3] * wz));
-            nq[1] = W.q0[cd + 4] + h * (R(0.5) * (th[0] * wx + th[3] * wy - th[2] * wz));
-            nq[2] = W.q0[cd + 5] + h * (R(0.5) * (-th[3] * wx + th[0] * wy + th[1] * wz));
-            nq[3] = W.q0[cd + 6] + h * (R(0.5) * (th[2] * wx - th[1] * wy + th[0] * wz));
-            const R nn = sqrt(nq[0] * nq[0] + nq[1] * nq[1] + nq[2] * nq[2] + nq[3] * nq[3]);
-            if ((double)nn < 1e-300) {
-              nq[0] = R(1);
-              nq[1] = nq[2] = nq[3] = R(0);
-            } else {
-              for (int k2 = 0; k2 < 4; ++k2) nq[k2] = nq[k2] / nn;
-            }
-            for (int k2 = 0; k2 < 4; ++k2) W.qp[cd + 3 + k2] = nq[k2];
-          }
-        }
+        t.sync();
+        for (int b = t.rank(); b < T.nb; b += t.size()) integrate_body(T, W.q0, W.qp, W.q, pu, b, h);
         t.sync();
         R* save_lam = W.lam;
         W.lam = pl;
         AsmStats ps{0.0, 0.0, 0.0, 0.0};
-        assemble(t, T, W, W.qp, pu, cfg, ps);
+        assemble<R, kTets>(t, T, W, W.qp, pu, cfg, ps);
         t.sync();
         double pg = 0.0;
         for (int b = t.rank(); b < T.nd3; b += t.size()) {
-          const V3<R> jl = pull(T, W, b, W.lam);
+          const V3<R> jl = pull(T, W, b, RowArr<R>{W.lam});
           const V3<R> dv = ld3(pu + 3 * b) - ld3(W.ut + 3 * b);
           V3<R> gv;
           if (T.d3_kind[b] == kRigidAng)
@@ -1063,32 +1149,14 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
         }
       }
     }
-    // ---- damped update + integration (newton.cpp:393-396, bodies.cpp:58-86).
-    // Each body owns its dofs, so u += t du and q = q- + h G(q) u run in one pass;
-    // G is evaluated at the current iterate before q is overwritten.
+    // ---- damped update + integration (newton.cpp:393-396). Each body owns its
+    // dofs, so u += t du and q = q- + h G(q) u run in one pass.
     for (int i = t.rank(); i < nr; i += t.size()) W.lam[i] += tstep * W.bx[i];
     for (int b = t.rank(); b < T.nb; b += t.size()) {
-      const int cd = T.bcoord[b], d = T.bdof[b];
+      const int d = T.bdof[b];
       const int nd = T.btype[b] == 1 ? 6 : 3;
       for (int k = 0; k < nd; ++k) W.u[d + k] += tstep * W.du[d + k];
-      for (int k = 0; k < 3; ++k) W.q[cd + k] = W.q0[cd + k] + h * W.u[d + k];
-      if (T.btype[b] == 1) {
-        R* th = W.q + cd + 3;
-        const R ox = W.u[d + 3], oy = W.u[d + 4], oz = W.u[d + 5];
-        R nq[4];
-        nq[0] = W.q0[cd + 3] + h * (R(0.5) * (-th[1] * ox - th[2] * oy - th[3] * oz));
-        nq[1] = W.q0[cd + 4] + h * (R(0.5) * (th[0] * ox + th[3] * oy - th[2] * oz));
-        nq[2] = W.q0[cd + 5] + h * (R(0.5) * (-th[3] * ox + th[0] * oy + th[1] * oz));
-        nq[3] = W.q0[cd + 6] + h * (R(0.5) * (th[2] * ox - th[1] * oy + th[0] * oz));
-        const R nn = sqrt(nq[0] * nq[0] + nq[1] * nq[1] + nq[2] * nq[2] + nq[3] * nq[3]);
-        if ((double)nn < 1e-300) {
-          nq[0] = R(1);
-          nq[1] = nq[2] = nq[3] = R(0);
-        } else {
-          for (int k = 0; k < 4; ++k) nq[k] = nq[k] / nn;
-        }
-        for (int k = 0; k < 4; ++k) th[k] = nq[k];
-      }
+      integrate_body(T, W.q0, W.q, W.q, W.u, b, h);
     }
     io.step_size = (double)tstep * sqrt(du2 + dl2);
     if (t.rank() == 0) {
@@ -1109,11 +1177,11 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
   }
   // ---- final assembly for classification and telemetry (newton.cpp:409-416)
   AsmStats fs{0.0, 0.0, 0.0, 0.0};
-  assemble(t, T, W, W.q, W.u, cfg, fs);
+  assemble<R, kTets>(t, T, W, W.q, W.u, cfg, fs);
   t.sync();
   double gmax = 0.0;
   for (int b = t.rank(); b < T.nd3; b += t.size()) {
-    const V3<R> jl = pull(T, W, b, W.lam);
+    const V3<R> jl = pull(T, W, b, RowArr<R>{W.lam});
     const V3<R> du = ld3(W.u + 3 * b) - ld3(W.ut + 3 * b);
     if (T.d3_kind[b] == kRigidAng) {
       const R* s6 = W.iw6 + 6 * b;
@@ -1128,39 +1196,17 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
   // contact telemetry + min gap (fill_contact_telemetry, newton.cpp:67-94)
   double mgap = W.nc ? __builtin_huge_val() : 0.0;
   for (int c = t.rank(); c < W.nc; c += t.size()) {
-    const int ba = W.cbody[2 * c], bb = W.cbody[2 * c + 1];
+    const CView<R> cv = contact_view(T, W, c);
     const R* g = W.cgeo + 17 * c;
-    const V3<R> la = ld3(g), lb = ld3(g + 3), n = ld3(g + 6), d1 = ld3(g + 9), d2 = ld3(g + 12);
-    V3<R> pa, pb, ra = v3(R(0), R(0), R(0)), rb = ra;
-    const bool rig_a = ba >= 0 && T.btype[ba] == 1, rig_b = bb >= 0 && T.btype[bb] == 1;
-    if (ba < 0) pa = la;
-    else if (!rig_a) pa = body_pos(T, W.q, ba);
-    else {
-      ra = mul(body_rot(T, W.q, ba), la);
-      pa = body_pos(T, W.q, ba) + ra;
-    }
-    if (bb < 0) pb = lb;
-    else if (!rig_b) pb = body_pos(T, W.q, bb);
-    else {
-      rb = mul(body_rot(T, W.q, bb), lb);
-      pb = body_pos(T, W.q, bb) + rb;
-    }
-    const R gap = dot(n, pa - pb) - g[15];
-    auto vel = [&](V3<R> d) {
-      R s = R(0);
-      if (ba >= 0) {
-        const int o = T.bdof[ba];
-        s += dot(d, ld3(W.u + o));
-        if (rig_a) s += dot(cross(ra, d), ld3(W.u + o + 3));
-      }
-      if (bb >= 0) {
-        const int o = T.bdof[bb];
-        s -= dot(d, ld3(W.u + o));
-        if (rig_b) s -= dot(cross(rb, d), ld3(W.u + o + 3));
-      }
-      return s;
-    };
-    const R v0 = vel(d1), v1 = vel(d2);
+    const int ba = cv.ba, bb = cv.bb;
+    V3<R> pa, pb;
+    if (ba < 0) pa = ld3(g);
+    else pa = body_pos(T, W.q, ba) + cv.ra;
+    if (bb < 0) pb = ld3(g + 3);
+    else pb = body_pos(T, W.q, bb) + cv.rb;
+    const R gap = dot(cv.n, pa - pb) - g[15];
+    const V3<R> dv = contact_dv(cv, W.u);
+    const R v0 = dot(cv.d1, dv), v1 = dot(cv.d2, dv);
     const int nrw = W.normal_begin + c, f0 = W.friction_begin + 2 * c;
     const R lf0 = W.lam[f0] / h, lf1 = W.lam[f0 + 1] / h;
     if (out.tel) {
