@@ -1,12 +1,15 @@
 // C-ABI implementation (include/nsdyn_gpu.h): handles, device memory, kernels.
 //
 //   k_single_block / k_single_grid  one scene, nsd_step (newton_step boundary)
-//   k_batch_warp / k_batch_block    many environments, nsd_batch_step
+//   k_batch_sub / k_batch_block     many environments, nsd_batch_step
 //                                   (device narrow phase + newton_step per env)
 #include "nsdyn_gpu.h"
 
 #include "nsd_collide.cuh"
 #include "nsd_engine.cuh"
+#include "nsd_batch.cuh"
+
+#include <type_traits>
 
 #include <cuda_runtime.h>
 
@@ -294,9 +297,10 @@ template <class R> struct DevTopo {
 // kernel (global memory otherwise); "cold" arrays stay in global memory.
 struct WorkPlan {
   // hot R
-  size_t q, u, g, w, du, hinv, iwi6, coeff, hv, cd, lam, x, r, z, p, ap, az, inv, bx, cdir, carm, cscale, hotR;
+  size_t q, u, g, w, du, hinv, iwi6, coeff, hv, cd, lam, x, r, z, p, ap, az, inv, bx, cdir, carm, cscale, jstage,
+      cstage, hotR;
   // hot int
-  size_t blk, cbody, cinc_off, cinc_ent, hotI;
+  size_t blk, cbody, cinc_off, cinc_ent, cbinc_off, cbinc, hotI;
   // cold R
   size_t q0, u0, qp, ut, iw6, gp, up, shift, ub, fx, ctet, xn, rn, zn, cgeo, xlam, coldR;
   // cold int
@@ -336,12 +340,16 @@ struct WorkPlan {
     cdir = a(9 * c);
     carm = a(6 * c);
     cscale = a(2 * c);
+    jstage = a(12 * static_cast<size_t>(T.nj));
+    cstage = a(9 * c);
     hotR = o;
     o = 0;
     blk = a(4 * rs);
     cbody = a(2 * c);
     cinc_off = a(T.nd3 + 1);
     cinc_ent = a(4 * c);
+    cbinc_off = a(T.nb + 1);
+    cbinc = a(2 * c);
     hotI = o;
     o = 0;
     q0 = a(T.ncoord);
@@ -467,6 +475,8 @@ template <class R> struct BatchArgs {
   int* overflow;        // n_env
   double* fin;          // n_env * 8
   nsd::IterOut* iters;  // n_env * newton_iterations
+  const int* jbinc_off;  // static joint incidence per body (warp solver)
+  const int* jbinc;
 };
 
 // One environment: extension forces, setup, device narrow phase, contact
@@ -573,45 +583,79 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr) {
   W.normal_begin = T.rows_static;
   W.friction_begin = T.rows_static + nc;
   W.nrows = T.rows_static + 3 * nc;
-  // ---- contact incidence per dof3 block (contact*4 + slot, contacts ascending)
-  int* coff = hi + P.cinc_off;
-  int* cent = hi + P.cinc_ent;
-  int* ccnt = ci + P.cinc_cnt;
-  for (int b = t.rank(); b < T.nd3; b += t.size()) {
-    int n = 0;
-    for (int c = 0; c < nc; ++c) {
-      int al, aa, bl, ba;
-      nsd::body_blocks(T, cbody[2 * c], al, aa);
-      nsd::body_blocks(T, cbody[2 * c + 1], bl, ba);
-      n += (al == b) + (aa == b) + (bl == b) + (ba == b);
-    }
-    ccnt[b] = n;
-  }
-  t.sync();
-  if (t.rank() == 0) {
-    int s = 0;
-    for (int b = 0; b < T.nd3; ++b) {
-      coff[b] = s;
-      s += ccnt[b];
-    }
-    coff[T.nd3] = s;
-  }
-  t.sync();
-  for (int b = t.rank(); b < T.nd3; b += t.size()) {
-    int o = coff[b];
-    for (int c = 0; c < nc; ++c) {
-      int b4[4];
-      nsd::body_blocks(T, cbody[2 * c], b4[0], b4[1]);
-      nsd::body_blocks(T, cbody[2 * c + 1], b4[2], b4[3]);
-      for (int s = 0; s < 4; ++s)
-        if (b4[s] == b) cent[o++] = 4 * c + s;
-    }
-  }
-  t.sync();
   nsd::StepOut out{};
   out.iters = A.iters ? A.iters + (size_t)env * A.cfg.newton_iterations : nullptr;
   out.fin = A.fin + (size_t)env * 8;
-  nsd::newton_solve<R, false>(t, T, W, A.cfg, out);
+  if constexpr (!std::is_same<Team, nsd::BlockTeam>::value) {
+    // ---- object-centric sub-warp solver: contact incidence per body (contact*2 + side)
+    int* cboff = hi + P.cbinc_off;
+    int* cbinc = hi + P.cbinc;
+    int* ccnt = ci + P.cinc_cnt;
+    for (int b = t.rank(); b < T.nb; b += t.size()) {
+      int n = 0;
+      for (int c = 0; c < nc; ++c) n += (cbody[2 * c] == b) + (cbody[2 * c + 1] == b);
+      ccnt[b] = n;
+    }
+    t.sync();
+    if (t.rank() == 0) {
+      int s = 0;
+      for (int b = 0; b < T.nb; ++b) {
+        cboff[b] = s;
+        s += ccnt[b];
+      }
+      cboff[T.nb] = s;
+    }
+    t.sync();
+    for (int b = t.rank(); b < T.nb; b += t.size()) {
+      int o = cboff[b];
+      for (int c = 0; c < nc; ++c) {
+        if (cbody[2 * c] == b) cbinc[o++] = 2 * c;
+        if (cbody[2 * c + 1] == b) cbinc[o++] = 2 * c + 1;
+      }
+    }
+    nsd::setup_row_blocks<R, false>(t, T, W);
+    t.sync();
+    nsd::ObjView<R> O{W, hr + P.jstage, hr + P.cstage, A.jbinc_off, A.jbinc, cboff, cbinc};
+    nsd::newton_solve_obj(t, T, O, A.cfg, out);
+    W = O.W;
+  } else {
+    // ---- contact incidence per dof3 block (contact*4 + slot, contacts ascending)
+    int* coff = hi + P.cinc_off;
+    int* cent = hi + P.cinc_ent;
+    int* ccnt = ci + P.cinc_cnt;
+    for (int b = t.rank(); b < T.nd3; b += t.size()) {
+      int n = 0;
+      for (int c = 0; c < nc; ++c) {
+        int al, aa, bl, ba;
+        nsd::body_blocks(T, cbody[2 * c], al, aa);
+        nsd::body_blocks(T, cbody[2 * c + 1], bl, ba);
+        n += (al == b) + (aa == b) + (bl == b) + (ba == b);
+      }
+      ccnt[b] = n;
+    }
+    t.sync();
+    if (t.rank() == 0) {
+      int s = 0;
+      for (int b = 0; b < T.nd3; ++b) {
+        coff[b] = s;
+        s += ccnt[b];
+      }
+      coff[T.nd3] = s;
+    }
+    t.sync();
+    for (int b = t.rank(); b < T.nd3; b += t.size()) {
+      int o = coff[b];
+      for (int c = 0; c < nc; ++c) {
+        int b4[4];
+        nsd::body_blocks(T, cbody[2 * c], b4[0], b4[1]);
+        nsd::body_blocks(T, cbody[2 * c + 1], b4[2], b4[3]);
+        for (int s = 0; s < 4; ++s)
+          if (b4[s] == b) cent[o++] = 4 * c + s;
+      }
+    }
+    t.sync();
+    nsd::newton_solve<R, false>(t, T, W, A.cfg, out);
+  }
   t.sync();
   for (int i = t.rank(); i < T.ncoord; i += t.size()) qs[i] = W.q[i];
   for (int i = t.rank(); i < T.ndof; i += t.size()) us[i] = W.u[i];
@@ -626,15 +670,16 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr) {
   }
 }
 
-// Warp per environment; the env's hot working set in shared memory.
-template <class R> __global__ void __launch_bounds__(128) k_batch_warp(BatchArgs<R> A) {
+// TPE lanes per environment (32/TPE environments per warp); each env's hot
+// working set in shared memory.
+template <class R, int TPE> __global__ void __launch_bounds__(128) k_batch_sub(BatchArgs<R> A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int wib = threadIdx.x >> 5;
-  const int env = blockIdx.x * A.envs_per_block + wib;
-  if (env >= A.n_env) return;  // warp-uniform
-  R* hr = A.hot_in_smem ? reinterpret_cast<R*>(smem + (size_t)wib * A.hot_bytes)
+  const int tib = threadIdx.x / TPE;  // team index in the block
+  const int env = blockIdx.x * A.envs_per_block + tib;
+  if (env >= A.n_env) return;  // team-uniform
+  R* hr = A.hot_in_smem ? reinterpret_cast<R*>(smem + (size_t)tib * A.hot_bytes)
                         : reinterpret_cast<R*>(A.hot_global + (size_t)env * A.hot_bytes);
-  nsd::WarpTeam t(threadIdx.x & 31);
+  nsd::SubWarpTeam<TPE> t(threadIdx.x & 31);
   batch_env(t, A, env, hr);
 }
 
@@ -912,12 +957,13 @@ template <class R> struct Batch final : BatchBase {
   nsd_config cfg;
   int n_env, maxc, ns, npairs;
   WorkPlan plan;
-  DBuf hotg, coldr, coldi, shapes, pairs, cand, paircnt, ncout, ovf, fin, iters, qs, us, torque;
+  DBuf hotg, coldr, coldi, shapes, pairs, cand, paircnt, ncout, ovf, fin, iters, qs, us, torque, jbinc;
+  int jbinc_n = 0;
   HBuf stage;
   double margin, mu_default;
   int team_threads = 32;  // 32: warp per env; >32: CTA per env
   int envs_per_block = 4;
-  bool hot_in_smem = true;
+  bool hot_in_smem = false;  // measured: L1-cached global beats smem-limited residency
   size_t smem_bytes = 0;
   std::vector<nsd::ShapeD<R>> hshapes;
 
@@ -953,29 +999,58 @@ template <class R> struct Batch final : BatchBase {
     if (ns) NSD_CK(cudaMemcpy(shapes.p, hshapes.data(), sizeof(nsd::ShapeD<R>) * ns, cudaMemcpyHostToDevice));
     if (npairs) NSD_CK(cudaMemcpy(pairs.p, hp.data(), sizeof(int2) * npairs, cudaMemcpyHostToDevice));
     plan.plan(H, maxc);
+    if (cfg.line_search) throw NsdError(NSD_UNSUPPORTED, "batched path: line search runs through nsd_step");
+    {  // static joint incidence per body for the warp solver: joint*2 + side (merged same-body -> side 0)
+      std::vector<std::vector<int>> per(H.nb);
+      for (int j = 0; j < H.nj; ++j) {
+        const int a = H.jbody[2 * j], b = H.jbody[2 * j + 1];
+        if (a >= 0) per[a].push_back(2 * j);
+        if (b >= 0 && b != a) per[b].push_back(2 * j + 1);
+      }
+      std::vector<int> flat(H.nb + 1, 0);
+      for (int b = 0; b < H.nb; ++b) flat[b + 1] = flat[b] + static_cast<int>(per[b].size());
+      for (int b = 0; b < H.nb; ++b) flat.insert(flat.end(), per[b].begin(), per[b].end());
+      jbinc_n = static_cast<int>(flat.size());
+      jbinc.alloc(sizeof(int) * flat.size());
+      NSD_CK(cudaMemcpy(jbinc.p, flat.data(), sizeof(int) * flat.size(), cudaMemcpyHostToDevice));
+    }
+    // Team shape: TPE lanes per env (4/8/16/32, sub-warp object solver) or a CTA per
+    // env (64/128/256, generic engine). Default 8 lanes: the ant's 8 joints map
+    // one per lane and the 4 envs of a warp run the same code path in lockstep.
     const char* env_team = std::getenv("NSD_BATCH_TEAM");
-    if (env_team) team_threads = std::max(32, std::atoi(env_team));
+    team_threads = 8;
+    if (env_team) team_threads = std::atoi(env_team);
+    if (team_threads != 4 && team_threads != 8 && team_threads != 16 && team_threads != 32 && team_threads != 64 &&
+        team_threads != 128 && team_threads != 256)
+      throw NsdError(NSD_INVALID, "NSD_BATCH_TEAM must be 4, 8, 16, 32, 64, 128 or 256");
+    const bool sub = team_threads <= 32;
+    envs_per_block = sub ? 32 / team_threads : 1;  // one warp per block by default
     const char* env_epb = std::getenv("NSD_ENVS_PER_BLOCK");
-    if (env_epb) envs_per_block = std::max(1, std::atoi(env_epb));
+    if (env_epb && sub) envs_per_block = std::max(1, std::min(128 / team_threads, std::atoi(env_epb)));
     const char* env_smem = std::getenv("NSD_HOT_SMEM");
     if (env_smem) hot_in_smem = std::atoi(env_smem) != 0;
     const size_t hb = plan.hot_bytes<R>();
     int max_optin = 0;
     NSD_CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-    if (team_threads == 32) {
-      envs_per_block = std::min(envs_per_block, 4);
-      while (envs_per_block > 1 && hb * envs_per_block > (size_t)max_optin) --envs_per_block;
-      smem_bytes = hb * envs_per_block;
-    } else {
-      smem_bytes = hb;
-    }
+    smem_bytes = hb * envs_per_block;
     if (smem_bytes > (size_t)max_optin) hot_in_smem = false;
     if (!hot_in_smem) {
       smem_bytes = 0;
       hotg.alloc(hb * n_env);
+      // no shared memory needed: give the unified L1/smem array to L1 so the
+      // resident environments' hot sets stay cached
+      const int carve = std::getenv("NSD_L1_CARVEOUT") ? std::atoi(std::getenv("NSD_L1_CARVEOUT")) : 0;
+      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 32>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     } else {
-      NSD_CK(cudaFuncSetAttribute(k_batch_warp<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
-      NSD_CK(cudaFuncSetAttribute(k_batch_block<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+      const int sb = static_cast<int>(smem_bytes);
+      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+      NSD_CK(cudaFuncSetAttribute(k_batch_block<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
     }
     coldr.alloc(sizeof(R) * plan.coldR * n_env);
     coldi.alloc(sizeof(int) * plan.coldI * n_env);
@@ -1046,7 +1121,7 @@ template <class R> struct Batch final : BatchBase {
     A.ns = ns;
     A.npairs = npairs;
     A.maxc = maxc;
-    A.envs_per_block = team_threads == 32 ? envs_per_block : 1;
+    A.envs_per_block = envs_per_block;
     A.hot_in_smem = hot_in_smem ? 1 : 0;
     A.pairs = pairs.as<int2>();
     A.shapes = shapes.as<nsd::ShapeD<R>>();
@@ -1083,9 +1158,18 @@ template <class R> struct Batch final : BatchBase {
     A.overflow = ovf.as<int>();
     A.fin = fin.as<double>();
     A.iters = iters.as<nsd::IterOut>();
-    if (team_threads == 32) {
-      const int epb = A.envs_per_block;
-      k_batch_warp<R><<<(n_env + epb - 1) / epb, 32 * epb, smem_bytes, stream>>>(A);
+    A.jbinc_off = jbinc.as<int>();
+    A.jbinc = jbinc.as<int>() + H.nb + 1;
+    const int epb = envs_per_block;
+    const int nblk = (n_env + epb - 1) / epb;
+    if (team_threads <= 32) {
+      const int thr = team_threads * epb;
+      switch (team_threads) {
+        case 4: k_batch_sub<R, 4><<<nblk, thr, smem_bytes, stream>>>(A); break;
+        case 8: k_batch_sub<R, 8><<<nblk, thr, smem_bytes, stream>>>(A); break;
+        case 16: k_batch_sub<R, 16><<<nblk, thr, smem_bytes, stream>>>(A); break;
+        default: k_batch_sub<R, 32><<<nblk, thr, smem_bytes, stream>>>(A); break;
+      }
     } else {
       k_batch_block<R><<<n_env, team_threads, smem_bytes, stream>>>(A);
     }

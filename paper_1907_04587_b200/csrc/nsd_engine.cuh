@@ -923,8 +923,8 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
     int lin_used = 0, breakdown = 0, hist_n = 0;
     double hist_last = 0.0;
     if (nr > 0) {
-      double s1[2] = {rr, rzr}, m0[1] = {0.0};
-      t.reduce(s1, m0);
+      double s1[2] = {rr, rzr};
+      t.reduce_sum(s1);
       hist_last = sqrt(s1[0]);
       double phist_last = sqrt(s1[1]);
       double best_res = hist_last;
@@ -947,8 +947,8 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
           W.az[i] = a;
           za += (double)z[i] * a;
         }
-        double s[1] = {za}, m[1] = {0.0};
-        t.reduce(s, m);
+        double s[1] = {za};
+        t.reduce_sum(s);
         zaz = s[0];
       }
       double beta = 0.0;
@@ -970,8 +970,8 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
           den += (double)api * (double)(W.inv[i] * api);
         }
         {
-          double s[1] = {den}, m[1] = {0.0};
-          t.reduce(s, m);
+          double s[1] = {den};
+          t.reduce_sum(s);
           den = s[0];
         }
         if (fabs(den) < 1e-300) {
@@ -994,8 +994,8 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
           rn2 += (double)rv * rv;
         }
         {
-          double s[2] = {pn2, rn2}, m[1] = {0.0};
-          t.reduce(s, m);
+          double s[2] = {pn2, rn2};
+          t.reduce_sum(s);
           pn2 = s[0];
           rn2 = s[1];
         }
@@ -1056,8 +1056,8 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
         }
         pending_best = false;
         {
-          double s[1] = {za}, m[1] = {0.0};
-          t.reduce(s, m);
+          double s[1] = {za};
+          t.reduce_sum(s);
           beta = s[0] / zaz;
           zaz = s[0];
         }
@@ -1141,8 +1141,8 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
           pg += (double)gv.x * gv.x + (double)gv.y * gv.y + (double)gv.z * gv.z;
         }
         W.lam = save_lam;
-        double s[2] = {pg, ps.hsq}, m[1] = {0.0};
-        t.reduce(s, m);
+        double s[2] = {pg, ps.hsq};
+        t.reduce_sum(s);
         if (sqrt(s[0] + s[1]) < io.merit_l2) {
           tstep = tr;
           break;

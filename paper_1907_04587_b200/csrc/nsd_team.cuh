@@ -47,6 +47,56 @@ struct WarpTeam {
 #pragma unroll
     for (int k = 0; k < NM; ++k) m[k] = __shfl_sync(0xffffffffu, warp_max_down(m[k]), 0);
   }
+  template <int NS> __device__ __forceinline__ void reduce_sum(double (&s)[NS]) {
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < NS; ++k) s[k] = __shfl_sync(0xffffffffu, warp_sum_down(s[k]), 0);
+  }
+};
+
+// TPE consecutive lanes of a warp per environment (TPE in {4, 8, 16, 32}).
+// Shuffles and barriers use the team's own lane mask, so the teams sharing a
+// warp may take different data-dependent paths (PCR exits, aborts) safely.
+template <int TPE> struct SubWarpTeam {
+  static_assert(TPE == 4 || TPE == 8 || TPE == 16 || TPE == 32, "TPE");
+  int lane;       // rank within the team
+  unsigned mask;  // the team's lanes
+  __device__ explicit SubWarpTeam(int warp_lane)
+      : lane(warp_lane & (TPE - 1)),
+        mask(TPE == 32 ? 0xffffffffu : (((1u << TPE) - 1u) << (warp_lane & ~(TPE - 1)))) {}
+  __device__ __forceinline__ int rank() const { return lane; }
+  __device__ __forceinline__ int size() const { return TPE; }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  template <int NS, int NM>
+  __device__ __forceinline__ void reduce(double (&s)[NS], double (&m)[NM]) {
+    __syncwarp(mask);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      double v = s[k];
+#pragma unroll
+      for (int off = TPE / 2; off > 0; off >>= 1) v += __shfl_down_sync(mask, v, off, TPE);
+      s[k] = __shfl_sync(mask, v, 0, TPE);
+    }
+#pragma unroll
+    for (int k = 0; k < NM; ++k) {
+      double v = m[k];
+#pragma unroll
+      for (int off = TPE / 2; off > 0; off >>= 1) v = fmax(v, __shfl_down_sync(mask, v, off, TPE));
+      m[k] = __shfl_sync(mask, v, 0, TPE);
+    }
+  }
+  template <int NS> __device__ __forceinline__ void reduce_sum(double (&s)[NS]) {
+    __syncwarp(mask);
+    double v[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) v[k] = s[k];
+#pragma unroll
+    for (int off = TPE / 2; off > 0; off >>= 1)
+#pragma unroll
+      for (int k = 0; k < NS; ++k) v[k] += __shfl_down_sync(mask, v[k], off, TPE);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) s[k] = __shfl_sync(mask, v[k], 0, TPE);
+  }
 };
 
 struct BlockTeam {
@@ -56,6 +106,10 @@ struct BlockTeam {
   __device__ __forceinline__ int rank() const { return threadIdx.x; }
   __device__ __forceinline__ int size() const { return blockDim.x; }
   __device__ __forceinline__ void sync() const { __syncthreads(); }
+  template <int NS> __device__ __forceinline__ void reduce_sum(double (&s)[NS]) {
+    double m[1] = {0.0};
+    reduce(s, m);
+  }
   template <int NS, int NM>
   __device__ __forceinline__ void reduce(double (&s)[NS], double (&m)[NM]) {
     constexpr int K = NS + NM;
@@ -102,6 +156,10 @@ struct GridTeam {
   __device__ __forceinline__ int rank() const { return blockIdx.x * blockDim.x + threadIdx.x; }
   __device__ __forceinline__ int size() const { return gridDim.x * blockDim.x; }
   __device__ __forceinline__ void sync() const { cooperative_groups::this_grid().sync(); }
+  template <int NS> __device__ __forceinline__ void reduce_sum(double (&s)[NS]) {
+    double m[1] = {0.0};
+    reduce(s, m);
+  }
   template <int NS, int NM>
   __device__ __forceinline__ void reduce(double (&s)[NS], double (&m)[NM]) {
     constexpr int K = NS + NM;

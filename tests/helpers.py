@@ -53,3 +53,23 @@ def rel_err(a, b, floor=1e-12):
     if a.size == 0:
         return 0.0
     return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), floor))
+
+
+def decision_mismatches(g, o, tol, floor_ratio=1e-9):
+    """PCR iteration counts per Newton iteration: returns (n_mismatch, n_non_borderline).
+    A count differs legitimately only where the run ended at a rounding-level
+    boundary: residual within 10x of the absolute tolerance, or at the numerical
+    floor (<= floor_ratio of the initial residual) where the monotone guard fires."""
+    bad = 0
+    mism = 0
+    for i in range(min(g["n_iterations"], o["n_iterations"])):
+        if g["stats"][i, 5] == o["stats"][i, 5]:
+            continue
+        mism += 1
+        h0 = max(g["hist"][i, 0], o["hist"][i, 0])
+        ends = [g["stats"][i, 6], o["stats"][i, 6]]
+        borderline = any(tol > 0 and tol / 10 <= e <= tol * 10 for e in ends) or \
+            any(e <= floor_ratio * h0 for e in ends)
+        if not borderline:
+            bad += 1
+    return mism, bad

