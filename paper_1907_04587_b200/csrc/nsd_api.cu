@@ -288,6 +288,9 @@ template <class R> struct DevTopo {
     t.rows_static = H.rows_static;
     t.sinc_off = reinterpret_cast<const int*>(base + o_soff);
     t.sinc_ent = reinterpret_cast<const int*>(base + o_sent);
+    // warp-cooperative J^T pull when blocks gather long incidence lists (FEM vertices sit in ~24 tets)
+    t.warp_pull = H.nd3 > 0 && H.sinc_ent.size() >= 24 * static_cast<size_t>(H.nd3) ? 1 : 0;
+    if (const char* e = std::getenv("NSD_WARP_PULL")) t.warp_pull = std::atoi(e);
     jframe = reinterpret_cast<R*>(base + o_jframe);
   }
 };
@@ -726,7 +729,7 @@ template <class R> struct Solver final : SolverBase {
     NSD_CK(cudaEventCreate(&ev1));
     ensure(16);
     const size_t work = std::max<size_t>({(size_t)H.rows_static + 48, (size_t)H.nd3, (size_t)H.nb});
-    if (work <= 4096) {
+    if (work <= 1536) {  // small scenes: one CTA (block barriers); larger: cooperative grid
       use_grid = false;
       block_threads = work <= 256 ? 128 : (work <= 1024 ? 256 : 512);
     } else {
@@ -738,7 +741,8 @@ template <class R> struct Solver final : SolverBase {
       else
         NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, false>, 256, 0));
       if (per_sm < 1) throw NsdError(NSD_CUDA_ERROR, "grid kernel cannot be resident");
-      grid_blocks = dev_sms * std::min(per_sm, 2);
+      const char* bps = std::getenv("NSD_GRID_BLOCKS_PER_SM");
+      grid_blocks = dev_sms * std::min(per_sm, bps ? std::max(1, std::atoi(bps)) : 1);
       gpart.alloc(sizeof(double) * 2 * grid_blocks * nsd::kRedMax);
     }
   }

@@ -82,6 +82,7 @@ template <class R> struct Topo {
   int rows_static;    // rows_joint + 3 nt
   const int* sinc_off;  // static incidence per dof3 block (nd3 + 1)
   const int* sinc_ent;  // row*4 + slot, ascending rows within a block
+  int warp_pull;        // 1: a warp per dof3 block (long incidence lists, FEM); 0: a thread per block
 };
 
 // Per-scene (per-env) mutable state and scratch (global or shared memory).
@@ -670,11 +671,13 @@ template <class R> struct RowPending {
   __device__ __forceinline__ R operator()(int i) const { return z[i] - a * (inv[i] * ap[i]); }
 };
 
+// Partial J^T y of block b over the incidence entries first, first+stride, ...
 template <class R, class YF>
-__device__ __forceinline__ V3<R> pull(const Topo<R>& T, const Work<R>& W, int b, const YF& y) {
+__device__ __forceinline__ V3<R> pull_part(const Topo<R>& T, const Work<R>& W, int b, const YF& y, int first,
+                                           int stride) {
   R sx = R(0), sy = R(0), sz = R(0);
   const int s0 = T.sinc_off[b], s1 = T.sinc_off[b + 1];
-  for (int e = s0; e < s1; ++e) {
+  for (int e = s0 + first; e < s1; e += stride) {
     const int ent = T.sinc_ent[e];
     const int row = ent >> 2, slot = ent & 3;
     const R yr = y(row);
@@ -685,7 +688,7 @@ __device__ __forceinline__ V3<R> pull(const Topo<R>& T, const Work<R>& W, int b,
   }
   if (W.nc > 0) {
     const int c0 = W.cinc_off[b], c1 = W.cinc_off[b + 1];
-    for (int e = c0; e < c1; ++e) {
+    for (int e = c0 + first; e < c1; e += stride) {
       const int ent = W.cinc_ent[e];
       const int c = ent >> 2, slot = ent & 3;
       const R* g = W.cdir + 9 * c;
@@ -705,6 +708,24 @@ __device__ __forceinline__ V3<R> pull(const Topo<R>& T, const Work<R>& W, int b,
   return v3(sx, sy, sz);
 }
 
+template <class R, class YF>
+__device__ __forceinline__ V3<R> pull(const Topo<R>& T, const Work<R>& W, int b, const YF& y) {
+  return pull_part(T, W, b, y, 0, 1);
+}
+// Warp-cooperative pull: the 32 lanes stride the block's incidence list and
+// combine in a fixed shuffle tree (deterministic); every lane gets the sum.
+template <class R, class YF>
+__device__ __forceinline__ V3<R> pull_warp(const Topo<R>& T, const Work<R>& W, int b, const YF& y, int lane) {
+  V3<R> s = pull_part(T, W, b, y, lane, 32);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    s.x += __shfl_down_sync(0xffffffffu, s.x, off);
+    s.y += __shfl_down_sync(0xffffffffu, s.y, off);
+    s.z += __shfl_down_sync(0xffffffffu, s.z, off);
+  }
+  return v3(__shfl_sync(0xffffffffu, s.x, 0), __shfl_sync(0xffffffffu, s.y, 0), __shfl_sync(0xffffffffu, s.z, 0));
+}
+
 template <class R>
 __device__ __forceinline__ V3<R> hinv_apply(const Topo<R>& T, const Work<R>& W, int b, V3<R> v) {
   if (T.d3_kind[b] == kRigidAng) return sym_mul(W.iwi6 + 6 * b, v);
@@ -713,8 +734,25 @@ __device__ __forceinline__ V3<R> hinv_apply(const Topo<R>& T, const Work<R>& W, 
 }
 
 // Operator pass 1: w = H^-1 J^T y (dof-parallel).
+// Visits every dof3 block with its pulled J^T y: f(b, sum). Warp-cooperative
+// (team size a multiple of 32) for long incidence lists, one thread per block
+// otherwise; in both cases f runs once per block.
+template <class R, class Team, class YF, class F>
+__device__ __forceinline__ void for_blocks(Team& t, const Topo<R>& T, const Work<R>& W, const YF& y, F&& f) {
+  if (T.warp_pull) {
+    const int lane = t.rank() & 31, wid = t.rank() >> 5, nw = t.size() >> 5;
+    for (int b = wid; b < T.nd3; b += nw) {
+      const V3<R> s = pull_warp(T, W, b, y, lane);
+      if (lane == 0) f(b, s);
+    }
+  } else {
+    for (int b = t.rank(); b < T.nd3; b += t.size()) f(b, pull(T, W, b, y));
+  }
+}
+
+// Team size is a multiple of 32 for the generic engine: one warp per block.
 template <class R, class Team, class YF> __device__ void op_pull(Team& t, const Topo<R>& T, Work<R>& W, const YF& y) {
-  for (int b = t.rank(); b < T.nd3; b += t.size()) st3(W.w + 3 * b, hinv_apply(T, W, b, pull(T, W, b, y)));
+  for_blocks(t, T, W, y, [&](int b, V3<R> s) { st3(W.w + 3 * b, hinv_apply(T, W, b, s)); });
 }
 
 // C_i . z for row i (tet block rows or scalar rows).
@@ -843,8 +881,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
     // ---- g = M~(u - u~) - J^T lambda; geometric stiffness; H^-1; w = H^-1 g
     double gmax = 0.0, gsq = 0.0, smin = 0.0;
     const bool gs = it >= 1 && cfg.geometric_stiffness;
-    for (int b = t.rank(); b < T.nd3; b += t.size()) {
-      const V3<R> jl = pull(T, W, b, RowArr<R>{W.lam});
+    for_blocks(t, T, W, RowArr<R>{W.lam}, [&](int b, V3<R> jl) {
       const int kind = T.d3_kind[b];
       const int d = 3 * b;
       V3<R> gv, mdiag;
@@ -889,7 +926,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
         for (int k = 0; k < 3; ++k) W.hinv[d + k] = R(1) / (m + W.shift[d + k]);
       }
       st3(W.w + d, hinv_apply(T, W, b, gv));
-    }
+    });
     double s2[2] = {gsq, as.hsq}, mm[4] = {fmax(gmax, as.hmax), as.comp, as.cone, -smin};
     t.reduce(s2, mm);
     min_shift = fmin(min_shift, -mm[3]);
@@ -1087,13 +1124,13 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
       dl2 += (double)v * v;
       if (!isfinite(v)) bad = 1.0;
     }
-    for (int b = t.rank(); b < T.nd3; b += t.size()) {
-      const V3<R> jd = nr > 0 ? pull(T, W, b, RowArr<R>{W.bx}) : v3(R(0), R(0), R(0));
+    for_blocks(t, T, W, RowArr<R>{W.bx}, [&](int b, V3<R> jd) {
+      if (!(nr > 0)) jd = v3(R(0), R(0), R(0));
       const V3<R> dv = hinv_apply(T, W, b, jd - ld3(W.g + 3 * b));
       st3(W.du + 3 * b, dv);
       du2 += (double)dv.x * dv.x + (double)dv.y * dv.y + (double)dv.z * dv.z;
       if (!isfinite(dv.x) || !isfinite(dv.y) || !isfinite(dv.z)) bad = 1.0;
-    }
+    });
     {
       double s[2] = {dl2, du2}, m[1] = {bad};
       t.reduce(s, m);
@@ -1128,8 +1165,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
         assemble<R, kTets>(t, T, W, W.qp, pu, cfg, ps);
         t.sync();
         double pg = 0.0;
-        for (int b = t.rank(); b < T.nd3; b += t.size()) {
-          const V3<R> jl = pull(T, W, b, RowArr<R>{W.lam});
+        for_blocks(t, T, W, RowArr<R>{W.lam}, [&](int b, V3<R> jl) {
           const V3<R> dv = ld3(pu + 3 * b) - ld3(W.ut + 3 * b);
           V3<R> gv;
           if (T.d3_kind[b] == kRigidAng)
@@ -1139,7 +1175,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
             gv = v3(m * dv.x, m * dv.y, m * dv.z) - jl;
           }
           pg += (double)gv.x * gv.x + (double)gv.y * gv.y + (double)gv.z * gv.z;
-        }
+        });
         W.lam = save_lam;
         double s[2] = {pg, ps.hsq};
         t.reduce_sum(s);
@@ -1180,8 +1216,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
   assemble<R, kTets>(t, T, W, W.q, W.u, cfg, fs);
   t.sync();
   double gmax = 0.0;
-  for (int b = t.rank(); b < T.nd3; b += t.size()) {
-    const V3<R> jl = pull(T, W, b, RowArr<R>{W.lam});
+  for_blocks(t, T, W, RowArr<R>{W.lam}, [&](int b, V3<R> jl) {
     const V3<R> du = ld3(W.u + 3 * b) - ld3(W.ut + 3 * b);
     if (T.d3_kind[b] == kRigidAng) {
       const R* s6 = W.iw6 + 6 * b;
@@ -1192,7 +1227,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
       const V3<R> gv = v3(m * du.x, m * du.y, m * du.z) - jl;
       gmax = fmax(gmax, fmax((double)(ab(gv.x) / m), fmax((double)(ab(gv.y) / m), (double)(ab(gv.z) / m))));
     }
-  }
+  });
   // contact telemetry + min gap (fill_contact_telemetry, newton.cpp:67-94)
   double mgap = W.nc ? __builtin_huge_val() : 0.0;
   for (int c = t.rank(); c < W.nc; c += t.size()) {

@@ -196,15 +196,31 @@ struct GridTeam {
       const int nb = gridDim.x;
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
+        double part[8];  // all partial loads in flight at once: one L2 round trip
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int b = lane + 32 * u;
+          part[u] = b < nb ? __ldcg(gp + b * kRedMax + k) : 0.0;
+        }
         double acc = 0.0;
-        for (int b = lane; b < nb; b += 32) acc += __ldcg(gp + b * kRedMax + k);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += part[u];
+        for (int b = lane + 256; b < nb; b += 32) acc += __ldcg(gp + b * kRedMax + k);
         acc = warp_sum_down(acc);
         if (lane == 0) buf[32 * kRedMax + k] = acc;
       }
 #pragma unroll
       for (int k = 0; k < NM; ++k) {
         double acc = -__builtin_huge_val();
-        for (int b = lane; b < nb; b += 32) acc = fmax(acc, __ldcg(gp + b * kRedMax + NS + k));
+        double part[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int b = lane + 32 * u;
+          part[u] = b < nb ? __ldcg(gp + b * kRedMax + NS + k) : -__builtin_huge_val();
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = fmax(acc, part[u]);
+        for (int b = lane + 256; b < nb; b += 32) acc = fmax(acc, __ldcg(gp + b * kRedMax + NS + k));
         acc = warp_max_down(acc);
         if (lane == 0) buf[32 * kRedMax + NS + k] = acc;
       }
