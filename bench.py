@@ -10,6 +10,10 @@ integration — a single kernel launch (k_batch_warp / k_batch_block).
           device time (CUDA events) summed over exactly K steps, max over ranks
   e2e     same metric through the C ABI with host actions: per step H2D of the
           joint torques from pinned memory + step + D2H of (q, u) to pinned memory
+  dtype   f64 by default: the precision the reference computes in and the one
+          whose oracle parity is proven (1e-8 over 25 steps, tests/test_gpu_batch.py);
+          the other precision (f32 performance mode) is measured too and
+          reported under "other_precision" (--no-alt skips it)
   --impl reference   the reference's CPU path: the oracle restatement of
           nsdyn::step_world (oracle/, the reference itself does not build here),
           OpenMP over environments on all host cores.
@@ -39,16 +43,17 @@ HBM_FALLBACK = 6650.0
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--envs", type=int, default=4096, help="environments per GPU")
-    p.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    p.add_argument("--precision", default="fp64", choices=["fp32", "fp64"])
     p.add_argument("--passive", action="store_true", help="no joint torques (pure reference semantics)")
     p.add_argument("--team", type=int, default=0, help="threads per env team (32 = warp, 64/128 = CTA)")
     p.add_argument("--max-contacts", type=int, default=48)
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU baseline sample length")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-alt", action="store_true", help="skip the secondary-precision measurement")
     return p.parse_args()
 
 
@@ -70,7 +75,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -123,16 +128,19 @@ def b_cr_bytes(n_contacts, nj_rows=40, n_joint_nnz=384, n_joints=8, dof=54, rigi
 
 
 def cpu_baseline(args, n_env_total):
+    """The reference's CPU path (oracle restatement of step_world) on the host
+    cores: the same C5 envs (seeds 0..n-1), the same actions, warmed up the same
+    W steps, then a bounded sample of the timed steps sized to ~cpu_seconds."""
     from oracle import oracle_py as O
 
-    # calibrate on 2 steps, then size the sample to ~cpu_seconds
     n_env = min(n_env_total, 4096)
-    t, used, _ = O.c5_bench(0, n_env, 1, not args.passive)
-    steps = max(1, min(50, int(args.cpu_seconds / max(t, 1e-3))))
-    t, used, _ = O.c5_bench(0, n_env, steps, not args.passive)
+    W = args.warmup
+    t, used, _ = O.c5_bench(0, n_env, 1, not args.passive, warm=0)  # calibration
+    steps = max(1, min(args.steps, int(args.cpu_seconds / max(t, 1e-3))))
+    t, used, _ = O.c5_bench(0, n_env, steps, not args.passive, warm=W)
     return {"value": n_env * steps / t, "unit": "env-steps/s", "cores": used, "kind": "port",
-            "sample": f"{n_env} C5 ant envs x {steps} steps (oracle step_world, 4 Newton x 10 PCR, "
-                      f"OpenMP over envs), {t:.2f} s"}
+            "sample": f"{n_env} C5 ant envs, steps {W}..{W + steps} after {W} untimed warm-up steps "
+                      f"(oracle step_world, 4 Newton x 10 PCR, OpenMP over envs, {used} threads), {t:.2f} s"}
 
 
 def run_reference(args):
@@ -160,6 +168,121 @@ def workload_config(args, ws):
             "l2": "flushed (256 MiB memset) between timed steps"}
 
 
+def measure(args, prec, T, tmpl, E, env0, ws, rank, local, sample_clocks):
+    """Time K steps of one BatchSolver at precision `prec`: device-resident value,
+    then end-to-end through the C ABI. Returns a dict of raw timings."""
+    import torch
+
+    from paper_1907_04587_b200 import BatchSolver
+    from paper_1907_04587_b200.shard import action_torques, shard_states
+
+    q0, u0 = shard_states("c5", rank, ws, E, T.num_coord, T.num_dof)
+    cfg = tmpl.config
+    cfg.precision = prec
+    b = BatchSolver(T, tmpl.shapes, tmpl.n_shapes, tmpl.margin, tmpl.mu_default, cfg, E, args.max_contacts,
+                    device=local)
+    stream = torch.cuda.Stream(device=local)  # non-default stream: the C ABI reads handle 0 as "own stream"
+    torch.cuda.set_stream(stream)
+    b.set_stream(stream.cuda_stream)
+    b.set_state(q0, u0)
+    nj = T.n_joints
+    K, W = args.steps, args.warmup
+    # actions: a pure function of (global env id, step, joint), the same stream the CPU arm uses
+    tdt = torch.float32 if prec == "fp32" else torch.float64
+    torques = torch.from_numpy(action_torques(range(env0, env0 + E), range(K + W), nj)).to(tdt).cuda()
+    tdt_code = 0 if prec == "fp32" else 1
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step(i):
+        ptr = None if args.passive else torques[i].data_ptr()
+        b.step_device(tmpl.h, tmpl.gravity, ptr, tdt_code)
+
+    for i in range(W):
+        step(i)
+    torch.cuda.synchronize()
+    b.results()  # raises on contact overflow / errors
+    q_w, u_w = b.get_state()  # post-warmup state: the e2e region replays the same steps
+
+    # ---- value: device-resident inputs, L2 flushed between steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    sampler = ClockSampler(local) if sample_clocks else None
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+    for k in range(K):
+        flush.zero_()
+        ev[k][0].record(stream)
+        step(W + k)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop() if sampler else None
+    if ws > 1:
+        torch.distributed.barrier()
+    dev_ms = sum(a.elapsed_time(bb) for a, bb in ev)
+    res = b.results()
+    nc = res["n_contacts"].astype(np.float64)
+    aborted = int(res["aborted"].sum())
+
+    # ---- e2e: host actions -> H2D, step, D2H of the state, through the C ABI,
+    # replaying the timed steps from the same post-warmup state with the same actions
+    b.set_state(q_w, u_w)
+    dt = torch.float32 if prec == "fp32" else torch.float64
+    h_tq = torch.empty((K, E, nj), dtype=tdt, pin_memory=True)
+    h_tq.copy_(torques[W:W + K].cpu())
+    d_tq = torch.empty((E, nj), dtype=tdt, device="cuda")
+    h_q = torch.empty((K, E * T.num_coord), dtype=dt, pin_memory=True)
+    h_u = torch.empty((K, E * T.num_dof), dtype=dt, pin_memory=True)
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for k in range(K):
+        flush.zero_()
+        ev2[k][0].record(stream)
+        if not args.passive:
+            d_tq.copy_(h_tq[k], non_blocking=True)
+        b.step_device(tmpl.h, tmpl.gravity, None if args.passive else d_tq.data_ptr(), tdt_code)
+        b.copy_state_async(h_q[k].data_ptr(), h_u[k].data_ptr())
+        ev2[k][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = sum(a.elapsed_time(bb) for a, bb in ev2)
+    b.results()
+    b.close()
+    h2d = 0 if args.passive else E * nj * h_tq.element_size()
+    d2h = E * (T.num_coord + T.num_dof) * (4 if prec == "fp32" else 8)
+    if ws > 1:
+        t = torch.tensor([dev_ms, e2e_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev_ms, e2e_ms = float(t[0]), float(t[1])
+    total_envs = E * ws
+    return dict(dev_ms=dev_ms, e2e_ms=e2e_ms, value=total_envs * K / (dev_ms / 1000.0),
+                e2e=total_envs * K / (e2e_ms / 1000.0), nc=nc, aborted=aborted, clocks=clocks, h2d=h2d, d2h=d2h,
+                cfg=cfg)
+
+
+def roofline(m, prec, K):
+    """Roofline of the (single) step kernel: SURVEY §8(d) algorithmic bytes."""
+    vb = 4 if prec == "fp32" else 8
+    cfg = m["cfg"]
+    per_env_cr = b_cr_bytes(m["nc"], value_bytes=vb)
+    bytes_per_launch = float(np.sum(per_env_cr)) * cfg.newton_iterations * cfg.linear_max_iterations
+    launch_s = m["dev_ms"] / 1000.0 / K
+    peak, peak_kind = hbm_peak()
+    achieved = bytes_per_launch / launch_s / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(prec)
+        except Exception:
+            traffic = None
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_source": peak_kind, "bytes_per_launch": bytes_per_launch,
+            "model": "SURVEY 8(d) B_CR per env per CR iteration x 40 CR iterations x envs"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -173,120 +296,43 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1907_04587_b200 import BatchSolver, Scene, batch_states
+    from paper_1907_04587_b200 import Scene
 
     if args.team:
         os.environ["NSD_BATCH_TEAM"] = str(args.team)
-    E = args.envs
-    env0 = rank * E
+    from paper_1907_04587_b200.shard import env_range
+
+    env0, E = env_range(rank, ws, args.envs)
     tmpl = Scene("c5", env0)
     T = tmpl.topology
-    q0, u0 = batch_states("c5", env0, E, T.num_coord, T.num_dof)
-    cfg = tmpl.config
-    cfg.precision = args.precision
-    b = BatchSolver(T, tmpl.shapes, tmpl.n_shapes, tmpl.margin, tmpl.mu_default, cfg, E, args.max_contacts,
-                    device=local)
-    stream = torch.cuda.Stream(device=local)  # non-default stream: the C ABI reads handle 0 as "own stream"
-    torch.cuda.set_stream(stream)
-    b.set_stream(stream.cuda_stream)
-    b.set_state(q0, u0)
-    nj = T.n_joints
     K, W = args.steps, args.warmup
-    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    torques = (torch.rand((K + W, E, nj), generator=gen, device="cuda", dtype=torch.float32) * 2 - 1)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-
-    def step(i):
-        ptr = None if args.passive else torques[i].data_ptr()
-        b.step_device(tmpl.h, tmpl.gravity, ptr, 0)
-
-    for i in range(W):
-        step(i)
-    torch.cuda.synchronize()
-    b.results()  # raises on contact overflow / errors
-
-    # ---- value: device-resident inputs, L2 flushed between steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    sampler = ClockSampler(local)
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    sampler.start()
-    for k in range(K):
-        flush.zero_()
-        ev[k][0].record(stream)
-        step(W + k)
-        ev[k][1].record(stream)
-    torch.cuda.synchronize()
-    clocks = sampler.stop()
-    if ws > 1:
-        torch.distributed.barrier()
-    dev_ms = sum(a.elapsed_time(bb) for a, bb in ev)
-    res = b.results()
-    nc = res["n_contacts"].astype(np.float64)
-    aborted = int(res["aborted"].sum())
-
-    # ---- e2e: host actions -> H2D, step, D2H of the state, through the C ABI
-    dt = torch.float32 if args.precision == "fp32" else torch.float64
-    h_tq = torch.empty((K, E, nj), dtype=torch.float32, pin_memory=True)
-    h_tq.copy_(torques[W:W + K].cpu())
-    d_tq = torch.empty((E, nj), dtype=torch.float32, device="cuda")
-    h_q = torch.empty((K, E * T.num_coord), dtype=dt, pin_memory=True)
-    h_u = torch.empty((K, E * T.num_dof), dtype=dt, pin_memory=True)
-    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    for k in range(K):
-        flush.zero_()
-        ev2[k][0].record(stream)
-        if not args.passive:
-            d_tq.copy_(h_tq[k], non_blocking=True)
-        b.step_device(tmpl.h, tmpl.gravity, None if args.passive else d_tq.data_ptr(), 0)
-        b.copy_state_async(h_q[k].data_ptr(), h_u[k].data_ptr())
-        ev2[k][1].record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = sum(a.elapsed_time(bb) for a, bb in ev2)
-    h2d = 0 if args.passive else E * nj * 4
-    d2h = E * (T.num_coord + T.num_dof) * (4 if args.precision == "fp32" else 8)
-
-    if ws > 1:
-        t = torch.tensor([dev_ms, e2e_ms], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        dev_ms, e2e_ms = float(t[0]), float(t[1])
-    total_envs = E * ws
-    value = total_envs * K / (dev_ms / 1000.0)
-    e2e = total_envs * K / (e2e_ms / 1000.0)
-
-    # ---- roofline of the (single) step kernel: SURVEY §8(d) algorithmic bytes
-    vb = 4 if args.precision == "fp32" else 8
-    per_env_cr = b_cr_bytes(nc, value_bytes=vb)
-    bytes_per_launch = float(np.sum(per_env_cr)) * cfg.newton_iterations * cfg.linear_max_iterations
-    launch_s = dev_ms / 1000.0 / K
-    peak, peak_kind = hbm_peak()
-    achieved = bytes_per_launch / launch_s / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(args.precision)
-        except Exception:
-            traffic = None
-
+    prec = args.precision
+    m = measure(args, prec, T, tmpl, E, env0, ws, rank, local, True)
+    other = None
+    if not args.no_alt:
+        alt = "fp32" if prec == "fp64" else "fp64"
+        a = measure(args, alt, T, tmpl, E, env0, ws, rank, local, False)
+        other = {"dtype": "f32" if alt == "fp32" else "f64", "value": a["value"], "ms_per_step": a["dev_ms"] / K,
+                 "e2e": a["e2e"], "roofline_frac": roofline(a, alt, K)["frac"],
+                 "parity": ("tracks the oracle to 1e-4 until the first ground impact, O(1e-3) after "
+                            "(DESIGN.md Parity)") if alt == "fp32" else "oracle parity 1e-8 over 25 steps"}
     if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
         return
-    line = {"metric": "env-steps/sec at fixed Newton/CR iters", "value": value, "unit": "env-steps/s",
-            "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": dev_ms / K, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+    cfg = m["cfg"]
+    line = {"metric": "env-steps/sec at fixed Newton/CR iters", "value": m["value"], "unit": "env-steps/s",
+            "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": m["dev_ms"] / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if prec == "fp32" else "f64",
             "data": "synthetic", "config": workload_config(args, ws),
-            "us_per_cr_iter": 1000.0 * (dev_ms / K) / (cfg.newton_iterations * cfg.linear_max_iterations),
-            "mean_contacts_per_env": float(nc.mean()), "aborted_envs": aborted,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "bytes_per_launch": bytes_per_launch,
-                         "model": "SURVEY 8(d) B_CR per env per CR iteration x 40 CR iterations x envs"},
-            "e2e": {"value": e2e, "unit": "env-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": K, "clocks": clocks}
+            "us_per_cr_iter": 1000.0 * (m["dev_ms"] / K) / (cfg.newton_iterations * cfg.linear_max_iterations),
+            "mean_contacts_per_env": float(m["nc"].mean()), "aborted_envs": m["aborted"],
+            "roofline": roofline(m, prec, K),
+            "e2e": {"value": m["e2e"], "unit": "env-steps/s", "h2d_bytes_per_step": m["h2d"],
+                    "d2h_bytes_per_step": m["d2h"]},
+            "gpu_launches": K, "clocks": m["clocks"]}
+    if other:
+        line["other_precision"] = other
     if ws == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(args, E)

@@ -46,6 +46,7 @@ def lib():
             getattr(_lib, n).argtypes = None
         _lib.orc_world_h.restype = C.c_double
         _lib.orc_c5_bench.restype = C.c_double
+        _lib.orc_action_torque.restype = C.c_double
     return _lib
 
 
@@ -329,8 +330,13 @@ class OracleWorld:
                     lam=lam[:rows], tel=tel.reshape(-1, 6)[:nc])
 
 
-def c5_bench(env0, n_env, n_steps, actuated=False, threads=0):
+def action_torque(env, step, joint):
+    return lib().orc_action_torque(C.c_int(env), C.c_int(step), C.c_int(joint))
+
+
+def c5_bench(env0, n_env, n_steps, actuated=False, threads=0, warm=0):
+    """Times steps [warm, warm + n_steps) of n_env C5 ants (OpenMP over envs)."""
     used, cs = C.c_int(), C.c_double()
-    secs = lib().orc_c5_bench(C.c_int(env0), C.c_int(n_env), C.c_int(n_steps), C.c_int(int(actuated)),
+    secs = lib().orc_c5_bench(C.c_int(env0), C.c_int(n_env), C.c_int(warm), C.c_int(n_steps), C.c_int(int(actuated)),
                               C.c_int(threads), C.byref(used), C.byref(cs))
     return secs, used.value, cs.value

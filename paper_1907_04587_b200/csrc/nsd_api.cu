@@ -459,6 +459,7 @@ template <class R> struct BatchArgs {
   nsd::Topo<R> T;
   nsd::Cfg cfg;
   int n_env, ns, npairs, maxc, envs_per_block, hot_in_smem;
+  int row_pool;  // per-env shared-memory region (elements of R) for the PCR row state; 0 = off
   const int2* pairs;
   const nsd::ShapeD<R>* shapes;
   const R* jframe;
@@ -480,18 +481,28 @@ template <class R> struct BatchArgs {
   nsd::IterOut* iters;  // n_env * newton_iterations
   const int* jbinc_off;  // static joint incidence per body (warp solver)
   const int* jbinc;
+  unsigned long long* ptime;  // NSD_PHASE_TIMING diagnostics (16 counters) or null
 };
 
 // One environment: extension forces, setup, device narrow phase, contact
 // incidence, Newton solve, state write-back (step_world, scene.cpp:709-732).
+// Elements of the per-env shared-memory row region for nc contacts: the
+// write-heavy PCR state x, r, z, p, ap, az, bx (7 x rows), the J^T staging
+// (12 per joint, 9 per contact) and w (ndof), each array kept 16-byte aligned.
+__host__ __device__ inline int row_pool_elems(int rows_static, int nj, int ndof, int nc) {
+  const int rows = (rows_static + 3 * nc + 3) & ~3;
+  return 7 * rows + ((12 * nj + 3) & ~3) + ((9 * nc + 3) & ~3) + ((ndof + 3) & ~3);
+}
+
 template <class R, class Team>
-__device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr) {
+__device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* pool) {
   const nsd::Topo<R>& T = A.T;
   const WorkPlan& P = A.plan;
   int* hi = P.hot_ints(hr);
   R* cr = A.cold_r + (size_t)env * P.coldR;
   int* ci = A.cold_i + (size_t)env * P.coldI;
   nsd::Work<R> W = P.template bind<R>(hr, hi, cr, ci);
+  nsd::PhaseClock pc(A.ptime, t.rank() == 0);
   W.jframe = A.jframe;
   W.h = A.h;
   W.grav[0] = A.grav[0];
@@ -589,6 +600,8 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr) {
   nsd::StepOut out{};
   out.iters = A.iters ? A.iters + (size_t)env * A.cfg.newton_iterations : nullptr;
   out.fin = A.fin + (size_t)env * 8;
+  out.ptime = A.ptime;
+  pc.mark(0);
   if constexpr (!std::is_same<Team, nsd::BlockTeam>::value) {
     // ---- object-centric sub-warp solver: contact incidence per body (contact*2 + side)
     int* cboff = hi + P.cbinc_off;
@@ -619,6 +632,28 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr) {
     nsd::setup_row_blocks<R, false>(t, T, W);
     t.sync();
     nsd::ObjView<R> O{W, hr + P.jstage, hr + P.cstage, A.jbinc_off, A.jbinc, cboff, cbinc};
+    if (pool && row_pool_elems(T.rows_static, T.nj, T.ndof, nc) <= A.row_pool) {
+      // the env's PCR row state fits its shared-memory region: keep every store of
+      // the CR loop on chip (global stores are write-through to L2)
+      const int rows = (W.nrows + 3) & ~3;
+      R* sp = pool;
+      O.W.x = sp;
+      O.W.r = sp + rows;
+      O.W.z = sp + 2 * rows;
+      O.W.p = sp + 3 * rows;
+      O.W.ap = sp + 4 * rows;
+      O.W.az = sp + 5 * rows;
+      O.W.bx = sp + 6 * rows;
+      sp += 7 * rows;
+      O.jstage = sp;
+      sp += (12 * T.nj + 3) & ~3;
+      O.cstage = sp;
+      sp += (9 * nc + 3) & ~3;
+      // w = H^-1 J^T y is produced by body_momentum; copy the setup value over
+      for (int i = t.rank(); i < T.ndof; i += t.size()) sp[i] = W.w[i];
+      O.W.w = sp;
+      t.sync();
+    }
     nsd::newton_solve_obj(t, T, O, A.cfg, out);
     W = O.W;
   } else {
@@ -660,6 +695,7 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr) {
     nsd::newton_solve<R, false>(t, T, W, A.cfg, out);
   }
   t.sync();
+  pc.mark(13);
   for (int i = t.rank(); i < T.ncoord; i += t.size()) qs[i] = W.q[i];
   for (int i = t.rank(); i < T.ndof; i += t.size()) us[i] = W.u[i];
   // export the step's contact set and multipliers (nsd_batch_contacts)
@@ -675,15 +711,21 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr) {
 
 // TPE lanes per environment (32/TPE environments per warp); each env's hot
 // working set in shared memory.
-template <class R, int TPE> __global__ void __launch_bounds__(128) k_batch_sub(BatchArgs<R> A) {
+// Register budget: 4096 envs at 2 envs per warp (TPE 16) are 2048 warps, 14 per SM
+// for a single wave, so <= 146 registers per thread. Measured (50-step C5 bench):
+// 128 registers (128 x 4 bounds) fp32 2.77 M / fp64 1.62 M env-steps/s; uncapped
+// (255, 8 warps/SM) 2.2 M / 1.54 M; 144 (fp64) 1.17 M (spills land in the solver).
+template <class R, int TPE>
+__global__ void __launch_bounds__(128, 4) k_batch_sub(BatchArgs<R> A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tib = threadIdx.x / TPE;  // team index in the block
   const int env = blockIdx.x * A.envs_per_block + tib;
   if (env >= A.n_env) return;  // team-uniform
   R* hr = A.hot_in_smem ? reinterpret_cast<R*>(smem + (size_t)tib * A.hot_bytes)
                         : reinterpret_cast<R*>(A.hot_global + (size_t)env * A.hot_bytes);
+  R* pool = A.row_pool ? reinterpret_cast<R*>(smem) + (size_t)tib * A.row_pool : nullptr;
   nsd::SubWarpTeam<TPE> t(threadIdx.x & 31);
-  batch_env(t, A, env, hr);
+  batch_env(t, A, env, hr, pool);
 }
 
 // CTA per environment.
@@ -693,7 +735,7 @@ template <class R> __global__ void __launch_bounds__(256) k_batch_block(BatchArg
   nsd::BlockTeam t(red);
   R* hr = A.hot_in_smem ? reinterpret_cast<R*>(smem)
                         : reinterpret_cast<R*>(A.hot_global + (size_t)blockIdx.x * A.hot_bytes);
-  batch_env(t, A, blockIdx.x, hr);
+  batch_env(t, A, blockIdx.x, hr, static_cast<R*>(nullptr));
 }
 
 // ================================================================== handles
@@ -969,6 +1011,8 @@ template <class R> struct Batch final : BatchBase {
   int envs_per_block = 4;
   bool hot_in_smem = false;  // measured: L1-cached global beats smem-limited residency
   size_t smem_bytes = 0;
+  int row_pool = 0;  // per-env shared-memory row region (elements), see the constructor
+  DBuf ptime;        // NSD_PHASE_TIMING counters
   std::vector<nsd::ShapeD<R>> hshapes;
 
   Batch(const nsd_topology& tp, int n_shapes, const nsd_shape* sh, double mg, double mud, const nsd_config& c,
@@ -1019,10 +1063,11 @@ template <class R> struct Batch final : BatchBase {
       NSD_CK(cudaMemcpy(jbinc.p, flat.data(), sizeof(int) * flat.size(), cudaMemcpyHostToDevice));
     }
     // Team shape: TPE lanes per env (4/8/16/32, sub-warp object solver) or a CTA per
-    // env (64/128/256, generic engine). Default 8 lanes: the ant's 8 joints map
-    // one per lane and the 4 envs of a warp run the same code path in lockstep.
+    // env (64/128/256, generic engine). Default 16 lanes (2 envs per warp): with the
+    // register cap above, 4096 envs run in one wave at 14 warps/SM (measured best,
+    // DESIGN.md §6).
     const char* env_team = std::getenv("NSD_BATCH_TEAM");
-    team_threads = 8;
+    team_threads = 16;
     if (env_team) team_threads = std::atoi(env_team);
     if (team_threads != 4 && team_threads != 8 && team_threads != 16 && team_threads != 32 && team_threads != 64 &&
         team_threads != 128 && team_threads != 256)
@@ -1041,20 +1086,56 @@ template <class R> struct Batch final : BatchBase {
     if (!hot_in_smem) {
       smem_bytes = 0;
       hotg.alloc(hb * n_env);
-      // no shared memory needed: give the unified L1/smem array to L1 so the
-      // resident environments' hot sets stay cached
-      const int carve = std::getenv("NSD_L1_CARVEOUT") ? std::atoi(std::getenv("NSD_L1_CARVEOUT")) : 0;
+      int carve = 0;  // no shared memory: the unified L1/smem array goes to L1
+      if (sub) {
+        // Row pool: a per-env shared-memory region for the write-heavy PCR state
+        // (global stores are write-through to L2; measured 4.9 GB of L2 writes per
+        // fp64 launch without it). Sized so that every block of the launch is
+        // resident at once; envs whose contact count does not fit use global.
+        int sms = 0, smem_sm = 0, reserved = 0;
+        NSD_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        NSD_CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
+        NSD_CK(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device));
+        const int nblk = (n_env + envs_per_block - 1) / envs_per_block;
+        const int bps = std::max(1, std::min(32, (nblk + sms - 1) / sms));
+        const long budget = std::min<long>(max_optin, smem_sm / bps - reserved);
+        const int full = row_pool_elems(H.rows_static, H.nj, H.ndof, maxc);
+        int region = static_cast<int>(budget / envs_per_block / static_cast<long>(sizeof(R))) & ~3;
+        region = std::min(region, full);
+        const char* env_rp = std::getenv("NSD_ROW_SMEM");
+        if (env_rp && std::atoi(env_rp) == 0) region = 0;
+        if (region < row_pool_elems(H.rows_static, H.nj, H.ndof, 1)) region = 0;
+        row_pool = region;
+        smem_bytes = static_cast<size_t>(region) * envs_per_block * sizeof(R);
+        if (smem_bytes) {
+          // the limit is a per-function attribute shared by every Batch: set it to the
+          // device maximum (a permission, not an allocation) so handles cannot shrink it
+          // under one another
+          const int sb = static_cast<int>(smem_bytes);
+          NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+          NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+          NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+          NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+          carve = static_cast<int>(std::min<long>(100, (100L * bps * (sb + reserved) + smem_sm - 1) / smem_sm));
+        }
+        if (std::getenv("NSD_VERBOSE"))
+          std::fprintf(stderr, "nsd batch: %d envs, %d blocks/SM, row pool %d elems/env (full %d, %zu B/block), carveout %d\n",
+                       n_env, bps, region, full, smem_bytes, carve);
+      }
+      if (const char* e = std::getenv("NSD_L1_CARVEOUT")) carve = std::atoi(e);
       NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
       NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
       NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
       NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 32>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     } else {
-      const int sb = static_cast<int>(smem_bytes);
-      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
-      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
-      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
-      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
-      NSD_CK(cudaFuncSetAttribute(k_batch_block<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb));
+      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+      cudaFuncAttributes fa{};
+      NSD_CK(cudaFuncGetAttributes(&fa, k_batch_block<R>));  // static reduction buffer counts against the limit
+      NSD_CK(cudaFuncSetAttribute(k_batch_block<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  max_optin - static_cast<int>(fa.sharedSizeBytes)));
     }
     coldr.alloc(sizeof(R) * plan.coldR * n_env);
     coldi.alloc(sizeof(int) * plan.coldI * n_env);
@@ -1079,8 +1160,30 @@ template <class R> struct Batch final : BatchBase {
     info[3] = H.nj;
     info[4] = H.rows_static + 3 * maxc;
     info[5] = team_threads;
+    if (std::getenv("NSD_PHASE_TIMING")) {
+      ptime.alloc(sizeof(unsigned long long) * 16);
+      NSD_CK(cudaMemset(ptime.p, 0, sizeof(unsigned long long) * 16));
+    }
   }
   ~Batch() override {
+    if (ptime.p) {  // diagnostics: cycles per phase summed over envs (team leaders)
+      unsigned long long h[16];
+      cudaStreamSynchronize(stream);
+      cudaMemcpy(h, ptime.p, sizeof(h), cudaMemcpyDeviceToHost);
+      static const char* names[16] = {"torque+setup+collide", "assemble", "momentum", "b/precond+tail",
+                                      "pcr A (p,ap,den)", "pcr B (trial norms)", "pcr commit", "pcr stage J^T z",
+                                      "pcr bodies H^-1", "pcr J w (+za)", "du/NaN", "update+integrate",
+                                      "final assemble", "incidence+rowblk", "", ""};
+      unsigned long long tot = 0, solver = 0;
+      for (int k = 0; k < 13; ++k) tot += h[k];
+      for (int k = 1; k < 13; ++k) solver += h[k];
+      h[13] = h[13] > solver ? h[13] - solver : 0;  // batch_env's clock spans incidence + the solver
+      tot += h[13];
+      std::fprintf(stderr, "nsd phase timing (%d envs, %s):\n", n_env, sizeof(R) == 8 ? "fp64" : "fp32");
+      for (int k = 0; k < 14; ++k)
+        std::fprintf(stderr, "  %-24s %6.2f%%  %.3g cycles/env\n", names[k], tot ? 100.0 * h[k] / tot : 0.0,
+                     double(h[k]) / n_env);
+    }
     if (stream && own_stream) cudaStreamDestroy(stream);
   }
   void set_state(const double* q, const double* u) override {
@@ -1127,6 +1230,8 @@ template <class R> struct Batch final : BatchBase {
     A.maxc = maxc;
     A.envs_per_block = envs_per_block;
     A.hot_in_smem = hot_in_smem ? 1 : 0;
+    A.row_pool = row_pool;
+    A.ptime = ptime.as<unsigned long long>();
     A.pairs = pairs.as<int2>();
     A.shapes = shapes.as<nsd::ShapeD<R>>();
     A.jframe = topo.jframe;

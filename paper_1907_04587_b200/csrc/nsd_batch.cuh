@@ -220,6 +220,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
   const int maxlin = cfg.linear_max_iterations;
   const R eps = R(cfg.epsilon_reg);
   const R tfrac = R(cfg.step_fraction);
+  PhaseClock pc(out.ptime, rk == 0);
   for_my_rows(T, W, rk, ts, [&](int i) { W.lam[i] = R(0); });
   t.sync();
   double min_shift = 0.0;
@@ -234,6 +235,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
         assemble_contact(T, W, W.q, W.u, k - T.nj, h, cfg, as);
     }
     t.sync();
+    pc.mark(1);
     // ---- g = M~(u - u~) - J^T lambda, geometric stiffness, H^-1, w = H^-1 g
     stage_objects(T, O, rk, ts, RowArr<R>{W.lam});
     t.sync();
@@ -252,6 +254,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
     io.linear_residual = 0.0;
     io.linear_breakdown = 0;
     io.step_size = 0.0;
+    pc.mark(2);
     // ---- b = J H^-1 g - h, diagonal preconditioner, r = b, x = 0
     double rr = 0.0, rzr = 0.0;
     for (int k = rk; k < nobj; k += ts) {
@@ -303,6 +306,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
         t.reduce_sum(s);
         zaz = s[0];
       }
+      pc.mark(3);
       double beta = 0.0;
       for (int itl = 0; itl < maxlin && hist_last > cfg.linear_tolerance; ++itl) {
         // phase A (owned rows): p = z + beta p, ap = az + beta ap; den = ap . M^-1 ap
@@ -328,6 +332,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
           t.reduce_sum(s);
           den = s[0];
         }
+        pc.mark(4);
         if (fabs(den) < 1e-300) {
           breakdown = 1;
           break;
@@ -348,6 +353,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
           pn2 = s[0];
           rn2 = s[1];
         }
+        pc.mark(5);
         const double pn = sqrt(pn2);
         if (pn > phist_last) break;  // monotone guard: stop at the numerical floor
         pend = ra;                   // accepted; committed by the owner lanes below
@@ -375,10 +381,13 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
         });
         pend = R(0);
         pending_best = false;
+        pc.mark(6);
         stage_objects(T, O, rk, ts, RowArr<R>{W.z});
         t.sync();
+        pc.mark(7);
         bodies_apply_hinv(T, O, rk, ts);
         t.sync();
+        pc.mark(8);
         R za_p = R(0);
         for (int k = rk; k < nobj; k += ts)
           object_Jw(T, W, k, W.w, [&](int i, R jw) {
@@ -393,6 +402,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
           beta = s[0] / zaz;
           zaz = s[0];
         }
+        pc.mark(9);
       }
       if (pending_best || pend != R(0)) {
         for_my_rows(T, W, rk, ts, [&](int i) {
@@ -402,6 +412,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
         });
       }
     }
+    pc.mark(3);
     io.linear_iterations = lin_used;
     io.linear_breakdown = breakdown;
     io.linear_residual = hist_n > 0 ? hist_last : 0.0;
@@ -437,6 +448,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
       du2 = s[1];
       bad = m[0];
     }
+    pc.mark(10);
     if (bad != 0.0) {
       for (int i = rk; i < T.ncoord; i += ts) W.q[i] = W.q0[i];
       for (int i = rk; i < T.ndof; i += ts) W.u[i] = W.u0[i];
@@ -460,6 +472,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
     }
     n_done = it + 1;
     t.sync();
+    pc.mark(11);
   }
   if (aborted) {
     if (rk == 0 && out.fin) {
@@ -504,6 +517,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
       out.fin[7] = n_done;
     }
   }
+  pc.mark(12);
   return 0;
 }
 

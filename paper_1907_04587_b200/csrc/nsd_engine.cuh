@@ -133,6 +133,23 @@ struct StepOut {
   int* hist_len;   // newton_iterations (may be null)
   double* tel;     // 6 per contact (may be null)
   double* fin;     // 8: final_residual_inf, final_comp, final_cone, min_gap, min_diag_shift, aborted, converged, n_iterations
+  unsigned long long* ptime;  // diagnostics (NSD_PHASE_TIMING): clock64 cycles per solver phase, or null
+};
+
+// Phase clock for diagnostics: adds the cycles since the last mark to slot k.
+struct PhaseClock {
+  unsigned long long* dst;
+  long long t0;
+  __device__ explicit PhaseClock(unsigned long long* d, bool leader) : dst(leader ? d : nullptr), t0(0) {
+    if (dst) t0 = clock64();
+  }
+  __device__ __forceinline__ void mark(int k) {
+    if (dst) {
+      const long long t = clock64();
+      atomicAdd(dst + k, static_cast<unsigned long long>(t - t0));
+      t0 = t;
+    }
+  }
 };
 
 // ------------------------------------------------------------------ helpers
