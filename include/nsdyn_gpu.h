@@ -191,6 +191,17 @@ int nsd_scene_shapes(const nsd_scene* s, nsd_shape* shapes, double* margin, doub
 int nsd_scene_state(const nsd_scene* s, double* q, double* u);
 int nsd_scene_config(const nsd_scene* s, nsd_config* cfg, double* h, double* gravity);
 int nsd_scene_destroy(nsd_scene* s);
+/* Current joint frames (21 per joint, nsd_topology layout; driven anchors move). */
+int nsd_scene_joint_frames(const nsd_scene* s, double* frames);
+/* Moves the world-side anchors of driven joints by h * anchor_velocity
+ * (step_world's first statement, scene.cpp:710-716). */
+int nsd_scene_advance_anchors(nsd_scene* s);
+/* Caller side of step_world on the host (scene.cpp:717-721): u~ from (q, u,
+ * optional f_extra), narrow phase over the scene's shapes plus the particle
+ * generators, predicted-gap rule, canonical order (collision.cpp:239-297).
+ * *n receives the contact count; NSD_INVALID if it exceeds capacity. */
+int nsd_scene_detect(const nsd_scene* s, const double* q, const double* u, const double* f_extra, int32_t capacity,
+                     nsd_contact* out, int32_t* n);
 /* Initial states of n copies of a seeded builder (seed0 .. seed0+n-1), e.g. the
  * per-environment C5 ants: q n*num_coord, u n*num_dof. */
 int nsd_scene_batch_state(const char* name, uint32_t seed0, int32_t n, double* q, double* u);

@@ -21,7 +21,7 @@ from . import _lib
 from ._lib import (NSD_ABORTED, NSD_FP32, NSD_FP64, NSD_OK, NsdError, check, lib, nsd_config, nsd_contact,
                    nsd_iter_stats, nsd_shape, nsd_step_in, nsd_step_out, nsd_topology)
 
-__all__ = ["NewtonConfig", "NewtonSolver", "BatchSolver", "Scene", "contacts_from_arrays", "contacts_to_arrays",
+__all__ = ["NewtonConfig", "NewtonSolver", "BatchSolver", "Scene", "World", "contacts_from_arrays", "contacts_to_arrays",
            "count_rows", "NsdError"]
 
 _R_STRAT = {"identity": 0, "h2": 1, "effmass": 2}
@@ -251,6 +251,80 @@ class Scene:
         self.config, self.h, self.gravity = NewtonConfig.from_c(cfg), hh.value, g
         lib().nsd_scene_destroy(h)
         self._h = None
+
+
+class World:
+    """World + step_world (scene.h:83-110, scene.cpp:709-732): a built scene whose
+    step() moves driven anchors, runs the caller-side contact detection on the
+    host at (q, u~) — as the reference does — and then the Newton step on the
+    GPU through nsd_step. `contacts` holds the step's contact arrays with the
+    multipliers written back; `report` the SolveReport of the last step."""
+
+    def __init__(self, name: str, seed: int = 0, precision: str | None = None, contact_capacity: int = 4096):
+        self.scene = Scene(name, seed)
+        h = C.c_void_p()
+        check(lib().nsd_scene_build(name.encode(), seed, C.byref(h)))
+        self._h = h
+        self.topology = self.scene.topology
+        self.config = self.scene.config
+        if precision is not None:
+            self.config.precision = precision
+        self.h, self.gravity = self.scene.h, self.scene.gravity
+        self.q, self.u = self.scene.q.copy(), self.scene.u.copy()
+        self.f_extra = None
+        self.cap = contact_capacity
+        self._buf = (nsd_contact * contact_capacity)()
+        self.solver = None  # created at the first step (device memory)
+        self.contacts = None
+        self.report = None
+        self.time = 0.0
+
+    def joint_frames(self):
+        fr = np.zeros(21 * self.topology.n_joints)
+        if fr.size:
+            check(lib().nsd_scene_joint_frames(self._h, _dp(fr)))
+        return fr
+
+    def detect(self):
+        n = C.c_int32()
+        fx = _dp(self.f_extra) if self.f_extra is not None else None
+        rc = lib().nsd_scene_detect(self._h, _dp(self.q), _dp(self.u), fx, self.cap,
+                                    C.cast(self._buf, C.POINTER(nsd_contact)), C.byref(n))
+        if rc != NSD_OK and n.value > self.cap:
+            self.cap = 2 * n.value
+            self._buf = (nsd_contact * self.cap)()
+            return self.detect()
+        check(rc)
+        return contacts_to_arrays(self._buf, n.value)
+
+    def step(self, n: int = 1):
+        """n x step_world; returns the last SolveReport (dict) — aborted steps roll back and are reported."""
+        for _ in range(n):
+            if self.solver is None:
+                self.solver = NewtonSolver(self.topology, self.config)
+            check(lib().nsd_scene_advance_anchors(self._h))
+            self.contacts = self.detect()
+            self.report = self.solver.newton_step(self.q, self.u, self.contacts, h=self.h,
+                                                  gravity=tuple(self.gravity), f_extra=self.f_extra,
+                                                  joint_frame=self.joint_frames())
+            self.q, self.u = self.report["q"], self.report["u"]
+            self.contacts = self.report.get("contacts", self.contacts)
+            self.time += self.h
+        return self.report
+
+    def close(self):
+        if self._h:
+            lib().nsd_scene_destroy(self._h)
+            self._h = None
+        if self.solver is not None:
+            self.solver.close()
+            self.solver = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def batch_states(name: str, seed0: int, n: int, num_coord: int, num_dof: int):

@@ -74,7 +74,8 @@ EXPORTS = [
     "nsd_batch_set_stream", "nsd_batch_step", "nsd_batch_step_device", "nsd_batch_sync", "nsd_batch_results",
     "nsd_batch_contacts", "nsd_batch_device_state", "nsd_batch_copy_state_async", "nsd_batch_info", "nsd_batch_destroy", "nsd_scene_build",
     "nsd_scene_dims", "nsd_scene_topology", "nsd_scene_shapes", "nsd_scene_state", "nsd_scene_config",
-    "nsd_scene_destroy", "nsd_scene_batch_state",
+    "nsd_scene_destroy", "nsd_scene_batch_state", "nsd_scene_joint_frames", "nsd_scene_advance_anchors",
+    "nsd_scene_detect",
 ]
 
 _lib = None
@@ -126,6 +127,9 @@ def lib():
     L.nsd_scene_state.argtypes = [C.c_void_p, D, D]
     L.nsd_scene_config.argtypes = [C.c_void_p, C.POINTER(nsd_config), D, D]
     L.nsd_scene_destroy.argtypes = [C.c_void_p]
+    L.nsd_scene_joint_frames.argtypes = [C.c_void_p, D]
+    L.nsd_scene_advance_anchors.argtypes = [C.c_void_p]
+    L.nsd_scene_detect.argtypes = [C.c_void_p, D, D, D, C.c_int32, C.POINTER(nsd_contact), I32]
     _lib = L
     return L
 

@@ -5,8 +5,10 @@
 // follow SURVEY.md Appendix C with the deviations recorded in DESIGN.md.
 #include "nsd_scene.h"
 
+#include "nsd_collide.cuh"
 #include "nsd_math.cuh"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -702,6 +704,123 @@ int nsd_scene_config(const nsd_scene* s, nsd_config* cfg, double* h, double* gra
 
 int nsd_scene_destroy(nsd_scene* s) {
   delete s;
+  return NSD_OK;
+}
+
+int nsd_scene_joint_frames(const nsd_scene* s, double* frames) {
+  if (!s || !frames) return NSD_INVALID;
+  if (!s->w.joint_frame.empty())
+    std::memcpy(frames, s->w.joint_frame.data(), sizeof(double) * s->w.joint_frame.size());
+  return NSD_OK;
+}
+
+// step_world's first statement (scene.cpp:710-716): world-side anchors of driven
+// joints move by h * anchor_velocity.
+int nsd_scene_advance_anchors(nsd_scene* s) {
+  if (!s) return NSD_INVALID;
+  nsdw::World& w = s->w;
+  for (const auto& dv : w.driven) {
+    const int j = dv.first;
+    double* fr = &w.joint_frame[21 * static_cast<size_t>(j)];
+    double* anchor = w.joint_body[2 * j] < 0 ? fr : (w.joint_body[2 * j + 1] < 0 ? fr + 3 : nullptr);
+    if (!anchor) continue;
+    anchor[0] += w.h * dv.second.x;
+    anchor[1] += w.h * dv.second.y;
+    anchor[2] += w.h * dv.second.z;
+  }
+  return NSD_OK;
+}
+
+// The caller side of step_world (scene.cpp:717-721) on the host, as in the
+// reference: u~ = u + h M~^-1 (f_gravity + f_gyro + f_extra) at q
+// (bodies.cpp:200-217), then the narrow phase over shape pairs and the
+// particle generators with the predicted-gap rule, in canonical
+// (a.body, b.body, feature) order (collision.cpp:239-297). The Newton step
+// that consumes the contacts runs on the GPU (nsd_step).
+int nsd_scene_detect(const nsd_scene* s, const double* q, const double* u, const double* f_extra, int32_t capacity,
+                     nsd_contact* out, int32_t* n) {
+  if (!s || !q || !u || !n || capacity < 0 || (capacity > 0 && !out)) return NSD_INVALID;
+  using V = nsd::V3<double>;
+  using M = nsd::M3<double>;
+  const nsdw::World& w = s->w;
+  const int nb = static_cast<int>(w.body_type.size());
+  std::vector<double> ut(static_cast<size_t>(w.num_dof));
+  const double h = w.h;
+  for (int b = 0; b < nb; ++b) {
+    const int d = w.dof_off[b], cd = w.coord_off[b];
+    const double m = w.body_mass[b];
+    V f = nsd::v3(m * w.gravity.x, m * w.gravity.y, m * w.gravity.z);
+    if (f_extra) f = f + nsd::v3(f_extra[d], f_extra[d + 1], f_extra[d + 2]);
+    for (int k = 0; k < 3; ++k) ut[d + k] = u[d + k] + h * (f[k] / m);
+    if (w.body_type[b] == 1) {
+      const M Rm = nsd::quat_rot(q[cd + 3], q[cd + 4], q[cd + 5], q[cd + 6]);
+      M I;
+      for (int i = 0; i < 9; ++i) I.a[i] = w.body_inertia[9 * static_cast<size_t>(b) + i];
+      const M Iw = nsd::mul(nsd::mul(Rm, I), nsd::transpose(Rm));
+      const M Ii = nsd::inverse3(Iw);
+      const V om = nsd::v3(u[d + 3], u[d + 4], u[d + 5]);
+      V tq = -nsd::cross(om, nsd::mul(Iw, om));
+      if (f_extra) tq = tq + nsd::v3(f_extra[d + 3], f_extra[d + 4], f_extra[d + 5]);
+      const V un = om + h * nsd::mul(Ii, tq);
+      for (int k = 0; k < 3; ++k) ut[d + 3 + k] = un[k];
+    }
+  }
+  nsd::BodyView<double> view{w.body_type.data(), w.dof_off.data(), w.coord_off.data(), q, ut.data()};
+  std::vector<nsd::ShapeD<double>> sh(w.shapes.size());
+  for (size_t i = 0; i < w.shapes.size(); ++i) {
+    const nsd_shape& a = w.shapes[i];
+    nsd::ShapeD<double>& d = sh[i];
+    d.body = a.body;
+    d.kind = a.kind;
+    for (int k = 0; k < 3; ++k) {
+      d.n[k] = a.normal[k];
+      d.he[k] = a.half_extents[k];
+    }
+    d.offset = a.offset;
+    d.radius = a.radius;
+    d.thick = a.thickness;
+    d.mu = a.mu;
+  }
+  std::vector<nsd::CandD<double>> cands;
+  nsd::CandD<double> c4[4];
+  double th = 0.0, mu = 0.0;
+  for (size_t i = 0; i < sh.size(); ++i)
+    for (size_t j = i + 1; j < sh.size(); ++j) {
+      const int k = nsd::pair_contacts(view, sh[i], sh[j], h, w.margin, w.mu_default, c4, &th, &mu);
+      cands.insert(cands.end(), c4, c4 + k);
+    }
+  for (const auto& pr : w.particle_ranges)
+    for (int b = pr.first; b < pr.first + pr.second; ++b)
+      for (const auto& shape : sh) {
+        const int k = nsd::particle_shape_contact(view, b, shape, h, w.margin, w.mu_default, 0.0, -1.0, c4, &th, &mu);
+        cands.insert(cands.end(), c4, c4 + k);
+      }
+  std::stable_sort(cands.begin(), cands.end(), [](const nsd::CandD<double>& x, const nsd::CandD<double>& y) {
+    return nsd::canonical_less(x.a, x.b, x.feature, y.a, y.b, y.feature);
+  });
+  *n = static_cast<int32_t>(cands.size());
+  if (static_cast<int32_t>(cands.size()) > capacity) return NSD_INVALID;  // *n tells the caller the size needed
+  for (size_t i = 0; i < cands.size(); ++i) {
+    const nsd::CandD<double>& c = cands[i];
+    nsd_contact& o = out[i];
+    std::memset(&o, 0, sizeof(o));
+    o.body_a = c.a;
+    o.body_b = c.b;
+    o.feature = c.feature;
+    for (int k = 0; k < 3; ++k) {
+      o.local_a[k] = c.la[k];
+      o.local_b[k] = c.lb[k];
+      o.normal[k] = c.n[k];
+    }
+    V d1, d2;
+    nsd::tangent_basis(nsd::v3(c.n[0], c.n[1], c.n[2]), d1, d2);
+    for (int k = 0; k < 3; ++k) {
+      o.d1[k] = d1[k];
+      o.d2[k] = d2[k];
+    }
+    o.thickness = c.thick;
+    o.mu = c.mu;
+  }
   return NSD_OK;
 }
 

@@ -73,3 +73,42 @@ def decision_mismatches(g, o, tol, floor_ratio=1e-9):
         if not borderline:
             bad += 1
     return mism, bad
+
+
+def oracle_self_divergence(name, seed=0, warm_steps=0, eps=1e-15, trials=3, overrides=None):
+    """Rounding sensitivity of one newton_step at a state: the largest relative
+    change of the ORACLE's own (q, u) when its input q is perturbed by eps
+    (relative, a few ulp). Where the PCR stops far from convergence (stiff FEM
+    with the 1e12 friction-W cap, or a Fischer-Burmeister decision taken at the
+    origin) two correct implementations that associate sums differently can
+    differ by this much; GPU-vs-oracle tolerances there are stated as a
+    multiple of it."""
+    ref = run_oracle(oracle_case(name, seed, warm_steps, overrides))
+    worst_q = worst_u = 0.0
+    for t in range(trials):
+        c = oracle_case(name, seed, warm_steps, overrides)
+        w = c["world"]
+        q, u = w.state()
+        rng = np.random.default_rng(1000 + t)
+        w.set_state(q * (1.0 + eps * rng.standard_normal(q.size)), u)
+        w.prepare()
+        p = run_oracle(c)
+        worst_q = max(worst_q, rel_err(p["q"], ref["q"]))
+        worst_u = max(worst_u, rel_err(p["u"], ref["u"], floor=1e-6))
+    return worst_q, worst_u
+
+
+def oracle_trajectory(name, seed, steps, perturb=0.0, perturb_seed=0):
+    """q, u after each of `steps` oracle step_world calls (optionally from a
+    relatively perturbed initial q), plus the per-step contact index arrays."""
+    w = O.OracleWorld(name, seed)
+    if perturb:
+        q, u = w.state()
+        rng = np.random.default_rng(perturb_seed)
+        w.set_state(q * (1.0 + perturb * rng.standard_normal(q.size)), u)
+    out = []
+    for _ in range(steps):
+        rc = w.step(1)
+        q, u = w.state()
+        out.append((q, u, w.contacts()[0], rc))
+    return out
