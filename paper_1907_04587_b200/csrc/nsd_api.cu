@@ -301,7 +301,7 @@ template <class R> struct DevTopo {
 struct WorkPlan {
   // hot R
   size_t q, u, g, w, du, hinv, iwi6, coeff, hv, cd, lam, x, r, z, p, ap, az, inv, bx, cdir, carm, cscale, jstage,
-      cstage, hotR;
+      cstage, jstr, hotR;
   // hot int
   size_t blk, cbody, cinc_off, cinc_ent, cbinc_off, cbinc, hotI;
   // cold R
@@ -345,6 +345,7 @@ struct WorkPlan {
     cscale = a(2 * c);
     jstage = a(12 * static_cast<size_t>(T.nj));
     cstage = a(9 * c);
+    jstr = a(24 * static_cast<size_t>(T.nj));
     hotR = o;
     o = 0;
     blk = a(4 * rs);
@@ -629,7 +630,7 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
         if (cbody[2 * c + 1] == b) cbinc[o++] = 2 * c + 1;
       }
     }
-    nsd::setup_row_blocks<R, false>(t, T, W);
+    W.jstr = hr + P.jstr;  // structured joint rows: the object solver never reads coeff/blk
     t.sync();
     nsd::ObjView<R> O{W, hr + P.jstage, hr + P.cstage, A.jbinc_off, A.jbinc, cboff, cbinc};
     if (pool && row_pool_elems(T.rows_static, T.nj, T.ndof, nc) <= A.row_pool) {

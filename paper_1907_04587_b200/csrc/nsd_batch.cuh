@@ -30,6 +30,24 @@ template <class R> struct ObjView {
   int* cbinc;       // contact*2 + side
 };
 
+// Structured joint (W.jstr, written by assemble_joint): bodies' dof3 blocks, the
+// point / axis row counts of the kind (joint_rows, constraints.cpp:141-220) and
+// the 24 values: arm_a, arm_b, point directions D0..D2, axis vectors C0..C2.
+template <class R> struct JView {
+  int al, aa, bl, bA, np, na;
+  const R* s;
+};
+template <class R> __device__ __forceinline__ JView<R> joint_view(const Topo<R>& T, const Work<R>& W, int j) {
+  JView<R> v;
+  body_blocks(T, T.jbody[2 * j], v.al, v.aa);
+  body_blocks(T, T.jbody[2 * j + 1], v.bl, v.bA);
+  const int kind = T.jkind[j];
+  v.np = kind <= 1 ? 3 : (kind == 2 ? 2 : 0);
+  v.na = kind == 0 ? 0 : (kind == 2 ? 3 : 2);
+  v.s = W.jstr + 24 * j;
+  return v;
+}
+
 // Runs f(row) over the rows owned by this lane (objects lane, lane+32, ...).
 template <class R, class F> __device__ __forceinline__ void for_my_rows(const Topo<R>& T, const Work<R>& W, int rk, int ts,
                                                                         F&& f) {
@@ -55,19 +73,17 @@ __device__ __forceinline__ void stage_objects(const Topo<R>& T, ObjView<R>& O, i
   const int nobj = T.nj + W.nc;
   for (int k = rk; k < nobj; k += ts) {
     if (k < T.nj) {
-      const int r0 = T.jrow[k], n = joint_nrows(T.jkind[k]);
-      R s[12];
-#pragma unroll
-      for (int q = 0; q < 12; ++q) s[q] = R(0);
-      for (int i = 0; i < n; ++i) {
-        const R yr = y(r0 + i);
-        const R* c = W.coeff + 12 * (r0 + i);
-#pragma unroll
-        for (int q = 0; q < 12; ++q) s[q] += c[q] * yr;
-      }
+      // J^T y of a joint: point rows sum to a force f at the anchors, axis rows to a torque
+      const JView<R> jv = joint_view(T, W, k);
+      const int r0 = T.jrow[k];
+      V3<R> f = v3(R(0), R(0), R(0)), ta = f;
+      for (int i = 0; i < jv.np; ++i) f = f + y(r0 + i) * ld3(jv.s + 6 + 3 * i);
+      for (int i = 0; i < jv.na; ++i) ta = ta + y(r0 + jv.np + i) * ld3(jv.s + 15 + 3 * i);
       R* d = O.jstage + 12 * k;
-#pragma unroll
-      for (int q = 0; q < 12; ++q) d[q] = s[q];
+      st3(d, f);
+      st3(d + 3, cross(ld3(jv.s), f) + ta);
+      st3(d + 6, -f);
+      st3(d + 9, -(cross(ld3(jv.s + 3), f) + ta));
     } else {
       const int c = k - T.nj;
       const R* g = W.cdir + 9 * c;
@@ -125,8 +141,27 @@ template <class R> __device__ __forceinline__ void bodies_apply_hinv(const Topo<
 template <class R, class F>
 __device__ __forceinline__ void object_Jw(const Topo<R>& T, const Work<R>& W, int k, const R* w, F&& f) {
   if (k < T.nj) {
-    const int r0 = T.jrow[k], n = joint_nrows(T.jkind[k]);
-    for (int i = 0; i < n; ++i) f(r0 + i, slot_dot(W.coeff + 12 * (r0 + i), W.blk + 4 * (r0 + i), w));
+    // relative anchor velocity (point rows) and relative angular velocity (axis rows)
+    const JView<R> jv = joint_view(T, W, k);
+    const int r0 = T.jrow[k];
+    V3<R> dv = v3(R(0), R(0), R(0)), wr = dv;
+    if (jv.al >= 0) {
+      dv = ld3(w + 3 * jv.al);
+      if (jv.aa >= 0) {
+        wr = ld3(w + 3 * jv.aa);
+        dv = dv + cross(wr, ld3(jv.s));
+      }
+    }
+    if (jv.bl >= 0) {
+      dv = dv - ld3(w + 3 * jv.bl);
+      if (jv.bA >= 0) {
+        const V3<R> wb = ld3(w + 3 * jv.bA);
+        dv = dv - cross(wb, ld3(jv.s + 3));
+        wr = wr - wb;
+      }
+    }
+    for (int i = 0; i < jv.np; ++i) f(r0 + i, dot(ld3(jv.s + 6 + 3 * i), dv));
+    for (int i = 0; i < jv.na; ++i) f(r0 + jv.np + i, dot(ld3(jv.s + 15 + 3 * i), wr));
   } else {
     const int c = k - T.nj;
     const CView<R> cv = contact_view(T, W, c);
@@ -142,8 +177,25 @@ __device__ __forceinline__ void object_Jw(const Topo<R>& T, const Work<R>& W, in
 template <class R, class F>
 __device__ __forceinline__ void object_quad(const Topo<R>& T, const Work<R>& W, int k, F&& f) {
   if (k < T.nj) {
-    const int r0 = T.jrow[k], n = joint_nrows(T.jkind[k]);
-    for (int i = 0; i < n; ++i) f(r0 + i, slot_quad(T, W, W.coeff + 12 * (r0 + i), W.blk + 4 * (r0 + i), true));
+    const JView<R> jv = joint_view(T, W, k);
+    const int r0 = T.jrow[k];
+    const V3<R> arm_a = ld3(jv.s), arm_b = ld3(jv.s + 3);
+    for (int i = 0; i < jv.np; ++i) {  // slot order a.lin, a.ang, b.lin, b.ang as slot_quad
+      const V3<R> d = ld3(jv.s + 6 + 3 * i);
+      R q = R(0);
+      if (jv.al >= 0) q += block_quad(T, W, jv.al, d, true);
+      if (jv.aa >= 0) q += block_quad(T, W, jv.aa, cross(arm_a, d), true);
+      if (jv.bl >= 0) q += block_quad(T, W, jv.bl, d, true);
+      if (jv.bA >= 0) q += block_quad(T, W, jv.bA, cross(arm_b, d), true);
+      f(r0 + i, q);
+    }
+    for (int i = 0; i < jv.na; ++i) {
+      const V3<R> c = ld3(jv.s + 15 + 3 * i);
+      R q = R(0);
+      if (jv.aa >= 0) q += block_quad(T, W, jv.aa, c, true);
+      if (jv.bA >= 0) q += block_quad(T, W, jv.bA, c, true);
+      f(r0 + jv.np + i, q);
+    }
   } else {
     const int c = k - T.nj;
     const CView<R> cv = contact_view(T, W, c);

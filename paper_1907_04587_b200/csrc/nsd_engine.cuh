@@ -109,6 +109,7 @@ template <class R> struct Work {
   int nrows, normal_begin, friction_begin;
   R* coeff;  // 12 per static row
   int* blk;  // 4 per static row
+  R* jstr;   // batched path: 24 per joint (structured rows, see assemble_joint) or null
   R* hv;
   R* cd;
   R* ctet;   // 9 per tet
@@ -445,7 +446,21 @@ __device__ void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, 
     st.hmax = fmax(st.hmax, (double)ab(hv));
     st.hsq += (double)hv * (double)hv;
   };
+  // Structured form of the joint's rows (batched path): lever arms, point-row
+  // directions, axis-row angular vectors. A point row along d has J = [d | arm_a x d
+  // | -d | -(arm_b x d)] (arm_a gains -(w_a - w_b) for prismatic: ra x d + d x t =
+  // (ra - t) x d, constraints.cpp:195-196); an axis row J = [0 | c | 0 | -c].
+  R* js = W.jstr ? W.jstr + 24 * j : nullptr;
+  if (js) {
+    st3(js, kind == 2 && rig_a ? ra - (wa - wb) : ra);
+    st3(js + 3, rb);
+  }
   auto point_row = [&](int k, V3<R> d, R value, bool prism) {
+    if (js) {
+      st3(js + 6 + 3 * k, d);
+      emit(k, value, comp);
+      return;
+    }
     R* c = W.coeff + 12 * (r0 + k);
     const int* b = W.blk + 4 * (r0 + k);
 #pragma unroll
@@ -457,7 +472,13 @@ __device__ void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, 
     if (prism && rig_a) slot_add(c, b, 1, aa, cross(d, wa - wb));  // t x d (constraints.cpp:195-196)
     emit(k, value, comp);
   };
+  const int n_point = (kind == 0 || kind == 1) ? 3 : (kind == 2 ? 2 : 0);
   auto axis_row = [&](int k, V3<R> xa, V3<R> xb, R restv, R e) {
+    if (js) {
+      st3(js + 15 + 3 * (k - n_point), cross(xa, xb));
+      emit(k, dot(xa, xb) - restv, e);
+      return;
+    }
     R* c = W.coeff + 12 * (r0 + k);
     const int* b = W.blk + 4 * (r0 + k);
 #pragma unroll
