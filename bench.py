@@ -54,6 +54,9 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU baseline sample length")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-alt", action="store_true", help="skip the secondary-precision measurement")
+    p.add_argument("--workload", default="c5",
+                   help="c5 (default: batched ants, the headline) or one single scene (c1, c2, c3, c4, c2:6, ...) "
+                        "stepped through World.step (host detect + GPU newton_step)")
     return p.parse_args()
 
 
@@ -283,10 +286,77 @@ def roofline(m, prec, K):
             "model": "SURVEY 8(d) B_CR per env per CR iteration x 40 CR iterations x envs"}
 
 
+def run_scene(args):
+    """One scene per GPU (C1-C4 are replicas only): K x step_world through
+    the public World API. value = steps/s from the device time of each step's kernel
+    (CUDA events inside nsd_step), L2 flushed between steps; e2e = wall clock of
+    World.step (host detect + H2D + kernel + D2H)."""
+    import torch
+
+    from paper_1907_04587_b200 import World
+
+    ws, rank, local = dist_info()
+    torch.cuda.set_device(local)
+    K, W = args.steps, args.warmup
+    w = World(args.workload, 0, precision=args.precision)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(W):
+        w.step()
+    dev, wall, pcr = [], [], 0
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(K):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = w.step()
+        wall.append(time.perf_counter() - t0)
+        dev.append(rep["ms"])
+        pcr += int(sum(rep["stats"][:, 5]))
+    clocks = sampler.stop()
+    cfg = w.config
+    ms = float(np.mean(dev))
+    cr_budget = cfg.newton_iterations * cfg.linear_max_iterations
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import oracle_py as O
+
+        ow = O.OracleWorld(args.workload, 0)
+        ow.step(W)
+        n = 0
+        t0 = time.perf_counter()
+        while n < K and time.perf_counter() - t0 < args.cpu_seconds:
+            ow.step(1)
+            n += 1
+        t = time.perf_counter() - t0
+        cpu = {"value": n / t, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{args.workload}: oracle step_world steps {W}..{W + n} ({t:.2f} s)"}
+    line = {"metric": "steps/sec at fixed Newton/CR iters (single scene)", "value": 1000.0 / ms, "unit": "steps/s",
+            "n_gpus": 1, "steps": K, "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "bodies": w.scene.dims["n_bodies"], "tets": w.scene.dims["n_tets"],
+                       "newton_iterations": cfg.newton_iterations, "linear_iterations": cfg.linear_max_iterations,
+                       "parallelism": "replicas only", "l2": "flushed (256 MiB memset) between timed steps"},
+            "us_per_cr_iter_budget": 1000.0 * ms / cr_budget, "pcr_iterations_used_per_step": pcr / K,
+            "us_per_cr_iter_used": 1000.0 * ms * K / max(pcr, 1),
+            "mean_contacts": float(len(w.contacts[0])) if w.contacts is not None else 0.0,
+            "e2e": {"value": 1.0 / float(np.mean(wall)), "unit": "steps/s",
+                    "h2d_bytes_per_step": 8 * (w.scene.dims["num_coord"] + w.scene.dims["num_dof"]),
+                    "d2h_bytes_per_step": 8 * (w.scene.dims["num_coord"] + w.scene.dims["num_dof"])},
+            "gpu_launches": K, "clocks": clocks}
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    w.close()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.workload != "c5":
+        run_scene(args)
         return
     import torch
 

@@ -699,7 +699,7 @@ SceneDesc build_c3_chain(int links) {
   return s;
 }
 
-SceneDesc build_c4_hand_ball(int n) {
+SceneDesc build_c4_hand_ball(int n, double speed) {
   SceneDesc s;
   s.bodies.push_back(static_ground());  // palm surface
   // Ball: n^3 grid carved to a sphere of radius 0.05 by element centroid.
@@ -759,11 +759,11 @@ SceneDesc build_c4_hand_ball(int n) {
     drive.b.body = -1;
     drive.anchor = V3(rad * d[0], rad * d[1], 0.152);
     drive.compliance = 1e-4;
-    drive.anchor_velocity = V3(-0.05 * d[0], -0.05 * d[1], 0.0);
+    drive.anchor_velocity = V3(-kC4Drive * d[0], -kC4Drive * d[1], 0.0);
     s.joints.push_back(drive);
   }
   (void)bz;
-  ball.velocity = V3(0.0, 0.0, -1.0);
+  ball.velocity = V3(0.0, 0.0, -speed);
   ball.initial = ball.vertices;
   jitter_vertices(ball.initial, 1e-3 * edge / n, 7);
   s.meshes.push_back(ball);
@@ -848,7 +848,8 @@ bool build_scene_by_name(const std::string& name, unsigned seed, SceneDesc& out)
   else if (base == "c1") out = build_c1_box_stack();
   else if (base == "c2") out = build_c2_fem_block(args.size() > 0 ? static_cast<int>(args[0]) : 12);
   else if (base == "c3") out = build_c3_chain(args.size() > 0 ? static_cast<int>(args[0]) : 100);
-  else if (base == "c4") out = build_c4_hand_ball(args.size() > 0 ? static_cast<int>(args[0]) : 12);
+  else if (base == "c4")
+    out = build_c4_hand_ball(args.size() > 0 ? static_cast<int>(args[0]) : 12, args.size() > 1 ? args[1] : kC4Speed);
   else if (base == "c5") out = build_c5_ant(seed);
   else return false;
   return true;

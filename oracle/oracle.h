@@ -396,7 +396,10 @@ SceneDesc build_stretch_sheet(MatModel model);
 SceneDesc build_c1_box_stack();
 SceneDesc build_c2_fem_block(int n = 12);
 SceneDesc build_c3_chain(int links = 100);
-SceneDesc build_c4_hand_ball(int n = 12);
+// C4 initial ball speed (m/s, downward); "c4:<n>:<speed>" overrides it.
+constexpr double kC4Drive = 0.02;  // fingertip drive speed (m/s); 0.05 squeezes the ball unstable by step 29
+constexpr double kC4Speed = 0.2;  // 1.0 m/s blows up at step 4 (8 mm Neo-Hookean elements, 6x50 budget)
+SceneDesc build_c4_hand_ball(int n = 12, double speed = kC4Speed);
 SceneDesc build_c5_ant(unsigned env_id);
 bool build_scene_by_name(const std::string& name, unsigned seed, SceneDesc& out);
 

@@ -1055,7 +1055,11 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
         }
         const double alpha = zaz / den;
         const R ra = R(alpha);
-        // phase B: x' = x + a p, r' = r - a ap, z' = z - a M^-1 ap
+        // phase B: x' = x + a p, r' = r - a ap, z' = z - a M^-1 ap, trial norms; in the
+        // same pass (it needs only alpha) the J^T pull of z' for the next operator
+        // application, speculatively: the reduction's barrier then also orders the
+        // pull before the row pass, one grid barrier fewer per iteration. A rejected
+        // trial (monotone guard) discards it.
         double pn2 = 0.0, rn2 = 0.0;
         for (int i = t.rank(); i < nr; i += t.size()) {
           const R api = W.ap[i];
@@ -1068,6 +1072,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
           pn2 += (double)rv * (double)(W.inv[i] * rv);
           rn2 += (double)rv * rv;
         }
+        if (fabs(zaz) >= 1e-300) op_pull(t, T, W, RowPending<R>{z, W.inv, W.ap, ra});  // w = H^-1 J^T z'
         {
           double s[2] = {pn2, rn2};
           t.reduce_sum(s);
@@ -1103,9 +1108,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
           break;
         }
         double za = 0.0;
-        if (kInPlace) {
-          op_pull(t, T, W, RowPending<R>{z, W.inv, W.ap, pend});  // az = A z', zaz' = z' . az
-          t.sync();
+        if (kInPlace) {  // w = H^-1 J^T z' is already pulled (phase B); az = A z', zaz' = z' . az
           for (int i = t.rank(); i < nr; i += t.size()) {
             const R api = W.ap[i];
             const R zi = z[i] - pend * (W.inv[i] * api);
@@ -1119,9 +1122,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
             if (pending_best) W.bx[i] = xi;
           }
           pend = R(0);
-        } else {
-          op_pull(t, T, W, RowArr<R>{z});  // az = A z', zaz' = z' . az
-          t.sync();
+        } else {  // w pulled in phase B from z - a M^-1 ap, the same expression as the committed zn
           for (int i = t.rank(); i < nr; i += t.size()) {
             const R a = row_J(T, W, i, W.w) + row_C<R, kTets>(T, W, i, z) + eps * z[i];
             W.az[i] = a;

@@ -246,7 +246,7 @@ Scene s_c3(int links) {
   s.solver.linear_max_iterations = 40;
   return s;
 }
-Scene s_c4(int n) {
+Scene s_c4(int n, double speed) {
   Scene s;
   s.solver = defaults();
   s.bodies.push_back(ground());
@@ -297,10 +297,10 @@ Scene s_c4(int n) {
     dr.b.body = -1;
     dr.anchor = Vec3{rad * d.x, rad * d.y, 0.152};
     dr.compliance = 1e-4;
-    dr.anchor_velocity = Vec3{-0.05 * d.x, -0.05 * d.y, 0.0};
+    dr.anchor_velocity = Vec3{-0.02 * d.x, -0.02 * d.y, 0.0};  // 0.05 m/s squeezes the ball unstable by step 29
     s.joints.push_back(dr);
   }
-  ball.velocity = Vec3{0.0, 0.0, -1.0};
+  ball.velocity = Vec3{0.0, 0.0, -speed};
   ball.initial = ball.vertices;
   jitter(ball.initial, 1e-3 * edge / n, 7);
   ball.particle_contacts = true;
@@ -420,7 +420,9 @@ Scene build(const std::string& name, unsigned seed, bool* ok) {
   if (base == "c1") return s_c1();
   if (base == "c2") return s_c2(args.size() > 0 ? static_cast<int>(args[0]) : 12);
   if (base == "c3") return s_c3(args.size() > 0 ? static_cast<int>(args[0]) : 100);
-  if (base == "c4") return s_c4(args.size() > 0 ? static_cast<int>(args[0]) : 12);
+  // C4 drop speed 0.2 m/s: at 1.0 m/s the 8 mm Neo-Hookean elements blow up at step 4
+  // under the 6 x 50 budget (the reference then throws in spmv_transpose)
+  if (base == "c4") return s_c4(args.size() > 0 ? static_cast<int>(args[0]) : 12, args.size() > 1 ? args[1] : 0.2);
   if (base == "c5") return s_c5(seed);
   *ok = false;
   return Scene{};

@@ -63,9 +63,9 @@ def test_driven_anchor_frames_advance():
     _lib.check(_lib.lib().nsd_scene_advance_anchors(pw._h))
     f1 = pw.joint_frames()
     moved = np.nonzero(np.any(f0.reshape(-1, 21) != f1.reshape(-1, 21), axis=1))[0]
-    assert len(moved) == 4  # the four fingertip drives (anchor_velocity 0.05 m/s inward)
+    assert len(moved) == 4  # the four fingertip drives (anchor_velocity 0.02 m/s inward)
     d = (f1 - f0).reshape(-1, 21)[moved]
-    assert np.allclose(np.linalg.norm(d[:, 3:6], axis=1), 0.05 * pw.h)
+    assert np.allclose(np.linalg.norm(d[:, 3:6], axis=1), 0.02 * pw.h)
 
 
 # Rigid scenes: fixed stated tolerances. FEM scenes and the incline: the
