@@ -504,6 +504,7 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
   int* ci = A.cold_i + (size_t)env * P.coldI;
   nsd::Work<R> W = P.template bind<R>(hr, hi, cr, ci);
   nsd::PhaseClock pc(A.ptime, t.rank() == 0);
+  const long long env_t0 = A.ptime ? clock64() : 0;
   W.jframe = A.jframe;
   W.h = A.h;
   W.grav[0] = A.grav[0];
@@ -704,6 +705,11 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
   int* xb = ci + P.xcbody;
   for (int i = t.rank(); i < W.nrows; i += t.size()) xl[i] = W.lam[i];
   for (int i = t.rank(); i < 2 * nc; i += t.size()) xb[i] = cbody[i];
+  if (A.ptime && t.rank() == 0) {  // diagnostics: straggler vs mean env time, contacts of the slowest
+    const unsigned long long dt = static_cast<unsigned long long>(clock64() - env_t0);
+    atomicMax(A.ptime + 14, dt);
+    atomicAdd(A.ptime + 15, dt);
+  }
   if (t.rank() == 0) {
     A.nc_out[env] = nc;
     A.overflow[env] = total > A.maxc ? total : 0;
@@ -1103,6 +1109,14 @@ template <class R> struct Batch final : BatchBase {
         const int full = row_pool_elems(H.rows_static, H.nj, H.ndof, maxc);
         int region = static_cast<int>(budget / envs_per_block / static_cast<long>(sizeof(R))) & ~3;
         region = std::min(region, full);
+        // Region contact capacity (envs with more contacts use global memory): the rest
+        // of the unified L1/shared array stays L1 for the read-mostly data. Measured
+        // (C5, 4096 envs): fp32 best at 20-26 contacts (3.62 M env-steps/s
+        // vs 3.14 M sized for all 48 = 96% carveout); fp64 best filling the budget
+        // (~17 contacts). NSD_POOL_NC overrides.
+        int pool_nc = sizeof(R) == 4 ? 24 : maxc;
+        if (const char* e = std::getenv("NSD_POOL_NC")) pool_nc = std::max(1, std::atoi(e));
+        region = std::min(region, row_pool_elems(H.rows_static, H.nj, H.ndof, std::min(pool_nc, maxc)));
         const char* env_rp = std::getenv("NSD_ROW_SMEM");
         if (env_rp && std::atoi(env_rp) == 0) region = 0;
         if (region < row_pool_elems(H.rows_static, H.nj, H.ndof, 1)) region = 0;
@@ -1184,6 +1198,8 @@ template <class R> struct Batch final : BatchBase {
       for (int k = 0; k < 14; ++k)
         std::fprintf(stderr, "  %-24s %6.2f%%  %.3g cycles/env\n", names[k], tot ? 100.0 * h[k] / tot : 0.0,
                      double(h[k]) / n_env);
+      std::fprintf(stderr, "  env time: max %.3g cycles (one step), mean %.3g cycles per env-step\n", double(h[14]),
+                   double(h[15]) / std::max(1.0, double(launches) * n_env));
     }
     if (stream && own_stream) cudaStreamDestroy(stream);
   }
@@ -1220,7 +1236,9 @@ template <class R> struct Batch final : BatchBase {
     if (q) NSD_CK(cudaMemcpyAsync(q, qs.p, sizeof(R) * (size_t)H.ncoord * n_env, cudaMemcpyDefault, stream));
     if (u) NSD_CK(cudaMemcpyAsync(u, us.p, sizeof(R) * (size_t)H.ndof * n_env, cudaMemcpyDefault, stream));
   }
+  long launches = 0;  // diagnostics
   void step(const void* tq, int on_device, int dtype, double h, const double* g) override {
+    ++launches;
     if (!(h > 0.0)) throw NsdError(NSD_INVALID, "integrate_coordinates: h must be positive");
     BatchArgs<R> A{};
     A.T = topo.t;

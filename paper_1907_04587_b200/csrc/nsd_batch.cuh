@@ -391,13 +391,16 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
         }
         const double alpha = zaz / den;
         const R ra = R(alpha);
-        // phase B: trial residual norms
+        // phase B: trial residual norms; in the same pass (it needs only alpha) the
+        // speculative J^T staging of z' = z - alpha M^-1 ap — the reduction's barrier
+        // then orders it before the body pass. A rejected trial discards it.
         R pn2_p = R(0), rn2_p = R(0);
         for_my_rows(T, W, rk, ts, [&](int i) {
           const R rv = W.r[i] - ra * W.ap[i];
           pn2_p += rv * (W.inv[i] * rv);
           rn2_p += rv * rv;
         });
+        if (fabs(zaz) >= 1e-300) stage_objects(T, O, rk, ts, RowPending<R>{W.z, W.inv, W.ap, ra});
         double pn2, rn2;
         {
           double s[2] = {(double)pn2_p, (double)rn2_p};
@@ -408,7 +411,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
         pc.mark(5);
         const double pn = sqrt(pn2);
         if (pn > phist_last) break;  // monotone guard: stop at the numerical floor
-        pend = ra;                   // accepted; committed by the owner lanes below
+        pend = ra;                   // accepted; committed by the owner lanes in the J w pass
         hist_last = sqrt(rn2);
         phist_last = pn;
         if (rk == 0 && out.hist && hist_n <= maxlin) out.hist[(size_t)it * (maxlin + 1) + hist_n] = hist_last;
@@ -422,32 +425,29 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
           breakdown = 1;
           break;
         }
-        // commit x, r, z (owned rows) and stage J^T z'
-        for_my_rows(T, W, rk, ts, [&](int i) {
-          const R api = W.ap[i];
-          W.z[i] = W.z[i] - pend * (W.inv[i] * api);
-          const R xi = W.x[i] + pend * W.p[i];
-          W.x[i] = xi;
-          W.r[i] = W.r[i] - pend * api;
-          if (pending_best) W.bx[i] = xi;
-        });
-        pend = R(0);
-        pending_best = false;
         pc.mark(6);
-        stage_objects(T, O, rk, ts, RowArr<R>{W.z});
-        t.sync();
         pc.mark(7);
         bodies_apply_hinv(T, O, rk, ts);
         t.sync();
         pc.mark(8);
+        // commit x, r, z of the owned rows and az = A z', zaz' = z' . az in one pass
         R za_p = R(0);
+        const bool best = pending_best;
         for (int k = rk; k < nobj; k += ts)
           object_Jw(T, W, k, W.w, [&](int i, R jw) {
-            const R zi = W.z[i];
+            const R api = W.ap[i];
+            const R zi = W.z[i] - pend * (W.inv[i] * api);
+            const R xi = W.x[i] + pend * W.p[i];
+            W.z[i] = zi;
+            W.x[i] = xi;
+            W.r[i] = W.r[i] - pend * api;
+            if (best) W.bx[i] = xi;
             const R a = jw + W.cd[i] * zi + eps * zi;
             W.az[i] = a;
             za_p += zi * a;
           });
+        pend = R(0);
+        pending_best = false;
         {
           double s[1] = {(double)za_p};
           t.reduce_sum(s);
