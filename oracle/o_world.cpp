@@ -699,14 +699,16 @@ SceneDesc build_c3_chain(int links) {
   return s;
 }
 
-SceneDesc build_c4_hand_ball(int n, double speed) {
+SceneDesc build_c4_hand_ball(int n, double speed, double scale) {
   SceneDesc s;
   s.bodies.push_back(static_ground());  // palm surface
-  // Ball: n^3 grid carved to a sphere of radius 0.05 by element centroid.
-  const double radius = 0.05, edge = 0.1;
+  // Ball: n^3 grid carved to a sphere of radius 0.05 * scale by element centroid;
+  // every length of the hand scales with it, masses with scale^3.
+  const double L = scale;
+  const double radius = 0.05 * L, edge = 0.1 * L;
   MeshDesc grid;
-  tessellate_grid(grid, n, n, n, V3(-0.05, -0.05, 0.0), V3(edge, edge, edge));
-  const V3 centre(0.0, 0.0, 0.05);
+  tessellate_grid(grid, n, n, n, V3(-0.05 * L, -0.05 * L, 0.0), V3(edge, edge, edge));
+  const V3 centre(0.0, 0.0, 0.05 * L);
   std::vector<int> keep_v(grid.vertices.size(), -1);
   std::vector<std::array<int, 4>> kept;
   for (const auto& t : grid.elements) {
@@ -734,14 +736,15 @@ SceneDesc build_c4_hand_ball(int n, double speed) {
   ball.density = 1000.0;
   const double bz = centre[2] + lift;
   // Fingers: 4 planar chains of 4 phalanges standing around the ball.
-  const V3 he(0.008, 0.008, 0.012);
-  const double rad = 0.075, z_anchor[4] = {0.014, 0.050, 0.086, 0.122}, z_centre[4] = {0.032, 0.068, 0.104, 0.140};
+  const V3 he(0.008 * L, 0.008 * L, 0.012 * L);
+  const double rad = 0.075 * L, z_anchor[4] = {0.014 * L, 0.050 * L, 0.086 * L, 0.122 * L},
+               z_centre[4] = {0.032 * L, 0.068 * L, 0.104 * L, 0.140 * L};
   for (int f = 0; f < 4; ++f) {
     const double th = 0.5 * M_PI * f;
     const V3 d(std::cos(th), std::sin(th), 0.0);
     const V3 tang(-std::sin(th), std::cos(th), 0.0);
     for (int k = 0; k < 4; ++k) {
-      s.bodies.push_back(rigid_box(V3(rad * d[0], rad * d[1], z_centre[k]), he, 0.02,
+      s.bodies.push_back(rigid_box(V3(rad * d[0], rad * d[1], z_centre[k]), he, 0.02 * L * L * L,
                                    quat_axis_angle(V3(0, 0, 1), th)));
       JointDesc j;
       j.kind = JointKind::Revolute;
@@ -757,7 +760,7 @@ SceneDesc build_c4_hand_ball(int n, double speed) {
     drive.kind = JointKind::FixedPoint;
     drive.a.body = 1 + 4 * f + 3;
     drive.b.body = -1;
-    drive.anchor = V3(rad * d[0], rad * d[1], 0.152);
+    drive.anchor = V3(rad * d[0], rad * d[1], 0.152 * L);
     drive.compliance = 1e-4;
     drive.anchor_velocity = V3(-kC4Drive * d[0], -kC4Drive * d[1], 0.0);
     s.joints.push_back(drive);
@@ -849,7 +852,8 @@ bool build_scene_by_name(const std::string& name, unsigned seed, SceneDesc& out)
   else if (base == "c2") out = build_c2_fem_block(args.size() > 0 ? static_cast<int>(args[0]) : 12);
   else if (base == "c3") out = build_c3_chain(args.size() > 0 ? static_cast<int>(args[0]) : 100);
   else if (base == "c4")
-    out = build_c4_hand_ball(args.size() > 0 ? static_cast<int>(args[0]) : 12, args.size() > 1 ? args[1] : kC4Speed);
+    out = build_c4_hand_ball(args.size() > 0 ? static_cast<int>(args[0]) : 12, args.size() > 1 ? args[1] : kC4Speed,
+                             args.size() > 2 ? args[2] : kC4Scale);
   else if (base == "c5") out = build_c5_ant(seed);
   else return false;
   return true;

@@ -399,7 +399,9 @@ SceneDesc build_c3_chain(int links = 100);
 // C4 initial ball speed (m/s, downward); "c4:<n>:<speed>" overrides it.
 constexpr double kC4Drive = 0.02;  // fingertip drive speed (m/s); 0.05 squeezes the ball unstable by step 29
 constexpr double kC4Speed = 0.2;  // 1.0 m/s blows up at step 4 (8 mm Neo-Hookean elements, 6x50 budget)
-SceneDesc build_c4_hand_ball(int n = 12, double speed = kC4Speed);
+constexpr double kC4Scale = 2.0;  // ball radius 0.05 * scale (0.1 m); "c4:<n>:<speed>:<scale>". At 1.0 the 8 mm
+                                  // elements blow up by step 13-28 under the 6 x 50 budget; 2.0 is stable (45 steps)
+SceneDesc build_c4_hand_ball(int n = 12, double speed = kC4Speed, double scale = kC4Scale);
 SceneDesc build_c5_ant(unsigned env_id);
 bool build_scene_by_name(const std::string& name, unsigned seed, SceneDesc& out);
 

@@ -445,8 +445,13 @@ __global__ void __launch_bounds__(512) k_single_block(nsd::Topo<R> T, nsd::Work<
   nsd::newton_solve<R, kTets>(t, T, W, cfg, out);
 }
 
+#ifndef NSD_GRID_THREADS
+#define NSD_GRID_THREADS 256  // measured: 512 (128 registers) makes C2 15% slower
+#endif
+// Threads per CTA of the cooperative grid kernel (one CTA per SM).
+constexpr int kGridThreads = NSD_GRID_THREADS;
 template <class R, bool kTets>
-__global__ void __launch_bounds__(256) k_single_grid(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out,
+__global__ void __launch_bounds__(kGridThreads) k_single_grid(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out,
                                                      double* gpart) {
   __shared__ double red[2 * 33 * nsd::kRedMax];
   nsd::GridTeam t(red, gpart);
@@ -487,12 +492,16 @@ template <class R> struct BatchArgs {
 
 // One environment: extension forces, setup, device narrow phase, contact
 // incidence, Newton solve, state write-back (step_world, scene.cpp:709-732).
+// Row vectors in the region: x r z p ap az bx, plus inv (M^-1 diagonal) and cd (C
+// diagonal) in fp32. Measured: fp32 3.62 M -> 3.92 M env-steps/s with inv/cd in
+// the region; fp64 1.90 M -> 1.60 M (its fixed budget then holds fewer contacts).
+template <class R> __host__ __device__ constexpr int pool_row_vecs() { return sizeof(R) == 4 ? 9 : 7; }
 // Elements of the per-env shared-memory row region for nc contacts: the
 // write-heavy PCR state x, r, z, p, ap, az, bx (7 x rows), the J^T staging
 // (12 per joint, 9 per contact) and w (ndof), each array kept 16-byte aligned.
-__host__ __device__ inline int row_pool_elems(int rows_static, int nj, int ndof, int nc) {
+template <class R> __host__ __device__ inline int row_pool_elems(int rows_static, int nj, int ndof, int nc) {
   const int rows = (rows_static + 3 * nc + 3) & ~3;
-  return 7 * rows + ((12 * nj + 3) & ~3) + ((9 * nc + 3) & ~3) + ((ndof + 3) & ~3);
+  return pool_row_vecs<R>() * rows + ((12 * nj + 3) & ~3) + ((9 * nc + 3) & ~3) + ((ndof + 3) & ~3);
 }
 
 template <class R, class Team>
@@ -634,7 +643,7 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
     W.jstr = hr + P.jstr;  // structured joint rows: the object solver never reads coeff/blk
     t.sync();
     nsd::ObjView<R> O{W, hr + P.jstage, hr + P.cstage, A.jbinc_off, A.jbinc, cboff, cbinc};
-    if (pool && row_pool_elems(T.rows_static, T.nj, T.ndof, nc) <= A.row_pool) {
+    if (pool && row_pool_elems<R>(T.rows_static, T.nj, T.ndof, nc) <= A.row_pool) {
       // the env's PCR row state fits its shared-memory region: keep every store of
       // the CR loop on chip (global stores are write-through to L2)
       const int rows = (W.nrows + 3) & ~3;
@@ -646,7 +655,11 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
       O.W.ap = sp + 4 * rows;
       O.W.az = sp + 5 * rows;
       O.W.bx = sp + 6 * rows;
-      sp += 7 * rows;
+      if (pool_row_vecs<R>() == 9) {
+        O.W.inv = sp + 7 * rows;
+        O.W.cd = sp + 8 * rows;
+      }
+      sp += pool_row_vecs<R>() * rows;
       O.jstage = sp;
       sp += (12 * T.nj + 3) & ~3;
       O.cstage = sp;
@@ -786,9 +799,9 @@ template <class R> struct Solver final : SolverBase {
       int dev_sms = 0, per_sm = 0;
       NSD_CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
       if (tets)
-        NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, true>, 256, 0));
+        NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, true>, kGridThreads, 0));
       else
-        NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, false>, 256, 0));
+        NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, false>, kGridThreads, 0));
       if (per_sm < 1) throw NsdError(NSD_CUDA_ERROR, "grid kernel cannot be resident");
       const char* bps = std::getenv("NSD_GRID_BLOCKS_PER_SM");
       grid_blocks = dev_sms * std::min(per_sm, bps ? std::max(1, std::atoi(bps)) : 1);
@@ -924,7 +937,7 @@ template <class R> struct Solver final : SolverBase {
       double* gp = gpart.as<double>();
       void* args[] = {&topo.t, &W, &kc, &so, &gp};
       void* fn = tets ? (void*)k_single_grid<R, true> : (void*)k_single_grid<R, false>;
-      NSD_CK(cudaLaunchCooperativeKernel(fn, dim3(grid_blocks), dim3(256), args, 0, stream));
+      NSD_CK(cudaLaunchCooperativeKernel(fn, dim3(grid_blocks), dim3(kGridThreads), args, 0, stream));
     }
     NSD_CK(cudaEventRecord(ev1, stream));
     // ---- download
@@ -1106,7 +1119,7 @@ template <class R> struct Batch final : BatchBase {
         const int nblk = (n_env + envs_per_block - 1) / envs_per_block;
         const int bps = std::max(1, std::min(32, (nblk + sms - 1) / sms));
         const long budget = std::min<long>(max_optin, smem_sm / bps - reserved);
-        const int full = row_pool_elems(H.rows_static, H.nj, H.ndof, maxc);
+        const int full = row_pool_elems<R>(H.rows_static, H.nj, H.ndof, maxc);
         int region = static_cast<int>(budget / envs_per_block / static_cast<long>(sizeof(R))) & ~3;
         region = std::min(region, full);
         // Region contact capacity (envs with more contacts use global memory): the rest
@@ -1116,10 +1129,10 @@ template <class R> struct Batch final : BatchBase {
         // (~17 contacts). NSD_POOL_NC overrides.
         int pool_nc = sizeof(R) == 4 ? 24 : maxc;
         if (const char* e = std::getenv("NSD_POOL_NC")) pool_nc = std::max(1, std::atoi(e));
-        region = std::min(region, row_pool_elems(H.rows_static, H.nj, H.ndof, std::min(pool_nc, maxc)));
+        region = std::min(region, row_pool_elems<R>(H.rows_static, H.nj, H.ndof, std::min(pool_nc, maxc)));
         const char* env_rp = std::getenv("NSD_ROW_SMEM");
         if (env_rp && std::atoi(env_rp) == 0) region = 0;
-        if (region < row_pool_elems(H.rows_static, H.nj, H.ndof, 1)) region = 0;
+        if (region < row_pool_elems<R>(H.rows_static, H.nj, H.ndof, 1)) region = 0;
         row_pool = region;
         smem_bytes = static_cast<size_t>(region) * envs_per_block * sizeof(R);
         if (smem_bytes) {

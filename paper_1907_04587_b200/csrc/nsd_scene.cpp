@@ -246,14 +246,14 @@ Scene s_c3(int links) {
   s.solver.linear_max_iterations = 40;
   return s;
 }
-Scene s_c4(int n, double speed) {
+Scene s_c4(int n, double speed, double L) {
   Scene s;
   s.solver = defaults();
   s.bodies.push_back(ground());
-  const double radius = 0.05, edge = 0.1;
+  const double radius = 0.05 * L, edge = 0.1 * L;  // every length scales with L, masses with L^3
   MeshSpec g;
-  grid(g, n, n, n, Vec3{-0.05, -0.05, 0.0}, Vec3{edge, edge, edge});
-  const V centre = nsd::v3(0.0, 0.0, 0.05);
+  grid(g, n, n, n, Vec3{-0.05 * L, -0.05 * L, 0.0}, Vec3{edge, edge, edge});
+  const V centre = nsd::v3(0.0, 0.0, 0.05 * L);
   std::vector<int> keep(g.vertices.size(), -1);
   std::vector<std::array<int, 4>> kept;
   for (const auto& t : g.elements) {
@@ -275,14 +275,15 @@ Scene s_c4(int n, double speed) {
   const double lift = 0.005 - zmin;
   for (Vec3& p : ball.vertices) p.z += lift;
   for (const auto& t : kept) ball.elements.push_back({keep[t[0]], keep[t[1]], keep[t[2]], keep[t[3]]});
-  const Vec3 he{0.008, 0.008, 0.012};
-  const double rad = 0.075, za[4] = {0.014, 0.050, 0.086, 0.122}, zc[4] = {0.032, 0.068, 0.104, 0.140};
+  const Vec3 he{0.008 * L, 0.008 * L, 0.012 * L};
+  const double rad = 0.075 * L, za[4] = {0.014 * L, 0.050 * L, 0.086 * L, 0.122 * L},
+               zc[4] = {0.032 * L, 0.068 * L, 0.104 * L, 0.140 * L};
   for (int f = 0; f < 4; ++f) {
     const double th = 0.5 * M_PI * f;
     const Vec3 d{std::cos(th), std::sin(th), 0.0};
     const Vec3 tg{-std::sin(th), std::cos(th), 0.0};
     for (int k = 0; k < 4; ++k) {
-      s.bodies.push_back(box(Vec3{rad * d.x, rad * d.y, zc[k]}, he, 0.02, axis_angle(Vec3{0, 0, 1}, th)));
+      s.bodies.push_back(box(Vec3{rad * d.x, rad * d.y, zc[k]}, he, 0.02 * L * L * L, axis_angle(Vec3{0, 0, 1}, th)));
       JointSpecDesc j;
       j.kind = 1;
       j.a.body = k == 0 ? -1 : 1 + 4 * f + (k - 1);
@@ -295,7 +296,7 @@ Scene s_c4(int n, double speed) {
     dr.kind = 0;
     dr.a.body = 1 + 4 * f + 3;
     dr.b.body = -1;
-    dr.anchor = Vec3{rad * d.x, rad * d.y, 0.152};
+    dr.anchor = Vec3{rad * d.x, rad * d.y, 0.152 * L};
     dr.compliance = 1e-4;
     dr.anchor_velocity = Vec3{-0.02 * d.x, -0.02 * d.y, 0.0};  // 0.05 m/s squeezes the ball unstable by step 29
     s.joints.push_back(dr);
@@ -422,7 +423,9 @@ Scene build(const std::string& name, unsigned seed, bool* ok) {
   if (base == "c3") return s_c3(args.size() > 0 ? static_cast<int>(args[0]) : 100);
   // C4 drop speed 0.2 m/s: at 1.0 m/s the 8 mm Neo-Hookean elements blow up at step 4
   // under the 6 x 50 budget (the reference then throws in spmv_transpose)
-  if (base == "c4") return s_c4(args.size() > 0 ? static_cast<int>(args[0]) : 12, args.size() > 1 ? args[1] : 0.2);
+  if (base == "c4")
+    return s_c4(args.size() > 0 ? static_cast<int>(args[0]) : 12, args.size() > 1 ? args[1] : 0.2,
+                args.size() > 2 ? args[2] : 2.0);  // scale 2: ball radius 0.1 m (1.0 blows up by step 13-28)
   if (base == "c5") return s_c5(seed);
   *ok = false;
   return Scene{};
