@@ -11,6 +11,8 @@
 //   count_rows, newton_step
 //   World, build_scene_by_name,   scene.h:83-110   same names; step_world's Newton solve runs on the GPU
 //   step_world
+//   RunOptions, load_world, run,  runner.h:11-43   same names, CSV formats and exit codes (builders only;
+//   sweep                                          the JSON scene format is out of this path's scope)
 //
 // Error behaviour follows the reference: invalid input throws
 // std::invalid_argument (bodies.cpp:80, constraints.cpp:142-144,
@@ -30,7 +32,10 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
+#include <filesystem>
+#include <fstream>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -674,6 +679,206 @@ inline SolveReport step_world(World& w) {
   SolveReport r = newton_step(ctx, w.solver);
   w.time += w.h;
   return r;
+}
+
+// ------------------------------------------------------------------ runner.h
+// Scene execution front end writing the reference's trajectory.csv /
+// convergence.csv / sweep.csv (runner.cpp:80-126, %.17g, atomic write) — the
+// on-disk format used to diff GPU runs against the CPU oracle.
+struct RunOptions {
+  std::string scene;  // builder name (JSON scene files are not part of this path)
+  int steps = 100;
+  std::optional<std::string> solver_method;  // pcr (jacobi | gs | pcg are not on the GPU Newton path)
+  std::optional<std::string> ncp;            // minmap | fb
+  std::optional<std::string> r_strategy;     // identity | h2 | effmass
+  std::optional<int> newton_iters;
+  std::optional<int> linear_iters;
+  std::optional<double> step_fraction;
+  std::optional<double> epsilon;
+  unsigned seed = 0;
+  std::string out_dir = ".";
+  Precision precision = Precision::FP64;  // extension
+};
+
+constexpr int kExitOk = 0;
+constexpr int kExitValidation = 1;
+constexpr int kExitNumerical = 2;
+
+namespace detail {
+inline std::string fmt17(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "%.17g", v);
+  return buf;
+}
+inline void write_atomic(const std::filesystem::path& path, const std::string& content) {
+  const std::filesystem::path tmp = path.string() + ".tmp";
+  {
+    std::ofstream out(tmp, std::ios::binary);
+    if (!out) throw std::runtime_error("cannot write " + tmp.string());
+    out << content;
+  }
+  std::filesystem::rename(tmp, path);
+}
+// runner.cpp:29-77 (same messages)
+inline void apply_overrides(const RunOptions& o, NewtonConfig& c) {
+  if (o.solver_method) {
+    const std::string& m = *o.solver_method;
+    if (m == "jacobi" || m == "gs" || m == "pcg")
+      throw std::runtime_error("solver \"" + m + "\" is not on the GPU Newton path (pcr only)");
+    if (m != "pcr") throw std::runtime_error("unknown solver \"" + m + "\"");
+    c.linear.method = LinearMethod::PCR;
+  }
+  if (o.ncp) {
+    if (*o.ncp == "minmap")
+      c.ncp_kind = NcpKind::MinimumMap;
+    else if (*o.ncp == "fb")
+      c.ncp_kind = NcpKind::FischerBurmeister;
+    else
+      throw std::runtime_error("unknown NCP function \"" + *o.ncp + "\"");
+  }
+  if (o.r_strategy) {
+    if (*o.r_strategy == "identity")
+      c.r_strategy = RStrategy::Identity;
+    else if (*o.r_strategy == "h2")
+      c.r_strategy = RStrategy::TimestepSquared;
+    else if (*o.r_strategy == "effmass")
+      c.r_strategy = RStrategy::EffectiveMass;
+    else
+      throw std::runtime_error("unknown r strategy \"" + *o.r_strategy + "\"");
+  }
+  if (o.newton_iters) {
+    if (*o.newton_iters < 1) throw std::runtime_error("--newton-iters must be >= 1");
+    c.newton_iterations = *o.newton_iters;
+  }
+  if (o.linear_iters) {
+    if (*o.linear_iters < 1) throw std::runtime_error("--linear-iters must be >= 1");
+    c.linear.max_iterations = *o.linear_iters;
+  }
+  if (o.step_fraction) {
+    if (*o.step_fraction <= 0.0 || *o.step_fraction > 1.0) throw std::runtime_error("--t must lie in (0, 1]");
+    c.step_fraction = *o.step_fraction;
+  }
+  if (o.epsilon) {
+    if (*o.epsilon < 0.0) throw std::runtime_error("--eps must be >= 0");
+    c.epsilon_reg = *o.epsilon;
+  }
+}
+inline void append_trajectory(std::string& csv, int step, const GeneralizedState& s) {  // runner.cpp:80-104
+  for (size_t b = 0; b < s.bodies.size(); ++b) {
+    csv += std::to_string(step) + ',' + std::to_string(b);
+    const Vec3 p = s.position(static_cast<int>(b));
+    for (int k = 0; k < 3; ++k) csv += ',' + fmt17(p[k]);
+    if (s.bodies[b].type == BodyType::Rigid) {
+      const Vec4 q = s.orientation(static_cast<int>(b));
+      csv += ',' + fmt17(q.w) + ',' + fmt17(q.x) + ',' + fmt17(q.y) + ',' + fmt17(q.z);
+    } else {
+      csv += ",1,0,0,0";
+    }
+    const Vec3 v = s.linear_velocity(static_cast<int>(b));
+    for (int k = 0; k < 3; ++k) csv += ',' + fmt17(v[k]);
+    if (s.bodies[b].type == BodyType::Rigid) {
+      const Vec3 w = s.angular_velocity(static_cast<int>(b));
+      for (int k = 0; k < 3; ++k) csv += ',' + fmt17(w[k]);
+    } else {
+      csv += ",0,0,0";
+    }
+    csv += '\n';
+  }
+}
+inline void append_convergence(std::string& csv, int step, const SolveReport& r, const std::string& prefix) {
+  for (size_t i = 0; i < r.iterations.size(); ++i) {  // runner.cpp:106-121
+    const NewtonIterationStats& it = r.iterations[i];
+    csv += prefix + std::to_string(step) + ',' + std::to_string(i) + ',' + fmt17(it.residual_inf) + ',' +
+           fmt17(it.comp_error_max) + ',' + fmt17(it.cone_violation_max) + ',' + fmt17(it.step_size) + ',' +
+           std::to_string(it.linear_iterations) + ',' + fmt17(it.linear_residual) + '\n';
+  }
+}
+inline constexpr const char* kTrajectoryHeader = "step,body,qx,qy,qz,q0,q1,q2,q3,ux,uy,uz,wx,wy,wz\n";
+inline constexpr const char* kConvergenceHeader =
+    "step,newton_iter,residual_inf,comp_error_n_max,cone_violation_max,step_size,linear_iters,"
+    "linear_residual_final\n";
+}  // namespace detail
+
+// load_world (runner.cpp:130-146): builder by name with the overrides applied.
+inline World load_world(const RunOptions& o) {
+  if (std::filesystem::exists(o.scene))
+    throw std::runtime_error("scene \"" + o.scene + "\": JSON scene files are not part of the GPU path (builders only)");
+  auto w = build_scene_by_name(o.scene, o.seed);
+  if (!w) throw std::runtime_error("scene \"" + o.scene + "\" is neither a file nor a known builder");
+  detail::apply_overrides(o, w->solver);
+  w->solver.precision = o.precision;
+  return std::move(*w);
+}
+
+// run (runner.cpp:148-180): steps the world, writes trajectory.csv and
+// convergence.csv atomically; 0 ok, 1 validation error, 2 numerical abort.
+inline int run(const RunOptions& o, std::string* error = nullptr) {
+  try {
+    if (o.steps < 1) throw std::runtime_error("--steps must be >= 1");
+    World w = load_world(o);
+    std::string traj = detail::kTrajectoryHeader, conv = detail::kConvergenceHeader;
+    bool aborted = false;
+    for (int step = 0; step < o.steps; ++step) {
+      const SolveReport r = step_world(w);
+      detail::append_trajectory(traj, step, w.state);
+      detail::append_convergence(conv, step, r, "");
+      if (r.aborted) {
+        aborted = true;
+        break;
+      }
+    }
+    std::filesystem::create_directories(o.out_dir);
+    detail::write_atomic(std::filesystem::path(o.out_dir) / "trajectory.csv", traj);
+    detail::write_atomic(std::filesystem::path(o.out_dir) / "convergence.csv", conv);
+    if (aborted) {
+      if (error) *error = "numerical abort (NaN) during solve";
+      return kExitNumerical;
+    }
+    return kExitOk;
+  } catch (const std::exception& e) {
+    if (error) *error = e.what();
+    return kExitValidation;
+  }
+}
+
+// sweep (runner.cpp:182-218): one run per axis value, merged sweep.csv. The
+// "solver" axis only has pcr on the GPU path.
+inline int sweep(const RunOptions& o, const std::string& axis, std::string* error = nullptr) {
+  try {
+    if (o.steps < 1) throw std::runtime_error("--steps must be >= 1");
+    std::vector<std::string> values;
+    if (axis == "solver")
+      values = {"pcr"};
+    else if (axis == "r_strategy")
+      values = {"identity", "h2", "effmass"};
+    else if (axis == "ncp")
+      values = {"minmap", "fb"};
+    else
+      throw std::runtime_error("unknown sweep axis \"" + axis + "\"");
+    std::string csv = std::string("axis_value,") + detail::kConvergenceHeader;
+    for (const std::string& v : values) {
+      RunOptions sub = o;
+      if (axis == "solver")
+        sub.solver_method = v;
+      else if (axis == "r_strategy")
+        sub.r_strategy = v;
+      else
+        sub.ncp = v;
+      World w = load_world(sub);
+      invalidate_device_cache();
+      for (int step = 0; step < o.steps; ++step) {
+        const SolveReport r = step_world(w);
+        detail::append_convergence(csv, step, r, v + ",");
+        if (r.aborted) break;
+      }
+    }
+    std::filesystem::create_directories(o.out_dir);
+    detail::write_atomic(std::filesystem::path(o.out_dir) / "sweep.csv", csv);
+    return kExitOk;
+  } catch (const std::exception& e) {
+    if (error) *error = e.what();
+    return kExitValidation;
+  }
 }
 
 }  // namespace nsdyn_b200

@@ -556,4 +556,73 @@ double orc_c5_bench(int env0, int n_env, int n_warm, int n_steps, int actuated, 
   return std::chrono::duration<double>(t1 - t0).count();
 }
 
+
+// Runner CSV output (restates src/runner.cpp:13-27, 80-126, 148-180 for the
+// GPU-vs-oracle file diff): trajectory.csv + convergence.csv, %.17g. Returns
+// the runner's exit code (0 ok, 1 validation error, 2 numerical abort).
+static std::string orc_fmt(double v) {
+  char b[64];
+  std::snprintf(b, sizeof(b), "%.17g", v);
+  return b;
+}
+int orc_run(const char* name, unsigned seed, int steps, const char* out_dir) {
+  try {
+    if (steps < 1) throw std::runtime_error("--steps must be >= 1");
+    SceneDesc sd;
+    if (!build_scene_by_name(name, seed, sd)) throw std::runtime_error("unknown scene");
+    World w = build_world(sd);
+    std::string traj = "step,body,qx,qy,qz,q0,q1,q2,q3,ux,uy,uz,wx,wy,wz\n";
+    std::string conv =
+        "step,newton_iter,residual_inf,comp_error_n_max,cone_violation_max,step_size,linear_iters,"
+        "linear_residual_final\n";
+    bool aborted = false;
+    for (int step = 0; step < steps; ++step) {
+      const Report r = step_world(w);
+      const State& st = w.state;
+      for (size_t b = 0; b < st.bodies.size(); ++b) {
+        traj += std::to_string(step) + ',' + std::to_string(b);
+        const V3 p = st.position(static_cast<int>(b));
+        for (int k = 0; k < 3; ++k) traj += ',' + orc_fmt(p[k]);
+        const bool rigid = st.bodies[b].type == BodyType::Rigid;
+        if (rigid) {
+          const V4 q = st.orientation(static_cast<int>(b));
+          for (int k = 0; k < 4; ++k) traj += ',' + orc_fmt(q[k]);
+        } else {
+          traj += ",1,0,0,0";
+        }
+        const int d = st.dof_off[b];
+        for (int k = 0; k < 3; ++k) traj += ',' + orc_fmt(st.u[d + k]);
+        if (rigid)
+          for (int k = 0; k < 3; ++k) traj += ',' + orc_fmt(st.u[d + 3 + k]);
+        else
+          traj += ",0,0,0";
+        traj += '\n';
+      }
+      for (size_t i = 0; i < r.iterations.size(); ++i) {
+        const IterStats& it = r.iterations[i];
+        conv += std::to_string(step) + ',' + std::to_string(i) + ',' + orc_fmt(it.residual_inf) + ',' +
+                orc_fmt(it.comp_error_max) + ',' + orc_fmt(it.cone_violation_max) + ',' + orc_fmt(it.step_size) +
+                ',' + std::to_string(it.linear_iterations) + ',' + orc_fmt(it.linear_residual) + '\n';
+      }
+      if (r.aborted) {
+        aborted = true;
+        break;
+      }
+    }
+    const std::string dir(out_dir);
+    std::FILE* f = std::fopen((dir + "/trajectory.csv").c_str(), "wb");
+    if (!f) throw std::runtime_error("cannot write trajectory.csv");
+    std::fwrite(traj.data(), 1, traj.size(), f);
+    std::fclose(f);
+    f = std::fopen((dir + "/convergence.csv").c_str(), "wb");
+    if (!f) throw std::runtime_error("cannot write convergence.csv");
+    std::fwrite(conv.data(), 1, conv.size(), f);
+    std::fclose(f);
+    return aborted ? 2 : 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 }  // extern "C"

@@ -330,6 +330,11 @@ class OracleWorld:
                     lam=lam[:rows], tel=tel.reshape(-1, 6)[:nc])
 
 
+def run(name, seed, steps, out_dir):
+    """Runner CSVs (trajectory.csv, convergence.csv) of the oracle's step_world; returns the exit code."""
+    return lib().orc_run(name.encode(), C.c_uint(seed), C.c_int(steps), str(out_dir).encode())
+
+
 def action_torque(env, step, joint):
     return lib().orc_action_torque(C.c_int(env), C.c_int(step), C.c_int(joint))
 

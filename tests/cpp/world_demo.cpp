@@ -5,6 +5,8 @@
 //   world_demo <scene> <seed> <steps> [fp32|fp64]   trajectory: per-step lines + final q, u
 //   world_demo --free-fall                          newton_step on a hand-built StepContext
 //   world_demo --invalid-h                          h <= 0 must throw std::invalid_argument
+//   world_demo --run <scene> <steps> <out_dir> [ncp] [r]   runner: trajectory.csv + convergence.csv
+//   world_demo --sweep <scene> <axis> <steps> <out_dir>   runner: sweep.csv
 #include "nsdyn_b200.hpp"
 
 #include <cstdio>
@@ -61,7 +63,33 @@ static int invalid_h() {
   return 1;
 }
 
+static int run_cmd(int argc, char** argv) {
+  nb::RunOptions o;
+  o.scene = argv[2];
+  o.steps = std::atoi(argv[3]);
+  o.out_dir = argv[4];
+  if (argc > 5) o.ncp = std::string(argv[5]);
+  if (argc > 6) o.r_strategy = std::string(argv[6]);
+  std::string err;
+  const int rc = nb::run(o, &err);
+  std::printf("run rc %d %s\n", rc, err.c_str());
+  return rc;
+}
+
+static int sweep_cmd(char** argv) {
+  nb::RunOptions o;
+  o.scene = argv[2];
+  o.steps = std::atoi(argv[4]);
+  o.out_dir = argv[5];
+  std::string err;
+  const int rc = nb::sweep(o, argv[3], &err);
+  std::printf("sweep rc %d %s\n", rc, err.c_str());
+  return rc;
+}
+
 int main(int argc, char** argv) {
+  if (argc >= 5 && std::strcmp(argv[1], "--run") == 0) return run_cmd(argc, argv);
+  if (argc >= 6 && std::strcmp(argv[1], "--sweep") == 0) return sweep_cmd(argv);
   if (argc >= 2 && std::strcmp(argv[1], "--free-fall") == 0) return free_fall();
   if (argc >= 2 && std::strcmp(argv[1], "--invalid-h") == 0) return invalid_h();
   if (argc < 4) {
