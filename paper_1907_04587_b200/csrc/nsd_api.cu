@@ -301,9 +301,9 @@ template <class R> struct DevTopo {
 struct WorkPlan {
   // hot R
   size_t q, u, g, w, du, hinv, iwi6, coeff, hv, cd, lam, x, r, z, p, ap, az, inv, bx, cdir, carm, cscale, jstage,
-      cstage, jstr, hotR;
+      cstage, jstr, crec, hotR;
   // hot int
-  size_t blk, cbody, cinc_off, cinc_ent, cbinc_off, cbinc, hotI;
+  size_t blk, cbody, cinc_off, cinc_ent, cbinc_off, cbinc, cblk, hotI;
   // cold R
   size_t q0, u0, qp, ut, iw6, gp, up, shift, ub, fx, ctet, xn, rn, zn, cgeo, xlam, coldR;
   // cold int
@@ -320,6 +320,10 @@ struct WorkPlan {
       const size_t off = o;
       o += (n + 1) & ~size_t(1);  // keep 8-byte alignment for doubles
       return off;
+    };
+    auto a16 = [&](size_t n) {  // 16-byte aligned start (vector loads): multiple of 4 elements
+      o = (o + 3) & ~size_t(3);
+      return a(n);
     };
     q = a(T.ncoord);
     u = a(T.ndof);
@@ -346,6 +350,7 @@ struct WorkPlan {
     jstage = a(12 * static_cast<size_t>(T.nj));
     cstage = a(9 * c);
     jstr = a(24 * static_cast<size_t>(T.nj));
+    crec = a16(20 * c);
     hotR = o;
     o = 0;
     blk = a(4 * rs);
@@ -354,6 +359,7 @@ struct WorkPlan {
     cinc_ent = a(4 * c);
     cbinc_off = a(T.nb + 1);
     cbinc = a(2 * c);
+    cblk = a16(4 * c);
     hotI = o;
     o = 0;
     q0 = a(T.ncoord);
@@ -488,6 +494,7 @@ template <class R> struct BatchArgs {
   const int* jbinc_off;  // static joint incidence per body (warp solver)
   const int* jbinc;
   unsigned long long* ptime;  // NSD_PHASE_TIMING diagnostics (16 counters) or null
+  const int4* jblk;           // static dof3 blocks per joint
 };
 
 // One environment: extension forces, setup, device narrow phase, contact
@@ -641,6 +648,9 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
       }
     }
     W.jstr = hr + P.jstr;  // structured joint rows: the object solver never reads coeff/blk
+    W.crec = hr + P.crec;  // contact records + block ids for vector loads
+    W.cblk = reinterpret_cast<int4*>(hi + P.cblk);
+    W.jblk = A.jblk;
     t.sync();
     nsd::ObjView<R> O{W, hr + P.jstage, hr + P.cstage, A.jbinc_off, A.jbinc, cboff, cbinc};
     if (pool && row_pool_elems<R>(T.rows_static, T.nj, T.ndof, nc) <= A.row_pool) {
@@ -1023,7 +1033,7 @@ template <class R> struct Batch final : BatchBase {
   nsd_config cfg;
   int n_env, maxc, ns, npairs;
   WorkPlan plan;
-  DBuf hotg, coldr, coldi, shapes, pairs, cand, paircnt, ncout, ovf, fin, iters, qs, us, torque, jbinc;
+  DBuf hotg, coldr, coldi, shapes, pairs, cand, paircnt, ncout, ovf, fin, iters, qs, us, torque, jbinc, jblk;
   int jbinc_n = 0;
   HBuf stage;
   double margin, mu_default;
@@ -1081,6 +1091,20 @@ template <class R> struct Batch final : BatchBase {
       jbinc_n = static_cast<int>(flat.size());
       jbinc.alloc(sizeof(int) * flat.size());
       NSD_CK(cudaMemcpy(jbinc.p, flat.data(), sizeof(int) * flat.size(), cudaMemcpyHostToDevice));
+      // static dof3 blocks per joint (body_blocks of both sides), one int4 each
+      std::vector<int4> jb(std::max(H.nj, 1));
+      auto blocks = [&](int b, int& lin, int& ang) {
+        lin = b < 0 ? -1 : H.bdof[b] / 3;
+        ang = b >= 0 && H.btype[b] == 1 ? lin + 1 : -1;
+      };
+      for (int j = 0; j < H.nj; ++j) {
+        int al, aa, bl, ba;
+        blocks(H.jbody[2 * j], al, aa);
+        blocks(H.jbody[2 * j + 1], bl, ba);
+        jb[j] = make_int4(al, aa, bl, ba);
+      }
+      jblk.alloc(sizeof(int4) * jb.size());
+      NSD_CK(cudaMemcpy(jblk.p, jb.data(), sizeof(int4) * jb.size(), cudaMemcpyHostToDevice));
     }
     // Team shape: TPE lanes per env (4/8/16/32, sub-warp object solver) or a CTA per
     // env (64/128/256, generic engine). Default 16 lanes (2 envs per warp): with the
@@ -1301,6 +1325,7 @@ template <class R> struct Batch final : BatchBase {
     A.iters = iters.as<nsd::IterOut>();
     A.jbinc_off = jbinc.as<int>();
     A.jbinc = jbinc.as<int>() + H.nb + 1;
+    A.jblk = jblk.as<int4>();
     const int epb = envs_per_block;
     const int nblk = (n_env + epb - 1) / epb;
     if (team_threads <= 32) {

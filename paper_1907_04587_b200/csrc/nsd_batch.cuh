@@ -30,6 +30,45 @@ template <class R> struct ObjView {
   int* cbinc;       // contact*2 + side
 };
 
+// Vector loads of one 16-byte-aligned record (float4 / 2 x double2 per 4 values).
+__device__ __forceinline__ void ld4(const float* p, float (&o)[4]) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  o[0] = v.x;
+  o[1] = v.y;
+  o[2] = v.z;
+  o[3] = v.w;
+}
+__device__ __forceinline__ void ld4(const double* p, double (&o)[4]) {
+  const double2 a = *reinterpret_cast<const double2*>(p), c = *reinterpret_cast<const double2*>(p + 2);
+  o[0] = a.x;
+  o[1] = a.y;
+  o[2] = c.x;
+  o[3] = c.y;
+}
+
+// Contact view from the batched record (W.crec, W.cblk): 5 vector loads + 1 int4.
+template <class R> __device__ __forceinline__ CView<R> contact_rec_view(const Work<R>& W, int c) {
+  R v[20];
+  const R* rc = W.crec + 20 * c;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) ld4(rc + 4 * k, *reinterpret_cast<R(*)[4]>(v + 4 * k));
+  const int4 bk = W.cblk[c];
+  CView<R> cv;
+  cv.ba = cv.bb = 0;  // unused by the operator paths
+  cv.al = bk.x;
+  cv.aa = bk.y;
+  cv.bl = bk.z;
+  cv.bA = bk.w;
+  cv.n = v3(v[0], v[1], v[2]);
+  cv.d1 = v3(v[3], v[4], v[5]);
+  cv.d2 = v3(v[6], v[7], v[8]);
+  cv.ra = v3(v[9], v[10], v[11]);
+  cv.rb = v3(v[12], v[13], v[14]);
+  cv.dc = v[15];
+  cv.act = v[16];
+  return cv;
+}
+
 // Structured joint (W.jstr, written by assemble_joint): bodies' dof3 blocks, the
 // point / axis row counts of the kind (joint_rows, constraints.cpp:141-220) and
 // the 24 values: arm_a, arm_b, point directions D0..D2, axis vectors C0..C2.
@@ -39,8 +78,11 @@ template <class R> struct JView {
 };
 template <class R> __device__ __forceinline__ JView<R> joint_view(const Topo<R>& T, const Work<R>& W, int j) {
   JView<R> v;
-  body_blocks(T, T.jbody[2 * j], v.al, v.aa);
-  body_blocks(T, T.jbody[2 * j + 1], v.bl, v.bA);
+  const int4 bk = W.jblk[j];  // static table: one int4 instead of body -> dof -> type chains
+  v.al = bk.x;
+  v.aa = bk.y;
+  v.bl = bk.z;
+  v.bA = bk.w;
   const int kind = T.jkind[j];
   v.np = kind <= 1 ? 3 : (kind == 2 ? 2 : 0);
   v.na = kind == 0 ? 0 : (kind == 2 ? 3 : 2);
@@ -86,16 +128,15 @@ __device__ __forceinline__ void stage_objects(const Topo<R>& T, ObjView<R>& O, i
       st3(d + 9, -(cross(ld3(jv.s + 3), f) + ta));
     } else {
       const int c = k - T.nj;
-      const R* g = W.cdir + 9 * c;
-      const R dc = W.cscale[2 * c], act = W.cscale[2 * c + 1];
+      const CView<R> cv = contact_rec_view(W, c);
       const int f0 = W.friction_begin + 2 * c;
-      const R yn = dc * y(W.normal_begin + c), y1 = act * y(f0), y2 = act * y(f0 + 1);
-      const V3<R> f = v3(yn * g[0] + y1 * g[3] + y2 * g[6], yn * g[1] + y1 * g[4] + y2 * g[7],
-                         yn * g[2] + y1 * g[5] + y2 * g[8]);
+      const R yn = cv.dc * y(W.normal_begin + c), y1 = cv.act * y(f0), y2 = cv.act * y(f0 + 1);
+      const V3<R> f = v3(yn * cv.n.x + y1 * cv.d1.x + y2 * cv.d2.x, yn * cv.n.y + y1 * cv.d1.y + y2 * cv.d2.y,
+                         yn * cv.n.z + y1 * cv.d1.z + y2 * cv.d2.z);
       R* d = O.cstage + 9 * c;
       st3(d, f);
-      st3(d + 3, cross(ld3(W.carm + 6 * c), f));
-      st3(d + 6, cross(ld3(W.carm + 6 * c + 3), f));
+      st3(d + 3, cross(cv.ra, f));
+      st3(d + 6, cross(cv.rb, f));
     }
   }
 }
@@ -164,7 +205,7 @@ __device__ __forceinline__ void object_Jw(const Topo<R>& T, const Work<R>& W, in
     for (int i = 0; i < jv.na; ++i) f(r0 + jv.np + i, dot(ld3(jv.s + 15 + 3 * i), wr));
   } else {
     const int c = k - T.nj;
-    const CView<R> cv = contact_view(T, W, c);
+    const CView<R> cv = contact_rec_view(W, c);
     const V3<R> dv = contact_dv(cv, w);
     f(W.normal_begin + c, cv.dc == R(0) ? R(0) : cv.dc * dot(cv.n, dv));
     const bool act = cv.act != R(0);
@@ -198,7 +239,7 @@ __device__ __forceinline__ void object_quad(const Topo<R>& T, const Work<R>& W, 
     }
   } else {
     const int c = k - T.nj;
-    const CView<R> cv = contact_view(T, W, c);
+    const CView<R> cv = contact_rec_view(W, c);
     f(W.normal_begin + c, cv.dc == R(0) ? R(0) : contact_quad(T, W, cv, cv.dc * cv.n, true));
     const bool act = cv.act != R(0);
     f(W.friction_begin + 2 * c, act ? contact_quad(T, W, cv, cv.d1, true) : R(0));

@@ -110,6 +110,9 @@ template <class R> struct Work {
   R* coeff;  // 12 per static row
   int* blk;  // 4 per static row
   R* jstr;   // batched path: 24 per joint (structured rows, see assemble_joint) or null
+  R* crec;   // batched path: 20 per contact (n d1 d2 r_a r_b dc act, 16-byte aligned) or null
+  int4* cblk;  // batched path: dof3 blocks (a.lin, a.ang, b.lin, b.ang) per contact
+  const int4* jblk;  // batched path: static dof3 blocks per joint (shared by all envs)
   R* hv;
   R* cd;
   R* ctet;   // 9 per tet
@@ -645,6 +648,15 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
   }
   cv.ra = ra;
   cv.rb = rb;
+  if (W.crec) {  // batched path: one vector-loadable record + block ids per contact
+    R* rc = W.crec + 20 * c;
+    st3(rc, cv.n);
+    st3(rc + 3, cv.d1);
+    st3(rc + 6, cv.d2);
+    st3(rc + 9, ra);
+    st3(rc + 12, rb);
+    W.cblk[c] = make_int4(cv.al, cv.aa, cv.bl, cv.bA);
+  }
   const int nr = W.normal_begin + c, f0 = W.friction_begin + 2 * c;
   const R gap = dot(cv.n, pa - pb) - thick;
   const R lam_n = W.lam[nr] / h;
@@ -654,6 +666,7 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
   W.hv[nr] = hn;
   W.cd[nr] = phi.dl / (h * h);
   W.cscale[2 * c] = phi.dc;  // row kept iff dc != 0 (newton.cpp:187)
+  if (W.crec) W.crec[20 * c + 15] = phi.dc;
   st.comp = fmax(st.comp, (double)ab(mn(gap, lam_n)));
   const R lf0 = W.lam[f0] / h, lf1 = W.lam[f0 + 1] / h;
   const R mu_ln = mu * lam_n;
@@ -670,11 +683,13 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
     h2 = v1 + wv * lf1;
     W.cd[f0] = W.cd[f0 + 1] = wv / h;
     W.cscale[2 * c + 1] = R(1);
+    if (W.crec) W.crec[20 * c + 16] = R(1);
   } else {
     h1 = lf0;
     h2 = lf1;
     W.cd[f0] = W.cd[f0 + 1] = R(1) / h;
     W.cscale[2 * c + 1] = R(0);
+    if (W.crec) W.crec[20 * c + 16] = R(0);
   }
   W.hv[f0] = h1;
   W.hv[f0 + 1] = h2;
