@@ -512,7 +512,7 @@ template <class R> __host__ __device__ inline int row_pool_elems(int rows_static
 }
 
 template <class R, class Team>
-__device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* pool) {
+__device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* pool, int tib) {
   const nsd::Topo<R>& T = A.T;
   const WorkPlan& P = A.plan;
   int* hi = P.hot_ints(hr);
@@ -653,7 +653,25 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
     W.jblk = A.jblk;
     t.sync();
     nsd::ObjView<R> O{W, hr + P.jstage, hr + P.cstage, A.jbinc_off, A.jbinc, cboff, cbinc};
-    if (pool && row_pool_elems<R>(T.rows_static, T.nj, T.ndof, nc) <= A.row_pool) {
+    // Slice of the block's shared-memory region. When the block is one full warp of
+    // teams, they exchange their needs and take prefix offsets, so a small env lends
+    // space to a large one (all 32 lanes reach this shuffle: a full block has no
+    // early-returned team).
+    const int need = row_pool_elems<R>(T.rows_static, T.nj, T.ndof, nc);
+    const int epb = A.envs_per_block, cap = epb * A.row_pool;
+    const bool block_full = (blockIdx.x + 1) * epb <= A.n_env;
+    int off = tib * A.row_pool, lim = (tib + 1) * A.row_pool;
+    if (pool && block_full && epb * Team::kSize == 32) {
+      int before = 0;
+      for (int j = 0; j < epb; ++j) {
+        const int nj_need = __shfl_sync(0xffffffffu, need, j * Team::kSize);
+        if (j < tib) before += nj_need;
+      }
+      off = before;
+      lim = cap;
+    }  // partial blocks keep the fixed split (teams past n_env returned early)
+    if (pool && off + need <= lim) {
+      pool += off;
       // the env's PCR row state fits its shared-memory region: keep every store of
       // the CR loop on chip (global stores are write-through to L2)
       const int rows = (W.nrows + 3) & ~3;
@@ -753,9 +771,9 @@ __global__ void __launch_bounds__(128, 4) k_batch_sub(BatchArgs<R> A) {
   if (env >= A.n_env) return;  // team-uniform
   R* hr = A.hot_in_smem ? reinterpret_cast<R*>(smem + (size_t)tib * A.hot_bytes)
                         : reinterpret_cast<R*>(A.hot_global + (size_t)env * A.hot_bytes);
-  R* pool = A.row_pool ? reinterpret_cast<R*>(smem) + (size_t)tib * A.row_pool : nullptr;
+  R* pool = A.row_pool ? reinterpret_cast<R*>(smem) : nullptr;  // the block's region; batch_env takes a slice
   nsd::SubWarpTeam<TPE> t(threadIdx.x & 31);
-  batch_env(t, A, env, hr, pool);
+  batch_env(t, A, env, hr, pool, tib);
 }
 
 // CTA per environment.
@@ -765,7 +783,7 @@ template <class R> __global__ void __launch_bounds__(256) k_batch_block(BatchArg
   nsd::BlockTeam t(red);
   R* hr = A.hot_in_smem ? reinterpret_cast<R*>(smem)
                         : reinterpret_cast<R*>(A.hot_global + (size_t)blockIdx.x * A.hot_bytes);
-  batch_env(t, A, blockIdx.x, hr, static_cast<R*>(nullptr));
+  batch_env(t, A, blockIdx.x, hr, static_cast<R*>(nullptr), 0);
 }
 
 // ================================================================== handles

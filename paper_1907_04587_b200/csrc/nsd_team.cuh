@@ -59,6 +59,7 @@ struct WarpTeam {
 // warp may take different data-dependent paths (PCR exits, aborts) safely.
 template <int TPE> struct SubWarpTeam {
   static_assert(TPE == 4 || TPE == 8 || TPE == 16 || TPE == 32, "TPE");
+  static constexpr int kSize = TPE;
   int lane;       // rank within the team
   unsigned mask;  // the team's lanes
   __device__ explicit SubWarpTeam(int warp_lane)

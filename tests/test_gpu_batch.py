@@ -104,3 +104,18 @@ def test_batch_overflow_reported():
     b.step(s0.h, s0.gravity)
     with pytest.raises(NsdError):
         b.results()
+
+
+def test_batch_odd_env_count_partial_block_fp64():
+    """n_env not a multiple of the envs per block: the last block's second team has no
+    env (fixed region split there, no pool exchange); every env still tracks the oracle."""
+    n_env = 5
+    b, s0 = _batch(n_env, "fp64")
+    worlds = [O.OracleWorld("c5", e) for e in range(n_env)]
+    for st in range(6):
+        for w in worlds:
+            assert w.step(1) == 0
+        b.step(s0.h, s0.gravity)
+    q, _ = b.get_state()
+    for e, w in enumerate(worlds):
+        assert rel_err(q[e], w.state()[0]) < 1e-8, e
