@@ -833,7 +833,8 @@ template <class R> struct Solver final : SolverBase {
       if (per_sm < 1) throw NsdError(NSD_CUDA_ERROR, "grid kernel cannot be resident");
       const char* bps = std::getenv("NSD_GRID_BLOCKS_PER_SM");
       grid_blocks = dev_sms * std::min(per_sm, bps ? std::max(1, std::atoi(bps)) : 1);
-      gpart.alloc(sizeof(double) * 2 * grid_blocks * nsd::kRedMax);
+      // partials, totals and the [count, generation] words of the grid barrier (nsd_team.cuh)
+      gpart.alloc(sizeof(double) * (2 * grid_blocks * nsd::kRedMax + 2 * nsd::kRedMax + 2));
     }
   }
   ~Solver() override {
@@ -963,6 +964,7 @@ template <class R> struct Solver final : SolverBase {
       NSD_CK(cudaGetLastError());
     } else {
       double* gp = gpart.as<double>();
+      NSD_CK(cudaMemsetAsync(gp + 2 * grid_blocks * nsd::kRedMax + 2 * nsd::kRedMax, 0, 2 * sizeof(unsigned), stream));
       void* args[] = {&topo.t, &W, &kc, &so, &gp};
       void* fn = tets ? (void*)k_single_grid<R, true> : (void*)k_single_grid<R, false>;
       NSD_CK(cudaLaunchCooperativeKernel(fn, dim3(grid_blocks), dim3(kGridThreads), args, 0, stream));

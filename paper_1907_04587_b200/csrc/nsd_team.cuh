@@ -149,14 +149,65 @@ struct BlockTeam {
   }
 };
 
+// Grid team: one cooperative launch, one CTA per SM. Barrier and all-reduce are
+// "last CTA reduces": each CTA publishes its partials and arrives on a global
+// counter; the last to arrive sums the partials in CTA order (deterministic,
+// bit-identical for every member), publishes the totals and bumps a generation
+// flag that the other CTAs spin on. One barrier-equivalent per reduction, and
+// only one CTA reads the partials (measured: the previous scheme — a CG grid sync
+// after which every CTA's warp 0 re-read all partials, value by value, from the
+// same L2 lines — held ~48% of the C2 kernel's stall samples).
+// Global scratch (gpart): [2 x nb x kRedMax partials][2 x kRedMax totals][count, gen];
+// count and gen are zeroed before every launch.
 struct GridTeam {
   double* red;    // shared: 2 * (33 * kRedMax)
-  double* gpart;  // global: 2 * gridDim.x * kRedMax
+  double* gpart;  // global partials
+  double* gres;   // global totals
+  unsigned* bar;  // [0] arrival count, [1] generation
   int parity;
-  __device__ GridTeam(double* smem_red, double* global_part) : red(smem_red), gpart(global_part), parity(0) {}
+  unsigned epoch;
+  __device__ GridTeam(double* smem_red, double* global_part)
+      : red(smem_red), gpart(global_part), gres(global_part + 2 * gridDim.x * kRedMax),
+        bar(reinterpret_cast<unsigned*>(global_part + 2 * gridDim.x * kRedMax + 2 * kRedMax)), parity(0), epoch(0) {}
   __device__ __forceinline__ int rank() const { return blockIdx.x * blockDim.x + threadIdx.x; }
   __device__ __forceinline__ int size() const { return gridDim.x * blockDim.x; }
-  __device__ __forceinline__ void sync() const { cooperative_groups::this_grid().sync(); }
+
+  // Arrive; returns true (block-uniform) in the last CTA to arrive. Caller must
+  // have made its global writes visible (thread 0's __threadfence below covers
+  // writes by thread 0; others sync through __syncthreads first).
+  __device__ __forceinline__ bool arrive(int* last_flag) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned prev = atomicAdd(bar, 1u);
+      *last_flag = prev == gridDim.x - 1;
+    }
+    __syncthreads();
+    return *last_flag != 0;
+  }
+  // Last CTA: reset the count and release the waiting CTAs; others: wait.
+  __device__ __forceinline__ void release_or_wait(bool last) {
+    ++epoch;
+    if (threadIdx.x == 0) {
+      if (last) {
+        atomicExch(bar, 0u);
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(epoch) : "memory");
+      } else {
+        unsigned g;
+        do {  // acquire load: no atomic traffic on the hot word while waiting
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+        } while (g != epoch);
+      }
+    }
+    __syncthreads();
+  }
+
+  __device__ __forceinline__ void sync() {
+    __shared__ int last_flag;
+    const bool last = arrive(&last_flag);
+    release_or_wait(last);
+  }
   template <int NS> __device__ __forceinline__ void reduce_sum(double (&s)[NS]) {
     double m[1] = {0.0};
     reduce(s, m);
@@ -165,8 +216,10 @@ struct GridTeam {
   __device__ __forceinline__ void reduce(double (&s)[NS], double (&m)[NM]) {
     constexpr int K = NS + NM;
     static_assert(K <= kRedMax, "too many values in one reduction");
+    __shared__ int last_flag;
     double* buf = red + parity * (33 * kRedMax);
     double* gp = gpart + parity * (gridDim.x * kRedMax);
+    double* gr = gres + parity * kRedMax;
     parity ^= 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
@@ -180,57 +233,46 @@ struct GridTeam {
       if (lane == 0) buf[warp * kRedMax + NS + k] = v;
     }
     __syncthreads();
-    if (warp == 0) {
+    if (warp == 0) {  // CTA partials (lane 0 writes all K, so thread 0's fence covers them)
+      double v[K];
 #pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        const double v = warp_sum_down(lane < nw ? buf[lane * kRedMax + k] : 0.0);
-        if (lane == 0) gp[blockIdx.x * kRedMax + k] = v;
-      }
+      for (int k = 0; k < NS; ++k) v[k] = warp_sum_down(lane < nw ? buf[lane * kRedMax + k] : 0.0);
 #pragma unroll
-      for (int k = 0; k < NM; ++k) {
-        const double v = warp_max_down(lane < nw ? buf[lane * kRedMax + NS + k] : -__builtin_huge_val());
-        if (lane == 0) gp[blockIdx.x * kRedMax + NS + k] = v;
-      }
+      for (int k = 0; k < NM; ++k) v[NS + k] = warp_max_down(lane < nw ? buf[lane * kRedMax + NS + k] : -__builtin_huge_val());
+      if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) gp[blockIdx.x * kRedMax + k] = v[k];
     }
-    cooperative_groups::this_grid().sync();
-    if (warp == 0) {
+    const bool last = arrive(&last_flag);
+    if (last && warp < K) {  // one warp per value, all values in parallel, CTA order fixed
+      const int k = warp;
+      const bool is_sum = k < NS;
       const int nb = gridDim.x;
+      double part[8];
 #pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        double part[8];  // all partial loads in flight at once: one L2 round trip
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int b = lane + 32 * u;
-          part[u] = b < nb ? __ldcg(gp + b * kRedMax + k) : 0.0;
-        }
-        double acc = 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc += part[u];
-        for (int b = lane + 256; b < nb; b += 32) acc += __ldcg(gp + b * kRedMax + k);
-        acc = warp_sum_down(acc);
-        if (lane == 0) buf[32 * kRedMax + k] = acc;
+      for (int u = 0; u < 8; ++u) {
+        const int b = lane + 32 * u;
+        part[u] = b < nb ? __ldcg(gp + b * kRedMax + k) : (is_sum ? 0.0 : -__builtin_huge_val());
       }
+      double acc = is_sum ? 0.0 : -__builtin_huge_val();
 #pragma unroll
-      for (int k = 0; k < NM; ++k) {
-        double acc = -__builtin_huge_val();
-        double part[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int b = lane + 32 * u;
-          part[u] = b < nb ? __ldcg(gp + b * kRedMax + NS + k) : -__builtin_huge_val();
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc = fmax(acc, part[u]);
-        for (int b = lane + 256; b < nb; b += 32) acc = fmax(acc, __ldcg(gp + b * kRedMax + NS + k));
-        acc = warp_max_down(acc);
-        if (lane == 0) buf[32 * kRedMax + NS + k] = acc;
+      for (int u = 0; u < 8; ++u) acc = is_sum ? acc + part[u] : fmax(acc, part[u]);
+      for (int b = lane + 256; b < nb; b += 32) {
+        const double x = __ldcg(gp + b * kRedMax + k);
+        acc = is_sum ? acc + x : fmax(acc, x);
+      }
+      acc = is_sum ? warp_sum_down(acc) : warp_max_down(acc);
+      if (lane == 0) {
+        __stcg(gr + k, acc);
+        __threadfence();  // each writer publishes its own total before the release
       }
     }
-    __syncthreads();
+    if (last) __syncthreads();  // totals written before thread 0 releases
+    release_or_wait(last);
 #pragma unroll
-    for (int k = 0; k < NS; ++k) s[k] = buf[32 * kRedMax + k];
+    for (int k = 0; k < NS; ++k) s[k] = __ldcg(gr + k);
 #pragma unroll
-    for (int k = 0; k < NM; ++k) m[k] = buf[32 * kRedMax + NS + k];
+    for (int k = 0; k < NM; ++k) m[k] = __ldcg(gr + NS + k);
   }
 };
 
