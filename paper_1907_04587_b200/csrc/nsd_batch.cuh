@@ -592,9 +592,10 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
   for (int c = rk; c < W.nc; c += ts) {
     const R* g = W.cgeo + 17 * c;
     const int ba = W.cbody[2 * c], bb = W.cbody[2 * c + 1];
-    const V3<R> pa = ba < 0 ? ld3(g) : body_pos(T, W.q, ba) + ld3(W.carm + 6 * c);
-    const V3<R> pb = bb < 0 ? ld3(g + 3) : body_pos(T, W.q, bb) + ld3(W.carm + 6 * c + 3);
-    mgap = fmin(mgap, (double)(dot(ld3(W.cdir + 9 * c), pa - pb) - g[15]));
+    const CView<R> cv = contact_rec_view(W, c);
+    const V3<R> pa = ba < 0 ? ld3(g) : body_pos(T, W.q, ba) + cv.ra;
+    const V3<R> pb = bb < 0 ? ld3(g + 3) : body_pos(T, W.q, bb) + cv.rb;
+    mgap = fmin(mgap, (double)(dot(cv.n, pa - pb) - g[15]));
   }
   {
     double s[1] = {0.0}, m[4] = {fmax(gmax, fs.hmax), fs.comp, fs.cone, -mgap};

@@ -630,8 +630,10 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
     rb = mul(body_rot(T, q, bb), lb);
     pb = body_pos(T, q, bb) + rb;
   }
-  st3(W.carm + 6 * c, ra);
-  st3(W.carm + 6 * c + 3, rb);
+  if (!W.crec) {  // the batched path keeps the same data in its contact record only
+    st3(W.carm + 6 * c, ra);
+    st3(W.carm + 6 * c + 3, rb);
+  }
   CView<R> cv;
   cv.ba = ba;
   cv.bb = bb;
@@ -640,7 +642,7 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
   cv.n = ld3(g + 6);
   cv.d1 = ld3(g + 9);
   cv.d2 = ld3(g + 12);
-  {
+  if (!W.crec) {
     R* cdir = W.cdir + 9 * c;
     st3(cdir, cv.n);
     st3(cdir + 3, cv.d1);
@@ -665,8 +667,10 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
   const R hn = phi.v / h;
   W.hv[nr] = hn;
   W.cd[nr] = phi.dl / (h * h);
-  W.cscale[2 * c] = phi.dc;  // row kept iff dc != 0 (newton.cpp:187)
-  if (W.crec) W.crec[20 * c + 15] = phi.dc;
+  if (W.crec)
+    W.crec[20 * c + 15] = phi.dc;
+  else
+    W.cscale[2 * c] = phi.dc;  // row kept iff dc != 0 (newton.cpp:187)
   st.comp = fmax(st.comp, (double)ab(mn(gap, lam_n)));
   const R lf0 = W.lam[f0] / h, lf1 = W.lam[f0 + 1] / h;
   const R mu_ln = mu * lam_n;
@@ -682,14 +686,18 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
     h1 = v0 + wv * lf0;
     h2 = v1 + wv * lf1;
     W.cd[f0] = W.cd[f0 + 1] = wv / h;
-    W.cscale[2 * c + 1] = R(1);
-    if (W.crec) W.crec[20 * c + 16] = R(1);
+    if (W.crec)
+      W.crec[20 * c + 16] = R(1);
+    else
+      W.cscale[2 * c + 1] = R(1);
   } else {
     h1 = lf0;
     h2 = lf1;
     W.cd[f0] = W.cd[f0 + 1] = R(1) / h;
-    W.cscale[2 * c + 1] = R(0);
-    if (W.crec) W.crec[20 * c + 16] = R(0);
+    if (W.crec)
+      W.crec[20 * c + 16] = R(0);
+    else
+      W.cscale[2 * c + 1] = R(0);
   }
   W.hv[f0] = h1;
   W.hv[f0 + 1] = h2;
