@@ -456,14 +456,14 @@ __global__ void __launch_bounds__(512) k_single_block(nsd::Topo<R> T, nsd::Work<
 #endif
 // Threads per CTA of the cooperative grid kernel (one CTA per SM).
 constexpr int kGridThreads = NSD_GRID_THREADS;
-template <class R, bool kTets>
+template <class R, bool kTets, int RPT>
 __global__ void __launch_bounds__(kGridThreads) k_single_grid(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out,
                                                      double* gpart) {
   __shared__ double red[2 * 33 * nsd::kRedMax];
   nsd::GridTeam t(red, gpart);
   nsd::newton_setup(t, T, W);
   t.sync();
-  nsd::newton_solve<R, kTets>(t, T, W, cfg, out);
+  nsd::newton_solve<R, kTets, nsd::GridTeam, RPT>(t, T, W, cfg, out);
 }
 
 // ------------------------------------------------------------------ batched
@@ -827,9 +827,9 @@ template <class R> struct Solver final : SolverBase {
       int dev_sms = 0, per_sm = 0;
       NSD_CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
       if (tets)
-        NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, true>, kGridThreads, 0));
+        NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, true, 0>, kGridThreads, 0));
       else
-        NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, false>, kGridThreads, 0));
+        NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, false, 0>, kGridThreads, 0));
       if (per_sm < 1) throw NsdError(NSD_CUDA_ERROR, "grid kernel cannot be resident");
       const char* bps = std::getenv("NSD_GRID_BLOCKS_PER_SM");
       grid_blocks = dev_sms * std::min(per_sm, bps ? std::max(1, std::atoi(bps)) : 1);
@@ -966,7 +966,11 @@ template <class R> struct Solver final : SolverBase {
       double* gp = gpart.as<double>();
       NSD_CK(cudaMemsetAsync(gp + 2 * grid_blocks * nsd::kRedMax + 2 * nsd::kRedMax, 0, 2 * sizeof(unsigned), stream));
       void* args[] = {&topo.t, &W, &kc, &so, &gp};
-      void* fn = tets ? (void*)k_single_grid<R, true> : (void*)k_single_grid<R, false>;
+      // register-resident PCR rows when every thread owns <= 2 rows (NSD_GRID_REGS=0 disables)
+      const bool regs = nrows <= 2 * grid_blocks * kGridThreads && !(std::getenv("NSD_GRID_REGS") &&
+                                                                       std::atoi(std::getenv("NSD_GRID_REGS")) == 0);
+      void* fn = tets ? (regs ? (void*)k_single_grid<R, true, 2> : (void*)k_single_grid<R, true, 0>)
+                      : (regs ? (void*)k_single_grid<R, false, 2> : (void*)k_single_grid<R, false, 0>);
       NSD_CK(cudaLaunchCooperativeKernel(fn, dim3(grid_blocks), dim3(kGridThreads), args, 0, stream));
     }
     NSD_CK(cudaEventRecord(ev1, stream));

@@ -910,7 +910,7 @@ template <class R> __device__ __forceinline__ void integrate_body(const Topo<R>&
 
 // The Newton loop, final classification and telemetry (newton.cpp:343-416).
 // Requires newton_setup() and a barrier, and the step's contact set + incidence.
-template <class R, bool kTets, class Team>
+template <class R, bool kTets, class Team, int RPT = 0>
 __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cfg, StepOut out) {
   const R h = W.h;
   const int nr = W.nrows;
@@ -1031,6 +1031,147 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
       // kTets == false (diagonal C): the accepted update x+=a p, r-=a ap, z-=a M^-1 ap
       // is committed in place during the next row pass (the operator reads the
       // pending z' on the fly), so no trial buffers xn/rn/zn are needed.
+      if constexpr (RPT > 0) {
+        // Register-resident PCR (grid kernel, nr <= RPT * team size): each thread's
+        // own rows keep x, r, z, p, ap, az, inv, bx in registers across all phases.
+        // Global memory carries only what other threads read: ap (the J^T pull's
+        // z' = z - a M^-1 ap) and the committed z (pull base, tet-block C z). Same
+        // recurrence, same arithmetic, same reductions as the memory path below;
+        // each grid barrier's acquire invalidates L1, so this saves the post-barrier
+        // L2 round trips of the row phases.
+        R zr[RPT], pr[RPT], apr[RPT], azr[RPT], xr[RPT], rr_[RPT], invr[RPT], bxr[RPT], xnr[RPT], rnr[RPT], znr[RPT];
+        const int rk = t.rank(), ts = t.size();
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          const int i = rk + k * ts;
+          const bool v = i < nr;
+          zr[k] = v ? W.z[i] : R(0);
+          rr_[k] = v ? W.r[i] : R(0);
+          invr[k] = v ? W.inv[i] : R(0);
+          xr[k] = bxr[k] = pr[k] = apr[k] = azr[k] = xnr[k] = rnr[k] = znr[k] = R(0);
+        }
+        R *zg = W.z, *zng = W.zn;
+        bool pending = false;
+        double zaz = 0.0;
+        if (maxlin > 0 && hist_last > cfg.linear_tolerance) {
+          op_pull(t, T, W, RowArr<R>{zg});
+          t.sync();
+          double za = 0.0;
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) {
+            const int i = rk + k * ts;
+            if (i < nr) {
+              const R a = row_J(T, W, i, W.w) + row_C<R, kTets>(T, W, i, zg) + eps * zr[k];
+              azr[k] = a;
+              za += (double)zr[k] * a;
+            }
+          }
+          double s[1] = {za};
+          t.reduce_sum(s);
+          zaz = s[0];
+        }
+        double beta = 0.0;
+        for (int itl = 0; itl < maxlin && hist_last > cfg.linear_tolerance; ++itl) {
+          double den = 0.0;
+          const R rb = R(beta);
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) {
+            const int i = rk + k * ts;
+            if (i < nr) {
+              if (itl == 0) {
+                pr[k] = zr[k];
+                apr[k] = azr[k];
+              } else {
+                pr[k] = zr[k] + rb * pr[k];
+                apr[k] = azr[k] + rb * apr[k];
+              }
+              W.ap[i] = apr[k];
+              den += (double)apr[k] * (double)(invr[k] * apr[k]);
+            }
+          }
+          {
+            double s[1] = {den};
+            t.reduce_sum(s);
+            den = s[0];
+          }
+          if (fabs(den) < 1e-300) {
+            breakdown = 1;
+            break;
+          }
+          const double alpha = zaz / den;
+          const R ra = R(alpha);
+          double pn2 = 0.0, rn2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) {
+            const int i = rk + k * ts;
+            if (i < nr) {
+              const R rv = rr_[k] - ra * apr[k];
+              xnr[k] = xr[k] + ra * pr[k];
+              rnr[k] = rv;
+              znr[k] = zr[k] - ra * (invr[k] * apr[k]);
+              zng[i] = znr[k];
+              pn2 += (double)rv * (double)(invr[k] * rv);
+              rn2 += (double)rv * rv;
+            }
+          }
+          if (fabs(zaz) >= 1e-300) op_pull(t, T, W, RowPending<R>{zg, W.inv, W.ap, ra});  // w = H^-1 J^T z'
+          {
+            double s[2] = {pn2, rn2};
+            t.reduce_sum(s);
+            pn2 = s[0];
+            rn2 = s[1];
+          }
+          const double pn = sqrt(pn2);
+          if (pn > phist_last) break;  // monotone guard
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) {  // commit
+            xr[k] = xnr[k];
+            rr_[k] = rnr[k];
+            zr[k] = znr[k];
+          }
+          R* tmp = zg;
+          zg = zng;
+          zng = tmp;
+          hist_last = sqrt(rn2);
+          phist_last = pn;
+          if (t.rank() == 0 && out.hist && hist_n <= maxlin) out.hist[(size_t)it * (maxlin + 1) + hist_n] = hist_last;
+          ++hist_n;
+          if (hist_last < best_res) {
+            best_res = hist_last;
+#pragma unroll
+            for (int k = 0; k < RPT; ++k) bxr[k] = xr[k];
+          }
+          lin_used = itl + 1;
+          if (fabs(zaz) < 1e-300) {
+            breakdown = 1;
+            break;
+          }
+          double za = 0.0;
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) {
+            const int i = rk + k * ts;
+            if (i < nr) {
+              const R a = row_J(T, W, i, W.w) + row_C<R, kTets>(T, W, i, zg) + eps * zr[k];
+              azr[k] = a;
+              za += (double)zr[k] * a;
+            }
+          }
+          {
+            double s[1] = {za};
+            t.reduce_sum(s);
+            beta = s[0] / zaz;
+            zaz = s[0];
+          }
+        }
+        (void)pending;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          const int i = rk + k * ts;
+          if (i < nr) W.bx[i] = bxr[k];
+        }
+        W.z = zg;
+        W.zn = zng;
+      } else {
       constexpr bool kInPlace = !kTets;
       bool pending_best = false;
       R pend = R(0);  // alpha of an accepted, not yet committed update (kInPlace)
@@ -1174,6 +1315,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
       W.rn = rn;
       W.z = z;
       W.zn = zn;
+      }  // memory path
     }
     io.linear_iterations = lin_used;
     io.linear_breakdown = breakdown;
