@@ -301,7 +301,7 @@ template <class R> struct DevTopo {
 struct WorkPlan {
   // hot R
   size_t q, u, g, w, du, hinv, iwi6, coeff, hv, cd, lam, x, r, z, p, ap, az, inv, bx, cdir, carm, cscale, jstage,
-      cstage, jstr, crec, hotR;
+      cstage, jstr, crec, qrot, hotR;
   // hot int
   size_t blk, cbody, cinc_off, cinc_ent, cbinc_off, cbinc, cblk, hotI;
   // cold R
@@ -351,6 +351,7 @@ struct WorkPlan {
     cstage = a(9 * c);
     jstr = a(24 * static_cast<size_t>(T.nj));
     crec = a16(20 * c);
+    qrot = a(9 * static_cast<size_t>(T.nb));
     hotR = o;
     o = 0;
     blk = a(4 * rs);
@@ -538,6 +539,15 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
   for (int i = t.rank(); i < T.ncoord; i += t.size()) q0[i] = qs[i];
   for (int i = t.rank(); i < T.ndof; i += t.size()) u0[i] = us[i];
   W.f_extra = nullptr;
+  // per-body rotations at q- (torque hook, narrow phase, first assembly): one
+  // quaternion -> matrix per body instead of one per joint / contact / shape pair
+  R* qrot = hr + P.qrot;
+  t.sync();
+  for (int b = t.rank(); b < T.nb; b += t.size())
+    if (T.btype[b] == 1) {
+      const nsd::M3<R> m = nsd::body_rot(T, q0, b);
+      for (int i = 0; i < 9; ++i) qrot[9 * b + i] = m.a[i];
+    }
   if (A.torque) {
     R* fx = cr + P.fx;
     t.sync();
@@ -553,7 +563,10 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
           const R tau = A.torque_double ? R(static_cast<const double*>(A.torque)[(size_t)env * T.nj + j])
                                         : R(static_cast<const float*>(A.torque)[(size_t)env * T.nj + j]);
           const nsd::V3<R> axl = nsd::ld3(A.jframe + 21 * j + 6);
-          const nsd::V3<R> ax = ja < 0 ? axl : nsd::mul(nsd::body_rot(T, q0, ja), axl);
+          nsd::M3<R> Rj;
+          if (ja >= 0)
+            for (int i = 0; i < 9; ++i) Rj.a[i] = qrot[9 * ja + i];
+          const nsd::V3<R> ax = ja < 0 ? axl : nsd::mul(Rj, axl);
           if (ja == b) f = f + tau * ax;
           if (jb == b) f = f - tau * ax;
         }
@@ -567,7 +580,7 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
   nsd::newton_setup(t, T, W);
   t.sync();
   // ---- narrow phase over shape pairs with the unconstrained velocity
-  nsd::BodyView<R> view{T.btype, T.bdof, T.bcoord, W.q0, W.ut};
+  nsd::BodyView<R> view{T.btype, T.bdof, T.bcoord, W.q0, W.ut, qrot};
   nsd::CandD<R>* cand = A.cand + (size_t)env * A.npairs * 4;
   int* cnt = A.pair_cnt + (size_t)env * A.npairs;
   for (int p = t.rank(); p < A.npairs; p += t.size()) {
@@ -653,6 +666,7 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
       }
     }
     W.jstr = hr + P.jstr;  // structured joint rows: the object solver never reads coeff/blk
+    W.qrot = qrot;         // rotations at q- now; refreshed before every later assembly
     W.crec = hr + P.crec;  // contact records + block ids for vector loads
     W.cblk = reinterpret_cast<int4*>(hi + P.cblk);
     W.jblk = A.jblk;

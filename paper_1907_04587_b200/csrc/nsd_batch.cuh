@@ -303,6 +303,18 @@ __device__ __forceinline__ void body_momentum(const Topo<R>& T, ObjView<R>& O, i
 
 // The Newton loop for one environment (warp). Requires newton_setup + barrier,
 // the contact set, the static row blocks and the body incidence lists.
+// Per-body rotations at the current iterate into W.qrot (one quaternion -> matrix
+// per body instead of one per joint/contact side); needs a team barrier after.
+template <class R, class Team> __device__ __forceinline__ void refresh_rotations(Team& t, const Topo<R>& T, Work<R>& W) {
+  if (!W.qrot) return;
+  for (int b = t.rank(); b < T.nb; b += t.size())
+    if (T.btype[b] == 1) {
+      const M3<R> m = body_rot(T, W.q, b);
+#pragma unroll
+      for (int i = 0; i < 9; ++i) W.qrot[9 * b + i] = m.a[i];
+    }
+}
+
 template <class R, class Team> __device__ int newton_solve_obj(Team& t, const Topo<R>& T, ObjView<R>& O, const Cfg& cfg,
                                                      StepOut out) {
   Work<R>& W = O.W;
@@ -319,7 +331,11 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
   double min_shift = 0.0;
   int n_done = 0, aborted = 0;
   for (int it = 0; it < cfg.newton_iterations; ++it) {
-    // ---- assemble (object lanes)
+    // ---- assemble (object lanes); iteration 0 runs at q- whose rotations batch_env cached
+    if (it > 0) {
+      refresh_rotations(t, T, W);
+      t.sync();
+    }
     AsmStats as{0.0, 0.0, 0.0, 0.0};
     for (int k = rk; k < nobj; k += ts) {
       if (k < T.nj)
@@ -576,6 +592,8 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
     return 1;
   }
   // ---- final assembly for classification (newton.cpp:409-415)
+  refresh_rotations(t, T, W);
+  t.sync();
   AsmStats fs{0.0, 0.0, 0.0, 0.0};
   for (int k = rk; k < nobj; k += ts) {
     if (k < T.nj)

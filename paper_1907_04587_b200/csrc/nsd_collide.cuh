@@ -28,7 +28,8 @@ template <class R> struct BodyView {
   const int* bdof;
   const int* bcoord;
   const R* q;
-  const R* u;  // predicted velocities
+  const R* u;    // predicted velocities
+  const R* rot;  // optional cache: 9 per body, row-major rotation at q (same values quat_rot gives)
 };
 
 template <class R> NSD_HD V3<R> bv_pos(const BodyView<R>& v, int b) {
@@ -37,6 +38,11 @@ template <class R> NSD_HD V3<R> bv_pos(const BodyView<R>& v, int b) {
 }
 template <class R> NSD_HD M3<R> bv_rot(const BodyView<R>& v, int b) {
   if (b < 0 || v.btype[b] == 0) return m3_identity<R>();
+  if (v.rot) {
+    M3<R> m;
+    for (int i = 0; i < 9; ++i) m.a[i] = v.rot[9 * b + i];
+    return m;
+  }
   const R* t = v.q + v.bcoord[b] + 3;
   return quat_rot(t[0], t[1], t[2], t[3]);
 }

@@ -113,6 +113,7 @@ template <class R> struct Work {
   R* crec;   // batched path: 20 per contact (n d1 d2 r_a r_b dc act, 16-byte aligned) or null
   int4* cblk;  // batched path: dof3 blocks (a.lin, a.ang, b.lin, b.ang) per contact
   const int4* jblk;  // batched path: static dof3 blocks per joint (shared by all envs)
+  R* qrot;           // batched path: per-body rotation at the current q (9 each), refreshed before assembly
   R* hv;
   R* cd;
   R* ctet;   // 9 per tet
@@ -174,6 +175,14 @@ template <class R> __device__ __forceinline__ M3<R> body_rot(const Topo<R>& T, c
   if (b < 0 || T.btype[b] == 0) return m3_identity<R>();
   const R* t = q + T.bcoord[b] + 3;
   return quat_rot(t[0], t[1], t[2], t[3]);
+}
+// Rotation from the per-body cache when present (batched path), else from q.
+template <class R> __device__ __forceinline__ M3<R> body_rot_c(const Topo<R>& T, const Work<R>& W, const R* q, int b) {
+  if (!W.qrot || b < 0 || T.btype[b] == 0) return body_rot(T, q, b);
+  M3<R> m;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) m.a[i] = W.qrot[9 * b + i];
+  return m;
 }
 template <class R> __device__ __forceinline__ V3<R> body_pos(const Topo<R>& T, const R* q, int b) {
   return ld3(q + T.bcoord[b]);
@@ -417,7 +426,7 @@ __device__ void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, 
   const R* fr = W.jframe + 21 * j;
   const V3<R> anc_a = ld3(fr), anc_b = ld3(fr + 3), ax_a = ld3(fr + 6), ax_a2 = ld3(fr + 9), ax_b1 = ld3(fr + 12),
               ax_b2 = ld3(fr + 15), rest = ld3(fr + 18);
-  const M3<R> Ra = body_rot(T, q, ba), Rb = body_rot(T, q, bb);
+  const M3<R> Ra = body_rot_c(T, W, q, ba), Rb = body_rot_c(T, W, q, bb);
   const bool rig_a = ba >= 0 && T.btype[ba] == 1, rig_b = bb >= 0 && T.btype[bb] == 1;
   V3<R> wa, wb, ra = v3(R(0), R(0), R(0)), rb = ra;
   if (ba < 0) wa = anc_a;
@@ -621,13 +630,13 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
   if (ba < 0) pa = la;
   else if (!rig_a) pa = body_pos(T, q, ba);
   else {
-    ra = mul(body_rot(T, q, ba), la);
+    ra = mul(body_rot_c(T, W, q, ba), la);
     pa = body_pos(T, q, ba) + ra;
   }
   if (bb < 0) pb = lb;
   else if (!rig_b) pb = body_pos(T, q, bb);
   else {
-    rb = mul(body_rot(T, q, bb), lb);
+    rb = mul(body_rot_c(T, W, q, bb), lb);
     pb = body_pos(T, q, bb) + rb;
   }
   if (!W.crec) {  // the batched path keeps the same data in its contact record only
