@@ -5,7 +5,7 @@
 //   world_demo <scene> <seed> <steps> [fp32|fp64]   trajectory: per-step lines + final q, u
 //   world_demo --free-fall                          newton_step on a hand-built StepContext
 //   world_demo --invalid-h                          h <= 0 must throw std::invalid_argument
-//   world_demo --run <scene> <steps> <out_dir> [ncp] [r]   runner: trajectory.csv + convergence.csv
+//   world_demo --run <scene> <steps> <out_dir> [seed] [ncp] [r]   runner: trajectory.csv + convergence.csv
 //   world_demo --sweep <scene> <axis> <steps> <out_dir>   runner: sweep.csv
 #include "nsdyn_b200.hpp"
 
@@ -68,8 +68,9 @@ static int run_cmd(int argc, char** argv) {
   o.scene = argv[2];
   o.steps = std::atoi(argv[3]);
   o.out_dir = argv[4];
-  if (argc > 5) o.ncp = std::string(argv[5]);
-  if (argc > 6) o.r_strategy = std::string(argv[6]);
+  if (argc > 5) o.seed = static_cast<unsigned>(std::atoi(argv[5]));
+  if (argc > 6) o.ncp = std::string(argv[6]);
+  if (argc > 7) o.r_strategy = std::string(argv[7]);
   std::string err;
   const int rc = nb::run(o, &err);
   std::printf("run rc %d %s\n", rc, err.c_str());
