@@ -119,3 +119,21 @@ def test_batch_odd_env_count_partial_block_fp64():
     q, _ = b.get_state()
     for e, w in enumerate(worlds):
         assert rel_err(q[e], w.state()[0]) < 1e-8, e
+
+
+def test_batch_nan_env_aborts_alone():
+    """One env with a NaN velocity aborts (rolled back, flagged); its neighbours in
+    the same warp/block are unaffected and keep tracking the oracle."""
+    b, s0 = _batch(4, "fp64")
+    q, u = b.get_state()
+    u = u.copy()
+    u[1, 2] = np.nan
+    b.set_state(q.reshape(-1), u.reshape(-1))
+    b.step(s0.h, s0.gravity)
+    res = b.results()
+    assert res["aborted"].tolist() == [False, True, False, False]
+    q1, _ = b.get_state()
+    assert np.array_equal(q1[1], q[1])
+    w = O.OracleWorld("c5", 2)
+    assert w.step(1) == 0
+    assert rel_err(q1[2], w.state()[0]) < 1e-12

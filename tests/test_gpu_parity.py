@@ -203,3 +203,25 @@ def test_determinism_bitwise():
     a = run_gpu(case, "fp32")
     b = run_gpu(case, "fp32")
     assert np.array_equal(a["q"], b["q"]) and np.array_equal(a["lam"], b["lam"])
+
+
+def test_nan_input_rolls_back_and_reports_abort():
+    """A NaN in the input velocity. The device follows newton.cpp:362-369: the
+    non-finite Newton update rolls q, u back to the step start and the step
+    reports aborted (the runner's exit code 2). The reference itself takes a
+    different road here (stated in DESIGN.md §2): the NaN reaches the Schur
+    right-hand side, BestTracker (solvers.cpp:12-21) never accepts an iterate,
+    and spmv_transpose throws on the empty solution (newton.cpp:291-293) — the
+    oracle reproduces that exception."""
+    case = oracle_case("c1", 0, 3)
+    q0, u0 = case["q"].copy(), case["u"].copy()
+    case["u"] = u0.copy()
+    case["u"][2] = np.nan
+    w = case["world"]
+    w.set_state(q0, case["u"])
+    g = run_gpu(case, "fp64")
+    assert g["aborted"]
+    assert np.array_equal(g["q"], q0)
+    assert np.isnan(g["u"][2]) and np.array_equal(np.delete(g["u"], 2), np.delete(u0, 2))
+    with pytest.raises(RuntimeError, match="spmv_transpose"):
+        run_oracle(case)
