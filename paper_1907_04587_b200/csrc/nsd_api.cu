@@ -512,9 +512,20 @@ template <class R> __host__ __device__ constexpr int pool_row_vecs() { return si
 // Elements of the per-env shared-memory row region for nc contacts: the
 // write-heavy PCR state x, r, z, p, ap, az, bx (7 x rows), the J^T staging
 // (12 per joint, 9 per contact) and w (ndof), each array kept 16-byte aligned.
+#ifndef NSD_POOL_EXTRA
+#define NSD_POOL_EXTRA 4
+#endif
+// Extra arrays in the fp32 region: 1 contact records, 2 joint records, 4 the H^-1
+// diagonal. Measured (C5 fp32, env-steps/s): none 4.25 M, +records 4.18 M, +joint
+// records 4.16 M (both cost L1 via the carveout), +H^-1 4.37 M -> 4.
+template <class R> __host__ __device__ constexpr int pool_extra() { return sizeof(R) == 4 ? NSD_POOL_EXTRA : 0; }
 template <class R> __host__ __device__ inline int row_pool_elems(int rows_static, int nj, int ndof, int nc) {
   const int rows = (rows_static + 3 * nc + 3) & ~3;
-  return pool_row_vecs<R>() * rows + ((12 * nj + 3) & ~3) + ((9 * nc + 3) & ~3) + ((ndof + 3) & ~3);
+  int n = pool_row_vecs<R>() * rows + ((12 * nj + 3) & ~3) + ((9 * nc + 3) & ~3) + ((ndof + 3) & ~3);
+  if (pool_extra<R>() & 1) n += 20 * nc;
+  if (pool_extra<R>() & 2) n += (24 * nj + 3) & ~3;
+  if (pool_extra<R>() & 4) n += (ndof + 3) & ~3;
+  return n;
 }
 
 template <class R, class Team>
@@ -716,6 +727,19 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
       // w = H^-1 J^T y is produced by body_momentum; copy the setup value over
       for (int i = t.rank(); i < T.ndof; i += t.size()) sp[i] = W.w[i];
       O.W.w = sp;
+      sp += (T.ndof + 3) & ~3;
+      if (pool_extra<R>() & 1) {
+        O.W.crec = sp;
+        sp += 20 * nc;
+      }
+      if (pool_extra<R>() & 2) {
+        O.W.jstr = sp;
+        sp += (24 * T.nj + 3) & ~3;
+      }
+      if (pool_extra<R>() & 4) {
+        O.W.hinv = sp;
+        sp += (T.ndof + 3) & ~3;
+      }
       t.sync();
     }
     nsd::newton_solve_obj(t, T, O, A.cfg, out);
