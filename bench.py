@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU baseline sample length")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-alt", action="store_true", help="skip the secondary-precision measurement")
+    p.add_argument("--no-scenes", action="store_true", help="skip the C1-C4 single-scene summary")
     p.add_argument("--workload", default="c5",
                    help="c5 (default: batched ants, the headline) or one single scene (c1, c2, c3, c4, c2:6, ...) "
                         "stepped through World.step (host detect + GPU newton_step)")
@@ -286,6 +287,35 @@ def roofline(m, prec, K):
             "model": "SURVEY 8(d) B_CR per env per CR iteration x 40 CR iterations x envs"}
 
 
+def scene_summary(name, precision, steps, warmup):
+    """ms/step and us per CR iteration of one single scene through World.step
+    (device time per step from CUDA events in nsd_step, L2 flushed between steps)."""
+    import torch
+
+    from paper_1907_04587_b200 import World
+
+    w = World(name, 0, precision=precision)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(warmup):
+        w.step()
+    dev, wall = [], []
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = w.step()
+        wall.append(time.perf_counter() - t0)
+        dev.append(rep["ms"])
+    cfg = w.config
+    ms = float(np.mean(dev))
+    out = {"ms_per_step": ms, "us_per_cr_iter": 1000.0 * ms / (cfg.newton_iterations * cfg.linear_max_iterations),
+           "steps_per_s": 1000.0 / ms, "e2e_steps_per_s": 1.0 / float(np.mean(wall)),
+           "budget": f"{cfg.newton_iterations}x{cfg.linear_max_iterations}", "tets": w.scene.dims["n_tets"],
+           "bodies": w.scene.dims["n_bodies"]}
+    w.close()
+    return out
+
+
 def run_scene(args):
     """One scene per GPU (C1-C4 are replicas only): K x step_world through
     the public World API. value = steps/s from the device time of each step's kernel
@@ -403,6 +433,14 @@ def main():
             "gpu_launches": K, "clocks": m["clocks"]}
     if other:
         line["other_precision"] = other
+    if ws == 1 and not args.no_scenes:
+        # the other BASELINE configs (single scenes, replicas only), fp64, 20 steps each
+        line["single_scenes"] = {}
+        for name in ("c1", "c3", "c2", "c4"):
+            try:
+                line["single_scenes"][name] = scene_summary(name, "fp64", 20, 3)
+            except Exception as e:  # reported, never fatal for the headline
+                line["single_scenes"][name] = {"error": str(e)}
     if ws == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(args, E)
