@@ -112,31 +112,33 @@ def count_rows(topology: Topology, n_contacts: int) -> int:
     return lib().nsd_count_rows(C.byref(topology.c), n_contacts)
 
 
+def _contact_views(arr, n):
+    """(n,4) int32 and (n,22) float64 views of an nsd_contact array: the C struct is
+    4 int32 (body_a, body_b, feature, pad) followed by 22 doubles in exactly the
+    array layout (local_a, local_b, normal, d1, d2, thickness, mu, lambda_n,
+    lambda_f[2], pad[2])."""
+    raw = np.frombuffer(arr, dtype=np.uint8)[: n * C.sizeof(nsd_contact)].reshape(n, C.sizeof(nsd_contact))
+    return raw[:, :16].view(np.int32), raw[:, 16:].view(np.float64)
+
+
 def contacts_from_arrays(ib, db):
     """(n,4) int [body_a, body_b, feature, 0] + (n,22) doubles -> nsd_contact array."""
     n = len(ib)
     arr = (nsd_contact * max(n, 1))()
-    for i in range(n):
-        c = arr[i]
-        c.body_a, c.body_b, c.feature = int(ib[i][0]), int(ib[i][1]), int(ib[i][2])
-        d = db[i]
-        for k in range(3):
-            c.local_a[k], c.local_b[k], c.normal[k], c.d1[k], c.d2[k] = d[k], d[3 + k], d[6 + k], d[9 + k], d[12 + k]
-        c.thickness, c.mu, c.lambda_n = d[15], d[16], d[17]
-        c.lambda_f[0], c.lambda_f[1] = d[18], d[19]
+    if n:
+        vi, vd = _contact_views(arr, n)
+        vi[:, :3] = np.asarray(ib)[:, :3]
+        vd[:, :20] = np.asarray(db, np.float64)[:, :20]
     return arr, n
 
 
 def contacts_to_arrays(arr, n):
     ib = np.zeros((n, 4), np.int32)
     db = np.zeros((n, 22))
-    for i in range(n):
-        c = arr[i]
-        ib[i] = (c.body_a, c.body_b, c.feature, 0)
-        db[i, 0:3], db[i, 3:6], db[i, 6:9] = list(c.local_a), list(c.local_b), list(c.normal)
-        db[i, 9:12], db[i, 12:15] = list(c.d1), list(c.d2)
-        db[i, 15], db[i, 16], db[i, 17] = c.thickness, c.mu, c.lambda_n
-        db[i, 18], db[i, 19] = c.lambda_f[0], c.lambda_f[1]
+    if n:
+        vi, vd = _contact_views(arr, n)
+        ib[:, :3] = vi[:, :3]
+        db[:, :20] = vd[:, :20]
     return ib, db
 
 
