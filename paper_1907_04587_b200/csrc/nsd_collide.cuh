@@ -69,22 +69,20 @@ template <class R> NSD_HD V3<R> corner(const R* he, int k) {
   return v3(sx * he[0], sy * he[1], sz * he[2]);
 }
 
-template <class R> NSD_HD bool gap_less(const CandD<R>& a, const CandD<R>& b) {
-  return a.gap != b.gap ? a.gap < b.gap : a.feature < b.feature;
-}
-
-// Keeps the 4 smallest (gap, feature) of n candidates, sorted (insertion sort).
-template <class R> NSD_HD int keep4(CandD<R>* c, int n) {
-  for (int i = 1; i < n; ++i) {
-    CandD<R> x = c[i];
-    int j = i - 1;
-    while (j >= 0 && gap_less(x, c[j])) {
-      c[j + 1] = c[j];
-      --j;
-    }
-    c[j + 1] = x;
+// Rank of candidate k among the valid ones by (gap, feature): features are
+// unique, so ranks 0..3 are exactly the 4 smallest in ascending order, the order
+// the reference's sorted keep-4 produces (collision.cpp:87-93). Fully unrolled over the
+// 8 corners so gaps and ranks stay in registers (no candidate array in local
+// memory).
+template <class R> NSD_HD void rank8(const R (&gap)[8], const bool (&valid)[8], int (&rank)[8]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int r = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      r += (valid[j] && (gap[j] < gap[k] || (gap[j] == gap[k] && j < k))) ? 1 : 0;
+    rank[k] = r;
   }
-  return n < 4 ? n : 4;
 }
 
 template <class R>
@@ -109,22 +107,30 @@ NSD_HD int box_halfspace(const BodyView<R>& v, const ShapeD<R>& box, const Shape
   const V3<R> n = normalize(get3(hs.n));
   const M3<R> r = shape_rot(v, box);
   const V3<R> x = shape_pos(v, box);
-  CandD<R> loc[8];
+  R gap[8];
+  bool valid[8];
+  int rank[8];
+#pragma unroll
   for (int k = 0; k < 8; ++k) {
+    gap[k] = dot(n, x + mul(r, corner(box.he, k))) - hs.offset;
+    valid[k] = true;
+  }
+  rank8(gap, valid, rank);  // feature = corner index k
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (rank[k] >= 4) continue;
     const V3<R> cl = corner(box.he, k);
     const V3<R> w = x + mul(r, cl);
-    CandD<R>& o = loc[k];
-    o.gap = dot(n, w) - hs.offset;
+    CandD<R>& o = out[rank[k]];
+    o.gap = gap[k];
     o.a = box.body;
     put3(o.la, cl);
     o.b = hs.body;
-    put3(o.lb, w - o.gap * n);
+    put3(o.lb, w - gap[k] * n);
     put3(o.n, n);
     o.feature = k;
   }
-  const int m = keep4(loc, 8);
-  for (int k = 0; k < m; ++k) out[k] = loc[k];
-  return m;
+  return 4;
 }
 
 template <class R>
@@ -230,32 +236,40 @@ NSD_HD int box_box(const BodyView<R>& v, const ShapeD<R>& sa, const ShapeD<R>& s
   const int ref = best_ref, inc = 1 - best_ref;
   const V3<R> nref = best_dir * col(rot[ref], best_axis);
   const V3<R> fp = pos[ref] + (best_dir * bx[ref]->he[best_axis]) * col(rot[ref], best_axis);
-  CandD<R> loc[8];
+  R gap[8];
+  bool valid[8];
+  int rank[8];
   int m = 0;
+#pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const V3<R> ck = corner(bx[inc]->he, k);
-    const V3<R> w = pos[inc] + mul(rot[inc], ck);
-    const R gap = dot(nref, w - fp);
-    if (gap > margin) continue;
+    const V3<R> w = pos[inc] + mul(rot[inc], corner(bx[inc]->he, k));
+    gap[k] = dot(nref, w - fp);
+    bool ok = !(gap[k] > margin);
     const V3<R> in_ref = mul_t(rot[ref], w - pos[ref]);
-    bool inside = true;
+#pragma unroll
     for (int axis = 0; axis < 3; ++axis) {
       if (axis == best_axis) continue;
-      if (ab(in_ref[axis]) > bx[ref]->he[axis] + R(1e-6)) inside = false;
+      if (ab(in_ref[axis]) > bx[ref]->he[axis] + R(1e-6)) ok = false;
     }
-    if (!inside) continue;
-    CandD<R>& o = loc[m++];
-    o.gap = gap;
+    valid[k] = ok;
+    m += ok ? 1 : 0;
+  }
+  rank8(gap, valid, rank);  // among the valid corners; feature = corner index k
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (!valid[k] || rank[k] >= 4) continue;
+    const V3<R> ck = corner(bx[inc]->he, k);
+    const V3<R> w = pos[inc] + mul(rot[inc], ck);
+    CandD<R>& o = out[rank[k]];
+    o.gap = gap[k];
     o.a = bx[inc]->body;
     put3(o.la, ck);
     o.b = bx[ref]->body;
-    put3(o.lb, to_local(v, *bx[ref], w - gap * nref));
+    put3(o.lb, to_local(v, *bx[ref], w - gap[k] * nref));
     put3(o.n, nref);
     o.feature = k;
   }
-  const int keep = keep4(loc, m);
-  for (int k = 0; k < keep; ++k) out[k] = loc[k];
-  return keep;
+  return m < 4 ? m : 4;
 }
 
 template <class R> NSD_HD V3<R> point_vel(const BodyView<R>& v, int body, V3<R> w) {
