@@ -204,25 +204,27 @@ NSD_HD int sphere_box(const BodyView<R>& v, const ShapeD<R>& sph, const ShapeD<R
 
 template <class R>
 NSD_HD int box_box(const BodyView<R>& v, const ShapeD<R>& sa, const ShapeD<R>& sb, R margin, CandD<R>* out) {
-  const ShapeD<R>* bx[2] = {&sa, &sb};
-  M3<R> rot[2];
-  V3<R> pos[2];
-  for (int k = 0; k < 2; ++k) {
-    rot[k] = shape_rot(v, *bx[k]);
-    pos[k] = shape_pos(v, *bx[k]);
-  }
+  // (the two boxes' frames are selected by value, never through a runtime index,
+  // so they stay in registers)
+  const M3<R> rot0 = shape_rot(v, sa), rot1 = shape_rot(v, sb);
+  const V3<R> pos0 = shape_pos(v, sa), pos1 = shape_pos(v, sb);
   int best_ref = -1, best_axis = -1;
   R best_dir = R(1), best_sep = -Lim<R>::inf();
-  for (int ref = 0; ref < 2; ++ref)
+#pragma unroll
+  for (int ref = 0; ref < 2; ++ref) {
+    const M3<R>& rr = ref == 0 ? rot0 : rot1;
+    const M3<R>& ro = ref == 0 ? rot1 : rot0;
+    const V3<R> pr = ref == 0 ? pos0 : pos1, po = ref == 0 ? pos1 : pos0;
+    const ShapeD<R>& br = ref == 0 ? sa : sb;
+    const ShapeD<R>& bo = ref == 0 ? sb : sa;
     for (int axis = 0; axis < 3; ++axis)
       for (int di = 0; di < 2; ++di) {
         const R dir = di == 0 ? R(1) : R(-1);
-        const V3<R> n = dir * col(rot[ref], axis);
-        const V3<R> fp = pos[ref] + (dir * bx[ref]->he[axis]) * col(rot[ref], axis);
-        const int other = 1 - ref;
+        const V3<R> n = dir * col(rr, axis);
+        const V3<R> fp = pr + (dir * br.he[axis]) * col(rr, axis);
         R mnp = Lim<R>::inf();
         for (int k = 0; k < 8; ++k) {
-          const V3<R> w = pos[other] + mul(rot[other], corner(bx[other]->he, k));
+          const V3<R> w = po + mul(ro, corner(bo.he, k));
           mnp = mn(mnp, dot(n, w - fp));
         }
         if (mnp > best_sep + R(1e-12)) {
@@ -232,24 +234,29 @@ NSD_HD int box_box(const BodyView<R>& v, const ShapeD<R>& sa, const ShapeD<R>& s
           best_dir = dir;
         }
       }
+  }
   if (best_sep > margin) return 0;
-  const int ref = best_ref, inc = 1 - best_ref;
-  const V3<R> nref = best_dir * col(rot[ref], best_axis);
-  const V3<R> fp = pos[ref] + (best_dir * bx[ref]->he[best_axis]) * col(rot[ref], best_axis);
+  const bool r0 = best_ref == 0;
+  const ShapeD<R>& bref = r0 ? sa : sb;
+  const ShapeD<R>& binc = r0 ? sb : sa;
+  const M3<R> rot_ref = r0 ? rot0 : rot1, rot_inc = r0 ? rot1 : rot0;
+  const V3<R> pos_ref = r0 ? pos0 : pos1, pos_inc = r0 ? pos1 : pos0;
+  const V3<R> nref = best_dir * col(rot_ref, best_axis);
+  const V3<R> fp = pos_ref + (best_dir * bref.he[best_axis]) * col(rot_ref, best_axis);
   R gap[8];
   bool valid[8];
   int rank[8];
   int m = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const V3<R> w = pos[inc] + mul(rot[inc], corner(bx[inc]->he, k));
+    const V3<R> w = pos_inc + mul(rot_inc, corner(binc.he, k));
     gap[k] = dot(nref, w - fp);
     bool ok = !(gap[k] > margin);
-    const V3<R> in_ref = mul_t(rot[ref], w - pos[ref]);
+    const V3<R> in_ref = mul_t(rot_ref, w - pos_ref);
 #pragma unroll
     for (int axis = 0; axis < 3; ++axis) {
       if (axis == best_axis) continue;
-      if (ab(in_ref[axis]) > bx[ref]->he[axis] + R(1e-6)) ok = false;
+      if (ab(in_ref[axis]) > bref.he[axis] + R(1e-6)) ok = false;
     }
     valid[k] = ok;
     m += ok ? 1 : 0;
@@ -258,14 +265,14 @@ NSD_HD int box_box(const BodyView<R>& v, const ShapeD<R>& sa, const ShapeD<R>& s
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     if (!valid[k] || rank[k] >= 4) continue;
-    const V3<R> ck = corner(bx[inc]->he, k);
-    const V3<R> w = pos[inc] + mul(rot[inc], ck);
+    const V3<R> ck = corner(binc.he, k);
+    const V3<R> w = pos_inc + mul(rot_inc, ck);
     CandD<R>& o = out[rank[k]];
     o.gap = gap[k];
-    o.a = bx[inc]->body;
+    o.a = binc.body;
     put3(o.la, ck);
-    o.b = bx[ref]->body;
-    put3(o.lb, to_local(v, *bx[ref], w - gap[k] * nref));
+    o.b = bref.body;
+    put3(o.lb, to_local(v, bref, w - gap[k] * nref));
     put3(o.n, nref);
     o.feature = k;
   }
@@ -293,7 +300,7 @@ NSD_HD int pair_contacts(const BodyView<R>& v, const ShapeD<R>& si, const ShapeD
                          CandD<R>* out, R* thick_out, R* mu_out) {
   if (si.body < 0 && sj.body < 0) return 0;
   if (si.body >= 0 && si.body == sj.body) return 0;
-  CandD<R> c[4];
+  CandD<R>* c = out;  // generated in place (no local staging array), compacted below
   int n = 0;
   const int ki = si.kind, kj = sj.kind;
   if (ki == 1 && kj == 0) n = sphere_halfspace(v, si, sj, c);
@@ -317,7 +324,8 @@ NSD_HD int pair_contacts(const BodyView<R>& v, const ShapeD<R>& si, const ShapeD
     if (predicted > margin) continue;
     c[k].thick = thick;
     c[k].mu = mu;
-    out[kept++] = c[k];
+    if (kept != k) out[kept] = c[k];  // in-place compaction: kept <= k
+    ++kept;
   }
   *thick_out = thick;
   *mu_out = mu;
