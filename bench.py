@@ -69,10 +69,13 @@ def dist_info():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region: the
+    sampler is started and waited for (its first line) before the region opens,
+    and only samples taken between begin() and end() are reported."""
 
     def __init__(self, device):
         self.device, self.samples, self.proc, self.thread = device, [], None, None
+        self.t0 = self.t1 = None
 
     def start(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -86,14 +89,26 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        deadline = time.time() + 5.0
+        while not self.samples and time.time() < deadline:  # nvidia-smi is up and sampling
+            time.sleep(0.01)
 
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 6:
-                self.samples.append(parts)
+                self.samples.append((time.time(), parts))
+
+    def begin(self):
+        self.t0 = time.time()
+
+    def end(self):
+        self.t1 = time.time()
 
     def stop(self):
+        if self.t1 is None:
+            self.end()
+        time.sleep(0.05)
         if self.proc:
             self.proc.terminate()
             try:
@@ -102,12 +117,14 @@ class ClockSampler:
                 self.proc.kill()
         if self.thread:
             self.thread.join(timeout=2)
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        t0 = self.t0 if self.t0 is not None else 0.0
+        inside = [p for t, p in self.samples if t0 <= t <= self.t1 + 0.02]
+        sm = [float(s[0]) for s in inside if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in inside if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i] and "Not" not in s[2 + i]})
+        reasons = sorted({names[i] for s in inside for i in range(4) if "Active" in s[2 + i] and "Not" not in s[2 + i]})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(inside)}
 
 
 def hbm_peak():
@@ -215,12 +232,15 @@ def measure(args, prec, T, tmpl, E, env0, ws, rank, local, sample_clocks):
     torch.cuda.synchronize()
     if sampler:
         sampler.start()
+        sampler.begin()
     for k in range(K):
         flush.zero_()
         ev[k][0].record(stream)
         step(W + k)
         ev[k][1].record(stream)
     torch.cuda.synchronize()
+    if sampler:
+        sampler.end()
     clocks = sampler.stop() if sampler else None
     if ws > 1:
         torch.distributed.barrier()
@@ -335,6 +355,7 @@ def run_scene(args):
     dev, wall, pcr = [], [], 0
     sampler = ClockSampler(local)
     sampler.start()
+    sampler.begin()
     for _ in range(K):
         flush.zero_()
         torch.cuda.synchronize()
