@@ -18,7 +18,7 @@
 // std::invalid_argument (bodies.cpp:80, constraints.cpp:142-144,
 // solvers.cpp:188-190); a NaN in the Newton update rolls q, u back and returns
 // a report with aborted = true (newton.cpp:362-369). A CUDA failure or an
-// option that is not on the GPU path (linear co-rotational tets, Jacobi/GS/PCG,
+// option that is not on the GPU path (linear co-rotational tets, Gauss-Seidel,
 // record_iterates) throws std::runtime_error — there is no CPU fallback.
 //
 // Device state: newton_step keeps one device solver per thread, keyed by the
@@ -362,8 +362,8 @@ struct FlatTopology {
 
 inline nsd_config to_c(const NewtonConfig& c) {
   if (c.record_iterates) throw std::runtime_error("nsdyn_b200: record_iterates is not on the GPU path");
-  if (c.linear.method != LinearMethod::PCR)
-    throw std::runtime_error("nsdyn_b200: only PCR runs on the GPU Newton path (solvers.cpp:127-174)");
+  if (c.linear.method == LinearMethod::GaussSeidel)
+    throw std::runtime_error("nsdyn_b200: Gauss-Seidel's sequential row sweep is not on the GPU path");
   nsd_config k{};
   nsd_config_default(&k, c.precision == Precision::FP64 ? NSD_FP64 : NSD_FP32);
   k.newton_iterations = c.newton_iterations;
@@ -372,7 +372,7 @@ inline nsd_config to_c(const NewtonConfig& c) {
   k.geometric_stiffness = c.geometric_stiffness ? 1 : 0;
   k.r_strategy = static_cast<int32_t>(c.r_strategy);
   k.ncp_kind = static_cast<int32_t>(c.ncp_kind);
-  k.linear_method = 3;
+  k.linear_method = static_cast<int32_t>(c.linear.method);  // 0 Jacobi, 2 PCG, 3 PCR
   k.linear_max_iterations = c.linear.max_iterations;
   k.linear_tolerance = c.linear.tolerance;
   k.preconditioner = static_cast<int32_t>(c.linear.preconditioner);
@@ -688,7 +688,7 @@ inline SolveReport step_world(World& w) {
 struct RunOptions {
   std::string scene;  // builder name (JSON scene files are not part of this path)
   int steps = 100;
-  std::optional<std::string> solver_method;  // pcr (jacobi | gs | pcg are not on the GPU Newton path)
+  std::optional<std::string> solver_method;  // jacobi | pcg | pcr (gs is not on the GPU Newton path)
   std::optional<std::string> ncp;            // minmap | fb
   std::optional<std::string> r_strategy;     // identity | h2 | effmass
   std::optional<int> newton_iters;
@@ -723,10 +723,15 @@ inline void write_atomic(const std::filesystem::path& path, const std::string& c
 inline void apply_overrides(const RunOptions& o, NewtonConfig& c) {
   if (o.solver_method) {
     const std::string& m = *o.solver_method;
-    if (m == "jacobi" || m == "gs" || m == "pcg")
-      throw std::runtime_error("solver \"" + m + "\" is not on the GPU Newton path (pcr only)");
-    if (m != "pcr") throw std::runtime_error("unknown solver \"" + m + "\"");
-    c.linear.method = LinearMethod::PCR;
+    if (m == "gs") throw std::runtime_error("solver \"gs\" (Gauss-Seidel) is not on the GPU Newton path");
+    if (m == "jacobi")
+      c.linear.method = LinearMethod::Jacobi;
+    else if (m == "pcg")
+      c.linear.method = LinearMethod::PCG;
+    else if (m == "pcr")
+      c.linear.method = LinearMethod::PCR;
+    else
+      throw std::runtime_error("unknown solver \"" + m + "\"");
   }
   if (o.ncp) {
     if (*o.ncp == "minmap")
@@ -842,13 +847,13 @@ inline int run(const RunOptions& o, std::string* error = nullptr) {
 }
 
 // sweep (runner.cpp:182-218): one run per axis value, merged sweep.csv. The
-// "solver" axis only has pcr on the GPU path.
+// "solver" axis runs jacobi, pcg and pcr (Gauss-Seidel is not on the GPU path).
 inline int sweep(const RunOptions& o, const std::string& axis, std::string* error = nullptr) {
   try {
     if (o.steps < 1) throw std::runtime_error("--steps must be >= 1");
     std::vector<std::string> values;
     if (axis == "solver")
-      values = {"pcr"};
+      values = {"jacobi", "pcg", "pcr"};
     else if (axis == "r_strategy")
       values = {"identity", "h2", "effmass"};
     else if (axis == "ncp")

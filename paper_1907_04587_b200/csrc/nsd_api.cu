@@ -110,13 +110,16 @@ nsd::Cfg to_cfg(const nsd_config& c) {
   o.preconditioner = c.preconditioner;
   o.newton_tolerance = c.newton_tolerance;
   o.line_search = c.line_search;
+  o.linear_method = c.linear_method;
   return o;
 }
 
 void check_cfg(const nsd_config& c) {
   if (c.precision != NSD_FP32 && c.precision != NSD_FP64) throw NsdError(NSD_INVALID, "precision must be 0 or 1");
-  if (c.linear_method != 3)
-    throw NsdError(NSD_UNSUPPORTED, "only PCR (linear_method 3) runs on the device path (SURVEY §8f row 4)");
+  if (c.linear_method == 1)
+    throw NsdError(NSD_UNSUPPORTED, "Gauss-Seidel's ascending-row sweep is sequential: not on the device path");
+  if (c.linear_method != 0 && c.linear_method != 2 && c.linear_method != 3)
+    throw NsdError(NSD_INVALID, "linear_method must be 0 (Jacobi), 2 (PCG) or 3 (PCR)");
   if (c.linear_max_iterations < 1) throw NsdError(NSD_INVALID, "solve_linear: max_iterations < 1");
   if (c.newton_iterations < 0) throw NsdError(NSD_INVALID, "newton_iterations < 0");
   if (c.r_strategy < 0 || c.r_strategy > 2 || c.ncp_kind < 0 || c.ncp_kind > 1 || c.preconditioner < 0 ||
@@ -1012,7 +1015,7 @@ template <class R> struct Solver final : SolverBase {
       NSD_CK(cudaMemsetAsync(gp + 2 * grid_blocks * nsd::kRedMax + 2 * nsd::kRedMax, 0, 2 * sizeof(unsigned), stream));
       void* args[] = {&topo.t, &W, &kc, &so, &gp};
       // register-resident PCR rows when every thread owns <= 2 rows (NSD_GRID_REGS=0 disables)
-      const bool regs = nrows <= 2 * grid_blocks * kGridThreads && !(std::getenv("NSD_GRID_REGS") &&
+      const bool regs = cfg.linear_method == 3 && nrows <= 2 * grid_blocks * kGridThreads && !(std::getenv("NSD_GRID_REGS") &&
                                                                        std::atoi(std::getenv("NSD_GRID_REGS")) == 0);
       void* fn = tets ? (regs ? (void*)k_single_grid<R, true, 2> : (void*)k_single_grid<R, true, 0>)
                       : (regs ? (void*)k_single_grid<R, false, 2> : (void*)k_single_grid<R, false, 0>);
@@ -1147,6 +1150,7 @@ template <class R> struct Batch final : BatchBase {
     if (npairs) NSD_CK(cudaMemcpy(pairs.p, hp.data(), sizeof(int2) * npairs, cudaMemcpyHostToDevice));
     plan.plan(H, maxc);
     if (cfg.line_search) throw NsdError(NSD_UNSUPPORTED, "batched path: line search runs through nsd_step");
+    if (cfg.linear_method != 3) throw NsdError(NSD_UNSUPPORTED, "batched path: PCR only (Jacobi/PCG run through nsd_step)");
     {  // static joint incidence per body for the warp solver: joint*2 + side (merged same-body -> side 0)
       std::vector<std::vector<int>> per(H.nb);
       for (int j = 0; j < H.nj; ++j) {

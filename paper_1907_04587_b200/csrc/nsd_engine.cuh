@@ -56,6 +56,7 @@ struct Cfg {
   int preconditioner;  // 0 none, 1 diagonal
   double newton_tolerance;
   int line_search;
+  int linear_method;   // 0 Jacobi, 2 PCG, 3 PCR (solvers.h:8); Gauss-Seidel is not on the device path
 };
 
 // Static topology (shared by every environment of a batch).
@@ -1015,7 +1016,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
     for (int i = t.rank(); i < nr; i += t.size()) {
       const R b = row_J(T, W, i, W.w) - W.hv[i];
       R inv = R(1);
-      if (cfg.preconditioner == 1) {
+      if (cfg.preconditioner == 1 || cfg.linear_method == 0) {  // Jacobi always uses the diagonal (solvers.cpp:35)
         const R sd = row_quad(T, W, i) + row_Cdiag<R, kTets>(T, W, i) + eps;
         inv = sd > R(0) ? R(1) / sd : R(1);
       }
@@ -1040,7 +1041,98 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
       // kTets == false (diagonal C): the accepted update x+=a p, r-=a ap, z-=a M^-1 ap
       // is committed in place during the next row pass (the operator reads the
       // pending z' on the fly), so no trial buffers xn/rn/zn are needed.
-      if constexpr (RPT > 0) {
+      if (cfg.linear_method == 0 || cfg.linear_method == 2) {
+        // Jacobi (solvers.cpp:32-50) and PCG (solvers.cpp:83-121) on the same
+        // matrix-free operator S v = J H^-1 J^T v + C v + eps v, x0 = 0, best iterate
+        // by residual 2-norm, breakdown tests at 1e-300 in double.
+        R *x = W.x, *r = W.r, *z = W.z, *p = W.p, *bb = W.zn;
+        const bool jac = cfg.linear_method == 0;
+        bool pending_best = false;
+        for (int i = t.rank(); i < nr; i += t.size()) {
+          bb[i] = r[i];
+          p[i] = z[i];
+        }
+        double rz = s1[1];  // r . M^-1 r of the setup reduction (PCG)
+        for (int itl = 0; itl < maxlin && hist_last > cfg.linear_tolerance; ++itl) {
+          double rr2 = 0.0, rzn = 0.0;
+          if (jac) {
+            for (int i = t.rank(); i < nr; i += t.size()) {  // x += D^-1 r
+              if (pending_best) W.bx[i] = x[i];
+              x[i] = x[i] + W.inv[i] * r[i];
+            }
+            pending_best = false;
+            t.sync();
+            op_pull(t, T, W, RowArr<R>{x});
+            t.sync();
+            for (int i = t.rank(); i < nr; i += t.size()) {  // r = b - S x
+              const R ri = bb[i] - (row_J(T, W, i, W.w) + row_C<R, kTets>(T, W, i, x) + eps * x[i]);
+              r[i] = ri;
+              rr2 += (double)ri * ri;
+            }
+            double s[1] = {rr2};
+            t.reduce_sum(s);
+            rr2 = s[0];
+          } else {
+            t.sync();
+            op_pull(t, T, W, RowArr<R>{p});
+            t.sync();
+            double pap = 0.0;
+            for (int i = t.rank(); i < nr; i += t.size()) {  // ap = S p
+              const R a = row_J(T, W, i, W.w) + row_C<R, kTets>(T, W, i, p) + eps * p[i];
+              W.ap[i] = a;
+              pap += (double)p[i] * a;
+            }
+            {
+              double s[1] = {pap};
+              t.reduce_sum(s);
+              pap = s[0];
+            }
+            if (fabs(pap) < 1e-300) {
+              breakdown = 1;
+              break;
+            }
+            const R ra = R(rz / pap);
+            for (int i = t.rank(); i < nr; i += t.size()) {
+              if (pending_best) W.bx[i] = x[i];
+              x[i] = x[i] + ra * p[i];
+              const R ri = r[i] - ra * W.ap[i];
+              r[i] = ri;
+              const R zi = cfg.preconditioner == 1 ? W.inv[i] * ri : ri;
+              z[i] = zi;
+              rr2 += (double)ri * ri;
+              rzn += (double)ri * zi;
+            }
+            pending_best = false;
+            double s[2] = {rr2, rzn};
+            t.reduce_sum(s);
+            rr2 = s[0];
+            rzn = s[1];
+          }
+          hist_last = sqrt(rr2);
+          if (t.rank() == 0 && out.hist && hist_n <= maxlin) out.hist[(size_t)it * (maxlin + 1) + hist_n] = hist_last;
+          ++hist_n;
+          if (hist_last < best_res) {
+            best_res = hist_last;
+            pending_best = true;
+          }
+          lin_used = itl + 1;
+          if (!jac) {
+            if (fabs(rz) < 1e-300) {
+              breakdown = 1;
+              break;
+            }
+            const R rb = R(rzn / rz);
+            rz = rzn;
+            for (int i = t.rank(); i < nr; i += t.size()) {
+              if (pending_best) W.bx[i] = x[i];
+              p[i] = z[i] + rb * p[i];
+            }
+            pending_best = false;
+          }
+        }
+        if (pending_best)
+          for (int i = t.rank(); i < nr; i += t.size()) W.bx[i] = x[i];
+      } else if constexpr (RPT > 0) {
         // Register-resident PCR (grid kernel, nr <= RPT * team size): each thread's
         // own rows keep x, r, z, p, ap, az, inv, bx in registers across all phases.
         // Global memory carries only what other threads read: ap (the J^T pull's

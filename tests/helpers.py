@@ -23,7 +23,7 @@ def newton_config(cfg, precision):
 
     return NewtonConfig(newton_iterations=cfg["newton_iterations"], step_fraction=cfg["step_fraction"],
                         epsilon_reg=cfg["epsilon_reg"], geometric_stiffness=bool(cfg["geometric_stiffness"]),
-                        r_strategy=cfg["r_strategy"], ncp_kind=cfg["ncp_kind"], linear_method=3,
+                        r_strategy=cfg["r_strategy"], ncp_kind=cfg["ncp_kind"], linear_method=cfg["linear_method"],
                         linear_max_iterations=cfg["linear_max_iterations"], linear_tolerance=cfg["linear_tolerance"],
                         preconditioner=cfg["preconditioner"], newton_tolerance=cfg["newton_tolerance"],
                         line_search=bool(cfg["line_search"]), precision=precision)

@@ -225,3 +225,25 @@ def test_nan_input_rolls_back_and_reports_abort():
     assert np.isnan(g["u"][2]) and np.array_equal(np.delete(g["u"], 2), np.delete(u0, 2))
     with pytest.raises(RuntimeError, match="spmv_transpose"):
         run_oracle(case)
+
+
+@pytest.mark.parametrize("name,seed,warm", [("c1", 0, 10), ("c3:20", 0, 3), ("c5", 3, 12), ("box_pile", 1, 20)])
+@pytest.mark.parametrize("method,precond", [(0, 1), (2, 1), (2, 0)])
+def test_linear_methods_jacobi_pcg_fp64(name, seed, warm, method, precond):
+    """Jacobi (solvers.cpp:32-50) and PCG (solvers.cpp:83-121) on
+    the same matrix-free Schur operator, against the oracle's explicit-S solvers."""
+    case = oracle_case(name, seed, warm, overrides=dict(linear_method=method, preconditioner=precond))
+    g = run_gpu(case, "fp64")
+    o = run_oracle(case)
+    assert g["aborted"] == (o["rc"] == 2)
+    assert rel_err(g["q"], o["q"]) < 1e-8, (name, method, rel_err(g["q"], o["q"]))
+    assert rel_err(g["u"], o["u"], floor=1e-6) < 1e-6
+
+
+def test_gauss_seidel_unsupported_on_device():
+    from paper_1907_04587_b200 import NsdError
+
+    case = oracle_case("c1", 0, 0, overrides=dict(linear_method=1))
+    with pytest.raises(NsdError) as e:
+        run_gpu(case, "fp64")
+    assert e.value.code == 4
