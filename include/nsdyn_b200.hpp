@@ -5,7 +5,7 @@
 //   reference (namespace nsdyn)                    here (namespace nsdyn_b200)
 //   GeneralizedState, Body        bodies.h:11-43   same names and fields (std::vector instead of Eigen)
 //   JointSpec, ContactConstraint  constraints.h    same names and fields
-//   TetElement, TetMeshElements   materials.h      same names and fields (Neo-Hookean only)
+//   TetElement, TetMeshElements   materials.h      same names and fields (Neo-Hookean and linear co-rotational)
 //   NewtonConfig, SolveReport,    newton.h:12-120  same names and fields, plus NewtonConfig::precision
 //   StepContext, MeshBinding,
 //   count_rows, newton_step
@@ -18,8 +18,8 @@
 // std::invalid_argument (bodies.cpp:80, constraints.cpp:142-144,
 // solvers.cpp:188-190); a NaN in the Newton update rolls q, u back and returns
 // a report with aborted = true (newton.cpp:362-369). A CUDA failure or an
-// option that is not on the GPU path (linear co-rotational tets, Gauss-Seidel,
-// record_iterates) throws std::runtime_error — there is no CPU fallback.
+// option that is not on the GPU path (Gauss-Seidel, record_iterates, mixed
+// material models in one scene) throws std::runtime_error — there is no CPU fallback.
 //
 // Device state: newton_step keeps one device solver per thread, keyed by the
 // StepContext's state/joints/meshes addresses and sizes and by the config;
@@ -189,6 +189,8 @@ struct TetMeshElements {
   std::vector<TetElement> elements;
   MaterialSpec material;
   NeoHookeanMaterial nh;
+  // Lame halves for both models (the linear model's isotropic stiffness is rebuilt
+  // from them on the device: mu = 2 c1, lambda = 2 d1)
   void prepare() { nh = lame_from_young_poisson(material.young, material.poisson); }
 };
 
@@ -312,8 +314,6 @@ struct FlatTopology {
     tet_material.clear();
     if (ctx.meshes)
       for (const MeshBinding& m : *ctx.meshes) {
-        if (m.mesh.material.model != MaterialModel::NeoHookean)
-          throw std::runtime_error("nsdyn_b200: linear co-rotational tets are not on the GPU path");
         for (const TetElement& e : m.mesh.elements) {
           for (int k = 0; k < 4; ++k) tet_body.push_back(m.particle_base + e.verts[k]);
           tet_dm_inv.insert(tet_dm_inv.end(), e.dm_inv.begin(), e.dm_inv.end());
@@ -321,7 +321,8 @@ struct FlatTopology {
           tet_material.push_back(m.mesh.nh.c1);
           tet_material.push_back(m.mesh.nh.d1);
           tet_material.push_back(m.mesh.nh.alpha);
-          tet_material.push_back(m.mesh.material.diagonal_compliance ? 1.0 : 0.0);
+          tet_material.push_back((m.mesh.material.diagonal_compliance ? 1.0 : 0.0) +
+                                 (m.mesh.material.model == MaterialModel::Linear ? 2.0 : 0.0));
         }
       }
   }
@@ -598,8 +599,9 @@ inline std::optional<World> build_scene_by_name(const std::string& name, unsigne
     }
     MeshBinding mb;
     mb.particle_base = base;
-    mb.mesh.nh = NeoHookeanMaterial{m0[0], m0[1], m0[2]};
-    mb.mesh.material.diagonal_compliance = m0[3] != 0.0;
+    mb.mesh.nh = NeoHookeanMaterial{m0[0], m0[1], m0[2]};  // Lame halves for both models
+    mb.mesh.material.diagonal_compliance = (static_cast<int>(m0[3]) & 1) != 0;
+    mb.mesh.material.model = (static_cast<int>(m0[3]) & 2) ? MaterialModel::Linear : MaterialModel::NeoHookean;
     for (int i = e; i < end; ++i) {
       TetElement te;
       for (int k = 0; k < 4; ++k) te.verts[k] = t.tet_body[4 * i + k] - base;

@@ -75,7 +75,8 @@ typedef struct nsd_topology {
   const int32_t* tet_body;     /* 4 per tet: global body index of each vertex particle */
   const double* tet_dm_inv;    /* 9 per tet, row-major */
   const double* tet_volume;
-  const double* tet_material;  /* 4 per tet: c1, d1, alpha, diagonal_compliance (0/1) */
+  const double* tet_material;  /* 4 per tet: c1 = mu/2, d1 = lambda/2, alpha, flags (1 diagonal compliance,
+                                  2 linear co-rotational: 6 rows per tet, 6x6 compliance; one model per scene) */
 } nsd_topology;
 
 /* ContactConstraint (constraints.h:40-50); body -1 = world point in local. */
@@ -124,7 +125,7 @@ typedef struct nsd_solver nsd_solver;
 
 const char* nsd_last_error(void);
 
-/* count_rows (newton.h:114): joints 3/5/5/2, 3 per tet, 3 per contact. */
+/* count_rows (newton.h:114): joints 3/5/5/2, 3 per Neo-Hookean / 6 per linear tet, 3 per contact. */
 int32_t nsd_count_rows(const nsd_topology* topo, int32_t n_contacts);
 
 int nsd_create(const nsd_topology* topo, const nsd_config* cfg, int32_t device, nsd_solver** out);

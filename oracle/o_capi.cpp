@@ -223,8 +223,11 @@ void orc_world_destroy(void* h) { delete static_cast<OWorld*>(h); }
 //       rows_joint, rows_mesh, newton_iters, linear_iters, n_meshes
 void orc_world_dims(void* h, int* d) {
   const World& w = static_cast<OWorld*>(h)->w;
-  int nt = 0, rj = 0;
-  for (const MeshBinding& m : w.meshes) nt += static_cast<int>(m.mesh.elements.size());
+  int nt = 0, rj = 0, rm = 0;
+  for (const MeshBinding& m : w.meshes) {
+    nt += static_cast<int>(m.mesh.elements.size());
+    rm += (m.mesh.material.model == MatModel::NeoHookean ? 3 : 6) * static_cast<int>(m.mesh.elements.size());
+  }
   for (const Joint& j : w.joints) rj += joint_row_count(j.kind);
   d[0] = static_cast<int>(w.state.bodies.size());
   d[1] = w.state.num_dof;
@@ -234,7 +237,7 @@ void orc_world_dims(void* h, int* d) {
   d[5] = static_cast<int>(w.shapes.size());
   d[6] = static_cast<int>(w.contacts.size());
   d[7] = rj;
-  d[8] = 3 * nt;
+  d[8] = rm;  // newton.cpp:32-33: 3 rows per Neo-Hookean tet, 6 per linear tet
   d[9] = w.solver.newton_iterations;
   d[10] = w.solver.linear.max_iterations;
   d[11] = static_cast<int>(w.meshes.size());
@@ -317,10 +320,18 @@ void orc_world_topology(void* hd, int* body_type, double* body_mass, double* bod
       for (int k = 0; k < 4; ++k) tet_body[4 * t + k] = m.particle_base + e.v[k];
       m3_to(e.dm_inv, tet_dm_inv + 9 * t);
       tet_volume[t] = e.vol;
-      tet_material[4 * t] = m.mesh.nh.c1;
-      tet_material[4 * t + 1] = m.mesh.nh.d1;
-      tet_material[4 * t + 2] = m.mesh.nh.alpha;
-      tet_material[4 * t + 3] = m.mesh.material.diagonal_compliance ? 1.0 : 0.0;
+      // flat C-ABI encoding (include/nsdyn_gpu.h): c1 = mu/2, d1 = lambda/2, alpha,
+      // flags (1 diagonal compliance, 2 linear co-rotational). For linear meshes the
+      // reference keeps only the stiffness (materials.cpp:117-122); its Lame constants
+      // are the same expressions lame_from_young_poisson evaluates.
+      const NH nh = m.mesh.material.model == MatModel::Linear
+                        ? lame(m.mesh.material.young, m.mesh.material.poisson)
+                        : m.mesh.nh;
+      tet_material[4 * t] = nh.c1;
+      tet_material[4 * t + 1] = nh.d1;
+      tet_material[4 * t + 2] = nh.alpha;
+      tet_material[4 * t + 3] = (m.mesh.material.diagonal_compliance ? 1.0 : 0.0) +
+                                (m.mesh.material.model == MatModel::Linear ? 2.0 : 0.0);
       ++t;
     }
   }

@@ -129,10 +129,35 @@ void check_cfg(const nsd_config& c) {
 
 // ------------------------------------------------------------------ host topology preprocessing
 struct HostTopo {
-  int nb = 0, ndof = 0, ncoord = 0, nd3 = 0, nj = 0, nt = 0, rows_joint = 0, rows_static = 0;
+  int nb = 0, ndof = 0, ncoord = 0, nd3 = 0, nj = 0, nt = 0, rows_joint = 0, rows_static = 0, tdim = 3;
   std::vector<int> btype, bdof, bcoord, d3_body, d3_kind, jkind, jbody, jrow, tbody, sinc_off, sinc_ent;
-  std::vector<double> bmass, binertia, jparam, jframe, tdminv, tvol, tmat;
+  std::vector<double> bmass, binertia, jparam, jframe, tdminv, tvol, tmat, tkinv;
 };
+
+// Inverse of the 6x6 isotropic stiffness by Gauss-Jordan with partial pivoting
+// (the linear material's compliance, materials.cpp:121,153), same elimination
+// order as the CPU oracle's restatement so both sides start from equal bits.
+void inverse6_h(const double (&k)[6][6], double (&o)[6][6]) {
+  double a[6][12];
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 12; ++j) a[i][j] = j < 6 ? k[i][j] : (j - 6 == i ? 1.0 : 0.0);
+  for (int c = 0; c < 6; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < 6; ++r)
+      if (std::abs(a[r][c]) > std::abs(a[piv][c])) piv = r;
+    if (piv != c)
+      for (int j = 0; j < 12; ++j) std::swap(a[c][j], a[piv][j]);
+    const double d = a[c][c];
+    for (int j = 0; j < 12; ++j) a[c][j] /= d;
+    for (int r = 0; r < 6; ++r) {
+      if (r == c) continue;
+      const double f = a[r][c];
+      for (int j = 0; j < 12; ++j) a[r][j] -= f * a[c][j];
+    }
+  }
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 6; ++j) o[i][j] = a[i][j + 6];
+}
 
 void body_blocks_h(const HostTopo& T, int b, int& lin, int& ang) {
   if (b < 0) {
@@ -194,7 +219,27 @@ HostTopo preprocess(const nsd_topology& tp) {
     T.tvol.push_back(tp.tet_volume[e]);
     for (int k = 0; k < 4; ++k) T.tmat.push_back(tp.tet_material[4 * e + k]);
   }
-  T.rows_static = T.rows_joint + 3 * T.nt;
+  // rows per tet: 3 (Neo-Hookean) or 6 (linear co-rotational, flag 2); one model per topology
+  for (int e = 0; e < T.nt; ++e) {
+    const int td = (static_cast<int>(T.tmat[4 * e + 3]) & 2) ? 6 : 3;
+    if (e == 0) T.tdim = td;
+    if (td != T.tdim)
+      throw NsdError(NSD_UNSUPPORTED, "mixed Neo-Hookean and linear co-rotational meshes in one scene");
+  }
+  if (T.tdim == 6)
+    for (int e = 0; e < T.nt; ++e) {  // K from the Lame constants: mu = 2 c1, lambda = 2 d1
+      const double mu = 2.0 * T.tmat[4 * e], lam = 2.0 * T.tmat[4 * e + 1];
+      double K[6][6] = {}, Ki[6][6];
+      for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) K[i][j] = lam;
+        K[i][i] = lam + 2.0 * mu;
+        K[i + 3][i + 3] = mu;
+      }
+      inverse6_h(K, Ki);
+      for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 6; ++j) T.tkinv.push_back(Ki[i][j]);
+    }
+  T.rows_static = T.rows_joint + T.tdim * T.nt;
   // static incidence: (row, slot) per dof3 block, rows ascending
   std::vector<std::vector<int>> inc(T.nd3);
   for (int j = 0; j < T.nj; ++j) {
@@ -212,8 +257,8 @@ HostTopo preprocess(const nsd_topology& tp) {
     }
   }
   for (int e = 0; e < T.nt; ++e)
-    for (int i = 0; i < 3; ++i) {
-      const int r = T.rows_joint + 3 * e + i;
+    for (int i = 0; i < T.tdim; ++i) {
+      const int r = T.rows_joint + T.tdim * e + i;
       for (int s = 0; s < 4; ++s) inc[T.bdof[T.tbody[4 * e + s]] / 3].push_back(4 * r + s);
     }
   T.sinc_off.assign(T.nd3 + 1, 0);
@@ -236,7 +281,8 @@ template <class R> struct DevTopo {
                  o_jbody = L.add<int>(2 * H.nj), o_jrow = L.add<int>(H.nj), o_tbody = L.add<int>(4 * H.nt),
                  o_soff = L.add<int>(H.nd3 + 1), o_sent = L.add<int>(H.sinc_ent.size()), o_bmass = L.add<R>(H.nb),
                  o_bin = L.add<R>(9 * H.nb), o_jparam = L.add<R>(2 * H.nj), o_jframe = L.add<R>(21 * H.nj),
-                 o_tdm = L.add<R>(9 * H.nt), o_tvol = L.add<R>(H.nt), o_tmat = L.add<R>(4 * H.nt);
+                 o_tdm = L.add<R>(9 * H.nt), o_tvol = L.add<R>(H.nt), o_tmat = L.add<R>(4 * H.nt),
+                 o_tkinv = L.add<R>(H.tkinv.size());
     std::vector<char> host(L.bytes, 0);
     auto put_i = [&](size_t off, const std::vector<int>& v) {
       if (!v.empty()) std::memcpy(host.data() + off, v.data(), v.size() * sizeof(int));
@@ -263,6 +309,7 @@ template <class R> struct DevTopo {
     put_r(o_tdm, H.tdminv);
     put_r(o_tvol, H.tvol);
     put_r(o_tmat, H.tmat);
+    put_r(o_tkinv, H.tkinv);
     buf.alloc(L.bytes);
     NSD_CK(cudaMemcpy(buf.p, host.data(), L.bytes, cudaMemcpyHostToDevice));
     char* base = static_cast<char*>(buf.p);
@@ -288,6 +335,8 @@ template <class R> struct DevTopo {
     t.tdminv = reinterpret_cast<const R*>(base + o_tdm);
     t.tvol = reinterpret_cast<const R*>(base + o_tvol);
     t.tmat = reinterpret_cast<const R*>(base + o_tmat);
+    t.tdim = H.tdim;
+    t.tkinv = reinterpret_cast<const R*>(base + o_tkinv);
     t.rows_static = H.rows_static;
     t.sinc_off = reinterpret_cast<const int*>(base + o_soff);
     t.sinc_ent = reinterpret_cast<const int*>(base + o_sent);
@@ -376,7 +425,7 @@ struct WorkPlan {
     shift = a(T.ndof);
     ub = a(T.ndof);
     fx = a(T.ndof);
-    ctet = a(9 * static_cast<size_t>(T.nt));
+    ctet = a(static_cast<size_t>(T.tdim) * T.tdim * T.nt);  // 3x3 (Neo-Hookean) or 6x6 (linear) blocks
     xn = a(rc);
     rn = a(rc);
     zn = a(rc);
@@ -1033,6 +1082,18 @@ template <class R> struct Solver final : SolverBase {
     NSD_CK(cudaMemcpyAsync(hu, hr + plan.u, sizeof(R) * H.ndof, cudaMemcpyDeviceToHost, stream));
     if (nrows) NSD_CK(cudaMemcpyAsync(hl, hr + plan.lam, sizeof(R) * nrows, cudaMemcpyDeviceToHost, stream));
     NSD_CK(cudaStreamSynchronize(stream));
+    if (std::getenv("NSD_DUMP_COEFF") && H.nt > 0) {  // DEBUG: first tet's rows (coefficients, blocks)
+      std::vector<R> co(12 * H.tdim);
+      std::vector<int> bk(4 * H.tdim);
+      NSD_CK(cudaMemcpy(co.data(), hr + plan.coeff + 12 * H.rows_joint, sizeof(R) * co.size(), cudaMemcpyDeviceToHost));
+      NSD_CK(cudaMemcpy(bk.data(), plan.hot_ints(hr) + plan.blk + 4 * H.rows_joint, sizeof(int) * bk.size(),
+                        cudaMemcpyDeviceToHost));
+      for (int i = 0; i < H.tdim; ++i) {
+        std::fprintf(stderr, "row %d blk %d %d %d %d :", i, bk[4 * i], bk[4 * i + 1], bk[4 * i + 2], bk[4 * i + 3]);
+        for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %.9g", double(co[12 * i + k]));
+        std::fprintf(stderr, "\n");
+      }
+    }
     float ms = 0.f;
     NSD_CK(cudaEventElapsedTime(&ms, ev0, ev1));
     last_ms = ms;
@@ -1520,7 +1581,9 @@ int32_t nsd_count_rows(const nsd_topology* topo, int32_t n_contacts) {
   if (!topo) return -1;
   int n = 0;
   for (int j = 0; j < topo->n_joints; ++j) n += nsd::joint_nrows(topo->joint_kind[j]);
-  return n + 3 * topo->n_tets + 3 * n_contacts;
+  for (int e = 0; e < topo->n_tets; ++e)  // 3 per Neo-Hookean tet, 6 per linear tet (newton.cpp:32-33)
+    n += (static_cast<int>(topo->tet_material[4 * e + 3]) & 2) ? 6 : 3;
+  return n + 3 * n_contacts;
 }
 
 int nsd_create(const nsd_topology* topo, const nsd_config* cfg, int32_t device, nsd_solver** out) {

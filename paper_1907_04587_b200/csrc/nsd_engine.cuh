@@ -79,8 +79,10 @@ template <class R> struct Topo {
   const int* tbody;   // 4 per tet (global body ids)
   const R* tdminv;    // 9 per tet
   const R* tvol;
-  const R* tmat;      // 4 per tet: c1, d1, alpha, diagonal flag
-  int rows_static;    // rows_joint + 3 nt
+  const R* tmat;      // 4 per tet: c1, d1, alpha, flags (1 diagonal compliance, 2 linear co-rotational)
+  int tdim;           // rows per tet: 3 Neo-Hookean, 6 linear co-rotational (one model per topology)
+  const R* tkinv;     // linear model: 36 per tet, the 6x6 isotropic stiffness inverse (materials.cpp:153)
+  int rows_static;    // rows_joint + tdim nt
   const int* sinc_off;  // static incidence per dof3 block (nd3 + 1)
   const int* sinc_ent;  // row*4 + slot, ascending rows within a block
   int warp_pull;        // 1: a warp per dof3 block (long incidence lists, FEM); 0: a thread per block
@@ -393,11 +395,11 @@ template <class R, bool kTets, class Team> __device__ void setup_row_blocks(Team
       }
     } else {
       const int e = g - T.nj;
-      const int r0 = T.rows_joint + 3 * e;
+      const int r0 = T.rows_joint + T.tdim * e;
       int vb[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) vb[k] = T.bdof[T.tbody[4 * e + k]] / 3;
-      for (int i = 0; i < 3; ++i) {
+      for (int i = 0; i < T.tdim; ++i) {
         int* b = W.blk + 4 * (r0 + i);
 #pragma unroll
         for (int k = 0; k < 4; ++k) b[k] = vb[k];
@@ -534,6 +536,107 @@ __device__ void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, 
   }
 }
 
+// Linear co-rotational element rows (materials.cpp:140-178): F = Ds Dm^-1, signed
+// SVD, R = U V^T, stretch S = V diag(s) V^T, strain = voigt(S - I) (Voigt order
+// xx yy zz 2yz 2xz 2xy, materials.cpp:132-136), c = V_e K strain, compliance
+// K^-1 / V_e; the rotation variation w = 2 G^-1 axial(R^T dF) with
+// G = tr(S) I - S enters each Jacobian column unless |det G| <= 1e-12 (frozen
+// frame). h = E (c + lambda/h) / h and C = E / h^2 over the 6x6 block
+// (newton.cpp:146-160).
+template <class R>
+__device__ void assemble_tet_linear(const Topo<R>& T, Work<R>& W, int e, R h, const M3<R>& dm, const Svd<R>& sv, R vol,
+                                    AsmStats& st) {
+  M3<R> Vt = transpose(sv.V);
+  M3<R> Rm = mul(sv.U, Vt);
+  M3<R> VS;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    VS(i, 0) = sv.V(i, 0) * sv.S.x;
+    VS(i, 1) = sv.V(i, 1) * sv.S.y;
+    VS(i, 2) = sv.V(i, 2) * sv.S.z;
+  }
+  const M3<R> S = mul(VS, Vt);
+  R strain[6] = {S(0, 0) - R(1), S(1, 1) - R(1), S(2, 2) - R(1), R(2) * S(1, 2), R(2) * S(0, 2), R(2) * S(0, 1)};
+  // isotropic stiffness from the Lame constants (mu = 2 c1, lambda = 2 d1; materials.cpp isotropic_stiffness)
+  const R mu = R(2) * T.tmat[4 * e], lam = R(2) * T.tmat[4 * e + 1];
+  R c[6];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    R k = R(0);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) k += (i == j ? lam + R(2) * mu : lam) * strain[j];
+    c[i] = vol * k;
+    c[3 + i] = vol * (mu * strain[3 + i]);
+  }
+  const R* ki = T.tkinv + 36 * e;
+  R E[36];
+#pragma unroll
+  for (int i = 0; i < 36; ++i) E[i] = ki[i] / vol;
+  const int r0 = T.rows_joint + 6 * e;
+  R cl[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) cl[i] = c[i] + W.lam[r0 + i] / h;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    R acc = R(0);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) acc += E[6 * i + j] * cl[j];
+    const R hv = acc / h;
+    W.hv[r0 + i] = hv;
+    st.hmax = fmax(st.hmax, (double)ab(hv));
+    st.hsq += (double)hv * (double)hv;
+  }
+#pragma unroll
+  for (int i = 0; i < 36; ++i) W.ctet[36 * e + i] = E[i] / (h * h);
+  // G = tr(S) I - S and its inverse (frozen frame when |det G| <= 1e-12)
+  const R tr = S(0, 0) + S(1, 1) + S(2, 2);
+  M3<R> G;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) G.a[i] = -S.a[i];
+  G(0, 0) += tr;
+  G(1, 1) += tr;
+  G(2, 2) += tr;
+  const bool rot_term = fabs((double)det3(G)) > 1e-12;
+  const M3<R> Gi = rot_term ? inverse3(G) : m3_zero<R>();
+  // Jacobian columns 3k + d: dF.row(d) = Dm^-1.row(k-1) (k > 0) or -sum_c Dm^-1.row(c).
+  // The rows are hoisted and selected by value: a runtime-indexed read of dm here
+  // returned identity rows on sm_100a (caught by tests/test_gpu_parity.py).
+  const V3<R> dm0 = v3(dm(0, 0), dm(0, 1), dm(0, 2)), dm1 = v3(dm(1, 0), dm(1, 1), dm(1, 2)),
+              dm2 = v3(dm(2, 0), dm(2, 1), dm(2, 2));
+  const V3<R> dmsum = -(dm0 + dm1 + dm2);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const V3<R> rowv = k == 0 ? dmsum : (k == 1 ? dm0 : (k == 2 ? dm1 : dm2));
+      // R^T dF with dF = e_d rowv^T: (R^T dF)(i, j) = R(d, i) rowv_j
+      M3<R> A;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) A(a, b) = Rm(d, a) * rowv[b];
+      if (rot_term) {
+        const V3<R> ax = v3(R(0.5) * (A(2, 1) - A(1, 2)), R(0.5) * (A(0, 2) - A(2, 0)), R(0.5) * (A(1, 0) - A(0, 1)));
+        const V3<R> w = R(2) * mul(Gi, ax);
+        M3<R> Wk = m3_zero<R>();  // skew(w)
+        Wk(0, 1) = -w.z;
+        Wk(0, 2) = w.y;
+        Wk(1, 0) = w.z;
+        Wk(1, 2) = -w.x;
+        Wk(2, 0) = -w.y;
+        Wk(2, 1) = w.x;
+        const M3<R> WS = mul(Wk, S);
+#pragma unroll
+        for (int i = 0; i < 9; ++i) A.a[i] -= WS.a[i];
+      }
+      const R sym[6] = {A(0, 0), A(1, 1), A(2, 2), R(2) * (R(0.5) * (A(1, 2) + A(2, 1))),
+                        R(2) * (R(0.5) * (A(0, 2) + A(2, 0))), R(2) * (R(0.5) * (A(0, 1) + A(1, 0)))};
+#pragma unroll
+      for (int i = 0; i < 6; ++i) W.coeff[12 * (r0 + i) + 3 * k + d] = sym[i];
+    }
+  }
+}
+
 // Neo-Hookean element rows (materials.cpp:180-193, 57-114).
 template <class R>
 __device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R h, AsmStats& st) {
@@ -555,8 +658,12 @@ __device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R 
   const M3<R> F = mul(ds, dm);
   const Svd<R> sv = svd3_signed(F);
   const R vol = T.tvol[e];
+  if (T.tdim == 6) {
+    assemble_tet_linear(T, W, e, h, dm, sv, vol, st);
+    return;
+  }
   const R c1 = T.tmat[4 * e], d1 = T.tmat[4 * e + 1], alpha = T.tmat[4 * e + 2];
-  const bool diag_only = T.tmat[4 * e + 3] != R(0);
+  const bool diag_only = (static_cast<int>(T.tmat[4 * e + 3]) & 1) != 0;
   const V3<R> s = sv.S;
   const R J = s.x * s.y * s.z;  // gradient with (J - alpha), materials.cpp:57-61
   const V3<R> dj = v3(s.y * s.z, s.x * s.z, s.x * s.y);
@@ -830,17 +937,20 @@ template <class R, class Team, class YF> __device__ void op_pull(Team& t, const 
 template <class R, bool kTets>
 __device__ __forceinline__ R row_C(const Topo<R>& T, const Work<R>& W, int i, const R* z) {
   if (kTets && i >= T.rows_joint && i < T.rows_static) {
-    const int e = (i - T.rows_joint) / 3, k = (i - T.rows_joint) - 3 * e;
-    const R* cb = W.ctet + 9 * e + 3 * k;
-    const int r0 = T.rows_joint + 3 * e;
-    return cb[0] * z[r0] + cb[1] * z[r0 + 1] + cb[2] * z[r0 + 2];
+    const int td = T.tdim, e = (i - T.rows_joint) / td, k = (i - T.rows_joint) - td * e;
+    const R* cb = W.ctet + td * td * e + td * k;
+    const int r0 = T.rows_joint + td * e;
+    if (td == 3) return cb[0] * z[r0] + cb[1] * z[r0 + 1] + cb[2] * z[r0 + 2];
+    R acc = R(0);
+    for (int j = 0; j < 6; ++j) acc += cb[j] * z[r0 + j];
+    return acc;
   }
   return W.cd[i] * z[i];
 }
 template <class R, bool kTets> __device__ __forceinline__ R row_Cdiag(const Topo<R>& T, const Work<R>& W, int i) {
   if (kTets && i >= T.rows_joint && i < T.rows_static) {
-    const int e = (i - T.rows_joint) / 3, k = (i - T.rows_joint) - 3 * e;
-    return W.ctet[9 * e + 4 * k];
+    const int td = T.tdim, e = (i - T.rows_joint) / td, k = (i - T.rows_joint) - td * e;
+    return W.ctet[td * td * e + (td + 1) * k];
   }
   return W.cd[i];
 }

@@ -172,11 +172,12 @@ Scene s_box_pile(unsigned seed) {
   s.solver.linear_max_iterations = 25;
   return s;
 }
-Scene s_stretch_sheet() {
+Scene s_stretch_sheet(bool linear) {  // scene.cpp:880-912 (Neo-Hookean or linear co-rotational)
   Scene s;
   s.solver = defaults();
   s.gravity = Vec3{0, 0, 0};
   MeshSpec m;
+  m.linear = linear;
   const Vec3 size{0.2, 0.1, 0.05};
   grid(m, 4, 2, 1, Vec3{0, 0, 0}, size);
   s.meshes.push_back(m);
@@ -416,7 +417,8 @@ Scene build(const std::string& name, unsigned seed, bool* ok) {
   if (base == "heavy_stack") return s_heavy_stack();
   if (base == "box_pile") return s_box_pile(seed);
   if (base == "box_on_plane") return s_box_on_plane();
-  if (base == "stretch_sheet") return s_stretch_sheet();
+  if (base == "stretch_sheet") return s_stretch_sheet(false);
+  if (base == "stretch_sheet_linear") return s_stretch_sheet(true);
   if (base == "incline") return s_incline(args.size() > 0 ? args[0] : 20.0, args.size() > 1 ? args[1] : 0.5);
   if (base == "c1") return s_c1();
   if (base == "c2") return s_c2(args.size() > 0 ? static_cast<int>(args[0]) : 12);
@@ -494,7 +496,7 @@ World build_world(const Scene& sc) {
       w.tet_material.push_back(c1);
       w.tet_material.push_back(d1);
       w.tet_material.push_back(alpha);
-      w.tet_material.push_back(d.diagonal_compliance ? 1.0 : 0.0);
+      w.tet_material.push_back((d.diagonal_compliance ? 1.0 : 0.0) + (d.linear ? 2.0 : 0.0));
       for (int v : idx) lumped[v] += d.density * vol / 4.0;
     }
     for (size_t v = 0; v < d.vertices.size(); ++v) {

@@ -58,6 +58,7 @@ struct MeshSpec {
   std::vector<std::array<int, 4>> elements;
   double young = 1e5, poisson = 0.45, density = 1000.0;
   bool diagonal_compliance = false;
+  bool linear = false;                        // MaterialModel::Linear (co-rotational, 6 rows per tet)
   Vec3 velocity;                              // extension: initial velocity
   std::vector<Vec3> initial;                  // extension: initial positions
   bool particle_contacts = false;             // extension: caller-side contact generator

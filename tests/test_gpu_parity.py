@@ -247,3 +247,21 @@ def test_gauss_seidel_unsupported_on_device():
     with pytest.raises(NsdError) as e:
         run_gpu(case, "fp64")
     assert e.value.code == 4
+
+
+@pytest.mark.parametrize("warm", [2, 6])
+def test_linear_corotational_tets_fp64(warm):
+    """linear co-rotational material (materials.cpp:140-178) — 6 Voigt
+    rows per tet, 6x6 compliance K^-1/V (newton.cpp:146-160) — on the stretched sheet
+    of scene.cpp:928 (stretch_sheet_linear), against the oracle's explicit-S step."""
+    case = oracle_case("stretch_sheet_linear", 0, warm)
+    g = run_gpu(case, "fp64")
+    o = run_oracle(case)
+    assert g["n_rows"] == case["dims"]["rows_joint"] + case["dims"]["rows_mesh"] + 3 * len(case["contacts"][0])
+    sq, su = oracle_self_divergence("stretch_sheet_linear", 0, warm)
+    eq, eu = rel_err(g["q"], o["q"]), rel_err(g["u"], o["u"], floor=1e-6)
+    assert eq <= max(1e-9, 10 * sq), (eq, sq)
+    assert eu <= max(1e-7, 10 * su), (eu, su)
+    # lambda: the same stated bound as the Neo-Hookean stretch sheet (60 PCR iterations
+    # end at the rounding floor on this stiff sheet; measured 4e-2 / 2e-4 at warm 2 / 6)
+    assert rel_err(g["lam"], o["lam"], floor=1e-9) < 1e-1
