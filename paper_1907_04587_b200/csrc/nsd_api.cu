@@ -1082,7 +1082,7 @@ template <class R> struct Solver final : SolverBase {
     NSD_CK(cudaMemcpyAsync(hu, hr + plan.u, sizeof(R) * H.ndof, cudaMemcpyDeviceToHost, stream));
     if (nrows) NSD_CK(cudaMemcpyAsync(hl, hr + plan.lam, sizeof(R) * nrows, cudaMemcpyDeviceToHost, stream));
     NSD_CK(cudaStreamSynchronize(stream));
-X
+    if (std::getenv("NSD_DUMP_COEFF") && H.nt > 0) {  // diagnostics: the first tet's row coefficients and blocks
       std::vector<R> co(12 * H.tdim);
       std::vector<int> bk(4 * H.tdim);
       NSD_CK(cudaMemcpy(co.data(), hr + plan.coeff + 12 * H.rows_joint, sizeof(R) * co.size(), cudaMemcpyDeviceToHost));
