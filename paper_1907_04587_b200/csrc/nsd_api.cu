@@ -552,15 +552,16 @@ template <class R> struct BatchArgs {
 
 // One environment: extension forces, setup, device narrow phase, contact
 // incidence, Newton solve, state write-back (step_world, scene.cpp:709-732).
-// Row vectors in the region (priority order in batch_env): all 9 in fp32; in fp64
+// Row vectors in the region (priority order in batch_env): all 8 in fp32; in fp64
 // the shared-memory budget is the limit, so fewer vectors let larger envs fit.
 // Measured (C5): fp32 3.62 M -> 3.92 M env-steps/s when inv/cd joined the region;
-// fp64 (priority order inv z ap p r x az bx cd): 4 vectors 2.00 M, 5 2.21 M, 6 2.37 M,
-// 7 2.22 M, 8 1.78 M env-steps/s -> 6.
+// fp64 (then 9 vectors, inv z ap p r x az bx cd): 4 vectors 2.00 M, 5 2.21 M, 6 2.37 M,
+// 7 2.22 M, 8 1.78 M env-steps/s -> 6. With z implicit (inv r ap p x az bx cd):
+// 6 2.83 M, 7 2.63 M, 8 2.09 M -> 6.
 #ifndef NSD_POOL_VECS64
 #define NSD_POOL_VECS64 6
 #endif
-template <class R> __host__ __device__ constexpr int pool_row_vecs() { return sizeof(R) == 4 ? 9 : NSD_POOL_VECS64; }
+template <class R> __host__ __device__ constexpr int pool_row_vecs() { return sizeof(R) == 4 ? 8 : NSD_POOL_VECS64; }
 // Elements of the per-env shared-memory row region for nc contacts: the
 // write-heavy PCR state x, r, z, p, ap, az, bx (7 x rows), the J^T staging
 // (12 per joint, 9 per contact) and w (ndof), each array kept 16-byte aligned.
@@ -758,19 +759,18 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
       // the CR loop on chip (global stores are write-through to L2)
       const int rows = (W.nrows + 3) & ~3;
       R* sp = pool;
-      // row vectors by accesses per CR iteration: inv (4 reads), z and ap (3R+1W),
-      // p and r (2R+1W), x, az (1R+1W), bx (1W), cd (1R); the first
-      // pool_row_vecs<R>() of them live in the region
+      // row vectors by accesses per CR iteration: inv (5 reads), r (4R+1W), ap
+      // (3R+1W), p (2R+1W), x, az (1R+1W), bx (1W), cd (1R); z = M^-1 r is not
+      // stored (newton_solve_obj); the first pool_row_vecs<R>() live in the region
       constexpr int nv = pool_row_vecs<R>();
       O.W.inv = sp;
-      O.W.z = sp + rows;
+      O.W.r = sp + rows;
       O.W.ap = sp + 2 * rows;
       if (nv >= 4) O.W.p = sp + 3 * rows;
-      if (nv >= 5) O.W.r = sp + 4 * rows;
-      if (nv >= 6) O.W.x = sp + 5 * rows;
-      if (nv >= 7) O.W.az = sp + 6 * rows;
-      if (nv >= 8) O.W.bx = sp + 7 * rows;
-      if (nv >= 9) O.W.cd = sp + 8 * rows;
+      if (nv >= 5) O.W.x = sp + 4 * rows;
+      if (nv >= 6) O.W.az = sp + 5 * rows;
+      if (nv >= 7) O.W.bx = sp + 6 * rows;
+      if (nv >= 8) O.W.cd = sp + 7 * rows;
       sp += nv * rows;
       O.jstage = sp;
       sp += (12 * T.nj + 3) & ~3;

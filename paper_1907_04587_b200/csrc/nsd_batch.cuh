@@ -382,7 +382,6 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
         }
         W.inv[i] = inv;
         const R b = W.r[i];
-        W.z[i] = inv * b;
         rzr += (double)b * (double)(inv * b);
       });
     }
@@ -400,16 +399,17 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
       R pend = R(0);
       double zaz = 0.0;
       if (maxlin > 0 && hist_last > cfg.linear_tolerance) {
-        stage_objects(T, O, rk, ts, RowArr<R>{W.z});
+        stage_objects(T, O, rk, ts, RowPrecond<R>{W.r, W.inv});
         t.sync();
         bodies_apply_hinv(T, O, rk, ts);
         t.sync();
         double za = 0.0;
         for (int k = rk; k < nobj; k += ts)
           object_Jw(T, W, k, W.w, [&](int i, R jw) {
-            const R a = jw + W.cd[i] * W.z[i] + eps * W.z[i];
+            const R zi = W.inv[i] * W.r[i];
+            const R a = jw + W.cd[i] * zi + eps * zi;
             W.az[i] = a;
-            za += (double)W.z[i] * a;
+            za += (double)zi * a;
           });
         double s[1] = {za};
         t.reduce_sum(s);
@@ -424,11 +424,12 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
         const bool first = itl == 0;
         for_my_rows(T, W, rk, ts, [&](int i) {
           R pi, api;
+          const R zi = W.inv[i] * W.r[i];
           if (first) {
-            pi = W.z[i];
+            pi = zi;
             api = W.az[i];
           } else {
-            pi = W.z[i] + rb * W.p[i];
+            pi = zi + rb * W.p[i];
             api = W.az[i] + rb * W.ap[i];
           }
           W.p[i] = pi;
@@ -457,7 +458,7 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
           pn2_p += rv * (W.inv[i] * rv);
           rn2_p += rv * rv;
         });
-        if (fabs(zaz) >= 1e-300) stage_objects(T, O, rk, ts, RowPending<R>{W.z, W.inv, W.ap, ra});
+        if (fabs(zaz) >= 1e-300) stage_objects(T, O, rk, ts, RowPrecondResidual<R>{W.r, W.inv, W.ap, ra});
         double pn2, rn2;
         {
           double s[2] = {(double)pn2_p, (double)rn2_p};
@@ -487,17 +488,21 @@ template <class R, class Team> __device__ int newton_solve_obj(Team& t, const To
         bodies_apply_hinv(T, O, rk, ts);
         t.sync();
         pc.mark(8);
-        // commit x, r, z of the owned rows and az = A z', zaz' = z' . az in one pass
+        // commit x, r of the owned rows and az = A z', zaz' = z' . az in one pass.
+        // z = M^-1 r is recomputed, not stored: the reference updates it by
+        // recursion (solvers.cpp PCR: z -= alpha M^-1 ap), equal in exact arithmetic
+        // for the diagonal preconditioner and one rounding apart here; dropping the
+        // array removes a row vector from the on-chip working set
         R za_p = R(0);
         const bool best = pending_best;
         for (int k = rk; k < nobj; k += ts)
           object_Jw(T, W, k, W.w, [&](int i, R jw) {
             const R api = W.ap[i];
-            const R zi = W.z[i] - pend * (W.inv[i] * api);
+            const R ri = W.r[i] - pend * api;
+            const R zi = W.inv[i] * ri;
             const R xi = W.x[i] + pend * W.p[i];
-            W.z[i] = zi;
             W.x[i] = xi;
-            W.r[i] = W.r[i] - pend * api;
+            W.r[i] = ri;
             if (best) W.bx[i] = xi;
             const R a = jw + W.cd[i] * zi + eps * zi;
             W.az[i] = a;

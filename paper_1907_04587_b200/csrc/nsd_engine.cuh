@@ -848,6 +848,17 @@ template <class R> struct RowPending {
   R a;
   __device__ __forceinline__ R operator()(int i) const { return z[i] - a * (inv[i] * ap[i]); }
 };
+// z = M^-1 r and z' = M^-1 (r - a ap) for a PCR that keeps z implicit (diagonal
+// preconditioner).
+template <class R> struct RowPrecond {
+  const R *r, *inv;
+  __device__ __forceinline__ R operator()(int i) const { return inv[i] * r[i]; }
+};
+template <class R> struct RowPrecondResidual {
+  const R *r, *inv, *ap;
+  R a;
+  __device__ __forceinline__ R operator()(int i) const { return inv[i] * (r[i] - a * ap[i]); }
+};
 
 // Partial J^T y of block b over the incidence entries first, first+stride, ...
 template <class R, class YF>
