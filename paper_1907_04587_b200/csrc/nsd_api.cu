@@ -1276,7 +1276,10 @@ template <class R> struct Batch final : BatchBase {
         NSD_CK(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device));
         const int nblk = (n_env + envs_per_block - 1) / envs_per_block;
         const int bps = std::max(1, std::min(32, (nblk + sms - 1) / sms));
-        const long budget = std::min<long>(max_optin, smem_sm / bps - reserved);
+        // shared memory is allocated in 128-byte units: an allowance that ignores the
+        // rounding can lose a block per SM (a second wave)
+        const long unit = 128;
+        const long budget = std::min<long>(max_optin, (smem_sm / bps - reserved) / unit * unit);
         const int full = row_pool_elems<R>(H.rows_static, H.nj, H.ndof, maxc);
         int region = static_cast<int>(budget / envs_per_block / static_cast<long>(sizeof(R))) & ~3;
         region = std::min(region, full);
