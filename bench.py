@@ -8,8 +8,11 @@ integration — a single kernel launch (k_batch_warp / k_batch_block).
 
   value   env-steps/s, actions pre-staged in HBM, L2 flushed between steps,
           device time (CUDA events) summed over exactly K steps, max over ranks
-  e2e     same metric through the C ABI with host actions: per step H2D of the
-          joint torques from pinned memory + step + D2H of (q, u) to pinned memory
+  e2e     same metric through the C ABI with host actions: per step the joint
+          torques from pinned memory in, (q, u) to pinned memory out. Headline:
+          nsd_batch_step_mapped (the step kernel moves those bytes over the bus
+          itself, overlapped with compute); copy_path_value: H2D copy + step +
+          D2H copy. Both replay the same steps and must end in the same state.
   dtype   f64 by default: the precision the reference computes in and the one
           whose oracle parity is proven (1e-8 over 25 steps, tests/test_gpu_batch.py);
           the other precision (f32 performance mode) is measured too and
@@ -258,31 +261,46 @@ def measure(args, prec, T, tmpl, E, env0, ws, rank, local, sample_clocks):
     d_tq = torch.empty((E, nj), dtype=tdt, device="cuda")
     h_q = torch.empty((K, E * T.num_coord), dtype=dt, pin_memory=True)
     h_u = torch.empty((K, E * T.num_dof), dtype=dt, pin_memory=True)
-    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    for k in range(K):
-        flush.zero_()
-        ev2[k][0].record(stream)
-        if not args.passive:
-            d_tq.copy_(h_tq[k], non_blocking=True)
-        b.step_device(tmpl.h, tmpl.gravity, None if args.passive else d_tq.data_ptr(), tdt_code)
-        b.copy_state_async(h_q[k].data_ptr(), h_u[k].data_ptr())
-        ev2[k][1].record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = sum(a.elapsed_time(bb) for a, bb in ev2)
+    def e2e_run(mapped):
+        # mapped (the headline): nsd_batch_step_mapped — the step kernel reads the
+        # actions from, and writes the state to, the pinned host buffers itself.
+        # copy: H2D copy of the actions, step_device, D2H copy of the state.
+        b.set_state(q_w, u_w)
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        for k in range(K):
+            flush.zero_()
+            ev2[k][0].record(stream)
+            if mapped:
+                b.step_mapped(tmpl.h, tmpl.gravity, None if args.passive else h_tq[k].data_ptr(), tdt_code,
+                              h_q[k].data_ptr(), h_u[k].data_ptr())
+            else:
+                if not args.passive:
+                    d_tq.copy_(h_tq[k], non_blocking=True)
+                b.step_device(tmpl.h, tmpl.gravity, None if args.passive else d_tq.data_ptr(), tdt_code)
+                b.copy_state_async(h_q[k].data_ptr(), h_u[k].data_ptr())
+            ev2[k][1].record(stream)
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(bb) for a, bb in ev2)
+
+    e2e_copy_ms = e2e_run(False)
+    q_copy, u_copy = h_q[K - 1].clone(), h_u[K - 1].clone()
+    e2e_ms = e2e_run(True)
+    if not (torch.equal(q_copy, h_q[K - 1]) and torch.equal(u_copy, h_u[K - 1])):
+        raise RuntimeError("nsd_batch_step_mapped and the copy path disagree on the final state")
     b.results()
     b.close()
     h2d = 0 if args.passive else E * nj * h_tq.element_size()
     d2h = E * (T.num_coord + T.num_dof) * (4 if prec == "fp32" else 8)
     if ws > 1:
-        t = torch.tensor([dev_ms, e2e_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([dev_ms, e2e_ms, e2e_copy_ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        dev_ms, e2e_ms = float(t[0]), float(t[1])
+        dev_ms, e2e_ms, e2e_copy_ms = float(t[0]), float(t[1]), float(t[2])
     total_envs = E * ws
     return dict(dev_ms=dev_ms, e2e_ms=e2e_ms, value=total_envs * K / (dev_ms / 1000.0),
-                e2e=total_envs * K / (e2e_ms / 1000.0), nc=nc, aborted=aborted, clocks=clocks, h2d=h2d, d2h=d2h,
+                e2e=total_envs * K / (e2e_ms / 1000.0), e2e_copy=total_envs * K / (e2e_copy_ms / 1000.0), nc=nc, aborted=aborted, clocks=clocks, h2d=h2d, d2h=d2h,
                 cfg=cfg)
 
 
@@ -434,7 +452,7 @@ def main():
         alt = "fp32" if prec == "fp64" else "fp64"
         a = measure(args, alt, T, tmpl, E, env0, ws, rank, local, False)
         other = {"dtype": "f32" if alt == "fp32" else "f64", "value": a["value"], "ms_per_step": a["dev_ms"] / K,
-                 "e2e": a["e2e"], "roofline_frac": roofline(a, alt, K)["frac"],
+                 "e2e": a["e2e"], "e2e_copy_path": a["e2e_copy"], "roofline_frac": roofline(a, alt, K)["frac"],
                  "parity": ("tracks the oracle to 1e-4 until the first ground impact, O(1e-3) after "
                             "(DESIGN.md Parity)") if alt == "fp32" else "oracle parity 1e-8 over 25 steps"}
     if rank != 0:
@@ -450,7 +468,10 @@ def main():
             "mean_contacts_per_env": float(m["nc"].mean()), "aborted_envs": m["aborted"],
             "roofline": roofline(m, prec, K),
             "e2e": {"value": m["e2e"], "unit": "env-steps/s", "h2d_bytes_per_step": m["h2d"],
-                    "d2h_bytes_per_step": m["d2h"]},
+                    "d2h_bytes_per_step": m["d2h"],
+                    "path": "nsd_batch_step_mapped: the step kernel reads the actions from and writes (q, u) to "
+                            "pinned host memory",
+                    "copy_path_value": m["e2e_copy"]},
             "gpu_launches": K, "clocks": m["clocks"]}
     if other:
         line["other_precision"] = other

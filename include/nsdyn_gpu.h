@@ -178,6 +178,19 @@ int nsd_batch_device_state(nsd_batch* b, void** q_dev, void** u_dev, int32_t* dt
  * (float or double, see nsd_batch_device_state) to q_dst / u_dst (pinned host
  * or device memory); either may be NULL. */
 int nsd_batch_copy_state_async(nsd_batch* b, void* q_dst, void* u_dst);
+/* nsd_batch_step_device with the transfers inside the step: joint_torque
+ * (n_env*n_joints, dtype 0 float / 1 double, NULL = passive) and q_out / u_out
+ * (n_env*num_coord / n_env*num_dof in the batch precision, either may be NULL)
+ * may be pinned host memory (cudaHostAlloc, or torch pin_memory): the step
+ * kernel reads each env's torques and writes its final state over the bus,
+ * overlapped with the other envs' compute. Device pointers are accepted too;
+ * pageable host memory is NSD_INVALID. q_out / u_out are complete once the
+ * batch stream has passed the step (nsd_batch_sync). The device state is
+ * updated as by nsd_batch_step_device. Replaces, in the reference's RL loop,
+ * the per-step torque upload + state read-back around step_world
+ * (scene.cpp:709-732 per env). */
+int nsd_batch_step_mapped(nsd_batch* b, const void* joint_torque, int32_t dtype, void* q_out, void* u_out, double h,
+                          const double gravity[3]);
 int nsd_batch_info(const nsd_batch* b, int32_t* info /* [n_env, num_coord, num_dof, n_joints, max_rows, team_threads] */);
 int nsd_batch_destroy(nsd_batch* b);
 

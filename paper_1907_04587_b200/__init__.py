@@ -381,6 +381,14 @@ class BatchSolver:
         g = np.ascontiguousarray(gravity, np.float64)
         check(lib().nsd_batch_step_device(self._h, C.c_void_p(torque_ptr) if torque_ptr else None, dtype, h, _dp(g)))
 
+    def step_mapped(self, h, gravity, torque_ptr=None, dtype=0, q_out_ptr=None, u_out_ptr=None):
+        """step_device with the transfers fused into the step kernel: torques read
+        from, and the final (q, u) written to, pinned host memory (or device memory)
+        by the kernel itself (nsd_batch_step_mapped)."""
+        g = np.ascontiguousarray(gravity, np.float64)
+        vp = lambda p: C.c_void_p(p) if p else None
+        check(lib().nsd_batch_step_mapped(self._h, vp(torque_ptr), dtype, vp(q_out_ptr), vp(u_out_ptr), h, _dp(g)))
+
     def sync(self):
         check(lib().nsd_batch_sync(self._h))
 

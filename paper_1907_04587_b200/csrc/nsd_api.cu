@@ -357,7 +357,7 @@ struct WorkPlan {
   // hot int
   size_t blk, cbody, cinc_off, cinc_ent, cbinc_off, cbinc, cblk, hotI;
   // cold R
-  size_t q0, u0, qp, ut, iw6, gp, up, shift, ub, fx, ctet, xn, rn, zn, cgeo, xlam, coldR;
+  size_t q0, u0, qp, ut, iw6, gp, up, shift, ub, fx, ctet, xn, rn, zn, cgeo, xlam, tq, coldR;
   // cold int
   size_t cfeat, cinc_cnt, xcbody, coldI;
   size_t hot_bytes_f, hot_bytes_d;  // bytes of the hot set per env for float / double
@@ -431,6 +431,7 @@ struct WorkPlan {
     zn = a(rc);
     cgeo = a(17 * c);
     xlam = a(rc);
+    tq = a(static_cast<size_t>(T.nj));
     coldR = o;
     o = 0;
     cfeat = a(c);
@@ -531,8 +532,10 @@ template <class R> struct BatchArgs {
   R margin, mu_default, h, grav[3];
   R* qs;  // persistent state (n_env * ncoord)
   R* us;
-  const void* torque;  // n_env * nj or null
+  const void* torque;  // n_env * nj or null (device memory or mapped pinned host memory)
   int torque_double;
+  R* q_out;  // optional second destination of the final state (mapped pinned host memory):
+  R* u_out;  // the step's device->host transfer made by the kernel, overlapped with other envs
   char* hot_global;  // per-env hot slices when not in shared memory
   size_t hot_bytes;
   R* cold_r;
@@ -614,6 +617,12 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
     }
   if (A.torque) {
     R* fx = cr + P.fx;
+    // the env's torques once per lane into scratch (a single bus round trip when the
+    // actions are read from mapped host memory), then the per-body sums
+    R* tq = cr + P.tq;
+    for (int j = t.rank(); j < T.nj; j += t.size())
+      tq[j] = A.torque_double ? R(static_cast<const double*>(A.torque)[(size_t)env * T.nj + j])
+                              : R(static_cast<const float*>(A.torque)[(size_t)env * T.nj + j]);
     t.sync();
     // joint torques about revolute axes at q- (extension hook): +tau*axis on a, -tau*axis on b
     for (int b = t.rank(); b < T.nb; b += t.size()) {
@@ -624,8 +633,7 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
           if (T.jkind[j] != 1) continue;
           const int ja = T.jbody[2 * j], jb = T.jbody[2 * j + 1];
           if (ja != b && jb != b) continue;
-          const R tau = A.torque_double ? R(static_cast<const double*>(A.torque)[(size_t)env * T.nj + j])
-                                        : R(static_cast<const float*>(A.torque)[(size_t)env * T.nj + j]);
+          const R tau = tq[j];
           const nsd::V3<R> axl = nsd::ld3(A.jframe + 21 * j + 6);
           nsd::M3<R> Rj;
           if (ja >= 0)
@@ -838,6 +846,10 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
   pc.mark(13);
   for (int i = t.rank(); i < T.ncoord; i += t.size()) qs[i] = W.q[i];
   for (int i = t.rank(); i < T.ndof; i += t.size()) us[i] = W.u[i];
+  if (A.q_out)
+    for (int i = t.rank(); i < T.ncoord; i += t.size()) A.q_out[(size_t)env * T.ncoord + i] = W.q[i];
+  if (A.u_out)
+    for (int i = t.rank(); i < T.ndof; i += t.size()) A.u_out[(size_t)env * T.ndof + i] = W.u[i];
   // export the step's contact set and multipliers (nsd_batch_contacts)
   R* xl = cr + P.xlam;
   int* xb = ci + P.xcbody;
@@ -1150,7 +1162,8 @@ struct BatchBase {
   virtual ~BatchBase() = default;
   virtual void set_state(const double* q, const double* u) = 0;
   virtual void get_state(double* q, double* u) = 0;
-  virtual void step(const void* torque, int on_device, int dtype, double h, const double* g) = 0;
+  virtual void step(const void* torque, int on_device, int dtype, double h, const double* g, void* q_out = nullptr,
+                    void* u_out = nullptr) = 0;
   virtual void results(int* nc, int* ab, double* fres, nsd_iter_stats* its) = 0;
   virtual void contacts(int env, nsd_contact* out, int* n) = 0;
   virtual void device_state(void** q, void** u, int* dtype) = 0;
@@ -1411,7 +1424,8 @@ template <class R> struct Batch final : BatchBase {
     if (u) NSD_CK(cudaMemcpyAsync(u, us.p, sizeof(R) * (size_t)H.ndof * n_env, cudaMemcpyDefault, stream));
   }
   long launches = 0;  // diagnostics
-  void step(const void* tq, int on_device, int dtype, double h, const double* g) override {
+  void step(const void* tq, int on_device, int dtype, double h, const double* g, void* q_out = nullptr,
+            void* u_out = nullptr) override {
     ++launches;
     if (!(h > 0.0)) throw NsdError(NSD_INVALID, "integrate_coordinates: h must be positive");
     BatchArgs<R> A{};
@@ -1434,6 +1448,8 @@ template <class R> struct Batch final : BatchBase {
     for (int k = 0; k < 3; ++k) A.grav[k] = R(g[k]);
     A.qs = qs.as<R>();
     A.us = us.as<R>();
+    A.q_out = static_cast<R*>(q_out);
+    A.u_out = static_cast<R*>(u_out);
     A.torque = nullptr;
     if (tq) {
       if (on_device) {
@@ -1697,6 +1713,33 @@ int nsd_batch_step_device(nsd_batch* b, const void* joint_torque_dev, int32_t dt
   return guarded([&] {
     if (!b || !gravity) throw NsdError(NSD_INVALID, "null argument");
     b->impl->step(joint_torque_dev, 1, dtype, h, gravity);
+    return NSD_OK;
+  });
+}
+
+// A pointer the device can dereference: device or managed memory as is, pinned host
+// memory through its device mapping (UVA: the same address for cudaHostAlloc'd memory).
+static void* device_view(const void* p, const char* what) {
+  if (!p) return nullptr;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    throw NsdError(NSD_INVALID, std::string(what) + ": not device memory or pinned host memory");
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return const_cast<void*>(p);
+  if (at.type == cudaMemoryTypeHost && at.devicePointer) return at.devicePointer;
+  throw NsdError(NSD_INVALID, std::string(what) + ": pageable host memory (pin it, e.g. cudaHostAlloc)");
+}
+
+int nsd_batch_step_mapped(nsd_batch* b, const void* joint_torque, int32_t dtype, void* q_out, void* u_out, double h,
+                          const double gravity[3]) {
+  return guarded([&] {
+    if (!b || !gravity) throw NsdError(NSD_INVALID, "null argument");
+    if (dtype != 0 && dtype != 1) throw NsdError(NSD_INVALID, "dtype must be 0 (float) or 1 (double)");
+    const void* tq = device_view(joint_torque, "joint_torque");
+    void* qo = device_view(q_out, "q_out");
+    void* uo = device_view(u_out, "u_out");
+    b->impl->step(tq, 1, dtype, h, gravity, qo, uo);
     return NSD_OK;
   });
 }

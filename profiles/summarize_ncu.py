@@ -78,6 +78,17 @@ def main():
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:40]:
         hs.append(f"{100 * v[0] / tot:6.1f} {100 * v[1] / toti:6.1f}  {k[0]}:{k[1]}  {k[2]}")
     open(out + "_source_hotspots.txt", "w").write("\n".join(hs) + "\n")
+    if "--sass" in sys.argv:  # the 60 SASS instructions with the most warp-stall samples
+        sass = list(csv.reader(io.StringIO(ncu(rep, "--page", "source", "--csv", "--print-source", "sass"))))
+        head = next((r for r in sass if r and r[0] == "Address"), None) or (sass[0] if sass else [])
+        rows = [r for r in sass if r and r is not head and len(r) == len(head)]
+        si = next((i for i, c in enumerate(head) if c.startswith("Warp Stall Sampling (All")), None)
+        if si is not None:
+            rows.sort(key=lambda r: -float((r[si] or "0").replace(",", "")) if (r[si] or "0").replace(",", "").replace(".", "").isdigit() else 0)
+            with open(out + "_sass_top.txt", "w") as f:
+                f.write(" | ".join(head) + "\n")
+                for r in rows[:60]:
+                    f.write(" | ".join(c.strip()[:90] for c in r) + "\n")
     print(json.dumps({"duration_ms": dur_ns / 1e6, "dram_traffic_bytes": traffic_mb * 1e6}))
 
 

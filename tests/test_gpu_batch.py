@@ -137,3 +137,44 @@ def test_batch_nan_env_aborts_alone():
     w = O.OracleWorld("c5", 2)
     assert w.step(1) == 0
     assert rel_err(q1[2], w.state()[0]) < 1e-12
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_batch_step_mapped_matches_device_step(prec):
+    """nsd_batch_step_mapped (the step kernel reads the torques from, and writes (q, u)
+    to, pinned host memory) gives the same bits as step_device + get_state, every step,
+    in both precisions and for float and double torques."""
+    import torch
+
+    n_env = 20
+    a, s0 = _batch(n_env, prec)
+    b, _ = _batch(n_env, prec)
+    nj, nq, nu = s0.topology.n_joints, s0.topology.num_coord, s0.topology.num_dof
+    dt = torch.float64 if prec == "fp64" else torch.float32
+    h_q = torch.zeros(n_env * nq, dtype=dt, pin_memory=True)
+    h_u = torch.zeros(n_env * nu, dtype=dt, pin_memory=True)
+    for st in range(6):
+        tdt = torch.float64 if st % 2 else torch.float32
+        tau = np.stack([_torques(e, st, nj) for e in range(n_env)])
+        h_tq = torch.tensor(tau, dtype=tdt).pin_memory()
+        d_tq = h_tq.cuda()
+        code = 1 if tdt == torch.float64 else 0
+        torch.cuda.synchronize()
+        a.step_device(s0.h, s0.gravity, d_tq.data_ptr(), code)
+        b.step_mapped(s0.h, s0.gravity, h_tq.data_ptr(), code, h_q.data_ptr(), h_u.data_ptr())
+        a.sync()
+        b.sync()
+        qa, ua = a.get_state()
+        qb, ub = b.get_state()
+        assert np.array_equal(qa, qb) and np.array_equal(ua, ub), st
+        assert np.array_equal(h_q.numpy().astype(np.float64), qb.reshape(-1)), st
+        assert np.array_equal(h_u.numpy().astype(np.float64), ub.reshape(-1)), st
+
+
+def test_batch_step_mapped_rejects_pageable_memory():
+    from paper_1907_04587_b200 import NsdError
+
+    b, s0 = _batch(4, "fp64")
+    q = np.zeros(4 * s0.topology.num_coord)
+    with pytest.raises(NsdError):
+        b.step_mapped(s0.h, s0.gravity, None, 1, q.ctypes.data, None)
