@@ -11,8 +11,10 @@
 //   count_rows, newton_step
 //   World, build_scene_by_name,   scene.h:83-110   same names; step_world's Newton solve runs on the GPU
 //   step_world
-//   RunOptions, load_world, run,  runner.h:11-43   same names, CSV formats and exit codes (builders only;
-//   sweep                                          the JSON scene format is out of this path's scope)
+//   RunOptions, load_world, run,  runner.h:11-43   same names, CSV formats and exit codes; a scene is a
+//   sweep                                          builder name or a JSON scene file
+//   world_from_json,               scene.h:74-77   parse_scene + build_world / serialize_scene (the
+//   serialize_scene                                reference's JSON scene format)
 //
 // Error behaviour follows the reference: invalid input throws
 // std::invalid_argument (bodies.cpp:80, constraints.cpp:142-144,
@@ -38,6 +40,7 @@
 #include <fstream>
 #include <memory>
 #include <optional>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -555,9 +558,37 @@ struct World {
 
 // Builder dispatch by name (scene.h:76-78), e.g. "c1", "c5", "incline:35:0.5",
 // "box_pile"; nullopt for unknown names.
+namespace detail {
+World world_from_handle(nsd_scene* raw);
+}
 inline std::optional<World> build_scene_by_name(const std::string& name, unsigned seed) {
   nsd_scene* raw = nullptr;
   if (nsd_scene_build(name.c_str(), seed, &raw) != NSD_OK) return std::nullopt;
+  return detail::world_from_handle(raw);
+}
+
+// parse_scene + build_world (scene.cpp:293-470, 587-707): a document in the
+// reference's JSON scene format; std::runtime_error with the reference's message
+// ("scene error at bodies[0].mass: must be positive") when it does not validate.
+inline World world_from_json(const std::string& text) {
+  nsd_scene* raw = nullptr;
+  char err[1024];
+  if (nsd_scene_parse(text.c_str(), &raw, err, sizeof(err)) != NSD_OK) throw std::runtime_error(err);
+  return detail::world_from_handle(raw);
+}
+
+// serialize_scene (scene.cpp:472-556) of the description the world was built from.
+inline std::string serialize_scene(const World& w) {
+  if (!w.scene) throw std::invalid_argument("serialize_scene: world has no scene description");
+  int64_t n = 0;
+  detail::check(nsd_scene_serialize(w.scene.get(), nullptr, 0, &n));
+  std::string out(static_cast<size_t>(n) + 1, '\0');
+  detail::check(nsd_scene_serialize(w.scene.get(), out.data(), n + 1, &n));
+  out.resize(static_cast<size_t>(n));
+  return out;
+}
+
+inline World detail::world_from_handle(nsd_scene* raw) {
   World w;
   w.scene.reset(raw, SceneDeleter{});
   nsd_topology t{};
@@ -806,10 +837,17 @@ inline constexpr const char* kConvergenceHeader =
     "linear_residual_final\n";
 }  // namespace detail
 
-// load_world (runner.cpp:130-146): builder by name with the overrides applied.
+// load_world (runner.cpp:130-146): a JSON scene file or a builder name, with the overrides applied.
 inline World load_world(const RunOptions& o) {
-  if (std::filesystem::exists(o.scene))
-    throw std::runtime_error("scene \"" + o.scene + "\": JSON scene files are not part of the GPU path (builders only)");
+  if (std::filesystem::exists(o.scene)) {
+    std::ifstream in(o.scene, std::ios::binary);
+    std::stringstream ss;
+    ss << in.rdbuf();
+    World w = world_from_json(ss.str());
+    detail::apply_overrides(o, w.solver);
+    w.solver.precision = o.precision;
+    return w;
+  }
   auto w = build_scene_by_name(o.scene, o.seed);
   if (!w) throw std::runtime_error("scene \"" + o.scene + "\" is neither a file nor a known builder");
   detail::apply_overrides(o, w->solver);

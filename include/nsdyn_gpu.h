@@ -198,6 +198,16 @@ int nsd_batch_destroy(nsd_batch* b);
 typedef struct nsd_scene nsd_scene;
 /* name: "c1".."c5", "box_on_plane", "heavy_stack", "incline:<deg>:<mu>", ... */
 int nsd_scene_build(const char* name, uint32_t seed, nsd_scene** out);
+/* The reference's JSON scene format. nsd_scene_parse: parse_scene + build_world
+ * (scene.cpp:293-470, 587-707): fully validated, unknown keys rejected; on error
+ * NSD_INVALID and the reference's message ("scene error at bodies[0].mass: must
+ * be positive", "scene syntax error: ...") in err (NUL-terminated, truncated to
+ * err_capacity). nsd_scene_serialize: serialize_scene (scene.cpp:472-556), the
+ * document with sorted keys and 2-space indentation; *length = its size without
+ * the NUL, written to buf when capacity > length (buf NULL: size query). Scenes
+ * from nsd_scene_build serialize too (product-only mesh extensions omitted). */
+int nsd_scene_parse(const char* json, nsd_scene** out, char* err, int32_t err_capacity);
+int nsd_scene_serialize(const nsd_scene* s, char* buf, int64_t capacity, int64_t* length);
 /* dims: n_bodies, num_dof, num_coord, n_joints, n_tets, n_shapes, newton_iterations, linear_max_iterations */
 int nsd_scene_dims(const nsd_scene* s, int32_t* dims);
 int nsd_scene_topology(const nsd_scene* s, nsd_topology* topo); /* pointers valid while s lives */

@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from ._lib import (NSD_ABORTED, NSD_FP32, NSD_FP64, NSD_OK, NsdError, check, lib, nsd_config, nsd_contact,
+from ._lib import (NSD_ABORTED, NSD_FP32, NSD_FP64, NSD_INVALID, NSD_OK, NsdError, check, lib, nsd_config, nsd_contact,
                    nsd_iter_stats, nsd_shape, nsd_step_in, nsd_step_out, nsd_topology)
 
 __all__ = ["NewtonConfig", "NewtonSolver", "BatchSolver", "Scene", "World", "contacts_from_arrays", "contacts_to_arrays",
@@ -216,12 +216,36 @@ class NewtonSolver:
                     ms=self.last_step_ms)
 
 
-class Scene:
-    """Product-side builders (nsd_scene_build): topology, shapes, state, config."""
-
-    def __init__(self, name: str, seed: int = 0):
-        h = C.c_void_p()
+def _open_scene(name, seed, json_text):
+    """nsd_scene_build(name, seed), or nsd_scene_parse(json_text) (the reference's JSON
+    scene format, scene.cpp:293-470) with its validation message on failure."""
+    h = C.c_void_p()
+    if json_text is None:
         check(lib().nsd_scene_build(name.encode(), seed, C.byref(h)))
+        return h
+    if isinstance(json_text, str):
+        json_text = json_text.encode()
+    err = C.create_string_buffer(1024)
+    if lib().nsd_scene_parse(json_text, C.byref(h), err, len(err)) != NSD_OK:
+        raise NsdError(NSD_INVALID, err.value.decode(errors="replace"))
+    return h
+
+
+def serialize_scene(handle) -> str:
+    n = C.c_int64()
+    check(lib().nsd_scene_serialize(handle, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(lib().nsd_scene_serialize(handle, buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
+class Scene:
+    """Product-side scenes: a builder (nsd_scene_build) or a document in the reference's
+    JSON scene format (Scene.from_json, nsd_scene_parse): topology, shapes, state,
+    config; to_json() is serialize_scene (scene.cpp:472-556)."""
+
+    def __init__(self, name: str = "", seed: int = 0, json_text=None):
+        h = _open_scene(name, seed, json_text)
         self._h = h
         d = np.zeros(8, np.int32)
         check(lib().nsd_scene_dims(h, _ip(d)))
@@ -251,8 +275,22 @@ class Scene:
         cfg, hh, g = nsd_config(), C.c_double(), np.zeros(3)
         check(lib().nsd_scene_config(h, C.byref(cfg), C.byref(hh), _dp(g)))
         self.config, self.h, self.gravity = NewtonConfig.from_c(cfg), hh.value, g
-        lib().nsd_scene_destroy(h)
-        self._h = None
+
+    @classmethod
+    def from_json(cls, text):
+        return cls(json_text=text)
+
+    def to_json(self) -> str:
+        return serialize_scene(self._h)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().nsd_scene_destroy(h)
+            except Exception:
+                pass
+            self._h = None
 
 
 class World:
@@ -262,11 +300,10 @@ class World:
     GPU through nsd_step. `contacts` holds the step's contact arrays with the
     multipliers written back; `report` the SolveReport of the last step."""
 
-    def __init__(self, name: str, seed: int = 0, precision: str | None = None, contact_capacity: int = 4096):
-        self.scene = Scene(name, seed)
-        h = C.c_void_p()
-        check(lib().nsd_scene_build(name.encode(), seed, C.byref(h)))
-        self._h = h
+    def __init__(self, name: str = "", seed: int = 0, precision: str | None = None, contact_capacity: int = 4096,
+                 json_text=None):
+        self.scene = Scene(name, seed, json_text=json_text)
+        self._h = _open_scene(name, seed, json_text)
         self.topology = self.scene.topology
         self.config = self.scene.config
         if precision is not None:

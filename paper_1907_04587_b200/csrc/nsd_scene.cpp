@@ -642,6 +642,7 @@ World build_world(const Scene& sc) {
 
 // ================================================================== C ABI (builders)
 struct nsd_scene {
+  nsdw::Scene sc;  // the description (serialize_scene)
   nsdw::World w;
 };
 
@@ -654,12 +655,43 @@ int nsd_scene_build(const char* name, uint32_t seed, nsd_scene** out) {
     nsdw::Scene s = nsdw::build(name, seed, &ok);
     if (!ok) return NSD_INVALID;
     auto* h = new nsd_scene();
+    h->sc = s;
     h->w = nsdw::build_world(s);
     *out = h;
     return NSD_OK;
   } catch (...) {
     return NSD_INVALID;
   }
+}
+
+int nsd_scene_parse(const char* json, nsd_scene** out, char* err, int32_t err_capacity) {
+  if (err && err_capacity > 0) err[0] = 0;
+  if (!json || !out) return NSD_INVALID;
+  try {
+    nsdw::Scene s = nsdw::parse_scene(json);
+    auto* h = new nsd_scene();
+    h->sc = s;
+    h->w = nsdw::build_world(s);
+    *out = h;
+    return NSD_OK;
+  } catch (const std::exception& e) {
+    if (err && err_capacity > 0) {
+      std::strncpy(err, e.what(), static_cast<size_t>(err_capacity) - 1);
+      err[err_capacity - 1] = 0;
+    }
+    return NSD_INVALID;
+  }
+}
+
+int nsd_scene_serialize(const nsd_scene* s, char* buf, int64_t capacity, int64_t* length) {
+  if (!s || !length) return NSD_INVALID;
+  const std::string doc = nsdw::serialize_scene(s->sc);
+  *length = static_cast<int64_t>(doc.size());
+  if (buf) {
+    if (capacity < static_cast<int64_t>(doc.size()) + 1) return NSD_INVALID;
+    std::memcpy(buf, doc.c_str(), doc.size() + 1);
+  }
+  return NSD_OK;
 }
 
 int nsd_scene_dims(const nsd_scene* s, int32_t* d) {

@@ -100,5 +100,9 @@ struct World {
 
 Scene build(const std::string& name, unsigned seed, bool* ok);
 World build_world(const Scene& s);
+// The reference's JSON scene format (scene.h:74-77; nsd_scene_json.cpp). parse_scene
+// throws std::runtime_error with the reference's messages.
+Scene parse_scene(const std::string& text);
+std::string serialize_scene(const Scene& s);
 
 }  // namespace nsdw

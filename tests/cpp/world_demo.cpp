@@ -12,6 +12,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cmath>
+#include <sstream>
+#include <fstream>
 #include <string>
 
 namespace nb = nsdyn_b200;
@@ -88,7 +91,42 @@ static int sweep_cmd(char** argv) {
   return rc;
 }
 
+// JSON scene format through the C++ API (no GPU needed): serialize_scene of a builder
+// world, world_from_json of that text, serialize again; prints the document and
+// whether the rebuilt world matches (state, joints, bodies).
+int json_roundtrip(const char* name) {
+  auto w = nb::build_scene_by_name(name, 0);
+  if (!w) return 2;
+  const std::string doc = nb::serialize_scene(*w);
+  const nb::World v = nb::world_from_json(doc);
+  const std::string doc2 = nb::serialize_scene(v);
+  // orientations are renormalised on parse (bodies.cpp:52-56): one rounding apart at most
+  bool same = doc.size() == doc2.size() && v.state.bodies.size() == w->state.bodies.size() &&
+              v.joints.size() == w->joints.size() && v.state.u == w->state.u && v.h == w->h;
+  for (size_t i = 0; same && i < v.state.q.size(); ++i) same = std::fabs(v.state.q[i] - w->state.q[i]) <= 1e-15;
+  std::fputs(doc.c_str(), stdout);
+  std::printf("json_roundtrip %s\n", same ? "ok" : "MISMATCH");
+  return same ? 0 : 1;
+}
+
+// world_from_json of a file; prints the validation message of a rejected document.
+int json_load(const char* path) {
+  std::ifstream in(path, std::ios::binary);
+  std::stringstream ss;
+  ss << in.rdbuf();
+  try {
+    const nb::World w = nb::world_from_json(ss.str());
+    std::printf("json_load ok bodies %zu joints %zu\n", w.state.bodies.size(), w.joints.size());
+    return 0;
+  } catch (const std::runtime_error& e) {
+    std::printf("json_error %s\n", e.what());
+    return 1;
+  }
+}
+
 int main(int argc, char** argv) {
+  if (argc >= 3 && std::strcmp(argv[1], "--json-roundtrip") == 0) return json_roundtrip(argv[2]);
+  if (argc >= 3 && std::strcmp(argv[1], "--json-load") == 0) return json_load(argv[2]);
   if (argc >= 5 && std::strcmp(argv[1], "--run") == 0) return run_cmd(argc, argv);
   if (argc >= 6 && std::strcmp(argv[1], "--sweep") == 0) return sweep_cmd(argv);
   if (argc >= 2 && std::strcmp(argv[1], "--free-fall") == 0) return free_fall();
