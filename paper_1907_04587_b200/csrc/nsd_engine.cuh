@@ -848,6 +848,18 @@ template <class R> struct RowPending {
   R a;
   __device__ __forceinline__ R operator()(int i) const { return z[i] - a * (inv[i] * ap[i]); }
 };
+// z' = z - a M^-1 ap' with ap' = az + b ap_prev (az alone on the first iteration),
+// formed by the pull from the previous iteration's vectors: bitwise the ap' the
+// row's owner forms in the same pass (grid PCR with one barrier fewer).
+template <class R> struct RowPendingAz {
+  const R *z, *inv, *az, *ap_prev;
+  R a, b;
+  bool first;
+  __device__ __forceinline__ R operator()(int i) const {
+    const R ap = first ? az[i] : az[i] + b * ap_prev[i];
+    return z[i] - a * (inv[i] * ap);
+  }
+};
 // z = M^-1 r and z' = M^-1 (r - a ap) for a PCR that keeps z implicit (diagonal
 // preconditioner).
 template <class R> struct RowPrecond {
@@ -1272,30 +1284,46 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
           invr[k] = v ? W.inv[i] : R(0);
           xr[k] = bxr[k] = pr[k] = apr[k] = azr[k] = xnr[k] = rnr[k] = znr[k] = R(0);
         }
-        R *zg = W.z, *zng = W.zn;
+        // Two grid barriers per CR iteration: den = ap'.M^-1 ap' of this iteration's
+        // ap' = az + beta ap is expanded as az.M^-1 az + 2 beta az.M^-1 ap + beta^2
+        // ap.M^-1 ap from sums reduced with z.az in the previous J w pass, so the
+        // p/ap update, the trial norms and the speculative pull share one pass (the
+        // reference forms ap' first, solvers.cpp PCR: den differs by rounding only).
+        // The pull forms ap' of other rows itself from az and the previous ap
+        // (RowPendingAz), so ap is double-buffered (W.ap / W.rn, unused on this path).
+        R *zg = W.z, *zng = W.zn, *apg = W.ap, *apo = W.rn;
         bool pending = false;
-        double zaz = 0.0;
+        double zaz = 0.0, den_next = 0.0;
         if (maxlin > 0 && hist_last > cfg.linear_tolerance) {
           op_pull(t, T, W, RowArr<R>{zg});
           t.sync();
-          double za = 0.0;
+          double za = 0.0, aa = 0.0;
 #pragma unroll
           for (int k = 0; k < RPT; ++k) {
             const int i = rk + k * ts;
             if (i < nr) {
               const R a = row_J(T, W, i, W.w) + row_C<R, kTets>(T, W, i, zg) + eps * zr[k];
               azr[k] = a;
+              W.az[i] = a;
               za += (double)zr[k] * a;
+              aa += (double)a * (double)(invr[k] * a);
             }
           }
-          double s[1] = {za};
+          double s[2] = {za, aa};
           t.reduce_sum(s);
           zaz = s[0];
+          den_next = s[1];  // ap' = az on the first iteration
         }
         double beta = 0.0;
         for (int itl = 0; itl < maxlin && hist_last > cfg.linear_tolerance; ++itl) {
-          double den = 0.0;
-          const R rb = R(beta);
+          const double den = den_next;
+          if (fabs(den) < 1e-300) {
+            breakdown = 1;
+            break;
+          }
+          const double alpha = zaz / den;
+          const R ra = R(alpha), rb = R(beta);
+          double pn2 = 0.0, rn2 = 0.0;
 #pragma unroll
           for (int k = 0; k < RPT; ++k) {
             const int i = rk + k * ts;
@@ -1307,26 +1335,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
                 pr[k] = zr[k] + rb * pr[k];
                 apr[k] = azr[k] + rb * apr[k];
               }
-              W.ap[i] = apr[k];
-              den += (double)apr[k] * (double)(invr[k] * apr[k]);
-            }
-          }
-          {
-            double s[1] = {den};
-            t.reduce_sum(s);
-            den = s[0];
-          }
-          if (fabs(den) < 1e-300) {
-            breakdown = 1;
-            break;
-          }
-          const double alpha = zaz / den;
-          const R ra = R(alpha);
-          double pn2 = 0.0, rn2 = 0.0;
-#pragma unroll
-          for (int k = 0; k < RPT; ++k) {
-            const int i = rk + k * ts;
-            if (i < nr) {
+              apg[i] = apr[k];
               const R rv = rr_[k] - ra * apr[k];
               xnr[k] = xr[k] + ra * pr[k];
               rnr[k] = rv;
@@ -1336,7 +1345,8 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
               rn2 += (double)rv * rv;
             }
           }
-          if (fabs(zaz) >= 1e-300) op_pull(t, T, W, RowPending<R>{zg, W.inv, W.ap, ra});  // w = H^-1 J^T z'
+          if (fabs(zaz) >= 1e-300)  // w = H^-1 J^T z'
+            op_pull(t, T, W, RowPendingAz<R>{zg, W.inv, W.az, apo, ra, rb, itl == 0});
           {
             double s[2] = {pn2, rn2};
             t.reduce_sum(s);
@@ -1368,22 +1378,31 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
             breakdown = 1;
             break;
           }
-          double za = 0.0;
+          double za = 0.0, aa = 0.0, ab = 0.0, bb = 0.0;
 #pragma unroll
           for (int k = 0; k < RPT; ++k) {
             const int i = rk + k * ts;
             if (i < nr) {
               const R a = row_J(T, W, i, W.w) + row_C<R, kTets>(T, W, i, zg) + eps * zr[k];
               azr[k] = a;
+              W.az[i] = a;
               za += (double)zr[k] * a;
+              const double ia = (double)(invr[k] * a);
+              aa += (double)a * ia;
+              ab += (double)apr[k] * ia;
+              bb += (double)apr[k] * (double)(invr[k] * apr[k]);
             }
           }
           {
-            double s[1] = {za};
+            double s[4] = {za, aa, ab, bb};
             t.reduce_sum(s);
             beta = s[0] / zaz;
             zaz = s[0];
+            den_next = s[1] + 2.0 * beta * s[2] + beta * beta * s[3];
           }
+          R* tap = apg;  // this iteration's ap is the next pull's ap_prev
+          apg = apo;
+          apo = tap;
         }
         (void)pending;
 #pragma unroll
