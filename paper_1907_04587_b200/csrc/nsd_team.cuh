@@ -172,26 +172,29 @@ struct GridTeam {
   __device__ __forceinline__ int rank() const { return blockIdx.x * blockDim.x + threadIdx.x; }
   __device__ __forceinline__ int size() const { return gridDim.x * blockDim.x; }
 
-  // Arrive; returns true (block-uniform) in the last CTA to arrive. Caller must
-  // have made its global writes visible (thread 0's __threadfence below covers
-  // writes by thread 0; others sync through __syncthreads first).
+  // Arrive; returns true (block-uniform) in the last CTA to arrive. The arrival
+  // count only grows within a launch (zeroed by the host before each launch): a
+  // CTA reaches barrier n + 1 only after every CTA arrived at barrier n, so the
+  // last arriver of barrier n sees a count of n * gridDim.x. The acq_rel atomic
+  // publishes thread 0's writes (the CTA partials; other threads' writes are
+  // ordered before it by the __syncthreads) and, in the last arriver, acquires
+  // every earlier arriver's — one L2 round trip, no separate fence.
   __device__ __forceinline__ bool arrive(int* last_flag) {
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();
-      const unsigned prev = atomicAdd(bar, 1u);
-      *last_flag = prev == gridDim.x - 1;
+      unsigned prev;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(bar) : "memory");
+      *last_flag = (prev + 1u) % gridDim.x == 0u;
     }
     __syncthreads();
     return *last_flag != 0;
   }
-  // Last CTA: reset the count and release the waiting CTAs; others: wait.
+  // Last CTA: release the waiting CTAs (its writes, ordered before thread 0 by
+  // __syncthreads, are published by the release store); others: wait.
   __device__ __forceinline__ void release_or_wait(bool last) {
     ++epoch;
     if (threadIdx.x == 0) {
       if (last) {
-        atomicExch(bar, 0u);
-        __threadfence();
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(epoch) : "memory");
       } else {
         unsigned g;
@@ -262,12 +265,9 @@ struct GridTeam {
         acc = is_sum ? acc + x : fmax(acc, x);
       }
       acc = is_sum ? warp_sum_down(acc) : warp_max_down(acc);
-      if (lane == 0) {
-        __stcg(gr + k, acc);
-        __threadfence();  // each writer publishes its own total before the release
-      }
+      if (lane == 0) __stcg(gr + k, acc);
     }
-    if (last) __syncthreads();  // totals written before thread 0 releases
+    if (last) __syncthreads();  // totals written before thread 0's release store
     release_or_wait(last);
 #pragma unroll
     for (int k = 0; k < NS; ++k) s[k] = __ldcg(gr + k);
