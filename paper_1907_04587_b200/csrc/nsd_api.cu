@@ -942,7 +942,7 @@ template <class R> struct Solver final : SolverBase {
       if (per_sm < 1) throw NsdError(NSD_CUDA_ERROR, "grid kernel cannot be resident");
       const char* bps = std::getenv("NSD_GRID_BLOCKS_PER_SM");
       grid_blocks = dev_sms * std::min(per_sm, bps ? std::max(1, std::atoi(bps)) : 1);
-      // partials, totals and the [count, generation] words of the grid barrier (nsd_team.cuh)
+      // partials (+ 2 x kRedMax spare slots) and the arrival count of the grid barrier (nsd_team.cuh)
       gpart.alloc(sizeof(double) * (2 * grid_blocks * nsd::kRedMax + 2 * nsd::kRedMax + 2));
     }
   }
