@@ -59,13 +59,16 @@ struct DBuf {
   ~DBuf() {
     if (p) cudaFree(p);
   }
+  // Grows by at least 1.5x: a contact count creeping up step by step must not
+  // re-allocate (cudaFree synchronises the device) on every step.
   void alloc(size_t bytes) {
     if (bytes <= n && p) return;
     if (p) cudaFree(p);
     p = nullptr;
+    const size_t want = std::max<size_t>(std::max<size_t>(bytes, 16), n + n / 2);
     n = 0;
-    NSD_CK(cudaMalloc(&p, bytes ? bytes : 16));
-    n = bytes;
+    NSD_CK(cudaMalloc(&p, want));
+    n = want;
   }
   template <class T> T* as(size_t off_elems = 0) const { return static_cast<T*>(p) + off_elems; }
 };
@@ -77,13 +80,15 @@ struct HBuf {
   ~HBuf() {
     if (p) cudaFreeHost(p);
   }
+  // Same 1.5x growth as DBuf: pinned (de)allocation costs milliseconds.
   void alloc(size_t bytes) {
     if (bytes <= n && p) return;
     if (p) cudaFreeHost(p);
     p = nullptr;
+    const size_t want = std::max<size_t>(std::max<size_t>(bytes, 16), n + n / 2);
     n = 0;
-    NSD_CK(cudaMallocHost(&p, bytes ? bytes : 16));
-    n = bytes;
+    NSD_CK(cudaMallocHost(&p, want));
+    n = want;
   }
 };
 
