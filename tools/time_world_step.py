@@ -5,7 +5,9 @@ import time
 
 import numpy as np
 
-from paper_1907_04587_b200 import World, lib, check
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1907_04587_b200 import World, lib, check  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 20
