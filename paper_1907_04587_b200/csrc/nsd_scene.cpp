@@ -14,6 +14,7 @@
 #include <limits>
 #include <memory>
 #include <random>
+#include <thread>
 #include <sstream>
 #include <stdexcept>
 
@@ -823,11 +824,37 @@ int nsd_scene_detect(const nsd_scene* s, const double* q, const double* u, const
   std::vector<nsd::CandD<double>> cands;
   nsd::CandD<double> c4[4];
   double th = 0.0, mu = 0.0;
-  for (size_t i = 0; i < sh.size(); ++i)
-    for (size_t j = i + 1; j < sh.size(); ++j) {
-      const int k = nsd::pair_contacts(view, sh[i], sh[j], h, w.margin, w.mu_default, c4, &th, &mu);
-      cands.insert(cands.end(), c4, c4 + k);
-    }
+  // Shape pairs, row i = pairs (i, j > i). Large scenes (C3: ~5k pairs) spread
+  // the rows over host threads; each row keeps its own candidates and the rows
+  // are concatenated in i order, so the sequence fed to the stable sort below
+  // is the serial one and the result is bit-identical.
+  const size_t ns = sh.size();
+  const size_t npairs = ns > 1 ? ns * (ns - 1) / 2 : 0;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned nth = npairs >= 2048 ? std::min<unsigned>(hw, 8u) : 1u;
+  if (nth > 1) {
+    std::vector<std::vector<nsd::CandD<double>>> rows(ns);
+    auto work = [&](unsigned t) {
+      nsd::CandD<double> b4[4];
+      double tth = 0.0, tmu = 0.0;
+      for (size_t i = t; i < ns; i += nth)  // strided rows balance the triangle
+        for (size_t j = i + 1; j < ns; ++j) {
+          const int k = nsd::pair_contacts(view, sh[i], sh[j], h, w.margin, w.mu_default, b4, &tth, &tmu);
+          rows[i].insert(rows[i].end(), b4, b4 + k);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nth; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th_ : pool) th_.join();
+    for (const auto& r : rows) cands.insert(cands.end(), r.begin(), r.end());
+  } else {
+    for (size_t i = 0; i < ns; ++i)
+      for (size_t j = i + 1; j < ns; ++j) {
+        const int k = nsd::pair_contacts(view, sh[i], sh[j], h, w.margin, w.mu_default, c4, &th, &mu);
+        cands.insert(cands.end(), c4, c4 + k);
+      }
+  }
   for (const auto& pr : w.particle_ranges)
     for (int b = pr.first; b < pr.first + pr.second; ++b)
       for (const auto& shape : sh) {
