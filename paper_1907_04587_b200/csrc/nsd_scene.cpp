@@ -855,12 +855,37 @@ int nsd_scene_detect(const nsd_scene* s, const double* q, const double* u, const
         cands.insert(cands.end(), c4, c4 + k);
       }
   }
+  // Particle generators: one row per particle body, threaded and concatenated
+  // in body order like the pair rows above.
+  std::vector<int> pbodies;
   for (const auto& pr : w.particle_ranges)
-    for (int b = pr.first; b < pr.first + pr.second; ++b)
+    for (int b = pr.first; b < pr.first + pr.second; ++b) pbodies.push_back(b);
+  const size_t nprow = pbodies.size();
+  const unsigned pth = nprow * ns >= 4096 ? std::min<unsigned>(hw, 8u) : 1u;
+  if (pth > 1) {
+    std::vector<std::vector<nsd::CandD<double>>> rows(nprow);
+    auto work = [&](unsigned t) {
+      nsd::CandD<double> b4[4];
+      double tth = 0.0, tmu = 0.0;
+      for (size_t r = t; r < nprow; r += pth)
+        for (const auto& shape : sh) {
+          const int k = nsd::particle_shape_contact(view, pbodies[r], shape, h, w.margin, w.mu_default, 0.0, -1.0,
+                                                    b4, &tth, &tmu);
+          rows[r].insert(rows[r].end(), b4, b4 + k);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < pth; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th_ : pool) th_.join();
+    for (const auto& r : rows) cands.insert(cands.end(), r.begin(), r.end());
+  } else {
+    for (const int b : pbodies)
       for (const auto& shape : sh) {
         const int k = nsd::particle_shape_contact(view, b, shape, h, w.margin, w.mu_default, 0.0, -1.0, c4, &th, &mu);
         cands.insert(cands.end(), c4, c4 + k);
       }
+  }
   std::stable_sort(cands.begin(), cands.end(), [](const nsd::CandD<double>& x, const nsd::CandD<double>& y) {
     return nsd::canonical_less(x.a, x.b, x.feature, y.a, y.b, y.feature);
   });
