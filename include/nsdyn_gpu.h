@@ -166,8 +166,11 @@ int nsd_batch_step(nsd_batch* b, const double* joint_torque, int32_t torque_on_d
 int nsd_batch_step_device(nsd_batch* b, const void* joint_torque_dev, int32_t dtype, double h,
                           const double gravity[3]);
 int nsd_batch_sync(nsd_batch* b);
-/* Per-env results of the last step: n_contacts[n_env], aborted[n_env],
- * final_residual_inf[n_env]; iters: n_env*newton_iterations (optional). */
+/* Per-env results: n_contacts[n_env] and final_residual_inf[n_env] of the last
+ * step; aborted[n_env] = 1 if the env rolled back (newton.cpp:362-369) in ANY
+ * step since the previous call; iters: n_env*newton_iterations of the last step
+ * (optional). A contact overflow (more than max_contacts) in any step since the
+ * previous call is NSD_INVALID. Overflow and abort flags are cleared by the call. */
 int nsd_batch_results(nsd_batch* b, int32_t* n_contacts, int32_t* aborted, double* final_residual_inf,
                       nsd_iter_stats* iters);
 /* Contact list of one env from the last step (count in *n). */
@@ -192,6 +195,14 @@ int nsd_batch_copy_state_async(nsd_batch* b, void* q_dst, void* u_dst);
 int nsd_batch_step_mapped(nsd_batch* b, const void* joint_torque, int32_t dtype, void* q_out, void* u_out, double h,
                           const double gravity[3]);
 int nsd_batch_info(const nsd_batch* b, int32_t* info /* [n_env, num_coord, num_dof, n_joints, max_rows, team_threads] */);
+/* Counters since the previous call (read and reset; synchronises the stream):
+ * out[0] PCR iterations run, summed over envs, Newton iterations and steps
+ * (the roofline numerator counts these); out[1] clock64 cycles spent inside the
+ * PCR loops and out[2] cycles per env step, both summed over envs (profile on,
+ * warp path); out[3] env-steps. */
+int nsd_batch_counters(nsd_batch* b, uint64_t* out);
+/* Enables (1) or disables (0) the in-kernel cycle counters of nsd_batch_counters. */
+int nsd_batch_profile(nsd_batch* b, int32_t enable);
 int nsd_batch_destroy(nsd_batch* b);
 
 /* ---------------- builders (scene.cpp:802-935 style) */

@@ -454,6 +454,17 @@ class BatchSolver:
         check(lib().nsd_batch_copy_state_async(self._h, C.c_void_p(q_ptr) if q_ptr else None,
                                                C.c_void_p(u_ptr) if u_ptr else None))
 
+    def counters(self):
+        """Counters since the previous call (nsd_batch_counters): PCR iterations run
+        (summed over envs, Newton iterations and steps), cycles inside the PCR loops
+        and per env step (profile on), env-steps."""
+        v = (C.c_uint64 * 4)()
+        check(lib().nsd_batch_counters(self._h, v))
+        return dict(cr_iterations=int(v[0]), cr_cycles=int(v[1]), env_cycles=int(v[2]), env_steps=int(v[3]))
+
+    def profile(self, enable=True):
+        check(lib().nsd_batch_profile(self._h, 1 if enable else 0))
+
     def device_state(self):
         q, u, dt = C.c_void_p(), C.c_void_p(), C.c_int32()
         check(lib().nsd_batch_device_state(self._h, C.byref(q), C.byref(u), C.byref(dt)))

@@ -72,7 +72,7 @@ EXPORTS = [
     "nsd_config_default", "nsd_last_error", "nsd_count_rows", "nsd_create", "nsd_set_config", "nsd_step",
     "nsd_last_step_ms", "nsd_destroy", "nsd_batch_create", "nsd_batch_set_state", "nsd_batch_get_state",
     "nsd_batch_set_stream", "nsd_batch_step", "nsd_batch_step_device", "nsd_batch_step_mapped", "nsd_batch_sync", "nsd_batch_results",
-    "nsd_batch_contacts", "nsd_batch_device_state", "nsd_batch_copy_state_async", "nsd_batch_info", "nsd_batch_destroy", "nsd_scene_build", "nsd_scene_parse", "nsd_scene_serialize",
+    "nsd_batch_contacts", "nsd_batch_device_state", "nsd_batch_copy_state_async", "nsd_batch_info", "nsd_batch_counters", "nsd_batch_profile", "nsd_batch_destroy", "nsd_scene_build", "nsd_scene_parse", "nsd_scene_serialize",
     "nsd_scene_dims", "nsd_scene_topology", "nsd_scene_shapes", "nsd_scene_state", "nsd_scene_config",
     "nsd_scene_destroy", "nsd_scene_batch_state", "nsd_scene_joint_frames", "nsd_scene_advance_anchors",
     "nsd_scene_detect",
@@ -118,6 +118,8 @@ def lib():
     L.nsd_batch_contacts.argtypes = [C.c_void_p, C.c_int32, C.POINTER(nsd_contact), I32]
     L.nsd_batch_device_state.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), I32]
     L.nsd_batch_info.argtypes = [C.c_void_p, I32]
+    L.nsd_batch_counters.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
+    L.nsd_batch_profile.argtypes = [C.c_void_p, C.c_int32]
     L.nsd_batch_copy_state_async.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     L.nsd_scene_batch_state.argtypes = [C.c_char_p, C.c_uint32, C.c_int32, D, D]
     L.nsd_batch_destroy.argtypes = [C.c_void_p]

@@ -3,13 +3,11 @@
 //   k_single_block / k_single_grid  one scene, nsd_step (newton_step boundary)
 //   k_batch_sub / k_batch_block     many environments, nsd_batch_step
 //                                   (device narrow phase + newton_step per env)
+//   k_batch_warp                    many rigid environments: one warp per env,
+//                                   after k_batch_sub's narrow-phase launch
 #include "nsdyn_gpu.h"
 
-#include "nsd_collide.cuh"
-#include "nsd_engine.cuh"
-#include "nsd_batch.cuh"
-
-#include <type_traits>
+#include "nsd_plan.cuh"
 
 #include <cuda_runtime.h>
 
@@ -22,6 +20,8 @@
 #include <vector>
 
 namespace {
+
+using namespace nsdi;
 
 thread_local std::string g_err;
 
@@ -133,11 +133,6 @@ void check_cfg(const nsd_config& c) {
 }
 
 // ------------------------------------------------------------------ host topology preprocessing
-struct HostTopo {
-  int nb = 0, ndof = 0, ncoord = 0, nd3 = 0, nj = 0, nt = 0, rows_joint = 0, rows_static = 0, tdim = 3;
-  std::vector<int> btype, bdof, bcoord, d3_body, d3_kind, jkind, jbody, jrow, tbody, sinc_off, sinc_ent;
-  std::vector<double> bmass, binertia, jparam, jframe, tdminv, tvol, tmat, tkinv;
-};
 
 // Inverse of the 6x6 isotropic stiffness by Gauss-Jordan with partial pivoting
 // (the linear material's compliance, materials.cpp:121,153), same elimination
@@ -352,553 +347,7 @@ template <class R> struct DevTopo {
   }
 };
 
-// Offsets (in elements) of one scene's Work arrays. "Hot" arrays are touched
-// every PCR iteration and live in shared memory for the warp-per-env batched
-// kernel (global memory otherwise); "cold" arrays stay in global memory.
-struct WorkPlan {
-  // hot R
-  size_t q, u, g, w, du, hinv, iwi6, coeff, hv, cd, lam, x, r, z, p, ap, az, inv, bx, cdir, carm, cscale, jstage,
-      cstage, jstr, crec, qrot, hotR;
-  // hot int
-  size_t blk, cbody, cinc_off, cinc_ent, cbinc_off, cbinc, cblk, hotI;
-  // cold R
-  size_t q0, u0, qp, ut, iw6, gp, up, shift, ub, fx, ctet, xn, rn, zn, cgeo, xlam, tq, coldR;
-  // cold int
-  size_t cfeat, cinc_cnt, xcbody, coldI;
-  size_t hot_bytes_f, hot_bytes_d;  // bytes of the hot set per env for float / double
-  int rcap = 0, ccap = 0;
-
-  void plan(const HostTopo& T, int cc) {
-    ccap = cc;
-    rcap = T.rows_static + 3 * cc;
-    const size_t rs = T.rows_static, rc = rcap, c = cc;
-    size_t o = 0;
-    auto a = [&](size_t n) {
-      const size_t off = o;
-      o += (n + 1) & ~size_t(1);  // keep 8-byte alignment for doubles
-      return off;
-    };
-    auto a16 = [&](size_t n) {  // 16-byte aligned start (vector loads): multiple of 4 elements
-      o = (o + 3) & ~size_t(3);
-      return a(n);
-    };
-    q = a(T.ncoord);
-    u = a(T.ndof);
-    g = a(T.ndof);
-    w = a(T.ndof);
-    du = a(T.ndof);
-    hinv = a(T.ndof);
-    iwi6 = a(6 * T.nd3);
-    coeff = a(12 * rs);
-    hv = a(rc);
-    cd = a(rc);
-    lam = a(rc);
-    x = a(rc);
-    r = a(rc);
-    z = a(rc);
-    p = a(rc);
-    ap = a(rc);
-    az = a(rc);
-    inv = a(rc);
-    bx = a(rc);
-    cdir = a(9 * c);
-    carm = a(6 * c);
-    cscale = a(2 * c);
-    jstage = a(12 * static_cast<size_t>(T.nj));
-    cstage = a(9 * c);
-    jstr = a(24 * static_cast<size_t>(T.nj));
-    crec = a16(20 * c);
-    qrot = a(9 * static_cast<size_t>(T.nb));
-    hotR = o;
-    o = 0;
-    blk = a(4 * rs);
-    cbody = a(2 * c);
-    cinc_off = a(T.nd3 + 1);
-    cinc_ent = a(4 * c);
-    cbinc_off = a(T.nb + 1);
-    cbinc = a(2 * c);
-    cblk = a16(4 * c);
-    hotI = o;
-    o = 0;
-    q0 = a(T.ncoord);
-    u0 = a(T.ndof);
-    qp = a(T.ncoord);
-    ut = a(T.ndof);
-    iw6 = a(6 * T.nd3);
-    gp = a(T.ndof);
-    up = a(T.ndof);
-    shift = a(T.ndof);
-    ub = a(T.ndof);
-    fx = a(T.ndof);
-    ctet = a(static_cast<size_t>(T.tdim) * T.tdim * T.nt);  // 3x3 (Neo-Hookean) or 6x6 (linear) blocks
-    xn = a(rc);
-    rn = a(rc);
-    zn = a(rc);
-    cgeo = a(17 * c);
-    xlam = a(rc);
-    tq = a(static_cast<size_t>(T.nj));
-    coldR = o;
-    o = 0;
-    cfeat = a(c);
-    cinc_cnt = a(T.nd3 + 1);
-    xcbody = a(2 * c);
-    coldI = o;
-    hot_bytes_f = ((hotR * 4 + 15) & ~size_t(15)) + hotI * 4;
-    hot_bytes_d = ((hotR * 8 + 15) & ~size_t(15)) + hotI * 4;
-    hot_bytes_f = (hot_bytes_f + 15) & ~size_t(15);
-    hot_bytes_d = (hot_bytes_d + 15) & ~size_t(15);
-  }
-  template <class R> size_t hot_bytes() const { return sizeof(R) == 8 ? hot_bytes_d : hot_bytes_f; }
-  template <class R> __host__ __device__ int* hot_ints(R* hr) const {
-    return reinterpret_cast<int*>(reinterpret_cast<char*>(hr) + ((hotR * sizeof(R) + 15) & ~size_t(15)));
-  }
-  template <class R> __host__ __device__ nsd::Work<R> bind(R* hr, int* hi, R* cr, int* ci) const {
-    nsd::Work<R> W{};
-    W.q = hr + q;
-    W.u = hr + u;
-    W.ut = cr + ut;
-    W.g = hr + g;
-    W.w = hr + w;
-    W.du = hr + du;
-    W.hinv = hr + hinv;
-    W.iw6 = cr + iw6;
-    W.iwi6 = hr + iwi6;
-    W.coeff = hr + coeff;
-    W.hv = hr + hv;
-    W.cd = hr + cd;
-    W.lam = hr + lam;
-    W.x = hr + x;
-    W.xn = cr + xn;
-    W.r = hr + r;
-    W.rn = cr + rn;
-    W.z = hr + z;
-    W.zn = cr + zn;
-    W.p = hr + p;
-    W.ap = hr + ap;
-    W.az = hr + az;
-    W.inv = hr + inv;
-    W.bx = hr + bx;
-    W.cgeo = cr + cgeo;
-    W.cdir = hr + cdir;
-    W.carm = hr + carm;
-    W.cscale = hr + cscale;
-    W.blk = hi + blk;
-    W.cbody = hi + cbody;
-    W.cinc_off = hi + cinc_off;
-    W.cinc_ent = hi + cinc_ent;
-    W.q0 = cr + q0;
-    W.u0 = cr + u0;
-    W.qp = cr + qp;
-    W.gp = cr + gp;
-    W.up = cr + up;
-    W.shift = cr + shift;
-    W.ub = cr + ub;
-    W.ctet = cr + ctet;
-    return W;
-  }
-};
-
 }  // namespace
-
-// ================================================================== kernels
-template <class R, bool kTets>
-__global__ void __launch_bounds__(512) k_single_block(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out) {
-  __shared__ double red[2 * 33 * nsd::kRedMax];
-  nsd::BlockTeam t(red);
-  nsd::newton_setup(t, T, W);
-  t.sync();
-  nsd::newton_solve<R, kTets>(t, T, W, cfg, out);
-}
-
-#ifndef NSD_GRID_THREADS
-#define NSD_GRID_THREADS 256  // measured: 512 (128 registers) makes C2 15% slower
-#endif
-// Threads per CTA of the cooperative grid kernel (one CTA per SM).
-constexpr int kGridThreads = NSD_GRID_THREADS;
-template <class R, bool kTets, int RPT>
-__global__ void __launch_bounds__(kGridThreads) k_single_grid(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out,
-                                                     double* gpart) {
-  __shared__ double red[2 * 33 * nsd::kRedMax];
-  nsd::GridTeam t(red, gpart);
-  nsd::newton_setup(t, T, W);
-  t.sync();
-  nsd::newton_solve<R, kTets, nsd::GridTeam, RPT>(t, T, W, cfg, out);
-}
-
-// ------------------------------------------------------------------ batched
-template <class R> struct BatchArgs {
-  nsd::Topo<R> T;
-  nsd::Cfg cfg;
-  int n_env, ns, npairs, maxc, envs_per_block, hot_in_smem;
-  int row_pool;  // per-env shared-memory region (elements of R) for the PCR row state; 0 = off
-  const int2* pairs;
-  const nsd::ShapeD<R>* shapes;
-  const R* jframe;
-  R margin, mu_default, h, grav[3];
-  R* qs;  // persistent state (n_env * ncoord)
-  R* us;
-  const void* torque;  // n_env * nj or null (device memory or mapped pinned host memory)
-  int torque_double;
-  R* q_out;  // optional second destination of the final state (mapped pinned host memory):
-  R* u_out;  // the step's device->host transfer made by the kernel, overlapped with other envs
-  char* hot_global;  // per-env hot slices when not in shared memory
-  size_t hot_bytes;
-  R* cold_r;
-  int* cold_i;
-  WorkPlan plan;
-  nsd::CandD<R>* cand;  // n_env * npairs * 4
-  int* pair_cnt;        // n_env * npairs
-  int* nc_out;          // n_env
-  int* overflow;        // n_env
-  double* fin;          // n_env * 8
-  nsd::IterOut* iters;  // n_env * newton_iterations
-  const int* jbinc_off;  // static joint incidence per body (warp solver)
-  const int* jbinc;
-  unsigned long long* ptime;  // NSD_PHASE_TIMING diagnostics (16 counters) or null
-  const int4* jblk;           // static dof3 blocks per joint
-};
-
-// One environment: extension forces, setup, device narrow phase, contact
-// incidence, Newton solve, state write-back (step_world, scene.cpp:709-732).
-// Row vectors in the region (priority order in batch_env): all 8 in fp32; in fp64
-// the shared-memory budget is the limit, so fewer vectors let larger envs fit.
-// Measured (C5): fp32 3.62 M -> 3.92 M env-steps/s when inv/cd joined the region;
-// fp64 (then 9 vectors, inv z ap p r x az bx cd): 4 vectors 2.00 M, 5 2.21 M, 6 2.37 M,
-// 7 2.22 M, 8 1.78 M env-steps/s -> 6. With z implicit (inv r ap p x az bx cd):
-// 6 2.83 M, 7 2.63 M, 8 2.09 M -> 6.
-#ifndef NSD_POOL_VECS64
-#define NSD_POOL_VECS64 6
-#endif
-template <class R> __host__ __device__ constexpr int pool_row_vecs() { return sizeof(R) == 4 ? 8 : NSD_POOL_VECS64; }
-// Elements of the per-env shared-memory row region for nc contacts: the
-// write-heavy PCR state x, r, z, p, ap, az, bx (7 x rows), the J^T staging
-// (12 per joint, 9 per contact) and w (ndof), each array kept 16-byte aligned.
-#ifndef NSD_POOL_EXTRA
-#define NSD_POOL_EXTRA 4
-#endif
-// Extra arrays in the fp32 region: 1 contact records, 2 joint records, 4 the H^-1
-// diagonal. Measured (C5 fp32, env-steps/s): none 4.25 M, +records 4.18 M, +joint
-// records 4.16 M (both cost L1 via the carveout), +H^-1 4.37 M -> 4.
-template <class R> __host__ __device__ constexpr int pool_extra() { return sizeof(R) == 4 ? NSD_POOL_EXTRA : 0; }
-template <class R> __host__ __device__ inline int row_pool_elems(int rows_static, int nj, int ndof, int nc) {
-  const int rows = (rows_static + 3 * nc + 3) & ~3;
-  int n = pool_row_vecs<R>() * rows + ((12 * nj + 3) & ~3) + ((9 * nc + 3) & ~3) + ((ndof + 3) & ~3);
-  if (pool_extra<R>() & 1) n += 20 * nc;
-  if (pool_extra<R>() & 2) n += (24 * nj + 3) & ~3;
-  if (pool_extra<R>() & 4) n += (ndof + 3) & ~3;
-  return n;
-}
-
-template <class R, class Team>
-__device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* pool, int tib) {
-  const nsd::Topo<R>& T = A.T;
-  const WorkPlan& P = A.plan;
-  int* hi = P.hot_ints(hr);
-  R* cr = A.cold_r + (size_t)env * P.coldR;
-  int* ci = A.cold_i + (size_t)env * P.coldI;
-  nsd::Work<R> W = P.template bind<R>(hr, hi, cr, ci);
-  nsd::PhaseClock pc(A.ptime, t.rank() == 0);
-  const long long env_t0 = A.ptime ? clock64() : 0;
-  W.jframe = A.jframe;
-  W.h = A.h;
-  W.grav[0] = A.grav[0];
-  W.grav[1] = A.grav[1];
-  W.grav[2] = A.grav[2];
-  R* qs = A.qs + (size_t)env * T.ncoord;
-  R* us = A.us + (size_t)env * T.ndof;
-  R* q0 = cr + P.q0;
-  R* u0 = cr + P.u0;
-  for (int i = t.rank(); i < T.ncoord; i += t.size()) q0[i] = qs[i];
-  for (int i = t.rank(); i < T.ndof; i += t.size()) u0[i] = us[i];
-  W.f_extra = nullptr;
-  // per-body rotations at q- (torque hook, narrow phase, first assembly): one
-  // quaternion -> matrix per body instead of one per joint / contact / shape pair
-  R* qrot = hr + P.qrot;
-  t.sync();
-  for (int b = t.rank(); b < T.nb; b += t.size())
-    if (T.btype[b] == 1) {
-      const nsd::M3<R> m = nsd::body_rot(T, q0, b);
-      for (int i = 0; i < 9; ++i) qrot[9 * b + i] = m.a[i];
-    }
-  if (A.torque) {
-    R* fx = cr + P.fx;
-    // the env's torques once per lane into scratch (a single bus round trip when the
-    // actions are read from mapped host memory), then the per-body sums
-    R* tq = cr + P.tq;
-    for (int j = t.rank(); j < T.nj; j += t.size())
-      tq[j] = A.torque_double ? R(static_cast<const double*>(A.torque)[(size_t)env * T.nj + j])
-                              : R(static_cast<const float*>(A.torque)[(size_t)env * T.nj + j]);
-    t.sync();
-    // joint torques about revolute axes at q- (extension hook): +tau*axis on a, -tau*axis on b
-    for (int b = t.rank(); b < T.nb; b += t.size()) {
-      const int d = T.bdof[b];
-      nsd::V3<R> f = nsd::v3(R(0), R(0), R(0));
-      if (T.btype[b] == 1) {
-        for (int j = 0; j < T.nj; ++j) {
-          if (T.jkind[j] != 1) continue;
-          const int ja = T.jbody[2 * j], jb = T.jbody[2 * j + 1];
-          if (ja != b && jb != b) continue;
-          const R tau = tq[j];
-          const nsd::V3<R> axl = nsd::ld3(A.jframe + 21 * j + 6);
-          nsd::M3<R> Rj;
-          if (ja >= 0)
-            for (int i = 0; i < 9; ++i) Rj.a[i] = qrot[9 * ja + i];
-          const nsd::V3<R> ax = ja < 0 ? axl : nsd::mul(Rj, axl);
-          if (ja == b) f = f + tau * ax;
-          if (jb == b) f = f - tau * ax;
-        }
-      }
-      for (int k = 0; k < 3; ++k) fx[d + k] = R(0);
-      if (T.btype[b] == 1) nsd::st3(fx + d + 3, f);
-    }
-    W.f_extra = fx;
-  }
-  t.sync();
-  nsd::newton_setup(t, T, W);
-  t.sync();
-  // ---- narrow phase over shape pairs with the unconstrained velocity
-  nsd::BodyView<R> view{T.btype, T.bdof, T.bcoord, W.q0, W.ut, qrot};
-  nsd::CandD<R>* cand = A.cand + (size_t)env * A.npairs * 4;
-  int* cnt = A.pair_cnt + (size_t)env * A.npairs;
-  for (int p = t.rank(); p < A.npairs; p += t.size()) {
-    const int2 ij = A.pairs[p];
-    R th, mu;
-    cnt[p] = nsd::pair_contacts(view, A.shapes[ij.x], A.shapes[ij.y], A.h, A.margin, A.mu_default, cand + 4 * p, &th,
-                                &mu);
-  }
-  t.sync();
-  int total = 0;
-  for (int p = 0; p < A.npairs; ++p) total += cnt[p];
-  const int nc = total < A.maxc ? total : A.maxc;
-  int* cbody = hi + P.cbody;
-  int* cfeat = ci + P.cfeat;
-  R* cgeo = cr + P.cgeo;
-  // canonical (a.body, b.body, feature) order, stable in generation order
-  for (int p = t.rank(); p < A.npairs; p += t.size()) {
-    for (int k = 0; k < cnt[p]; ++k) {
-      const nsd::CandD<R> c = cand[4 * p + k];
-      int rank = 0;
-      for (int p2 = 0; p2 < A.npairs; ++p2) {
-        const int n2 = cnt[p2];
-        for (int k2 = 0; k2 < n2; ++k2) {
-          const nsd::CandD<R>& o = cand[4 * p2 + k2];
-          if (nsd::canonical_less(o.a, o.b, o.feature, c.a, c.b, c.feature) ||
-              (o.a == c.a && o.b == c.b && o.feature == c.feature && (p2 < p || (p2 == p && k2 < k))))
-            ++rank;
-        }
-      }
-      if (rank >= nc) continue;
-      cbody[2 * rank] = c.a;
-      cbody[2 * rank + 1] = c.b;
-      cfeat[rank] = c.feature;
-      R* g = cgeo + 17 * rank;
-      nsd::V3<R> n = nsd::get3(c.n), d1, d2;
-      nsd::tangent_basis(n, d1, d2);
-      for (int i = 0; i < 3; ++i) {
-        g[i] = c.la[i];
-        g[3 + i] = c.lb[i];
-        g[6 + i] = c.n[i];
-      }
-      nsd::st3(g + 9, d1);
-      nsd::st3(g + 12, d2);
-      g[15] = c.thick;
-      g[16] = c.mu;
-    }
-  }
-  t.sync();
-  W.nc = nc;
-  W.normal_begin = T.rows_static;
-  W.friction_begin = T.rows_static + nc;
-  W.nrows = T.rows_static + 3 * nc;
-  nsd::StepOut out{};
-  out.iters = A.iters ? A.iters + (size_t)env * A.cfg.newton_iterations : nullptr;
-  out.fin = A.fin + (size_t)env * 8;
-  out.ptime = A.ptime;
-  pc.mark(0);
-  if constexpr (!std::is_same<Team, nsd::BlockTeam>::value) {
-    // ---- object-centric sub-warp solver: contact incidence per body (contact*2 + side)
-    int* cboff = hi + P.cbinc_off;
-    int* cbinc = hi + P.cbinc;
-    int* ccnt = ci + P.cinc_cnt;
-    for (int b = t.rank(); b < T.nb; b += t.size()) {
-      int n = 0;
-      for (int c = 0; c < nc; ++c) n += (cbody[2 * c] == b) + (cbody[2 * c + 1] == b);
-      ccnt[b] = n;
-    }
-    t.sync();
-    if (t.rank() == 0) {
-      int s = 0;
-      for (int b = 0; b < T.nb; ++b) {
-        cboff[b] = s;
-        s += ccnt[b];
-      }
-      cboff[T.nb] = s;
-    }
-    t.sync();
-    for (int b = t.rank(); b < T.nb; b += t.size()) {
-      int o = cboff[b];
-      for (int c = 0; c < nc; ++c) {
-        if (cbody[2 * c] == b) cbinc[o++] = 2 * c;
-        if (cbody[2 * c + 1] == b) cbinc[o++] = 2 * c + 1;
-      }
-    }
-    W.jstr = hr + P.jstr;  // structured joint rows: the object solver never reads coeff/blk
-    W.qrot = qrot;         // rotations at q- now; refreshed before every later assembly
-    W.crec = hr + P.crec;  // contact records + block ids for vector loads
-    W.cblk = reinterpret_cast<int4*>(hi + P.cblk);
-    W.jblk = A.jblk;
-    t.sync();
-    nsd::ObjView<R> O{W, hr + P.jstage, hr + P.cstage, A.jbinc_off, A.jbinc, cboff, cbinc};
-    // Slice of the block's shared-memory region. When the block is one full warp of
-    // teams, they exchange their needs and take prefix offsets, so a small env lends
-    // space to a large one (all 32 lanes reach this shuffle: a full block has no
-    // early-returned team).
-    const int need = row_pool_elems<R>(T.rows_static, T.nj, T.ndof, nc);
-    const int epb = A.envs_per_block, cap = epb * A.row_pool;
-    const bool block_full = (blockIdx.x + 1) * epb <= A.n_env;
-    int off = tib * A.row_pool, lim = (tib + 1) * A.row_pool;
-    if (pool && block_full && epb * Team::kSize == 32) {
-      int before = 0;
-      for (int j = 0; j < epb; ++j) {
-        const int nj_need = __shfl_sync(0xffffffffu, need, j * Team::kSize);
-        if (j < tib) before += nj_need;
-      }
-      off = before;
-      lim = cap;
-    }  // partial blocks keep the fixed split (teams past n_env returned early)
-    if (pool && off + need <= lim) {
-      pool += off;
-      // the env's PCR row state fits its shared-memory region: keep every store of
-      // the CR loop on chip (global stores are write-through to L2)
-      const int rows = (W.nrows + 3) & ~3;
-      R* sp = pool;
-      // row vectors by accesses per CR iteration: inv (5 reads), r (4R+1W), ap
-      // (3R+1W), p (2R+1W), x, az (1R+1W), bx (1W), cd (1R); z = M^-1 r is not
-      // stored (newton_solve_obj); the first pool_row_vecs<R>() live in the region
-      constexpr int nv = pool_row_vecs<R>();
-      O.W.inv = sp;
-      O.W.r = sp + rows;
-      O.W.ap = sp + 2 * rows;
-      if (nv >= 4) O.W.p = sp + 3 * rows;
-      if (nv >= 5) O.W.x = sp + 4 * rows;
-      if (nv >= 6) O.W.az = sp + 5 * rows;
-      if (nv >= 7) O.W.bx = sp + 6 * rows;
-      if (nv >= 8) O.W.cd = sp + 7 * rows;
-      sp += nv * rows;
-      O.jstage = sp;
-      sp += (12 * T.nj + 3) & ~3;
-      O.cstage = sp;
-      sp += (9 * nc + 3) & ~3;
-      // w = H^-1 J^T y is produced by body_momentum; copy the setup value over
-      for (int i = t.rank(); i < T.ndof; i += t.size()) sp[i] = W.w[i];
-      O.W.w = sp;
-      sp += (T.ndof + 3) & ~3;
-      if (pool_extra<R>() & 1) {
-        O.W.crec = sp;
-        sp += 20 * nc;
-      }
-      if (pool_extra<R>() & 2) {
-        O.W.jstr = sp;
-        sp += (24 * T.nj + 3) & ~3;
-      }
-      if (pool_extra<R>() & 4) {
-        O.W.hinv = sp;
-        sp += (T.ndof + 3) & ~3;
-      }
-      t.sync();
-    }
-    nsd::newton_solve_obj(t, T, O, A.cfg, out);
-    W = O.W;
-  } else {
-    // ---- contact incidence per dof3 block (contact*4 + slot, contacts ascending)
-    int* coff = hi + P.cinc_off;
-    int* cent = hi + P.cinc_ent;
-    int* ccnt = ci + P.cinc_cnt;
-    for (int b = t.rank(); b < T.nd3; b += t.size()) {
-      int n = 0;
-      for (int c = 0; c < nc; ++c) {
-        int al, aa, bl, ba;
-        nsd::body_blocks(T, cbody[2 * c], al, aa);
-        nsd::body_blocks(T, cbody[2 * c + 1], bl, ba);
-        n += (al == b) + (aa == b) + (bl == b) + (ba == b);
-      }
-      ccnt[b] = n;
-    }
-    t.sync();
-    if (t.rank() == 0) {
-      int s = 0;
-      for (int b = 0; b < T.nd3; ++b) {
-        coff[b] = s;
-        s += ccnt[b];
-      }
-      coff[T.nd3] = s;
-    }
-    t.sync();
-    for (int b = t.rank(); b < T.nd3; b += t.size()) {
-      int o = coff[b];
-      for (int c = 0; c < nc; ++c) {
-        int b4[4];
-        nsd::body_blocks(T, cbody[2 * c], b4[0], b4[1]);
-        nsd::body_blocks(T, cbody[2 * c + 1], b4[2], b4[3]);
-        for (int s = 0; s < 4; ++s)
-          if (b4[s] == b) cent[o++] = 4 * c + s;
-      }
-    }
-    t.sync();
-    nsd::newton_solve<R, false>(t, T, W, A.cfg, out);
-  }
-  t.sync();
-  pc.mark(13);
-  for (int i = t.rank(); i < T.ncoord; i += t.size()) qs[i] = W.q[i];
-  for (int i = t.rank(); i < T.ndof; i += t.size()) us[i] = W.u[i];
-  if (A.q_out)
-    for (int i = t.rank(); i < T.ncoord; i += t.size()) A.q_out[(size_t)env * T.ncoord + i] = W.q[i];
-  if (A.u_out)
-    for (int i = t.rank(); i < T.ndof; i += t.size()) A.u_out[(size_t)env * T.ndof + i] = W.u[i];
-  // export the step's contact set and multipliers (nsd_batch_contacts)
-  R* xl = cr + P.xlam;
-  int* xb = ci + P.xcbody;
-  for (int i = t.rank(); i < W.nrows; i += t.size()) xl[i] = W.lam[i];
-  for (int i = t.rank(); i < 2 * nc; i += t.size()) xb[i] = cbody[i];
-  if (A.ptime && t.rank() == 0) {  // diagnostics: straggler vs mean env time, contacts of the slowest
-    const unsigned long long dt = static_cast<unsigned long long>(clock64() - env_t0);
-    atomicMax(A.ptime + 14, dt);
-    atomicAdd(A.ptime + 15, dt);
-  }
-  if (t.rank() == 0) {
-    A.nc_out[env] = nc;
-    A.overflow[env] = total > A.maxc ? total : 0;
-  }
-}
-
-// TPE lanes per environment (32/TPE environments per warp); each env's hot
-// working set in shared memory.
-// Register budget: 4096 envs at 2 envs per warp (TPE 16) are 2048 warps, 14 per SM
-// for a single wave, so <= 146 registers per thread. Measured (50-step C5 bench):
-// 128 registers (128 x 4 bounds) fp32 2.77 M / fp64 1.62 M env-steps/s; uncapped
-// (255, 8 warps/SM) 2.2 M / 1.54 M; 144 (fp64) 1.17 M (spills land in the solver).
-template <class R, int TPE>
-__global__ void __launch_bounds__(128, 4) k_batch_sub(BatchArgs<R> A) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int tib = threadIdx.x / TPE;  // team index in the block
-  const int env = blockIdx.x * A.envs_per_block + tib;
-  if (env >= A.n_env) return;  // team-uniform
-  R* hr = A.hot_in_smem ? reinterpret_cast<R*>(smem + (size_t)tib * A.hot_bytes)
-                        : reinterpret_cast<R*>(A.hot_global + (size_t)env * A.hot_bytes);
-  R* pool = A.row_pool ? reinterpret_cast<R*>(smem) : nullptr;  // the block's region; batch_env takes a slice
-  nsd::SubWarpTeam<TPE> t(threadIdx.x & 31);
-  batch_env(t, A, env, hr, pool, tib);
-}
-
-// CTA per environment.
-template <class R> __global__ void __launch_bounds__(256) k_batch_block(BatchArgs<R> A) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double red[2 * 33 * nsd::kRedMax];
-  nsd::BlockTeam t(red);
-  R* hr = A.hot_in_smem ? reinterpret_cast<R*>(smem)
-                        : reinterpret_cast<R*>(A.hot_global + (size_t)blockIdx.x * A.hot_bytes);
-  batch_env(t, A, blockIdx.x, hr, static_cast<R*>(nullptr), 0);
-}
 
 // ================================================================== handles
 struct SolverBase {
@@ -940,10 +389,7 @@ template <class R> struct Solver final : SolverBase {
       use_grid = true;
       int dev_sms = 0, per_sm = 0;
       NSD_CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
-      if (tets)
-        NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, true, 0>, kGridThreads, 0));
-      else
-        NSD_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, false, 0>, kGridThreads, 0));
+      per_sm = single_grid_blocks_per_sm<R>(tets);
       if (per_sm < 1) throw NsdError(NSD_CUDA_ERROR, "grid kernel cannot be resident");
       const char* bps = std::getenv("NSD_GRID_BLOCKS_PER_SM");
       grid_blocks = dev_sms * std::min(per_sm, bps ? std::max(1, std::atoi(bps)) : 1);
@@ -1071,21 +517,14 @@ template <class R> struct Solver final : SolverBase {
     nsd::Cfg kc = to_cfg(cfg);
     NSD_CK(cudaEventRecord(ev0, stream));
     if (!use_grid) {
-      if (tets)
-        k_single_block<R, true><<<1, block_threads, 0, stream>>>(topo.t, W, kc, so);
-      else
-        k_single_block<R, false><<<1, block_threads, 0, stream>>>(topo.t, W, kc, so);
-      NSD_CK(cudaGetLastError());
+      NSD_CK(launch_single_block<R>(tets, block_threads, stream, topo.t, W, kc, so));
     } else {
       double* gp = gpart.as<double>();
       NSD_CK(cudaMemsetAsync(gp + 2 * grid_blocks * nsd::kRedMax + 2 * nsd::kRedMax, 0, 2 * sizeof(unsigned), stream));
-      void* args[] = {&topo.t, &W, &kc, &so, &gp};
       // register-resident PCR rows when every thread owns <= 2 rows (NSD_GRID_REGS=0 disables)
       const bool regs = cfg.linear_method == 3 && nrows <= 2 * grid_blocks * kGridThreads && !(std::getenv("NSD_GRID_REGS") &&
                                                                        std::atoi(std::getenv("NSD_GRID_REGS")) == 0);
-      void* fn = tets ? (regs ? (void*)k_single_grid<R, true, 2> : (void*)k_single_grid<R, true, 0>)
-                      : (regs ? (void*)k_single_grid<R, false, 2> : (void*)k_single_grid<R, false, 0>);
-      NSD_CK(cudaLaunchCooperativeKernel(fn, dim3(grid_blocks), dim3(kGridThreads), args, 0, stream));
+      NSD_CK(launch_single_grid<R>(tets, regs, grid_blocks, stream, topo.t, W, kc, so, gp));
     }
     NSD_CK(cudaEventRecord(ev1, stream));
     // ---- download
@@ -1173,6 +612,8 @@ struct BatchBase {
   virtual void contacts(int env, nsd_contact* out, int* n) = 0;
   virtual void device_state(void** q, void** u, int* dtype) = 0;
   virtual void copy_state_async(void* q, void* u) = 0;
+  virtual void counters(unsigned long long* out) = 0;
+  virtual void set_profile(int on) = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   int info[6] = {0, 0, 0, 0, 0, 0};
@@ -1185,6 +626,14 @@ template <class R> struct Batch final : BatchBase {
   int n_env, maxc, ns, npairs;
   WorkPlan plan;
   DBuf hotg, coldr, coldi, shapes, pairs, cand, paircnt, ncout, ovf, fin, iters, qs, us, torque, jbinc, jblk;
+  DBuf abany, ctr, wjinc, wlam, wptime;  // sticky abort flags; counters; k_batch_warp's joint incidence (both sides)
+  bool warp_path = false;  // k_batch_warp for rigid scenes (narrow-phase launch + warp solver + large-env launch)
+  nsd::wp::Plan wplan{};
+  int warp_epb = 2;        // environments (warps) per block of k_batch_warp (64 threads, 7 blocks/SM)
+  int warp_max_obj = 32;   // NSD_WARP_MAX_OBJ (tests) routes smaller envs to the object solver too
+  size_t warp_smem = 0;
+  long env_steps = 0;
+  bool profile = false;
   int jbinc_n = 0;
   HBuf stage;
   double margin, mu_default;
@@ -1319,10 +768,7 @@ template <class R> struct Batch final : BatchBase {
           // device maximum (a permission, not an allocation) so handles cannot shrink it
           // under one another
           const int sb = static_cast<int>(smem_bytes);
-          NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
-          NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
-          NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
-          NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+          NSD_CK(batch_sub_attrs<R>(max_optin, -1));
           carve = static_cast<int>(std::min<long>(100, (100L * bps * (sb + reserved) + smem_sm - 1) / smem_sm));
         }
         if (std::getenv("NSD_VERBOSE"))
@@ -1330,19 +776,10 @@ template <class R> struct Batch final : BatchBase {
                        n_env, bps, region, full, smem_bytes, carve);
       }
       if (const char* e = std::getenv("NSD_L1_CARVEOUT")) carve = std::atoi(e);
-      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 32>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+      NSD_CK(batch_sub_attrs<R>(-1, carve));
     } else {
-      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
-      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
-      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
-      NSD_CK(cudaFuncSetAttribute(k_batch_sub<R, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
-      cudaFuncAttributes fa{};
-      NSD_CK(cudaFuncGetAttributes(&fa, k_batch_block<R>));  // static reduction buffer counts against the limit
-      NSD_CK(cudaFuncSetAttribute(k_batch_block<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  max_optin - static_cast<int>(fa.sharedSizeBytes)));
+      NSD_CK(batch_sub_attrs<R>(max_optin, -1));
+      NSD_CK(batch_block_attrs<R>(max_optin));
     }
     coldr.alloc(sizeof(R) * plan.coldR * n_env);
     coldi.alloc(sizeof(int) * plan.coldI * n_env);
@@ -1371,6 +808,45 @@ template <class R> struct Batch final : BatchBase {
       ptime.alloc(sizeof(unsigned long long) * 16);
       NSD_CK(cudaMemset(ptime.p, 0, sizeof(unsigned long long) * 16));
     }
+    abany.alloc(sizeof(int) * n_env);
+    NSD_CK(cudaMemset(abany.p, 0, sizeof(int) * n_env));
+    ctr.alloc(sizeof(unsigned long long) * 4);
+    NSD_CK(cudaMemset(ctr.p, 0, sizeof(unsigned long long) * 4));
+    // Warp-per-env solver (nsd_warp.cuh): rigid bodies only, <= 32 bodies and joints,
+    // the default team shape and slabs in global memory (NSD_BATCH_FAST=0 disables).
+    bool all_rigid = H.nb > 0;
+    for (int b = 0; b < H.nb; ++b) all_rigid = all_rigid && H.btype[b] == 1;
+    const char* fe = std::getenv("NSD_BATCH_FAST");
+    warp_path = all_rigid && H.nb <= 32 && H.nj <= 32 && team_threads == 16 && !env_team && !hot_in_smem &&
+                !(fe && std::atoi(fe) == 0);
+    if (warp_path) {
+      std::vector<std::vector<int>> per(H.nb);
+      for (int j = 0; j < H.nj; ++j) {
+        const int a = H.jbody[2 * j], b = H.jbody[2 * j + 1];
+        if (a >= 0) per[a].push_back(2 * j);
+        if (b >= 0) per[b].push_back(2 * j + 1);
+      }
+      std::vector<int> flat(H.nb + 1, 0);
+      for (int b = 0; b < H.nb; ++b) flat[b + 1] = flat[b] + static_cast<int>(per[b].size());
+      for (int b = 0; b < H.nb; ++b) flat.insert(flat.end(), per[b].begin(), per[b].end());
+      wjinc.alloc(sizeof(int) * flat.size());
+      NSD_CK(cudaMemcpy(wjinc.p, flat.data(), sizeof(int) * flat.size(), cudaMemcpyHostToDevice));
+      wplan = nsd::wp::Plan::make<R>(H.nb);
+      wlam.alloc(sizeof(R) * nsd::wp::kRows * 32 * (size_t)n_env);
+      if (std::getenv("NSD_PHASE_TIMING")) {
+        wptime.alloc(sizeof(unsigned long long) * nsd::wp::kWPhases);
+        NSD_CK(cudaMemset(wptime.p, 0, sizeof(unsigned long long) * nsd::wp::kWPhases));
+      }
+      if (const char* e = std::getenv("NSD_WARP_EPB")) warp_epb = std::max(1, std::min(8, std::atoi(e)));
+      if (const char* e = std::getenv("NSD_WARP_MAX_OBJ")) warp_max_obj = std::max(0, std::min(32, std::atoi(e)));
+      warp_smem = static_cast<size_t>(wplan.bytes) * warp_epb;
+      int per_sm = 0;
+      NSD_CK(batch_warp_setup<R>(max_optin, 32 * warp_epb, warp_smem, &per_sm));
+      if (per_sm < 1) warp_path = false;
+      if (std::getenv("NSD_VERBOSE"))
+        std::fprintf(stderr, "nsd batch warp path: %d B/env, %d envs/block, %d blocks/SM\n", wplan.bytes, warp_epb,
+                     per_sm);
+    }
   }
   ~Batch() override {
     if (ptime.p) {  // diagnostics: cycles per phase summed over envs (team leaders)
@@ -1392,6 +868,21 @@ template <class R> struct Batch final : BatchBase {
                      double(h[k]) / n_env);
       std::fprintf(stderr, "  env time: max %.3g cycles (one step), mean %.3g cycles per env-step\n", double(h[14]),
                    double(h[15]) / std::max(1.0, double(launches) * n_env));
+    }
+    if (wptime.p) {  // diagnostics: the warp solver's lane-0 cycles per phase, summed over envs
+      unsigned long long h[nsd::wp::kWPhases];
+      cudaStreamSynchronize(stream);
+      cudaMemcpy(h, wptime.p, sizeof(h), cudaMemcpyDeviceToHost);
+      static const char* names[nsd::wp::kWPhases] = {
+          "setup+incidence", "assemble", "momentum (g, w)", "rhs/precond + PCR tail", "PCR A z setup",
+          "PCR A (p, ap, den)", "PCR trial + stage J^T z'", "PCR accept", "PCR bodies H^-1 J^T",
+          "PCR J w (az, zaz)", "du / NaN check", "update + integrate", "final assemble", "write-back"};
+      unsigned long long tot = 0;
+      for (int k = 0; k < nsd::wp::kWPhases; ++k) tot += h[k];
+      std::fprintf(stderr, "nsd warp-solver phase timing (%d envs, %s):\n", n_env, sizeof(R) == 8 ? "fp64" : "fp32");
+      for (int k = 0; k < nsd::wp::kWPhases; ++k)
+        std::fprintf(stderr, "  %-28s %6.2f%%  %.4g cycles/env-step\n", names[k], tot ? 100.0 * h[k] / tot : 0.0,
+                     double(h[k]) / std::max(1.0, double(launches) * n_env));
     }
     if (stream && own_stream) cudaStreamDestroy(stream);
   }
@@ -1484,26 +975,49 @@ template <class R> struct Batch final : BatchBase {
     A.jbinc_off = jbinc.as<int>();
     A.jbinc = jbinc.as<int>() + H.nb + 1;
     A.jblk = jblk.as<int4>();
+    A.aborted_any = abany.as<int>();
+    A.counters = ctr.as<unsigned long long>();
+    A.wjinc_off = wjinc.as<int>();
+    A.wjinc = warp_path ? wjinc.as<int>() + H.nb + 1 : nullptr;
+    A.wplan = wplan;
+    A.warp_max_obj = warp_max_obj;
+    A.wlam = wlam.as<R>();
+    A.wptime = wptime.as<unsigned long long>();
+    A.mode = 0;
+    A.profile = profile ? 1 : 0;
+    ++env_steps;
     const int epb = envs_per_block;
     const int nblk = (n_env + epb - 1) / epb;
+    if (warp_path) {
+      // narrow phase + setup (no shared-memory row region), the warp solver, then the
+      // environments with more than 32 constraint objects through the object solver
+      BatchArgs<R> A1 = A;
+      A1.mode = 1;
+      A1.row_pool = 0;
+      A1.ptime = nullptr;
+      NSD_CK(launch_batch_sub<R>(16, nblk, 16 * epb, 0, stream, A1));
+      NSD_CK(launch_batch_warp<R>((n_env + warp_epb - 1) / warp_epb, 32 * warp_epb, warp_smem, stream, A));
+      A.mode = 2;
+      NSD_CK(launch_batch_sub<R>(16, nblk, 16 * epb, smem_bytes, stream, A));
+      return;
+    }
     if (team_threads <= 32) {
       const int thr = team_threads * epb;
-      switch (team_threads) {
-        case 4: k_batch_sub<R, 4><<<nblk, thr, smem_bytes, stream>>>(A); break;
-        case 8: k_batch_sub<R, 8><<<nblk, thr, smem_bytes, stream>>>(A); break;
-        case 16: k_batch_sub<R, 16><<<nblk, thr, smem_bytes, stream>>>(A); break;
-        default: k_batch_sub<R, 32><<<nblk, thr, smem_bytes, stream>>>(A); break;
-      }
+      NSD_CK(launch_batch_sub<R>(team_threads, nblk, thr, smem_bytes, stream, A));
     } else {
-      k_batch_block<R><<<n_env, team_threads, smem_bytes, stream>>>(A);
+      NSD_CK(launch_batch_block<R>(n_env, team_threads, smem_bytes, stream, A));
     }
-    NSD_CK(cudaGetLastError());
   }
   void results(int* nc, int* ab, double* fres, nsd_iter_stats* its) override {
     std::vector<int> hn(n_env), ho(n_env);
     std::vector<double> hf(8 * (size_t)n_env);
+    std::vector<int> ha(n_env);
     NSD_CK(cudaMemcpyAsync(hn.data(), ncout.p, sizeof(int) * n_env, cudaMemcpyDeviceToHost, stream));
     NSD_CK(cudaMemcpyAsync(ho.data(), ovf.p, sizeof(int) * n_env, cudaMemcpyDeviceToHost, stream));
+    NSD_CK(cudaMemcpyAsync(ha.data(), abany.p, sizeof(int) * n_env, cudaMemcpyDeviceToHost, stream));
+    // overflow and abort are sticky over the steps since the previous call: read, then clear
+    NSD_CK(cudaMemsetAsync(ovf.p, 0, sizeof(int) * n_env, stream));
+    NSD_CK(cudaMemsetAsync(abany.p, 0, sizeof(int) * n_env, stream));
     NSD_CK(cudaMemcpyAsync(hf.data(), fin.p, sizeof(double) * 8 * n_env, cudaMemcpyDeviceToHost, stream));
     std::vector<nsd::IterOut> hi;
     const int N = cfg.newton_iterations;
@@ -1515,7 +1029,7 @@ template <class R> struct Batch final : BatchBase {
     int overflow_env = -1;
     for (int e = 0; e < n_env; ++e) {
       if (nc) nc[e] = hn[e];
-      if (ab) ab[e] = hf[8 * e + 5] != 0.0;
+      if (ab) ab[e] = ha[e] != 0;
       if (fres) fres[e] = hf[8 * e];
       if (ho[e] && overflow_env < 0) overflow_env = e;
     }
@@ -1535,6 +1049,16 @@ template <class R> struct Batch final : BatchBase {
                                       std::to_string(ho[overflow_env]) + " contacts > max_contacts " +
                                       std::to_string(maxc));
   }
+  // [0] PCR iterations summed over envs and steps, [1] cycles inside the PCR loops
+  // (warp path, profile on), [2] cycles per env step (same), [3] env-steps; read and reset
+  void counters(unsigned long long* out) override {
+    NSD_CK(cudaStreamSynchronize(stream));
+    NSD_CK(cudaMemcpy(out, ctr.p, sizeof(unsigned long long) * 3, cudaMemcpyDeviceToHost));
+    out[3] = static_cast<unsigned long long>(env_steps) * n_env;
+    env_steps = 0;
+    NSD_CK(cudaMemset(ctr.p, 0, sizeof(unsigned long long) * 4));
+  }
+  void set_profile(int on) override { profile = on != 0; }
   void contacts(int env, nsd_contact* out, int* n) override {
     if (env < 0 || env >= n_env) throw NsdError(NSD_INVALID, "env out of range");
     int nc = 0;
@@ -1786,6 +1310,24 @@ int nsd_batch_copy_state_async(nsd_batch* b, void* q_dst, void* u_dst) {
   return guarded([&] {
     if (!b) throw NsdError(NSD_INVALID, "null argument");
     b->impl->copy_state_async(q_dst, u_dst);
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_counters(nsd_batch* b, uint64_t* out) {
+  return guarded([&] {
+    if (!b || !out) throw NsdError(NSD_INVALID, "null argument");
+    unsigned long long v[4];
+    b->impl->counters(v);
+    for (int i = 0; i < 4; ++i) out[i] = v[i];
+    return NSD_OK;
+  });
+}
+
+int nsd_batch_profile(nsd_batch* b, int32_t enable) {
+  return guarded([&] {
+    if (!b) throw NsdError(NSD_INVALID, "null argument");
+    b->impl->set_profile(enable);
     return NSD_OK;
   });
 }

@@ -1,0 +1,71 @@
+// Single-scene kernels (nsd_step, the newton_step boundary): one CTA for small
+// scenes, a persistent cooperative grid for the FEM configs.
+#include "nsd_plan.cuh"
+
+using namespace nsdi;
+
+template <class R, bool kTets>
+__global__ void __launch_bounds__(512) k_single_block(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out) {
+  __shared__ double red[2 * 33 * nsd::kRedMax];
+  nsd::BlockTeam t(red);
+  nsd::newton_setup(t, T, W);
+  t.sync();
+  nsd::newton_solve<R, kTets>(t, T, W, cfg, out);
+}
+
+template <class R, bool kTets, int RPT>
+__global__ void __launch_bounds__(kGridThreads) k_single_grid(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out,
+                                                     double* gpart) {
+  __shared__ double red[2 * 33 * nsd::kRedMax];
+  nsd::GridTeam t(red, gpart);
+  nsd::newton_setup(t, T, W);
+  t.sync();
+  nsd::newton_solve<R, kTets, nsd::GridTeam, RPT>(t, T, W, cfg, out);
+}
+
+
+namespace nsdi {
+
+template <class R> int single_grid_blocks_per_sm(bool tets) {
+  int per_sm = 0;
+  if (tets)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, true, 0>, kGridThreads, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_single_grid<R, false, 0>, kGridThreads, 0);
+  return per_sm;
+}
+
+template <class R>
+cudaError_t launch_single_block(bool tets, int threads, cudaStream_t s, const nsd::Topo<R>& T, const nsd::Work<R>& W,
+                                const nsd::Cfg& c, const nsd::StepOut& o) {
+  if (tets)
+    k_single_block<R, true><<<1, threads, 0, s>>>(T, W, c, o);
+  else
+    k_single_block<R, false><<<1, threads, 0, s>>>(T, W, c, o);
+  return cudaGetLastError();
+}
+
+template <class R>
+cudaError_t launch_single_grid(bool tets, bool regs, int blocks, cudaStream_t s, const nsd::Topo<R>& T,
+                               const nsd::Work<R>& W, const nsd::Cfg& c, const nsd::StepOut& o, double* gpart) {
+  nsd::Topo<R> t = T;
+  nsd::Work<R> w = W;
+  nsd::Cfg cf = c;
+  nsd::StepOut so = o;
+  void* args[] = {&t, &w, &cf, &so, &gpart};
+  void* fn = tets ? (regs ? (void*)k_single_grid<R, true, 2> : (void*)k_single_grid<R, true, 0>)
+                  : (regs ? (void*)k_single_grid<R, false, 2> : (void*)k_single_grid<R, false, 0>);
+  return cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kGridThreads), args, 0, s);
+}
+
+#define NSD_INST(R)                                                                                                \
+  template int single_grid_blocks_per_sm<R>(bool);                                                                 \
+  template cudaError_t launch_single_block<R>(bool, int, cudaStream_t, const nsd::Topo<R>&, const nsd::Work<R>&,   \
+                                              const nsd::Cfg&, const nsd::StepOut&);                               \
+  template cudaError_t launch_single_grid<R>(bool, bool, int, cudaStream_t, const nsd::Topo<R>&,                   \
+                                             const nsd::Work<R>&, const nsd::Cfg&, const nsd::StepOut&, double*);
+NSD_INST(float)
+NSD_INST(double)
+#undef NSD_INST
+
+}  // namespace nsdi

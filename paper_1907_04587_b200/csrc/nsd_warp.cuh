@@ -1,0 +1,941 @@
+// Batched rigid-body environments, one full warp per environment (C5 path).
+//
+// The same newton_step as nsd_engine.cuh (newton.cpp:321-418; PCR recurrence of
+// solvers.cpp:127-174 with z = M^-1 r updated by recursion exactly as the
+// reference), laid out for a tiny articulated scene (an ant: 9 rigid bodies,
+// 8 joints / 40 rows, ~12 contacts / 36 rows):
+//
+//   * one constraint object per lane: lane k < nj owns joint k, lane nj + c owns
+//     contact c (nj + nc <= 32; larger environments are solved by the
+//     sub-warp object solver, nsd_batch.cuh). An object owns its rows
+//     (<= 5), so every PCR row vector lives in that lane's REGISTERS: the
+//     row-parallel phases (p/ap update, trial norms, commit) touch no memory;
+//   * joints and contacts share one row form: np point rows along directions
+//     D_i through lever arms (r_a, r_b) and na axis rows along C_i, so
+//     J w and J^T y are one code path for every lane (no joint/contact
+//     divergence inside the warp). A contact is np = 3 with D = (n, d1, d2)
+//     and row scales (dphi/dC, active, active); a revolute joint np = 3 with
+//     D = (e_x, e_y, e_z) plus na = 2 axis rows;
+//   * J^T y: each object stages its two body-side wrenches in shared memory,
+//     then lane b < nb gathers body b's wrenches in a fixed order (static joint
+//     incidence, then the step's contact incidence): deterministic, no atomics;
+//     w = H^-1 J^T y goes back to shared memory for the J w pass;
+//   * reductions are xor-butterfly shuffles: every lane ends with the same bits
+//     (IEEE addition is commutative), so the data-dependent PCR exits are
+//     warp-uniform without a broadcast.
+// Shared memory per environment: body state (q, rotation cache, u, I_w^-1, w),
+// the objects' records (lever arms and row directions, [value][lane] layout,
+// conflict-free) and the staging area (14-double stride, conflict-free 16-byte
+// stores). Step-start data (q-, u-, u~, I_w, the contact set) comes from the
+// per-env slabs that the narrow-phase launch wrote (k_batch_sub, collide mode).
+#pragma once
+
+#include "nsd_engine.cuh"
+#include "nsd_warp_plan.h"
+
+namespace nsd {
+namespace wp {
+
+// Warp all-reduce, xor butterfly: identical bits on every lane.
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  return v;
+}
+__device__ __forceinline__ double wmax(double v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, m));
+  return v;
+}
+__device__ __forceinline__ void wsum2(double& a, double& b) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) {
+    const double x = __shfl_xor_sync(0xffffffffu, a, m), y = __shfl_xor_sync(0xffffffffu, b, m);
+    a += x;
+    b += y;
+  }
+}
+
+template <class R> __device__ __forceinline__ V3<R> lds3(const R* p) { return v3(p[0], p[1], p[2]); }
+template <class R> __device__ __forceinline__ void sts3(R* p, V3<R> v) {
+  p[0] = v.x;
+  p[1] = v.y;
+  p[2] = v.z;
+}
+// This lane's record (arm_a, arm_b, 5 row directions) from its [lane][stride] slot
+// with 16-byte loads; single values are stored with scalar stores (assembly).
+template <class R> struct Rec {
+  V3<R> arm_a, arm_b, d[kRows];
+};
+__device__ __forceinline__ void ld_vals(const double* p, double (&v)[22]) {
+#pragma unroll
+  for (int k = 0; k < 11; ++k) {
+    const double2 t = reinterpret_cast<const double2*>(p)[k];
+    v[2 * k] = t.x;
+    v[2 * k + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void ld_vals(const float* p, float (&v)[24]) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const float4 t = reinterpret_cast<const float4*>(p)[k];
+    v[4 * k] = t.x;
+    v[4 * k + 1] = t.y;
+    v[4 * k + 2] = t.z;
+    v[4 * k + 3] = t.w;
+  }
+}
+// One 3-vector of this lane's record (value offset v = 0, 3, ..., 18): a 16-byte
+// and an 8-byte load (for fp64; the slot's alignment alternates with v).
+template <int V> __device__ __forceinline__ V3<double> rec_v3(const double* rec, int lane) {
+  const double* p = rec + rec_stride<double>() * lane + V;
+  if constexpr (V % 2 == 0) {
+    const double2 a = *reinterpret_cast<const double2*>(p);
+    return v3(a.x, a.y, p[2]);
+  } else {
+    const double2 b = *reinterpret_cast<const double2*>(p + 1);
+    return v3(p[0], b.x, b.y);
+  }
+}
+template <int V> __device__ __forceinline__ V3<float> rec_v3(const float* rec, int lane) {
+  const float* p = rec + rec_stride<float>() * lane + V;
+  return v3(p[0], p[1], p[2]);
+}
+template <class R> __device__ __forceinline__ Rec<R> rec_load(const R* rec, int lane) {
+  Rec<R> o;
+  o.arm_a = rec_v3<0>(rec, lane);
+  o.arm_b = rec_v3<3>(rec, lane);
+  o.d[0] = rec_v3<6>(rec, lane);
+  o.d[1] = rec_v3<9>(rec, lane);
+  o.d[2] = rec_v3<12>(rec, lane);
+  o.d[3] = rec_v3<15>(rec, lane);
+  o.d[4] = rec_v3<18>(rec, lane);
+  return o;
+}
+template <class R> __device__ __forceinline__ void rec3_put(R* rec, int v, int lane, V3<R> x) {
+  R* p = rec + rec_stride<R>() * lane + v;
+  p[0] = x.x;
+  p[1] = x.y;
+  p[2] = x.z;
+}
+
+// This lane's constraint object.
+struct Obj {
+  int kind;  // joint kind 0..3, 4 contact, -1 none
+  int idx;   // joint or contact index
+  int a, b;  // bodies (-1 world)
+  int np, na, nr;
+};
+
+// Lin (unshifted 1/m, divided as the reference's BlockDiagMass::inverse_quadratic)
+// and angular (I_w^-1) quadratic forms of one body side.
+template <class R> __device__ __forceinline__ R lin_quad_unshifted(V3<R> c, R m) {
+  return c.x * c.x / m + c.y * c.y / m + c.z * c.z / m;
+}
+template <class R> __device__ __forceinline__ R lin_quad_shifted(V3<R> c, R hi) {
+  return c.x * c.x * hi + c.y * c.y * hi + c.z * c.z * hi;
+}
+
+template <class R> struct Env {
+  const Topo<R>& T;
+  R* bq;
+  R* brot;
+  R* bu;
+  R* biwi;
+  R* bhi;
+  R* bw;
+  R* stg;
+  R* rec;
+  R* x;  // [row][lane]
+  R* bx;
+  int* gent_off;  // per body: its staged wrenches (joints, then contacts ascending)
+  int* gent;
+  int nj, nc, nb;
+};
+
+// Quadratic form d^T J M^-1 J^T d of a point row along d through the arms, summed
+// in the reference's order a.lin + a.ang + b.lin + b.ang (contact_quad /
+// object_quad). shifted: H^-1 = 1/(m + 0) per linear dof; else the unshifted
+// c^2/m of BlockDiagMass::inverse_quadratic (bodies.cpp:149-177).
+template <class R>
+__device__ __forceinline__ R point_quad(const Topo<R>& T, const R* biwi, int a, int b, V3<R> d, V3<R> arm_a, V3<R> arm_b,
+                                        bool shifted) {
+  R s = R(0);
+  if (a >= 0) {
+    const R m = T.bmass[a];
+    s += shifted ? lin_quad_shifted(d, R(1) / (m + R(0))) : lin_quad_unshifted(d, m);
+    s += sym_quad(biwi + 6 * a, cross(arm_a, d));
+  }
+  if (b >= 0) {
+    const R m = T.bmass[b];
+    s += shifted ? lin_quad_shifted(d, R(1) / (m + R(0))) : lin_quad_unshifted(d, m);
+    s += sym_quad(biwi + 6 * b, cross(arm_b, d));
+  }
+  return s;
+}
+
+// J^T y of this lane's object into its staging slot: a side (f, r_a x f + tau),
+// b side (-f, -(r_b x f + tau)); f = sum_i (s_i y_i) D_i, tau = sum_i y_i C_i.
+template <class R, class YF>
+__device__ __forceinline__ void stage_f(const Env<R>& E, const Obj& o, int lane, const R (&s)[3], const YF& y) {
+  if (o.kind < 0) return;
+  V3<R> f = v3(R(0), R(0), R(0)), ta = f;
+  if (0 < o.np) f = f + (s[0] * y(0)) * rec_v3<6>(E.rec, lane);
+  if (1 < o.np) f = f + (s[1] * y(1)) * rec_v3<9>(E.rec, lane);
+  if (2 < o.np) f = f + (s[2] * y(2)) * rec_v3<12>(E.rec, lane);
+  if (0 >= o.np && 0 < o.nr) ta = ta + y(0) * rec_v3<6>(E.rec, lane);
+  if (1 >= o.np && 1 < o.nr) ta = ta + y(1) * rec_v3<9>(E.rec, lane);
+  if (2 >= o.np && 2 < o.nr) ta = ta + y(2) * rec_v3<12>(E.rec, lane);
+  if (3 < o.nr) ta = ta + y(3) * rec_v3<15>(E.rec, lane);
+  if (4 < o.nr) ta = ta + y(4) * rec_v3<18>(E.rec, lane);
+  R* d = E.stg + kStg * lane;
+  if (o.a >= 0) {
+    sts3(d, f);
+    sts3(d + 3, cross(rec_v3<0>(E.rec, lane), f) + ta);
+  }
+  if (o.b >= 0) {
+    sts3(d + 6, -f);
+    sts3(d + 9, -(cross(rec_v3<3>(E.rec, lane), f) + ta));
+  }
+}
+
+template <class R>
+__device__ __forceinline__ void stage(const Env<R>& E, const Obj& o, int lane, const R (&s)[3], const R (&y)[kRows]) {
+  stage_f(E, o, lane, s, [&](int i) { return y[i]; });
+}
+
+// Body gather of the staged wrenches (joints first, then contacts ascending).
+template <class R> __device__ __forceinline__ void gather(const Env<R>& E, int b, V3<R>& lin, V3<R>& ang) {
+  lin = v3(R(0), R(0), R(0));
+  ang = lin;
+  for (int e = E.gent_off[b]; e < E.gent_off[b + 1]; ++e) {
+    const R* s = E.stg + E.gent[e];
+    lin = lin + lds3(s);
+    ang = ang + lds3(s + 3);
+  }
+}
+
+// One component k of body b's gathered J^T y: the body's staged wrenches summed in
+// entry order (the order of gather()); the offsets and values of four entries are
+// loaded before their ordered adds.
+template <class R> __device__ __forceinline__ R gather_comp(const Env<R>& E, int b, int k) {
+  const int e0 = E.gent_off[b], n = E.gent_off[b + 1] - e0;
+  const int* ge = E.gent + e0;
+  const R* sk = E.stg + k;
+  R acc = R(0);
+  int e = 0;
+  for (; e + 4 <= n; e += 4) {
+    const int o0 = ge[e], o1 = ge[e + 1], o2 = ge[e + 2], o3 = ge[e + 3];
+    const R v0 = sk[o0], v1 = sk[o1], v2 = sk[o2], v3 = sk[o3];
+    acc = acc + v0;
+    acc = acc + v1;
+    acc = acc + v2;
+    acc = acc + v3;
+  }
+  for (; e < n; ++e) acc = acc + sk[ge[e]];
+  return acc;
+}
+
+// w = H^-1 J^T y for every body with the whole warp: 5 bodies per round, lane
+// 6 g + k owns component k of body 5 r + g. Linear rows scale by 1/m; angular row
+// k - 3 applies I_w^-1 (sym_mul's expression) to the torque held by the group's
+// lanes 3..5, exchanged by shuffles. Needs __syncwarp() before (staging) and after.
+template <class R> __device__ __forceinline__ void bodies_w(const Env<R>& E, int lane) {
+  const int g = lane / 6, k = lane - 6 * g;
+  const int g3 = 6 * g + 3;
+  for (int b0 = 0; b0 < E.nb; b0 += 5) {
+    const int b = b0 + g;
+    const bool on = g < 5 && b < E.nb;
+    const R t = on ? gather_comp(E, b, k) : R(0);
+    const R tx = __shfl_sync(0xffffffffu, t, g3 < 32 ? g3 : 0);
+    const R ty = __shfl_sync(0xffffffffu, t, g3 + 1 < 32 ? g3 + 1 : 0);
+    const R tz = __shfl_sync(0xffffffffu, t, g3 + 2 < 32 ? g3 + 2 : 0);
+    if (on) {
+      R w;
+      if (k < 3) {
+        w = t * E.bhi[b];
+      } else {
+        const R* s6 = E.biwi + 6 * b;  // xx yy zz xy xz yz; row k - 3 of sym_mul
+        const int r = k - 3;
+        const R c0 = r == 0 ? s6[0] : (r == 1 ? s6[3] : s6[4]);
+        const R c1 = r == 0 ? s6[3] : (r == 1 ? s6[1] : s6[5]);
+        const R c2 = r == 0 ? s6[4] : (r == 1 ? s6[5] : s6[2]);
+        w = c0 * tx + c1 * ty + c2 * tz;
+      }
+      E.bw[6 * b + k] = w;
+    }
+  }
+}
+
+template <class R>
+__device__ __forceinline__ void jw(const Env<R>& E, const Obj& o, int lane, const R (&s)[3], R (&out)[kRows]) {
+  V3<R> dv = v3(R(0), R(0), R(0)), wr = dv;
+  if (o.a >= 0) {
+    const R* w = E.bw + 6 * o.a;
+    wr = lds3(w + 3);
+    dv = lds3(w) + cross(wr, rec_v3<0>(E.rec, lane));
+  }
+  if (o.b >= 0) {
+    const R* w = E.bw + 6 * o.b;
+    const V3<R> wb = lds3(w + 3);
+    dv = dv - lds3(w);
+    dv = dv - cross(wb, rec_v3<3>(E.rec, lane));
+    wr = wr - wb;
+  }
+  auto row = [&](int i, V3<R> d) {
+    if (i < o.np) {
+      const R t = dot(d, dv);
+      return s[i] == R(0) ? R(0) : s[i] * t;
+    }
+    return i < o.nr ? dot(d, wr) : R(0);
+  };
+  out[0] = row(0, rec_v3<6>(E.rec, lane));
+  out[1] = row(1, rec_v3<9>(E.rec, lane));
+  out[2] = row(2, rec_v3<12>(E.rec, lane));
+  out[3] = 3 < o.nr ? dot(rec_v3<15>(E.rec, lane), wr) : R(0);
+  out[4] = 4 < o.nr ? dot(rec_v3<18>(E.rec, lane), wr) : R(0);
+}
+
+// J_i H^-1 J_i^T (shifted H; rigid bodies carry no shift) for this lane's rows.
+template <class R> __device__ __forceinline__ void quads(const Env<R>& E, const Obj& o, int lane, const R (&s)[3], R (&q)[kRows]) {
+  const Rec<R> rc = rec_load(E.rec, lane);
+#pragma unroll
+  for (int i = 0; i < kRows; ++i) {
+    q[i] = R(0);
+    if (i < o.np) {
+      if (s[i] != R(0)) q[i] = point_quad(E.T, E.biwi, o.a, o.b, s[i] * rc.d[i], rc.arm_a, rc.arm_b, true);
+    } else if (i < o.nr) {
+      R t = R(0);
+      if (o.a >= 0) t += sym_quad(E.biwi + 6 * o.a, rc.d[i]);
+      if (o.b >= 0) t += sym_quad(E.biwi + 6 * o.b, rc.d[i]);
+      q[i] = t;
+    }
+  }
+}
+
+// Assembly of this lane's object at the current iterate (newton.cpp:100-231):
+// writes the record (arms, row directions), the row scales s, h and the C
+// diagonal per row, and accumulates the telemetry maxima / |h|^2.
+template <class R>
+__device__ __forceinline__ void assemble_obj(const Env<R>& E, const Obj& o, int lane, const R* jframe, const R* jparam,
+                                             const R* cgeo, R h, const Cfg& cfg, const R (&lam)[kRows], R (&s)[3],
+                                             R (&hv)[kRows], R (&cd)[kRows], AsmStats& st) {
+  s[0] = s[1] = s[2] = R(1);
+  if (o.kind < 0) return;
+  auto pos = [&](int b) { return lds3(E.bq + 8 * b); };
+  auto rot = [&](int b) {
+    M3<R> m;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) m.a[i] = E.brot[9 * b + i];
+    return m;
+  };
+  if (o.kind == 4) {  // contact rows (newton.cpp:166-218)
+    const R* g = cgeo + 17 * o.idx;
+    const V3<R> la = lds3(g), lb = lds3(g + 3), n = lds3(g + 6), d1 = lds3(g + 9), d2 = lds3(g + 12);
+    const R thick = g[15], mu = g[16];
+    V3<R> pa = la, pb = lb, ra = v3(R(0), R(0), R(0)), rb = ra;
+    if (o.a >= 0) {
+      ra = mul(rot(o.a), la);
+      pa = pos(o.a) + ra;
+    }
+    if (o.b >= 0) {
+      rb = mul(rot(o.b), lb);
+      pb = pos(o.b) + rb;
+    }
+    rec3_put(E.rec, 0, lane, ra);
+    rec3_put(E.rec, 3, lane, rb);
+    rec3_put(E.rec, 6, lane, n);
+    rec3_put(E.rec, 9, lane, d1);
+    rec3_put(E.rec, 12, lane, d2);
+    const R gap = dot(n, pa - pb) - thick;
+    const R lam_n = lam[0] / h;
+    const R rn = r_factor(point_quad(E.T, E.biwi, o.a, o.b, n, ra, rb, false), h, true, cfg.r_strategy);
+    const PhiV<R> phi = phi_n(gap, lam_n, rn, cfg.ncp_kind);
+    const R hn = phi.v / h;
+    hv[0] = hn;
+    cd[0] = phi.dl / (h * h);
+    s[0] = phi.dc;  // normal J row kept iff dphi/dC != 0 (newton.cpp:187)
+    st.comp = fmax(st.comp, (double)ab(mn(gap, lam_n)));
+    const R lf0 = lam[1] / h, lf1 = lam[2] / h;
+    const R mu_ln = mu * lam_n;
+    const R lfn = sqrt(lf0 * lf0 + lf1 * lf1);
+    st.cone = fmax(st.cone, (double)mx(R(0), lfn - mu_ln));
+    R h1, h2;
+    if (mu_ln > R(0)) {  // friction active (newton.cpp:200-210)
+      V3<R> dv = v3(R(0), R(0), R(0));
+      if (o.a >= 0) dv = lds3(E.bu + 6 * o.a) + cross(lds3(E.bu + 6 * o.a + 3), ra);
+      if (o.b >= 0) {
+        dv = dv - lds3(E.bu + 6 * o.b);
+        dv = dv - cross(lds3(E.bu + 6 * o.b + 3), rb);
+      }
+      const R v0 = dot(d1, dv), v1 = dot(d2, dv);
+      const R q1 = point_quad(E.T, E.biwi, o.a, o.b, d1, ra, rb, false);
+      const R q2 = point_quad(E.T, E.biwi, o.a, o.b, d2, ra, rb, false);
+      const R rf = r_factor(R(0.5) * (q1 + q2), h, false, cfg.r_strategy);
+      const R wv = friction_W(sqrt(v0 * v0 + v1 * v1), lfn, mu_ln, rf, cfg.ncp_kind);
+      h1 = v0 + wv * lf0;
+      h2 = v1 + wv * lf1;
+      cd[1] = cd[2] = wv / h;
+      s[1] = s[2] = R(1);
+    } else {
+      h1 = lf0;
+      h2 = lf1;
+      cd[1] = cd[2] = R(1) / h;
+      s[1] = s[2] = R(0);
+    }
+    hv[1] = h1;
+    hv[2] = h2;
+    st.hmax = fmax(st.hmax, fmax((double)ab(hn), fmax((double)ab(h1), (double)ab(h2))));
+    st.hsq += (double)hn * hn + (double)h1 * h1 + (double)h2 * h2;
+    return;
+  }
+  // joint rows (constraints.cpp:141-220; newton.cpp:118-128)
+  const int j = o.idx, kind = o.kind;
+  const R* fr = jframe + 21 * j;
+  const V3<R> anc_a = lds3(fr), anc_b = lds3(fr + 3), ax_a = lds3(fr + 6), ax_a2 = lds3(fr + 9), ax_b1 = lds3(fr + 12),
+              ax_b2 = lds3(fr + 15), rest = lds3(fr + 18);
+  const M3<R> Ra = o.a >= 0 ? rot(o.a) : m3_identity<R>(), Rb = o.b >= 0 ? rot(o.b) : m3_identity<R>();
+  V3<R> wa = anc_a, wb = anc_b, ra = v3(R(0), R(0), R(0)), rb = ra;
+  if (o.a >= 0) {
+    ra = mul(Ra, anc_a);
+    wa = pos(o.a) + ra;
+  }
+  if (o.b >= 0) {
+    rb = mul(Rb, anc_b);
+    wb = pos(o.b) + rb;
+  }
+  const R comp = jparam[2 * j];
+  const R e_bend = jparam[2 * j + 1] > R(0) ? R(1) / jparam[2 * j + 1] : R(0);
+  const V3<R> axw = o.a < 0 ? ax_a : mul(Ra, ax_a);
+  rec3_put(E.rec, 0, lane, kind == 2 && o.a >= 0 ? ra - (wa - wb) : ra);  // prismatic: (r_a - t) x d
+  rec3_put(E.rec, 3, lane, rb);
+  auto emit = [&](int k, R value, R e) {
+    const R hk = (value + e * (lam[k] / h)) / h;
+    hv[k] = hk;
+    cd[k] = e / (h * h);
+    st.hmax = fmax(st.hmax, (double)ab(hk));
+    st.hsq += (double)hk * (double)hk;
+  };
+  auto point = [&](int k, V3<R> d, R value) {
+    rec3_put(E.rec, 6 + 3 * k, lane, d);
+    emit(k, value, comp);
+  };
+  auto axis = [&](int k, V3<R> xa, V3<R> xb, R restv, R e) {
+    rec3_put(E.rec, 6 + 3 * k, lane, cross(xa, xb));
+    emit(k, dot(xa, xb) - restv, e);
+  };
+  const V3<R> e0 = v3(R(1), R(0), R(0)), e1 = v3(R(0), R(1), R(0)), e2 = v3(R(0), R(0), R(1));
+  if (kind == 0 || kind == 1) {
+    point(0, e0, wa.x - wb.x);
+    point(1, e1, wa.y - wb.y);
+    point(2, e2, wa.z - wb.z);
+    if (kind == 1) {
+      const V3<R> b1 = o.b < 0 ? ax_b1 : mul(Rb, ax_b1), b2 = o.b < 0 ? ax_b2 : mul(Rb, ax_b2);
+      axis(3, axw, b1, rest.x, comp);
+      axis(4, axw, b2, rest.y, comp);
+    }
+  } else if (kind == 2) {
+    int sm = 0;  // tangent_basis(axis) (constraints.cpp:93-101)
+    if (ab(axw.y) < ab(axw.x)) sm = 1;
+    if (ab(axw.z) < ab(axw[sm])) sm = 2;
+    V3<R> ee = v3(R(0), R(0), R(0));
+    ee[sm] = R(1);
+    const V3<R> t1 = normalize(ee - dot(ee, axw) * axw);
+    const V3<R> t2 = cross(axw, t1);
+    const V3<R> d = wa - wb;
+    point(0, t1, dot(t1, d));
+    point(1, t2, dot(t2, d));
+    const V3<R> a2 = o.a < 0 ? ax_a2 : mul(Ra, ax_a2);
+    const V3<R> b1 = o.b < 0 ? ax_b1 : mul(Rb, ax_b1), b2 = o.b < 0 ? ax_b2 : mul(Rb, ax_b2);
+    axis(2, axw, b1, rest.x, comp);
+    axis(3, axw, b2, rest.y, comp);
+    axis(4, a2, b2, rest.z, comp);
+  } else {
+    const V3<R> b1 = o.b < 0 ? ax_b1 : mul(Rb, ax_b1), b2 = o.b < 0 ? ax_b2 : mul(Rb, ax_b2);
+    axis(0, axw, b1, rest.x, e_bend);
+    axis(1, axw, b2, rest.y, e_bend);
+  }
+}
+
+// Refresh the rotation cache of body b from its quaternion.
+template <class R> __device__ __forceinline__ void refresh_rot(const Env<R>& E, int b) {
+  const R* t = E.bq + 8 * b + 3;
+  const M3<R> m = quat_rot(t[0], t[1], t[2], t[3]);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) E.brot[9 * b + i] = m.a[i];
+}
+
+// Inputs/outputs of one environment's step (views into the batch's slabs).
+template <class R> struct EnvIO {
+  const R* q0;     // step-start coordinates (cold slab)
+  const R* u0;     // step-start velocities
+  const R* ut;     // unconstrained velocity u~ (newton_setup in the narrow-phase launch)
+  const R* iw6;    // I_w per rigid dof3 block (cold), sym 6
+  const R* iwi6;   // I_w^-1 per rigid dof3 block (hot)
+  const int* cbody;
+  const R* cgeo;
+  R* lam;          // [row][lane] multipliers, 5 x 32 (global scratch, per Newton iteration)
+  const int* jinc_off;  // static joint incidence per body: joint * 2 + side (both sides)
+  const int* jinc;
+  R* g;            // ndof scratch (cold)
+  R* du;           // ndof scratch (cold)
+  R* qs;           // persistent state (out)
+  R* us;
+  R* q_out;        // optional mapped host copies
+  R* u_out;
+  R* xlam;         // exported multipliers (reference row order)
+  int* xcbody;
+  double* fin;     // 8
+  IterOut* iters;  // newton_iterations or null
+  unsigned long long* cr_iters;  // sum of PCR iterations (batch counter) or null
+  unsigned long long* cr_cycles; // clock64 cycles inside the PCR loops (lane 0) or null
+  unsigned long long* env_cycles;
+  unsigned long long* phase;     // kWPhases counters (NSD_PHASE_TIMING) or null
+};
+
+// Diagnostics (NSD_PHASE_TIMING): lane 0's clock64 cycles per solver phase.
+struct WClock {
+  unsigned long long* dst;
+  long long t0;
+  __device__ explicit WClock(unsigned long long* d) : dst(d), t0(0) {
+    if (dst) t0 = clock64();
+  }
+  __device__ __forceinline__ void mark(int k) {
+    if (dst) {
+      const long long t = clock64();
+      atomicAdd(dst + k, static_cast<unsigned long long>(t - t0));
+      t0 = t;
+    }
+  }
+};
+
+// Lane-private row vector in shared memory ([row][lane]).
+template <class R> __device__ __forceinline__ void rows_load(const R* v, int lane, R (&o)[kRows]) {
+#pragma unroll
+  for (int i = 0; i < kRows; ++i) o[i] = v[32 * i + lane];
+}
+
+// Body b's gradient block g = M~(u - u~) - J^T lambda (after staging lambda);
+// accumulates residual_inf / |g|^2 in the reference's order (bodies rigid).
+template <class R>
+__device__ __forceinline__ void body_grad(const Topo<R>& T, const Env<R>& E, const EnvIO<R>& io, int b, V3<R>& gl,
+                                          V3<R>& ga, double& gmax, double& gsq) {
+  const int d = T.bdof[b];
+  V3<R> jl, ja;
+  gather(E, b, jl, ja);
+  const R m = T.bmass[b];
+  const V3<R> du = lds3(E.bu + 6 * b) - lds3(io.ut + d);
+  gl = v3(m * du.x, m * du.y, m * du.z) - jl;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    gmax = fmax(gmax, (double)(ab(gl[k]) / m));
+    gsq += (double)gl[k] * (double)gl[k];
+  }
+  const R* s6 = io.iw6 + 6 * (d / 3 + 1);
+  const V3<R> da = lds3(E.bu + 6 * b + 3) - lds3(io.ut + d + 3);
+  ga = sym_mul(s6, da) - ja;
+  gmax = fmax(gmax, fmax((double)(ab(ga.x) / s6[0]), fmax((double)(ab(ga.y) / s6[1]), (double)(ab(ga.z) / s6[2]))));
+  gsq += (double)ga.x * ga.x + (double)ga.y * ga.y + (double)ga.z * ga.z;
+}
+
+template <class R>
+__device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h, Env<R>& E, const EnvIO<R>& io,
+                          int lane) {
+  const int nb = T.nb, nj = T.nj, nc = E.nc;
+  const long long t_env0 = io.env_cycles ? clock64() : 0;
+  WClock pc(lane == 0 ? io.phase : nullptr);
+  // ---- step-start state into shared memory: q = q-, u = 0 (zero start, newton.cpp:327-338)
+  if (lane < nb) {
+    const int b = lane, cdd = T.bcoord[b], d = T.bdof[b];
+    R* q = E.bq + 8 * b;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) q[k] = io.q0[cdd + k];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      E.bu[6 * b + k] = R(0);
+      E.biwi[6 * b + k] = io.iwi6[6 * (d / 3 + 1) + k];
+    }
+    refresh_rot(E, b);
+    E.bhi[b] = R(1) / (T.bmass[b] + R(0));
+    // body b's staged wrenches: its joints' sides, then its contacts' sides ascending
+    const int nji = io.jinc_off[b + 1] - io.jinc_off[b];
+    int n = nji;
+    for (int c = 0; c < nc; ++c) n += (io.cbody[2 * c] == b) + (io.cbody[2 * c + 1] == b);
+    E.gent_off[b + 1] = n;
+  }
+#pragma unroll
+  for (int i = 0; i < kRows; ++i) {
+    io.lam[32 * i + lane] = R(0);
+    E.x[32 * i + lane] = R(0);
+    E.bx[32 * i + lane] = R(0);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    E.gent_off[0] = 0;
+    for (int b = 0; b < nb; ++b) E.gent_off[b + 1] += E.gent_off[b];
+  }
+  __syncwarp();
+  if (lane < nb) {
+    int o = E.gent_off[lane];
+    for (int e = io.jinc_off[lane]; e < io.jinc_off[lane + 1]; ++e) {
+      const int ent = io.jinc[e];  // joint * 2 + side
+      E.gent[o++] = kStg * (ent >> 1) + 6 * (ent & 1);
+    }
+    for (int c = 0; c < nc; ++c) {
+      if (io.cbody[2 * c] == lane) E.gent[o++] = kStg * (nj + c);
+      if (io.cbody[2 * c + 1] == lane) E.gent[o++] = kStg * (nj + c) + 6;
+    }
+  }
+  // ---- this lane's object and its rows in the reference layout (newton.cpp:18-41)
+  Obj o{};
+  o.kind = -1;
+  o.idx = 0;
+  o.a = o.b = -1;
+  o.np = o.na = o.nr = 0;
+  int row0 = 0, row1 = 0;  // joint: rows row0..; contact: normal row0, friction row1, row1 + 1
+  if (lane < nj) {
+    o.kind = T.jkind[lane];
+    o.idx = lane;
+    o.a = T.jbody[2 * lane];
+    o.b = T.jbody[2 * lane + 1];
+    o.np = o.kind <= 1 ? 3 : (o.kind == 2 ? 2 : 0);
+    o.nr = joint_nrows(o.kind);
+    o.na = o.nr - o.np;
+    row0 = T.jrow[lane];
+    row1 = row0 + 1;
+  } else if (lane < nj + nc) {
+    const int c = lane - nj;
+    o.kind = 4;
+    o.idx = c;
+    o.a = io.cbody[2 * c];
+    o.b = io.cbody[2 * c + 1];
+    o.np = o.nr = 3;
+    row0 = T.rows_static + c;
+    row1 = T.rows_static + nc + 2 * c;
+  }
+  const R eps = R(cfg.epsilon_reg), tfrac = R(cfg.step_fraction);
+  const int maxlin = cfg.linear_max_iterations;
+  R s[3], cd[kRows], lam[kRows];
+  long long cr_cyc = 0;
+  unsigned cr_it = 0;
+  int n_done = 0, aborted = 0;
+  __syncwarp();
+  for (int it = 0; it < cfg.newton_iterations; ++it) {
+    // ---- assemble (rotation cache refreshed after every integration)
+    R hv[kRows];
+    AsmStats as{0.0, 0.0, 0.0, 0.0};
+    pc.mark(0);
+    rows_load(io.lam, lane, lam);
+    assemble_obj(E, o, lane, jframe, T.jparam, io.cgeo, h, cfg, lam, s, hv, cd, as);
+    pc.mark(1);
+    // ---- g = M~(u - u~) - J^T lambda; H^-1 = M~^-1 (no shift on rigid dofs); w = H^-1 g
+    stage(E, o, lane, s, lam);
+    __syncwarp();
+    double gmax = 0.0, gsq = 0.0;
+    if (lane < nb) {
+      const int b = lane, d = T.bdof[b];
+      V3<R> gl, ga;
+      body_grad(T, E, io, b, gl, ga, gmax, gsq);
+      sts3(io.g + d, gl);
+      sts3(io.g + d + 3, ga);
+      const R hi = E.bhi[b];
+      R* w = E.bw + 6 * b;
+      sts3(w, v3(gl.x * hi, gl.y * hi, gl.z * hi));
+      sts3(w + 3, sym_mul(E.biwi + 6 * b, ga));
+    }
+    double s_g = gsq, s_h = as.hsq;
+    wsum2(s_g, s_h);
+    IterOut st;
+    st.residual_inf = wmax(fmax(gmax, as.hmax));
+    st.merit_l2 = sqrt(s_g + s_h);
+    st.comp_error_max = wmax(as.comp);
+    st.cone_violation_max = wmax(as.cone);
+    st.linear_iterations = 0;
+    st.linear_residual = 0.0;
+    st.linear_breakdown = 0;
+    st.step_size = 0.0;
+    __syncwarp();
+    pc.mark(2);
+    // ---- Schur rhs b = J H^-1 g - h, diagonal preconditioner, r = b, x = 0, z = M^-1 r
+    R r[kRows], z[kRows], p[kRows], ap[kRows], az[kRows], inv[kRows];
+    {
+      R jwv[kRows], qd[kRows];
+      jw(E, o, lane, s, jwv);
+      quads(E, o, lane, s, qd);
+      double rr = 0.0, rzr = 0.0;
+#pragma unroll
+      for (int i = 0; i < kRows; ++i) {
+        p[i] = ap[i] = az[i] = R(0);
+        inv[i] = r[i] = z[i] = R(0);
+        E.x[32 * i + lane] = R(0);
+        E.bx[32 * i + lane] = R(0);
+        if (i < o.nr) {
+          const R bi = jwv[i] - hv[i];
+          R iv = R(1);
+          if (cfg.preconditioner == 1) {
+            const R sd = qd[i] + cd[i] + eps;
+            iv = sd > R(0) ? R(1) / sd : R(1);
+          }
+          inv[i] = iv;
+          r[i] = bi;
+          z[i] = iv * bi;
+          rr += (double)bi * bi;
+          rzr += (double)bi * (double)(iv * bi);
+        }
+      }
+      wsum2(rr, rzr);
+      pc.mark(3);
+      double hist_last = sqrt(rr), phist_last = sqrt(rzr), best_res = hist_last;
+      int lin_used = 0, breakdown = 0;
+      const long long tc0 = io.cr_cycles ? clock64() : 0;
+      if (maxlin > 0 && hist_last > cfg.linear_tolerance) {
+        // az = A z, zaz = z . az (solvers.cpp PCR setup)
+        stage(E, o, lane, s, z);
+        __syncwarp();
+        bodies_w(E, lane);
+        __syncwarp();
+        R jz[kRows];
+        jw(E, o, lane, s, jz);
+        double za = 0.0;
+#pragma unroll
+        for (int i = 0; i < kRows; ++i)
+          if (i < o.nr) {
+            az[i] = jz[i] + cd[i] * z[i] + eps * z[i];
+            za += (double)z[i] * az[i];
+          }
+        double zaz = wsum(za), beta = 0.0;
+        pc.mark(4);
+        for (int itl = 0; itl < maxlin && hist_last > cfg.linear_tolerance; ++itl) {
+          // p = z + beta p, ap = az + beta ap; den = ap . M^-1 ap
+          const R rb = R(beta);
+          double den = 0.0;
+#pragma unroll
+          for (int i = 0; i < kRows; ++i)
+            if (i < o.nr) {
+              if (itl == 0) {
+                p[i] = z[i];
+                ap[i] = az[i];
+              } else {
+                p[i] = z[i] + rb * p[i];
+                ap[i] = az[i] + rb * ap[i];
+              }
+              den += (double)ap[i] * (double)(inv[i] * ap[i]);
+            }
+          den = wsum(den);
+          pc.mark(5);
+          if (fabs(den) < 1e-300) {
+            breakdown = 1;
+            break;
+          }
+          const R ra = R(zaz / den);
+          // trial r' = r - a ap, z' = z - a M^-1 ap and its norms; J^T z' staged
+          // speculatively in the same pass (a rejected trial discards it)
+          double pn2 = 0.0, rn2 = 0.0;
+#pragma unroll
+          for (int i = 0; i < kRows; ++i)
+            if (i < o.nr) {
+              const R rv = r[i] - ra * ap[i];
+              pn2 += (double)rv * (double)(inv[i] * rv);
+              rn2 += (double)rv * rv;
+            }
+          const bool zaz_ok = fabs(zaz) >= 1e-300;
+          if (zaz_ok) stage_f(E, o, lane, s, [&](int i) { return z[i] - ra * (inv[i] * ap[i]); });
+          wsum2(pn2, rn2);
+          pc.mark(6);
+          const double pn = sqrt(pn2);
+          if (pn > phist_last) break;  // monotone guard (no breakdown flag)
+          hist_last = sqrt(rn2);
+          phist_last = pn;
+          const bool best = hist_last < best_res;
+          if (best) best_res = hist_last;
+#pragma unroll
+          for (int i = 0; i < kRows; ++i) {  // accept: the trial's expressions, same bits
+            const R xi = E.x[32 * i + lane] + ra * p[i];
+            E.x[32 * i + lane] = xi;
+            if (best) E.bx[32 * i + lane] = xi;
+            r[i] = r[i] - ra * ap[i];
+            z[i] = z[i] - ra * (inv[i] * ap[i]);
+          }
+          pc.mark(7);
+          lin_used = itl + 1;
+          if (!zaz_ok) {
+            breakdown = 1;
+            break;
+          }
+          __syncwarp();
+          bodies_w(E, lane);
+          __syncwarp();
+          pc.mark(8);
+          R jz2[kRows];
+          jw(E, o, lane, s, jz2);
+          double za2 = 0.0;
+#pragma unroll
+          for (int i = 0; i < kRows; ++i)
+            if (i < o.nr) {
+              az[i] = jz2[i] + cd[i] * z[i] + eps * z[i];
+              za2 += (double)z[i] * az[i];
+            }
+          za2 = wsum(za2);
+          beta = za2 / zaz;
+          zaz = za2;
+          pc.mark(9);
+        }
+      }
+      if (io.cr_cycles) cr_cyc += clock64() - tc0;
+      pc.mark(3);
+      cr_it += lin_used;
+      st.linear_iterations = lin_used;
+      st.linear_breakdown = breakdown;
+      st.linear_residual = hist_last;
+    }
+    // ---- du = H^-1 (J^T dlambda - g); NaN check (newton.cpp:295,362-369)
+    R bx[kRows];
+    rows_load(E.bx, lane, bx);
+    double dl2 = 0.0, du2 = 0.0, bad = 0.0;
+#pragma unroll
+    for (int i = 0; i < kRows; ++i)
+      if (i < o.nr) {
+        dl2 += (double)bx[i] * bx[i];
+        if (!isfinite(bx[i])) bad = 1.0;
+      }
+    __syncwarp();
+    stage(E, o, lane, s, bx);
+    __syncwarp();
+    if (lane < nb) {
+      const int b = lane, d = T.bdof[b];
+      V3<R> lin, ang;
+      gather(E, b, lin, ang);
+      const R hi = E.bhi[b];
+      const V3<R> rl = lin - lds3(io.g + d);
+      const V3<R> dl = v3(rl.x * hi, rl.y * hi, rl.z * hi);
+      const V3<R> da = sym_mul(E.biwi + 6 * b, ang - lds3(io.g + d + 3));
+      du2 += (double)dl.x * dl.x + (double)dl.y * dl.y + (double)dl.z * dl.z;
+      du2 += (double)da.x * da.x + (double)da.y * da.y + (double)da.z * da.z;
+      if (!isfinite(dl.x) || !isfinite(dl.y) || !isfinite(dl.z) || !isfinite(da.x) || !isfinite(da.y) ||
+          !isfinite(da.z))
+        bad = 1.0;
+      sts3(io.du + d, dl);
+      sts3(io.du + d + 3, da);
+    }
+    wsum2(dl2, du2);
+    bad = wmax(bad);
+    pc.mark(10);
+    if (bad != 0.0) {  // rollback to q-, u- (newton.cpp:362-369)
+      if (lane == 0 && io.iters) io.iters[it] = st;
+      aborted = 1;
+      n_done = it + 1;
+      break;
+    }
+    // ---- damped update + integration (newton.cpp:393-396; bodies.cpp:58-86)
+#pragma unroll
+    for (int i = 0; i < kRows; ++i) io.lam[32 * i + lane] = lam[i] + tfrac * bx[i];
+    if (lane < nb) {
+      const int b = lane, d = T.bdof[b], cdd = T.bcoord[b];
+      R* u = E.bu + 6 * b;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) u[k] += tfrac * io.du[d + k];
+      R* q = E.bq + 8 * b;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) q[k] = io.q0[cdd + k] + h * u[k];
+      const R t0 = q[3], t1 = q[4], t2 = q[5], t3 = q[6];
+      const R ox = u[3], oy = u[4], oz = u[5];
+      R nq[4];
+      nq[0] = io.q0[cdd + 3] + h * (R(0.5) * (-t1 * ox - t2 * oy - t3 * oz));
+      nq[1] = io.q0[cdd + 4] + h * (R(0.5) * (t0 * ox + t3 * oy - t2 * oz));
+      nq[2] = io.q0[cdd + 5] + h * (R(0.5) * (-t3 * ox + t0 * oy + t1 * oz));
+      nq[3] = io.q0[cdd + 6] + h * (R(0.5) * (t2 * ox - t1 * oy + t0 * oz));
+      const R nn = sqrt(nq[0] * nq[0] + nq[1] * nq[1] + nq[2] * nq[2] + nq[3] * nq[3]);
+      if ((double)nn < 1e-300) {
+        nq[0] = R(1);
+        nq[1] = nq[2] = nq[3] = R(0);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nq[k] = nq[k] / nn;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q[3 + k] = nq[k];
+      refresh_rot(E, b);
+    }
+    st.step_size = (double)tfrac * sqrt(du2 + dl2);
+    if (lane == 0 && io.iters) io.iters[it] = st;
+    n_done = it + 1;
+    __syncwarp();
+    pc.mark(11);
+  }
+  if (aborted) {
+    if (lane < nb) {  // q = q-, u = u-
+      const int b = lane, cdd = T.bcoord[b], d = T.bdof[b];
+#pragma unroll
+      for (int k = 0; k < 7; ++k) E.bq[8 * b + k] = io.q0[cdd + k];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) E.bu[6 * b + k] = io.u0[d + k];
+    }
+    if (lane == 0) {
+      io.fin[5] = 1.0;
+      io.fin[6] = 0.0;
+      io.fin[7] = n_done;
+    }
+  } else {
+    // ---- final assembly for classification and telemetry (newton.cpp:409-416)
+    R hv[kRows];
+    AsmStats fs{0.0, 0.0, 0.0, 0.0};
+    rows_load(io.lam, lane, lam);
+    assemble_obj(E, o, lane, jframe, T.jparam, io.cgeo, h, cfg, lam, s, hv, cd, fs);
+    stage(E, o, lane, s, lam);
+    __syncwarp();
+    double gmax = 0.0, gsq = 0.0;
+    if (lane < nb) {
+      V3<R> gl, ga;
+      body_grad(T, E, io, lane, gl, ga, gmax, gsq);
+    }
+    double mgap = __builtin_huge_val();
+    if (o.kind == 4) {
+      const R* g = io.cgeo + 17 * o.idx;
+      const Rec<R> rc = rec_load(E.rec, lane);
+      const V3<R> pa = o.a < 0 ? lds3(g) : lds3(E.bq + 8 * o.a) + rc.arm_a;
+      const V3<R> pb = o.b < 0 ? lds3(g + 3) : lds3(E.bq + 8 * o.b) + rc.arm_b;
+      mgap = (double)(dot(lds3(g + 6), pa - pb) - g[15]);
+    }
+    const double fr = wmax(fmax(gmax, fs.hmax)), fcomp = wmax(fs.comp), fcone = wmax(fs.cone);
+    mgap = -wmax(-mgap);
+    if (lane == 0) {
+      io.fin[0] = fr;
+      io.fin[1] = fcomp;
+      io.fin[2] = fcone;
+      io.fin[3] = nc ? mgap : 0.0;
+      io.fin[4] = 0.0;  // no geometric-stiffness shift on rigid dofs (newton.cpp:316-317)
+      io.fin[5] = 0.0;
+      io.fin[6] = fr < cfg.newton_tolerance ? 1.0 : 0.0;
+      io.fin[7] = n_done;
+    }
+  }
+  __syncwarp();
+  pc.mark(12);
+  // ---- write-back: state, mapped host copies, multipliers in the reference row order
+  if (lane < nb) {
+    const int b = lane, cdd = T.bcoord[b], d = T.bdof[b];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) io.qs[cdd + k] = E.bq[8 * b + k];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) io.us[d + k] = E.bu[6 * b + k];
+    if (io.q_out)
+#pragma unroll
+      for (int k = 0; k < 7; ++k) io.q_out[cdd + k] = E.bq[8 * b + k];
+    if (io.u_out)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) io.u_out[d + k] = E.bu[6 * b + k];
+  }
+#pragma unroll
+  for (int i = 0; i < kRows; ++i)
+    if (i < o.nr) io.xlam[o.kind == 4 ? (i == 0 ? row0 : row1 + i - 1) : row0 + i] = io.lam[32 * i + lane];
+  for (int i = lane; i < 2 * nc; i += 32) io.xcbody[i] = io.cbody[i];
+  pc.mark(13);
+  if (lane == 0) {
+    if (io.cr_iters) atomicAdd(io.cr_iters, (unsigned long long)cr_it);
+    if (io.cr_cycles) atomicAdd(io.cr_cycles, (unsigned long long)cr_cyc);
+    if (io.env_cycles) atomicAdd(io.env_cycles, (unsigned long long)(clock64() - t_env0));
+  }
+}
+
+}  // namespace wp
+}  // namespace nsd

@@ -12,13 +12,16 @@ from tests.helpers import rel_err
 pytestmark = pytest.mark.gpu
 
 
-def _batch(n_env, prec, env0=0, max_contacts=48, team=None):
+def _batch(n_env, prec, env0=0, max_contacts=48, team=None, env=None):
     import os
 
     from paper_1907_04587_b200 import BatchSolver, Scene
 
+    env = dict(env or {})
     if team:
-        os.environ["NSD_BATCH_TEAM"] = str(team)
+        env["NSD_BATCH_TEAM"] = str(team)
+    saved = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     s0 = Scene("c5", 0)
     qs, us = [], []
     for e in range(env0, env0 + n_env):
@@ -27,9 +30,14 @@ def _batch(n_env, prec, env0=0, max_contacts=48, team=None):
         us.append(s.u)
     cfg = s0.config
     cfg.precision = prec
-    b = BatchSolver(s0.topology, s0.shapes, s0.n_shapes, s0.margin, s0.mu_default, cfg, n_env, max_contacts)
-    if team:
-        del os.environ["NSD_BATCH_TEAM"]
+    try:
+        b = BatchSolver(s0.topology, s0.shapes, s0.n_shapes, s0.margin, s0.mu_default, cfg, n_env, max_contacts)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     b.set_state(np.concatenate(qs), np.concatenate(us))
     return b, s0
 
@@ -178,3 +186,90 @@ def test_batch_step_mapped_rejects_pageable_memory():
     q = np.zeros(4 * s0.topology.num_coord)
     with pytest.raises(NsdError):
         b.step_mapped(s0.h, s0.gravity, None, 1, q.ctypes.data, None)
+
+
+# The default C5 path is the warp-per-env solver (nsd_warp.cuh) between the
+# narrow-phase launch and the large-env launch; NSD_BATCH_FAST=0 runs the
+# sub-warp object solver for every env, NSD_WARP_MAX_OBJ=k routes envs with more
+# than k constraint objects (8 joints + contacts) to it.
+@pytest.mark.parametrize("routing", [{"NSD_BATCH_FAST": "0"}, {"NSD_WARP_MAX_OBJ": "20"}, {"NSD_WARP_MAX_OBJ": "0"}])
+def test_batch_warp_solver_matches_object_solver_fp64(routing):
+    n_env = 48
+    a, s0 = _batch(n_env, "fp64")
+    b, _ = _batch(n_env, "fp64", env=routing)
+    nj = s0.topology.n_joints
+    for st in range(20):
+        tau = np.stack([_torques(e, st, nj) for e in range(n_env)]).reshape(-1)
+        a.step(s0.h, s0.gravity, torque=tau)
+        b.step(s0.h, s0.gravity, torque=tau)
+        ra, rb = a.results(with_iters=True), b.results(with_iters=True)
+        assert np.array_equal(ra["n_contacts"], rb["n_contacts"]), st
+        assert not ra["aborted"].any() and not rb["aborted"].any()
+        # PCR iteration counts per Newton iteration agree (rounding-level operator differences)
+        assert np.mean(ra["stats"][:, :, 5] == rb["stats"][:, :, 5]) > 0.98, st
+    qa, ua = a.get_state()
+    qb, ub = b.get_state()
+    assert rel_err(qa, qb) < 1e-10
+    assert rel_err(ua, ub, floor=1e-3) < 1e-8
+    for e in (0, 7, 31, 47):
+        ia, da = a.contacts(e)
+        ib, db = b.contacts(e)
+        assert np.array_equal(ia, ib)
+        assert rel_err(da, db, floor=1e-6) < 1e-6  # geometry + multipliers
+
+
+def test_batch_large_envs_track_oracle_fp64():
+    """Envs routed to the large-env launch (NSD_WARP_MAX_OBJ=18: more than 10 contacts)
+    and the warp solver side by side in one actuated batch, both against the oracle."""
+    n_env = 16
+    b, s0 = _batch(n_env, "fp64", env={"NSD_WARP_MAX_OBJ": "18"})
+    nj = s0.topology.n_joints
+    worlds = [O.OracleWorld("c5", e) for e in range(n_env)]
+    routed_total = 0
+    for st in range(25):
+        tau = np.stack([_torques(e, st, nj) for e in range(n_env)])
+        for e, w in enumerate(worlds):
+            w.set_joint_torques(tau[e])
+            assert w.step(1) == 0
+        b.step(s0.h, s0.gravity, torque=tau.reshape(-1))
+        res = b.results()
+        routed_total += int((res["n_contacts"] > 10).sum())
+        q, _ = b.get_state()
+        for e, w in enumerate(worlds):
+            assert res["n_contacts"][e] == len(w.contacts()[0]), (st, e)
+            assert rel_err(q[e], w.state()[0]) < 1e-8, (st, e)
+    assert 0 < routed_total < 25 * n_env  # both launches solved envs
+
+
+def test_batch_counters_count_pcr_iterations():
+    """nsd_batch_counters()[0] is the sum of linear_iterations over envs and Newton
+    iterations (what bench.py's roofline numerator uses)."""
+    b, s0 = _batch(12, "fp64")
+    b.counters()
+    b.step(s0.h, s0.gravity)
+    res = b.results(with_iters=True)
+    c = b.counters()
+    assert c["cr_iterations"] == int(res["stats"][:, :, 5].sum())
+    assert c["env_steps"] == 12
+    b.profile(True)
+    b.step(s0.h, s0.gravity)
+    c = b.counters()
+    assert 0 < c["cr_cycles"] < c["env_cycles"]
+
+
+def test_batch_flags_sticky_until_results():
+    """An abort in an earlier step stays reported until nsd_batch_results clears it."""
+    b, s0 = _batch(4, "fp64")
+    q, u = b.get_state()
+    u = u.copy()
+    u[2, 0] = np.nan
+    b.set_state(q.reshape(-1), u.reshape(-1))
+    b.step(s0.h, s0.gravity)
+    q1, u1 = b.get_state()
+    u1 = u1.copy()
+    u1[2, 0] = 0.0
+    b.set_state(q1.reshape(-1), u1.reshape(-1))
+    b.step(s0.h, s0.gravity)  # env 2 steps normally now
+    assert b.results()["aborted"].tolist() == [False, False, True, False]
+    b.step(s0.h, s0.gravity)
+    assert not b.results()["aborted"].any()
