@@ -4,7 +4,10 @@
 One "step" = one step_world for every environment on the GPU: device narrow
 phase (sphere/box vs half-space and body pairs) + the full non-smooth Newton
 solve (4 Newton x 10 PCR, Fischer-Burmeister, effective-mass r, friction) +
-integration — a single kernel launch (k_batch_warp / k_batch_block).
+integration. Three launches per step: the narrow-phase/setup launch
+(k_batch_sub, mode 1), the warp-per-env solver (k_batch_warp, the dominant
+kernel) and the launch that solves envs with more than 32 constraint objects
+(k_batch_sub, mode 2; exits at once when there are none).
 
   value   env-steps/s, actions pre-staged in HBM, L2 flushed between steps,
           device time (CUDA events) summed over exactly K steps, max over ranks
@@ -21,9 +24,18 @@ integration — a single kernel launch (k_batch_warp / k_batch_block).
           nsdyn::step_world (oracle/, the reference itself does not build here),
           OpenMP over environments on all host cores.
 
-Multi-GPU: one process per GPU (torchrun), each rank owns envs
-[rank*E, (rank+1)*E) with global-env-id seeds; no collective on the data path
-(SURVEY §8e); "scaling": "weak".
+  roofline  SURVEY §8(d) algorithmic bytes of the PCR iterations actually run
+          (nsd_batch_counters: sum of linear_iterations, and of iterations x the
+          env's contact count — B_CR is affine in it) over the dominant kernel's
+          CUDA-event time inside the timed region ("frac"); also over the whole
+          step ("frac_step") and over the PCR loops alone ("frac_cr_loop": the
+          kernel time x the in-kernel clock64 share of the PCR loops, measured in
+          a separate untimed replay of the same steps).
+
+Multi-GPU: one process per GPU, each rank owns envs [rank*E, (rank+1)*E) with
+global-env-id seeds; no collective on the data path; "scaling":
+"weak". `bench.py --gpus N` without a torchrun environment re-launches itself
+under torch.distributed.run with N processes (both arms).
 """
 import argparse
 import json
@@ -62,6 +74,20 @@ def parse():
                    help="c5 (default: batched ants, the headline) or one single scene (c1, c2, c3, c4, c2:6, ...) "
                         "stepped through World.step (host detect + GPU newton_step)")
     return p.parse_args()
+
+
+def maybe_relaunch(args):
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run (N ranks)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 def dist_info():
@@ -139,9 +165,9 @@ def hbm_peak():
 
 
 def b_cr_bytes(n_contacts, nj_rows=40, n_joint_nnz=384, n_joints=8, dof=54, rigid=9, value_bytes=4):
-    """SURVEY §8(d) algorithmic bytes of one CR iteration for one env:
+    """SURVEY §8(d) algorithmic bytes of one CR iteration for one ant env:
     B_CR = 2(vZ + 4X) + v n_C + 2vD + v D_particle + 7v B_rigid + 13 v R
-    (fp32: v = 4 -> 2(4Z+4X) + 4n_C + 8D + 4D_p + 28B_rigid + 52R)."""
+    (fp32: v = 4 -> 2(4Z+4X) + 4n_C + 8D + 4D_p + 28B_rigid + 52R); affine in nc."""
     nc = np.asarray(n_contacts, dtype=np.float64)
     R = nj_rows + 3 * nc
     Z = n_joint_nnz + 18 * nc
@@ -149,6 +175,38 @@ def b_cr_bytes(n_contacts, nj_rows=40, n_joint_nnz=384, n_joints=8, dof=54, rigi
     n_C = R
     v = value_bytes
     return 2 * (v * Z + 4 * X) + v * n_C + 2 * v * dof + 7 * v * rigid + 13 * v * R
+
+
+def scene_b_cr(dims, topo, n_contacts, contact_bodies, value_bytes=8):
+    """SURVEY §8(d) B_CR of one PCR iteration of a single scene, from its exact
+    structure: Z (J nonzeros), X (int32 ids), n_C (C entries), R, D, D_particle,
+    B_rigid. contact_bodies: (body_a, body_b) per contact (-1 = world)."""
+    bt = np.asarray(topo.a["body_type"])
+    side = lambda b: 0 if b < 0 else (6 if bt[b] == 1 else 3)
+    Z = X = n_C = R = 0
+    kinds, jb = np.asarray(topo.a["joint_kind"]), np.asarray(topo.a["joint_body"]).reshape(-1, 2)
+    for k, (a, b) in zip(kinds, jb):
+        npnt = 3 if k <= 1 else (2 if k == 2 else 0)
+        nr = 2 if k == 3 else (3 if k == 0 else 5)
+        Z += npnt * (side(a) + side(b)) + (nr - npnt) * (3 * (a >= 0 and bt[a] == 1) + 3 * (b >= 0 and bt[b] == 1))
+        X += 2
+        R += nr
+        n_C += nr
+    nt = int(dims["n_tets"])
+    Z += nt * 3 * 12
+    X += 4 * nt
+    R += 3 * nt
+    n_C += 9 * nt
+    for a, b in contact_bodies:
+        Z += 3 * (side(a) + side(b))
+        X += 2
+        R += 3
+        n_C += 3
+    D = int(dims["num_dof"])
+    Dp = int(3 * np.sum(bt == 0))
+    Br = int(np.sum(bt == 1))
+    v = value_bytes
+    return 2 * (v * Z + 4 * X) + v * n_C + 2 * v * D + v * Dp + 7 * v * Br + 13 * v * R
 
 
 def cpu_baseline(args, n_env_total):
@@ -174,7 +232,7 @@ def run_reference(args):
     cb = cpu_baseline(args, args.envs)
     # each bench "step" = one bounded sample step over the workload; report the rate
     line = {"impl": "reference", "metric": "env-steps/sec at fixed Newton/CR iters", "value": cb["value"],
-            "unit": "env-steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "unit": "env-steps/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * args.envs / cb["value"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args, ws),
@@ -227,9 +285,12 @@ def measure(args, prec, T, tmpl, E, env0, ws, rank, local, sample_clocks):
     b.results()  # raises on contact overflow / errors
     q_w, u_w = b.get_state()  # post-warmup state: the e2e region replays the same steps
 
-    # ---- value: device-resident inputs, L2 flushed between steps
+    # ---- value: device-resident inputs, L2 flushed between steps; CUDA events around
+    # every step, plus (inside the library) around each of the step's launches
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     sampler = ClockSampler(local) if sample_clocks else None
+    b.profile(cycles=False, launch_timing=True)
+    b.counters()  # reset
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -248,9 +309,23 @@ def measure(args, prec, T, tmpl, E, env0, ws, rank, local, sample_clocks):
     if ws > 1:
         torch.distributed.barrier()
     dev_ms = sum(a.elapsed_time(bb) for a, bb in ev)
-    res = b.results()
+    ctr = b.counters()
+    b.profile(cycles=False, launch_timing=False)
+    res = b.results()  # raises if any env overflowed max_contacts in any timed step
     nc = res["n_contacts"].astype(np.float64)
-    aborted = int(res["aborted"].sum())
+    aborted = int(res["aborted"].sum())  # envs that rolled back in any timed step
+
+    # ---- PCR-loop share of the solver's time: clock64 counters in an untimed replay
+    # of the same steps (the counters' atomics stay out of the timed region)
+    b.set_state(q_w, u_w)
+    b.profile(cycles=True, launch_timing=False)
+    b.counters()
+    for k in range(min(K, 20)):
+        step(W + k)
+    prof = b.counters()
+    b.profile(cycles=False, launch_timing=False)
+    b.results()
+    cr_share = prof["cr_cycles"] / prof["env_cycles"] if prof["env_cycles"] else None
 
     # ---- e2e: host actions -> H2D, step, D2H of the state, through the C ABI,
     # replaying the timed steps from the same post-warmup state with the same actions
@@ -300,29 +375,92 @@ def measure(args, prec, T, tmpl, E, env0, ws, rank, local, sample_clocks):
         dev_ms, e2e_ms, e2e_copy_ms = float(t[0]), float(t[1]), float(t[2])
     total_envs = E * ws
     return dict(dev_ms=dev_ms, e2e_ms=e2e_ms, value=total_envs * K / (dev_ms / 1000.0),
-                e2e=total_envs * K / (e2e_ms / 1000.0), e2e_copy=total_envs * K / (e2e_copy_ms / 1000.0), nc=nc, aborted=aborted, clocks=clocks, h2d=h2d, d2h=d2h,
-                cfg=cfg)
+                e2e=total_envs * K / (e2e_ms / 1000.0), e2e_copy=total_envs * K / (e2e_copy_ms / 1000.0), nc=nc,
+                aborted=aborted, clocks=clocks, h2d=h2d, d2h=d2h, cfg=cfg, ctr=ctr, cr_share=cr_share, E=E)
+
+
+def traffic_record(kernel_key):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture,
+    only if the kernel sources still hash to what was profiled (else null)."""
+    import hashlib
+
+    path = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    try:
+        rec = json.load(open(path)).get(kernel_key)
+        h = hashlib.sha256()
+        for f in rec["sources"]:
+            h.update(open(os.path.join(ROOT, f), "rb").read())
+        return rec["bytes"] if h.hexdigest() == rec["sha256"] else None
+    except Exception:
+        return None
 
 
 def roofline(m, prec, K):
-    """Roofline of the (single) step kernel: SURVEY §8(d) algorithmic bytes."""
+    """Roofline of the dominant kernel (k_batch_warp): SURVEY §8(d) algorithmic bytes
+    of the PCR iterations actually run ÷ its CUDA-event time in the timed region."""
     vb = 4 if prec == "fp32" else 8
-    cfg = m["cfg"]
-    per_env_cr = b_cr_bytes(m["nc"], value_bytes=vb)
-    bytes_per_launch = float(np.sum(per_env_cr)) * cfg.newton_iterations * cfg.linear_max_iterations
-    launch_s = m["dev_ms"] / 1000.0 / K
+    c = m["ctr"]
+    b0 = float(b_cr_bytes(0, value_bytes=vb))
+    b1 = float(b_cr_bytes(1, value_bytes=vb)) - b0  # bytes per contact
+    bytes_total = b0 * c["cr_iterations"] + b1 * c["cr_iterations_x_contacts"]
     peak, peak_kind = hbm_peak()
-    achieved = bytes_per_launch / launch_s / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(prec)
-        except Exception:
-            traffic = None
-    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "peak_source": peak_kind, "bytes_per_launch": bytes_per_launch,
-            "model": "SURVEY 8(d) B_CR per env per CR iteration x 40 CR iterations x envs"}
+    t_kernel = c["warp_solver_ms"] / 1000.0
+    t_step = m["dev_ms"] / 1000.0
+    per_launch = bytes_total / max(K, 1)
+    out = {"bound": "hbm", "achieved": bytes_total / t_kernel / 1e9 if t_kernel else None, "peak": peak,
+           "unit": "GB/s", "frac": None, "traffic": traffic_record(f"k_batch_warp<{'double' if vb == 8 else 'float'}>"),
+           "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else peak_kind,
+           "kernel": f"k_batch_warp<{'double' if vb == 8 else 'float'}>",
+           "bytes_per_launch": per_launch, "kernel_ms_per_launch": 1000.0 * t_kernel / max(K, 1),
+           "pcr_iterations_per_env_step": c["cr_iterations"] / max(c["env_steps"], 1),
+           "model": "SURVEY 8(d) B_CR(nc) per env per PCR iteration actually run (nsd_batch_counters), "
+                    "summed over envs; kernel time from CUDA events around its launches in the timed region"}
+    if out["achieved"]:
+        out["frac"] = out["achieved"] / peak
+    out["frac_step"] = bytes_total / t_step / 1e9 / peak
+    if m["cr_share"] and t_kernel:
+        t_cr = t_kernel * m["cr_share"]
+        out["frac_cr_loop"] = bytes_total / t_cr / 1e9 / peak
+        out["cr_loop_share_of_kernel"] = m["cr_share"]
+        out["us_per_cr_iter_loop"] = 1e6 * t_cr / max(K, 1) / (c["cr_iterations"] / max(c["env_steps"], 1))
+    out["launch_ms_per_step"] = {"narrow_phase": c["narrow_phase_ms"] / max(K, 1),
+                                 "warp_solver": c["warp_solver_ms"] / max(K, 1),
+                                 "large_envs": c["large_env_ms"] / max(K, 1)}
+    return out
+
+
+def scene_steps(w, steps, vb):
+    """K timed World.step calls (L2 flushed before each): device ms per step from the
+    CUDA events inside nsd_step (the step is ONE kernel launch), wall seconds, PCR
+    iterations run, and the SURVEY §8(d) bytes of those iterations (B_CR from the
+    step's exact structure and contact set)."""
+    import torch
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    dev, wall, pcr, nbytes, ncs = [], [], 0, 0.0, []
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = w.step()
+        wall.append(time.perf_counter() - t0)
+        dev.append(rep["ms"])
+        it = int(sum(rep["stats"][:, 5]))
+        pcr += it
+        ib = w.contacts[0] if w.contacts is not None else np.zeros((0, 3), np.int32)
+        ncs.append(len(ib))
+        nbytes += it * scene_b_cr(w.scene.dims, w.topology, len(ib), [(int(a), int(b)) for a, b in ib[:, :2]], vb)
+    return dev, wall, pcr, nbytes, ncs
+
+
+def scene_roofline(dev, nbytes):
+    peak, kind = hbm_peak()
+    t = sum(dev) / 1000.0
+    ach = nbytes / t / 1e9 if t else None
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak if ach else None,
+            "traffic": None, "peak_source": kind, "bytes_per_launch": nbytes / max(len(dev), 1),
+            "model": "SURVEY 8(d) B_CR of the step's structure x PCR iterations run, over the nsd_step kernel's "
+                     "CUDA-event time (the whole step: assembly, SVD/eigen per tet and PCR in one launch)"}
 
 
 def scene_summary(name, precision, steps, warmup):
@@ -333,23 +471,17 @@ def scene_summary(name, precision, steps, warmup):
     from paper_1907_04587_b200 import World
 
     w = World(name, 0, precision=precision)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(warmup):
         w.step()
-    dev, wall = [], []
-    for _ in range(steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        rep = w.step()
-        wall.append(time.perf_counter() - t0)
-        dev.append(rep["ms"])
+    dev, wall, pcr, nbytes, ncs = scene_steps(w, steps, 4 if precision == "fp32" else 8)
     cfg = w.config
     ms = float(np.mean(dev))
-    out = {"ms_per_step": ms, "us_per_cr_iter": 1000.0 * ms / (cfg.newton_iterations * cfg.linear_max_iterations),
+    out = {"ms_per_step": ms, "us_per_cr_iter_budget": 1000.0 * ms / (cfg.newton_iterations * cfg.linear_max_iterations),
+           "us_per_cr_iter_used": 1000.0 * ms * steps / max(pcr, 1), "pcr_iterations_per_step": pcr / steps,
            "steps_per_s": 1000.0 / ms, "e2e_steps_per_s": 1.0 / float(np.mean(wall)),
            "budget": f"{cfg.newton_iterations}x{cfg.linear_max_iterations}", "tets": w.scene.dims["n_tets"],
-           "bodies": w.scene.dims["n_bodies"]}
+           "bodies": w.scene.dims["n_bodies"], "mean_contacts": float(np.mean(ncs)),
+           "roofline": scene_roofline(dev, nbytes)}
     w.close()
     return out
 
@@ -367,21 +499,12 @@ def run_scene(args):
     torch.cuda.set_device(local)
     K, W = args.steps, args.warmup
     w = World(args.workload, 0, precision=args.precision)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(W):
         w.step()
-    dev, wall, pcr = [], [], 0
     sampler = ClockSampler(local)
     sampler.start()
     sampler.begin()
-    for _ in range(K):
-        flush.zero_()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        rep = w.step()
-        wall.append(time.perf_counter() - t0)
-        dev.append(rep["ms"])
-        pcr += int(sum(rep["stats"][:, 5]))
+    dev, wall, pcr, nbytes, ncs = scene_steps(w, K, 4 if args.precision == "fp32" else 8)
     clocks = sampler.stop()
     cfg = w.config
     ms = float(np.mean(dev))
@@ -401,14 +524,14 @@ def run_scene(args):
         cpu = {"value": n / t, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
                "sample": f"{args.workload}: oracle step_world steps {W}..{W + n} ({t:.2f} s)"}
     line = {"metric": "steps/sec at fixed Newton/CR iters (single scene)", "value": 1000.0 / ms, "unit": "steps/s",
-            "n_gpus": 1, "steps": K, "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic",
             "config": {"workload": args.workload, "bodies": w.scene.dims["n_bodies"], "tets": w.scene.dims["n_tets"],
                        "newton_iterations": cfg.newton_iterations, "linear_iterations": cfg.linear_max_iterations,
                        "parallelism": "replicas only", "l2": "flushed (256 MiB memset) between timed steps"},
             "us_per_cr_iter_budget": 1000.0 * ms / cr_budget, "pcr_iterations_used_per_step": pcr / K,
-            "us_per_cr_iter_used": 1000.0 * ms * K / max(pcr, 1),
-            "mean_contacts": float(len(w.contacts[0])) if w.contacts is not None else 0.0,
+            "us_per_cr_iter_used": 1000.0 * ms * K / max(pcr, 1), "mean_contacts": float(np.mean(ncs)),
+            "roofline": scene_roofline(dev, nbytes),
             "e2e": {"value": 1.0 / float(np.mean(wall)), "unit": "steps/s",
                     "h2d_bytes_per_step": 8 * (w.scene.dims["num_coord"] + w.scene.dims["num_dof"]),
                     "d2h_bytes_per_step": 8 * (w.scene.dims["num_coord"] + w.scene.dims["num_dof"])},
@@ -421,6 +544,7 @@ def run_scene(args):
 
 def main():
     args = parse()
+    maybe_relaunch(args)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -464,7 +588,9 @@ def main():
             "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": m["dev_ms"] / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if prec == "fp32" else "f64",
             "data": "synthetic", "config": workload_config(args, ws),
-            "us_per_cr_iter": 1000.0 * (m["dev_ms"] / K) / (cfg.newton_iterations * cfg.linear_max_iterations),
+            "us_per_cr_iter": 1000.0 * (m["dev_ms"] / K) / (m["ctr"]["cr_iterations"] / max(m["ctr"]["env_steps"], 1)),
+            "us_per_cr_iter_note": "whole step (3 launches) per PCR iteration run per env-step; "
+                                   "roofline.us_per_cr_iter_loop is the PCR loops alone",
             "mean_contacts_per_env": float(m["nc"].mean()), "aborted_envs": m["aborted"],
             "roofline": roofline(m, prec, K),
             "e2e": {"value": m["e2e"], "unit": "env-steps/s", "h2d_bytes_per_step": m["h2d"],
@@ -472,7 +598,7 @@ def main():
                     "path": "nsd_batch_step_mapped: the step kernel reads the actions from and writes (q, u) to "
                             "pinned host memory",
                     "copy_path_value": m["e2e_copy"]},
-            "gpu_launches": K, "clocks": m["clocks"]}
+            "gpu_launches": 3 * K, "clocks": m["clocks"]}
     if other:
         line["other_precision"] = other
     if ws == 1 and not args.no_scenes:

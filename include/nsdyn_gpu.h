@@ -195,14 +195,18 @@ int nsd_batch_copy_state_async(nsd_batch* b, void* q_dst, void* u_dst);
 int nsd_batch_step_mapped(nsd_batch* b, const void* joint_torque, int32_t dtype, void* q_out, void* u_out, double h,
                           const double gravity[3]);
 int nsd_batch_info(const nsd_batch* b, int32_t* info /* [n_env, num_coord, num_dof, n_joints, max_rows, team_threads] */);
-/* Counters since the previous call (read and reset; synchronises the stream):
- * out[0] PCR iterations run, summed over envs, Newton iterations and steps
- * (the roofline numerator counts these); out[1] clock64 cycles spent inside the
- * PCR loops and out[2] cycles per env step, both summed over envs (profile on,
- * warp path); out[3] env-steps. */
+/* Counters since the previous call (read and reset; synchronises the stream),
+ * out[9]: [0] PCR iterations run, summed over envs, Newton iterations and steps
+ * (the roofline numerator counts these); [1] clock64 cycles spent inside the
+ * PCR loops and [2] cycles per env step, both summed over envs (profile bit 0,
+ * warp path); [3] env-steps; [4..6] nanoseconds between CUDA events recorded on
+ * the batch stream around the step's narrow-phase launch, warp-solver launch and
+ * large-env launch, summed over [7] timed steps (profile bit 1, warp path);
+ * [8] PCR iterations x the env's contact count, summed like [0] (the per-env
+ * algorithmic bytes of one PCR iteration are affine in the contact count). */
 int nsd_batch_counters(nsd_batch* b, uint64_t* out);
-/* Enables (1) or disables (0) the in-kernel cycle counters of nsd_batch_counters. */
-int nsd_batch_profile(nsd_batch* b, int32_t enable);
+/* profile flags: bit 0 in-kernel cycle counters, bit 1 per-launch CUDA events. */
+int nsd_batch_profile(nsd_batch* b, int32_t flags);
 int nsd_batch_destroy(nsd_batch* b);
 
 /* ---------------- builders (scene.cpp:802-935 style) */

@@ -457,13 +457,16 @@ class BatchSolver:
     def counters(self):
         """Counters since the previous call (nsd_batch_counters): PCR iterations run
         (summed over envs, Newton iterations and steps), cycles inside the PCR loops
-        and per env step (profile on), env-steps."""
-        v = (C.c_uint64 * 4)()
+        and per env step (cycles on), env-steps, and the CUDA-event time of each
+        launch of the step (launch timing on)."""
+        v = (C.c_uint64 * 9)()
         check(lib().nsd_batch_counters(self._h, v))
-        return dict(cr_iterations=int(v[0]), cr_cycles=int(v[1]), env_cycles=int(v[2]), env_steps=int(v[3]))
+        return dict(cr_iterations=int(v[0]), cr_cycles=int(v[1]), env_cycles=int(v[2]), env_steps=int(v[3]),
+                    narrow_phase_ms=v[4] * 1e-6, warp_solver_ms=v[5] * 1e-6, large_env_ms=v[6] * 1e-6,
+                    timed_steps=int(v[7]), cr_iterations_x_contacts=int(v[8]))
 
-    def profile(self, enable=True):
-        check(lib().nsd_batch_profile(self._h, 1 if enable else 0))
+    def profile(self, cycles=True, launch_timing=False):
+        check(lib().nsd_batch_profile(self._h, (1 if cycles else 0) | (2 if launch_timing else 0)))
 
     def device_state(self):
         q, u, dt = C.c_void_p(), C.c_void_p(), C.c_int32()

@@ -633,7 +633,10 @@ template <class R> struct Batch final : BatchBase {
   int warp_max_obj = 32;   // NSD_WARP_MAX_OBJ (tests) routes smaller envs to the object solver too
   size_t warp_smem = 0;
   long env_steps = 0;
-  bool profile = false;
+  bool profile = false;     // bit 0 of nsd_batch_profile: in-kernel cycle counters
+  bool time_launches = false;  // bit 1: CUDA events around each launch of the step
+  std::vector<cudaEvent_t> evpool;  // 4 per timed step: before narrow phase, after it, after warp, after large
+  size_t ev_used = 0;
   int jbinc_n = 0;
   HBuf stage;
   double margin, mu_default;
@@ -884,6 +887,7 @@ template <class R> struct Batch final : BatchBase {
         std::fprintf(stderr, "  %-28s %6.2f%%  %.4g cycles/env-step\n", names[k], tot ? 100.0 * h[k] / tot : 0.0,
                      double(h[k]) / std::max(1.0, double(launches) * n_env));
     }
+    for (cudaEvent_t e : evpool) cudaEventDestroy(e);
     if (stream && own_stream) cudaStreamDestroy(stream);
   }
   void set_state(const double* q, const double* u) override {
@@ -985,6 +989,18 @@ template <class R> struct Batch final : BatchBase {
     A.wptime = wptime.as<unsigned long long>();
     A.mode = 0;
     A.profile = profile ? 1 : 0;
+    cudaEvent_t* ev = nullptr;
+    if (time_launches && warp_path) {
+      if (ev_used + 4 > evpool.size()) {
+        for (int k = 0; k < 64; ++k) {
+          cudaEvent_t e;
+          NSD_CK(cudaEventCreate(&e));
+          evpool.push_back(e);
+        }
+      }
+      ev = &evpool[ev_used];
+      ev_used += 4;
+    }
     ++env_steps;
     const int epb = envs_per_block;
     const int nblk = (n_env + epb - 1) / epb;
@@ -995,10 +1011,14 @@ template <class R> struct Batch final : BatchBase {
       A1.mode = 1;
       A1.row_pool = 0;
       A1.ptime = nullptr;
+      if (ev) NSD_CK(cudaEventRecord(ev[0], stream));
       NSD_CK(launch_batch_sub<R>(16, nblk, 16 * epb, 0, stream, A1));
+      if (ev) NSD_CK(cudaEventRecord(ev[1], stream));
       NSD_CK(launch_batch_warp<R>((n_env + warp_epb - 1) / warp_epb, 32 * warp_epb, warp_smem, stream, A));
+      if (ev) NSD_CK(cudaEventRecord(ev[2], stream));
       A.mode = 2;
       NSD_CK(launch_batch_sub<R>(16, nblk, 16 * epb, smem_bytes, stream, A));
+      if (ev) NSD_CK(cudaEventRecord(ev[3], stream));
       return;
     }
     if (team_threads <= 32) {
@@ -1053,12 +1073,28 @@ template <class R> struct Batch final : BatchBase {
   // (warp path, profile on), [2] cycles per env step (same), [3] env-steps; read and reset
   void counters(unsigned long long* out) override {
     NSD_CK(cudaStreamSynchronize(stream));
-    NSD_CK(cudaMemcpy(out, ctr.p, sizeof(unsigned long long) * 3, cudaMemcpyDeviceToHost));
+    unsigned long long c4[4];
+    NSD_CK(cudaMemcpy(c4, ctr.p, sizeof(c4), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 3; ++k) out[k] = c4[k];
     out[3] = static_cast<unsigned long long>(env_steps) * n_env;
+    out[8] = c4[3];
     env_steps = 0;
     NSD_CK(cudaMemset(ctr.p, 0, sizeof(unsigned long long) * 4));
+    double us[3] = {0.0, 0.0, 0.0};
+    for (size_t i = 0; i + 4 <= ev_used; i += 4)
+      for (int k = 0; k < 3; ++k) {
+        float ms = 0.f;
+        NSD_CK(cudaEventElapsedTime(&ms, evpool[i + k], evpool[i + k + 1]));
+        us[k] += 1000.0 * ms;
+      }
+    for (int k = 0; k < 3; ++k) out[4 + k] = static_cast<unsigned long long>(us[k] * 1000.0 + 0.5);  // ns
+    out[7] = ev_used / 4;
+    ev_used = 0;
   }
-  void set_profile(int on) override { profile = on != 0; }
+  void set_profile(int on) override {
+    profile = (on & 1) != 0;
+    time_launches = (on & 2) != 0;
+  }
   void contacts(int env, nsd_contact* out, int* n) override {
     if (env < 0 || env >= n_env) throw NsdError(NSD_INVALID, "env out of range");
     int nc = 0;
@@ -1317,9 +1353,9 @@ int nsd_batch_copy_state_async(nsd_batch* b, void* q_dst, void* u_dst) {
 int nsd_batch_counters(nsd_batch* b, uint64_t* out) {
   return guarded([&] {
     if (!b || !out) throw NsdError(NSD_INVALID, "null argument");
-    unsigned long long v[4];
+    unsigned long long v[9];
     b->impl->counters(v);
-    for (int i = 0; i < 4; ++i) out[i] = v[i];
+    for (int i = 0; i < 9; ++i) out[i] = v[i];
     return NSD_OK;
   });
 }

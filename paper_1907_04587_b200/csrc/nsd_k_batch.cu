@@ -301,6 +301,7 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
       unsigned long long n = 0;
       for (int k = 0; k < static_cast<int>(out.fin[7]); ++k) n += out.iters[k].linear_iterations;
       atomicAdd(A.counters, n);
+      atomicAdd(A.counters + 3, n * static_cast<unsigned long long>(nc));
     }
   }
 }

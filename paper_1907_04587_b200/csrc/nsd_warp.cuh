@@ -931,7 +931,10 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
   for (int i = lane; i < 2 * nc; i += 32) io.xcbody[i] = io.cbody[i];
   pc.mark(13);
   if (lane == 0) {
-    if (io.cr_iters) atomicAdd(io.cr_iters, (unsigned long long)cr_it);
+    if (io.cr_iters) {
+      atomicAdd(io.cr_iters, (unsigned long long)cr_it);
+      atomicAdd(io.cr_iters + 3, (unsigned long long)cr_it * (unsigned long long)nc);  // for the nc-weighted bytes
+    }
     if (io.cr_cycles) atomicAdd(io.cr_cycles, (unsigned long long)cr_cyc);
     if (io.env_cycles) atomicAdd(io.env_cycles, (unsigned long long)(clock64() - t_env0));
   }

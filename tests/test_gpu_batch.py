@@ -219,26 +219,33 @@ def test_batch_warp_solver_matches_object_solver_fp64(routing):
 
 
 def test_batch_large_envs_track_oracle_fp64():
-    """Envs routed to the large-env launch (NSD_WARP_MAX_OBJ=18: more than 10 contacts)
-    and the warp solver side by side in one actuated batch, both against the oracle."""
-    n_env = 16
-    b, s0 = _batch(n_env, "fp64", env={"NSD_WARP_MAX_OBJ": "18"})
+    """Envs routed to the large-env launch (more than NSD_WARP_MAX_OBJ - 8 contacts, the
+    threshold picked from the oracle's contact counts so that the batch mixes both) and the
+    warp solver side by side in one actuated batch, both against the oracle every step."""
+    n_env, steps = 16, 25
+    s0 = _batch(1, "fp64")[1]
     nj = s0.topology.n_joints
     worlds = [O.OracleWorld("c5", e) for e in range(n_env)]
-    routed_total = 0
-    for st in range(25):
+    taus, states, counts = [], [], []
+    for st in range(steps):
         tau = np.stack([_torques(e, st, nj) for e in range(n_env)])
         for e, w in enumerate(worlds):
             w.set_joint_torques(tau[e])
             assert w.step(1) == 0
-        b.step(s0.h, s0.gravity, torque=tau.reshape(-1))
+        taus.append(tau)
+        states.append([w.state()[0] for w in worlds])
+        counts.append([len(w.contacts()[0]) for w in worlds])
+    counts = np.array(counts)
+    thr = int(np.median(counts))
+    assert 0 < int((counts > thr).sum()) < counts.size
+    b, _ = _batch(n_env, "fp64", env={"NSD_WARP_MAX_OBJ": str(nj + thr)})
+    for st in range(steps):
+        b.step(s0.h, s0.gravity, torque=taus[st].reshape(-1))
         res = b.results()
-        routed_total += int((res["n_contacts"] > 10).sum())
         q, _ = b.get_state()
-        for e, w in enumerate(worlds):
-            assert res["n_contacts"][e] == len(w.contacts()[0]), (st, e)
-            assert rel_err(q[e], w.state()[0]) < 1e-8, (st, e)
-    assert 0 < routed_total < 25 * n_env  # both launches solved envs
+        assert np.array_equal(res["n_contacts"], counts[st]), st
+        for e in range(n_env):
+            assert rel_err(q[e], states[st][e]) < 1e-8, (st, e)
 
 
 def test_batch_counters_count_pcr_iterations():
@@ -249,12 +256,16 @@ def test_batch_counters_count_pcr_iterations():
     b.step(s0.h, s0.gravity)
     res = b.results(with_iters=True)
     c = b.counters()
-    assert c["cr_iterations"] == int(res["stats"][:, :, 5].sum())
+    its = res["stats"][:, :, 5].sum(axis=1)
+    assert c["cr_iterations"] == int(its.sum())
+    assert c["cr_iterations_x_contacts"] == int((its * res["n_contacts"]).sum())
     assert c["env_steps"] == 12
-    b.profile(True)
-    b.step(s0.h, s0.gravity)
+    b.profile(cycles=True, launch_timing=True)
+    for _ in range(3):
+        b.step(s0.h, s0.gravity)
     c = b.counters()
     assert 0 < c["cr_cycles"] < c["env_cycles"]
+    assert c["timed_steps"] == 3 and c["warp_solver_ms"] > 0 and c["narrow_phase_ms"] > 0
 
 
 def test_batch_flags_sticky_until_results():
