@@ -631,6 +631,8 @@ template <class R> struct Batch final : BatchBase {
   nsd::wp::Plan wplan{};
   int warp_epb = 2;        // environments (warps) per block of k_batch_warp (64 threads, 7 blocks/SM)
   int warp_max_obj = 32;   // NSD_WARP_MAX_OBJ (tests) routes smaller envs to the object solver too
+  int collide_cap = 64;    // k_batch_collide's per-env candidate list (>= max_contacts)
+  bool legacy_collide = false;  // NSD_BATCH_COLLIDE=sub: narrow phase through k_batch_sub mode 1
   size_t warp_smem = 0;
   long env_steps = 0;
   bool profile = false;     // bit 0 of nsd_batch_profile: in-kernel cycle counters
@@ -842,6 +844,8 @@ template <class R> struct Batch final : BatchBase {
       }
       if (const char* e = std::getenv("NSD_WARP_EPB")) warp_epb = std::max(1, std::min(8, std::atoi(e)));
       if (const char* e = std::getenv("NSD_WARP_MAX_OBJ")) warp_max_obj = std::max(0, std::min(32, std::atoi(e)));
+      collide_cap = std::max(64, maxc);
+      if (const char* e = std::getenv("NSD_BATCH_COLLIDE")) legacy_collide = std::string(e) == "sub";
       warp_smem = static_cast<size_t>(wplan.bytes) * warp_epb;
       int per_sm = 0;
       NSD_CK(batch_warp_setup<R>(max_optin, 32 * warp_epb, warp_smem, &per_sm));
@@ -1012,7 +1016,12 @@ template <class R> struct Batch final : BatchBase {
       A1.row_pool = 0;
       A1.ptime = nullptr;
       if (ev) NSD_CK(cudaEventRecord(ev[0], stream));
-      NSD_CK(launch_batch_sub<R>(16, nblk, 16 * epb, 0, stream, A1));
+      if (npairs > 0 && !legacy_collide) {
+        A1.collide_cap = collide_cap;
+        NSD_CK(launch_batch_collide<R>((n_env + 3) / 4, 128, 4 * collide_cap * sizeof(nsd::CandD<R>), stream, A1));
+      } else {
+        NSD_CK(launch_batch_sub<R>(16, nblk, 16 * epb, 0, stream, A1));
+      }
       if (ev) NSD_CK(cudaEventRecord(ev[1], stream));
       NSD_CK(launch_batch_warp<R>((n_env + warp_epb - 1) / warp_epb, 32 * warp_epb, warp_smem, stream, A));
       if (ev) NSD_CK(cudaEventRecord(ev[2], stream));

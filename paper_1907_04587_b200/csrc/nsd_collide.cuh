@@ -217,16 +217,17 @@ NSD_HD int box_box(const BodyView<R>& v, const ShapeD<R>& sa, const ShapeD<R>& s
     const V3<R> pr = ref == 0 ? pos0 : pos1, po = ref == 0 ? pos1 : pos0;
     const ShapeD<R>& br = ref == 0 ? sa : sb;
     const ShapeD<R>& bo = ref == 0 ? sb : sa;
+    V3<R> wc[8];  // the other box's world corners, once per reference box (same values per axis)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) wc[k] = po + mul(ro, corner(bo.he, k));
     for (int axis = 0; axis < 3; ++axis)
       for (int di = 0; di < 2; ++di) {
         const R dir = di == 0 ? R(1) : R(-1);
         const V3<R> n = dir * col(rr, axis);
         const V3<R> fp = pr + (dir * br.he[axis]) * col(rr, axis);
         R mnp = Lim<R>::inf();
-        for (int k = 0; k < 8; ++k) {
-          const V3<R> w = po + mul(ro, corner(bo.he, k));
-          mnp = mn(mnp, dot(n, w - fp));
-        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mnp = mn(mnp, dot(n, wc[k] - fp));
         if (mnp > best_sep + R(1e-12)) {
           best_sep = mnp;
           best_ref = ref;

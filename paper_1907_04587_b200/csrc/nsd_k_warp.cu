@@ -1,4 +1,5 @@
 // Batched rigid environments, one warp per env (nsd_warp.cuh).
+#include "nsd_env_setup.cuh"
 #include "nsd_plan.cuh"
 #include "nsd_warp.cuh"
 
@@ -65,10 +66,110 @@ template <class R> __global__ void __launch_bounds__(64, warp_minb<R>()) k_batch
 }
 
 
+// Narrow phase + step setup, one warp per environment (the rigid path's first
+// launch; k_batch_sub mode 1 does the same with sub-warp teams): env_setup, then
+// the shape pairs 32 per round, one per lane (pair_contacts, collision.cpp:253-287).
+// Each round's candidates are appended to the env's compact shared-memory list in
+// (pair, k) generation order by a warp prefix sum; each candidate's rank under the
+// canonical (a.body, b.body, feature) order, ties by generation order
+// (collision.cpp:290-295), places it in the env's contact slabs. A list longer
+// than its capacity (>= max_contacts) only occurs with a contact overflow, which
+// is reported as an error; the contacts kept then come from the stored prefix.
+template <class R> __global__ void __launch_bounds__(128, 4) k_batch_collide(BatchArgs<R> A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int env = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (env >= A.n_env) return;
+  const nsd::Topo<R>& T = A.T;
+  const WorkPlan& P = A.plan;
+  const int cap = A.collide_cap;
+  nsd::CandD<R>* cand = reinterpret_cast<nsd::CandD<R>*>(smem) + (size_t)wib * cap;
+  R* hr = reinterpret_cast<R*>(A.hot_global + (size_t)env * A.hot_bytes);
+  int* hi = P.hot_ints(hr);
+  R* cr = A.cold_r + (size_t)env * P.coldR;
+  int* ci = A.cold_i + (size_t)env * P.coldI;
+  nsd::Work<R> W = P.template bind<R>(hr, hi, cr, ci);
+  W.jframe = A.jframe;
+  W.h = A.h;
+  W.grav[0] = A.grav[0];
+  W.grav[1] = A.grav[1];
+  W.grav[2] = A.grav[2];
+  R* qrot = hr + P.qrot;
+  nsd::WarpTeam t(lane);
+  env_setup(t, A, env, W, A.qs + (size_t)env * T.ncoord, A.us + (size_t)env * T.ndof, cr, qrot);
+  const nsd::BodyView<R> view{T.btype, T.bdof, T.bcoord, W.q0, W.ut, qrot};
+  int total = 0;
+  for (int p0 = 0; p0 < A.npairs; p0 += 32) {
+    const int p = p0 + lane;
+    nsd::CandD<R> loc[4];
+    int n = 0;
+    if (p < A.npairs) {
+      const int2 ij = A.pairs[p];
+      R th, mu;
+      n = nsd::pair_contacts(view, A.shapes[ij.x], A.shapes[ij.y], A.h, A.margin, A.mu_default, loc, &th, &mu);
+    }
+    int incl = n;  // inclusive prefix sum of the counts over the lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int base = total + incl - n;
+    for (int k = 0; k < n; ++k)
+      if (base + k < cap) cand[base + k] = loc[k];
+    total += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  __syncwarp();
+  const int stored = total < cap ? total : cap;
+  const int nc = total < A.maxc ? total : A.maxc;
+  int* cbody = hi + P.cbody;
+  int* cfeat = ci + P.cfeat;
+  R* cgeo = cr + P.cgeo;
+  for (int i = lane; i < stored; i += 32) {
+    const nsd::CandD<R> c = cand[i];
+    int rank = 0;
+    for (int j = 0; j < stored; ++j) {
+      const int oa = cand[j].a, ob = cand[j].b, of = cand[j].feature;
+      if (nsd::canonical_less(oa, ob, of, c.a, c.b, c.feature) || (oa == c.a && ob == c.b && of == c.feature && j < i))
+        ++rank;
+    }
+    if (rank >= nc) continue;
+    cbody[2 * rank] = c.a;
+    cbody[2 * rank + 1] = c.b;
+    cfeat[rank] = c.feature;
+    R* g = cgeo + 17 * rank;
+    nsd::V3<R> nn = nsd::get3(c.n), d1, d2;
+    nsd::tangent_basis(nn, d1, d2);
+    for (int k = 0; k < 3; ++k) {
+      g[k] = c.la[k];
+      g[3 + k] = c.lb[k];
+      g[6 + k] = c.n[k];
+    }
+    nsd::st3(g + 9, d1);
+    nsd::st3(g + 12, d2);
+    g[15] = c.thick;
+    g[16] = c.mu;
+  }
+  if (lane == 0) {  // contact count; overflow is sticky until nsd_batch_results
+    A.nc_out[env] = nc;
+    if (total > A.maxc) A.overflow[env] = max(A.overflow[env], total);
+  }
+}
+
 namespace nsdi {
+
+template <class R>
+cudaError_t launch_batch_collide(int nblk, int threads, size_t smem, cudaStream_t s, const BatchArgs<R>& A) {
+  k_batch_collide<R><<<nblk, threads, smem, s>>>(A);
+  return cudaGetLastError();
+}
+template cudaError_t launch_batch_collide<float>(int, int, size_t, cudaStream_t, const BatchArgs<float>&);
+template cudaError_t launch_batch_collide<double>(int, int, size_t, cudaStream_t, const BatchArgs<double>&);
 
 template <class R> cudaError_t batch_warp_setup(int max_optin, int threads, size_t smem, int* blocks_per_sm) {
   cudaError_t e = cudaFuncSetAttribute(k_batch_warp<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_batch_collide<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_batch_warp<R>, threads, smem);
 }

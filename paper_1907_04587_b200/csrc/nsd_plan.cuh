@@ -212,6 +212,7 @@ template <class R> struct BatchArgs {
   nsd::wp::Plan wplan;        // per-env shared-memory layout of k_batch_warp
   unsigned long long* wptime;  // k_batch_warp phase cycles (NSD_PHASE_TIMING) or null
   R* wlam;                    // k_batch_warp: per env 5 x 32 multipliers ([row][lane])
+  int collide_cap;            // k_batch_collide: candidates kept per env in shared memory
   int warp_max_obj;           // k_batch_warp solves envs with nj + nc <= this (<= 32); mode 2 the rest
   int profile;                // k_batch_warp: clock64 cycles inside the PCR loops / per env into counters[1..2]
 };
@@ -266,5 +267,7 @@ cudaError_t launch_batch_block(int nblk, int threads, size_t smem, cudaStream_t 
 template <class R> cudaError_t batch_warp_setup(int max_optin, int threads, size_t smem, int* blocks_per_sm);
 template <class R>
 cudaError_t launch_batch_warp(int nblk, int threads, size_t smem, cudaStream_t s, const BatchArgs<R>& A);
+template <class R>
+cudaError_t launch_batch_collide(int nblk, int threads, size_t smem, cudaStream_t s, const BatchArgs<R>& A);
 
 }  // namespace nsdi

@@ -219,33 +219,37 @@ def test_batch_warp_solver_matches_object_solver_fp64(routing):
 
 
 def test_batch_large_envs_track_oracle_fp64():
-    """Envs routed to the large-env launch (more than NSD_WARP_MAX_OBJ - 8 contacts, the
-    threshold picked from the oracle's contact counts so that the batch mixes both) and the
-    warp solver side by side in one actuated batch, both against the oracle every step."""
+    """Envs routed to the large-env launch (more than 10 contacts: NSD_WARP_MAX_OBJ=18)
+    and envs solved by the warp solver side by side in one actuated batch, both against
+    the oracle every step. Half the ants start 0.3 m higher, so they land later and the
+    batch holds both contact counts."""
     n_env, steps = 16, 25
-    s0 = _batch(1, "fp64")[1]
+    b, s0 = _batch(n_env, "fp64", env={"NSD_WARP_MAX_OBJ": "18"})
     nj = s0.topology.n_joints
+    q, u = b.get_state()
+    q = q.copy()
+    bt = s0.topology.a["body_type"]
+    zc = [7 * i + 2 for i in range(len(bt))]  # z of every (rigid) body
+    q[: n_env // 2, zc] += 0.3
+    b.set_state(q.reshape(-1), u.reshape(-1))
     worlds = [O.OracleWorld("c5", e) for e in range(n_env)]
-    taus, states, counts = [], [], []
+    for e, w in enumerate(worlds):
+        w.set_state(q[e], u[e])
+    mixed = 0
     for st in range(steps):
         tau = np.stack([_torques(e, st, nj) for e in range(n_env)])
         for e, w in enumerate(worlds):
             w.set_joint_torques(tau[e])
             assert w.step(1) == 0
-        taus.append(tau)
-        states.append([w.state()[0] for w in worlds])
-        counts.append([len(w.contacts()[0]) for w in worlds])
-    counts = np.array(counts)
-    thr = int(np.median(counts))
-    assert 0 < int((counts > thr).sum()) < counts.size
-    b, _ = _batch(n_env, "fp64", env={"NSD_WARP_MAX_OBJ": str(nj + thr)})
-    for st in range(steps):
-        b.step(s0.h, s0.gravity, torque=taus[st].reshape(-1))
+        b.step(s0.h, s0.gravity, torque=tau.reshape(-1))
         res = b.results()
-        q, _ = b.get_state()
-        assert np.array_equal(res["n_contacts"], counts[st]), st
-        for e in range(n_env):
-            assert rel_err(q[e], states[st][e]) < 1e-8, (st, e)
+        routed = int((res["n_contacts"] > 10).sum())
+        mixed += 0 < routed < n_env
+        qg, _ = b.get_state()
+        for e, w in enumerate(worlds):
+            assert res["n_contacts"][e] == len(w.contacts()[0]), (st, e)
+            assert rel_err(qg[e], w.state()[0]) < 1e-8, (st, e)
+    assert mixed > 0
 
 
 def test_batch_counters_count_pcr_iterations():
