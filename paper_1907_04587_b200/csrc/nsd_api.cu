@@ -632,7 +632,8 @@ template <class R> struct Batch final : BatchBase {
   int warp_epb = 2;        // environments (warps) per block of k_batch_warp (64 threads, 7 blocks/SM)
   int warp_max_obj = 32;   // NSD_WARP_MAX_OBJ (tests) routes smaller envs to the object solver too
   int collide_cap = 64;    // k_batch_collide's per-env candidate list (>= max_contacts)
-  bool legacy_collide = false;  // NSD_BATCH_COLLIDE=sub: narrow phase through k_batch_sub mode 1
+  size_t collide_smem = 0;
+  DBuf wsetup;             // rigid path: per env u~, I_w, I_w^-1
   size_t warp_smem = 0;
   long env_steps = 0;
   bool profile = false;     // bit 0 of nsd_batch_profile: in-kernel cycle counters
@@ -845,7 +846,9 @@ template <class R> struct Batch final : BatchBase {
       if (const char* e = std::getenv("NSD_WARP_EPB")) warp_epb = std::max(1, std::min(8, std::atoi(e)));
       if (const char* e = std::getenv("NSD_WARP_MAX_OBJ")) warp_max_obj = std::max(0, std::min(32, std::atoi(e)));
       collide_cap = std::max(64, maxc);
-      if (const char* e = std::getenv("NSD_BATCH_COLLIDE")) legacy_collide = std::string(e) == "sub";
+      const int nview = (H.ncoord + H.ndof + 9 * H.nb + 1) & ~1;
+      collide_smem = 4 * (sizeof(R) * nview + sizeof(int4) * collide_cap);
+      wsetup.alloc(sizeof(R) * (size_t)(H.ndof + 12 * H.nd3) * n_env);
       warp_smem = static_cast<size_t>(wplan.bytes) * warp_epb;
       int per_sm = 0;
       NSD_CK(batch_warp_setup<R>(max_optin, 32 * warp_epb, warp_smem, &per_sm));
@@ -989,6 +992,9 @@ template <class R> struct Batch final : BatchBase {
     A.wjinc = warp_path ? wjinc.as<int>() + H.nb + 1 : nullptr;
     A.wplan = wplan;
     A.warp_max_obj = warp_max_obj;
+    A.collide_cap = collide_cap;
+    A.wsetup = wsetup.as<R>();
+    A.wsetup_stride = H.ndof + 12 * H.nd3;
     A.wlam = wlam.as<R>();
     A.wptime = wptime.as<unsigned long long>();
     A.mode = 0;
@@ -1016,12 +1022,7 @@ template <class R> struct Batch final : BatchBase {
       A1.row_pool = 0;
       A1.ptime = nullptr;
       if (ev) NSD_CK(cudaEventRecord(ev[0], stream));
-      if (npairs > 0 && !legacy_collide) {
-        A1.collide_cap = collide_cap;
-        NSD_CK(launch_batch_collide<R>((n_env + 3) / 4, 128, 4 * collide_cap * sizeof(nsd::CandD<R>), stream, A1));
-      } else {
-        NSD_CK(launch_batch_sub<R>(16, nblk, 16 * epb, 0, stream, A1));
-      }
+      NSD_CK(launch_batch_collide<R>((n_env + 3) / 4, 128, collide_smem, stream, A1));
       if (ev) NSD_CK(cudaEventRecord(ev[1], stream));
       NSD_CK(launch_batch_warp<R>((n_env + warp_epb - 1) / warp_epb, 32 * warp_epb, warp_smem, stream, A));
       if (ev) NSD_CK(cudaEventRecord(ev[2], stream));

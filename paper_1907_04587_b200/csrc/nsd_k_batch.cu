@@ -32,11 +32,10 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
   R* qrot = hr + P.qrot;
   int* cbody = hi + P.cbody;
   int nc = 0, total = 0;
-  if (A.mode == 2) {  // narrow phase and setup ran in the mode-1 launch; the slabs hold them
-    nc = A.nc_out[env];
-    W.f_extra = nullptr;
-  } else {
   env_setup(t, A, env, W, qs, us, cr, qrot);
+  if (A.mode == 2) {  // the contact set comes from the narrow-phase launch (k_batch_collide)
+    nc = A.nc_out[env];
+  } else {
   // ---- narrow phase over shape pairs with the unconstrained velocity
   nsd::BodyView<R> view{T.btype, T.bdof, T.bcoord, W.q0, W.ut, qrot};
   nsd::CandD<R>* cand = A.cand + (size_t)env * A.npairs * 4;
@@ -89,7 +88,6 @@ __device__ void batch_env(Team& t, const BatchArgs<R>& A, int env, R* hr, R* poo
     A.nc_out[env] = nc;
     if (total > A.maxc) A.overflow[env] = max(A.overflow[env], total);
   }
-  if (A.mode == 1) return;
   }  // narrow phase
   W.nc = nc;
   W.normal_begin = T.rows_static;

@@ -37,11 +37,12 @@ template <class R> __global__ void __launch_bounds__(64, warp_minb<R>()) k_batch
   R* cr = A.cold_r + (size_t)env * P.coldR;
   int* ci = A.cold_i + (size_t)env * P.coldI;
   nsd::wp::EnvIO<R> io;
-  io.q0 = cr + P.q0;
-  io.u0 = cr + P.u0;
-  io.ut = cr + P.ut;
-  io.iw6 = cr + P.iw6;
-  io.iwi6 = hr + P.iwi6;
+  const R* ws = A.wsetup + (size_t)env * A.wsetup_stride;
+  io.q0 = A.qs + (size_t)env * T.ncoord;  // written back only at the end of the step
+  io.u0 = A.us + (size_t)env * T.ndof;
+  io.ut = ws;
+  io.iw6 = ws + T.ndof;
+  io.iwi6 = ws + T.ndof + 6 * T.nd3;
   io.cbody = hi + P.cbody;
   io.cgeo = cr + P.cgeo;
   io.lam = A.wlam + (size_t)env * (nsd::wp::kRows * 32);
@@ -66,16 +67,78 @@ template <class R> __global__ void __launch_bounds__(64, warp_minb<R>()) k_batch
 }
 
 
-// Narrow phase + step setup, one warp per environment (the rigid path's first
-// launch; k_batch_sub mode 1 does the same with sub-warp teams): env_setup, then
-// the shape pairs 32 per round, one per lane (pair_contacts, collision.cpp:253-287).
-// Each round's candidates are appended to the env's compact shared-memory list in
-// (pair, k) generation order by a warp prefix sum; each candidate's rank under the
-// canonical (a.body, b.body, feature) order, ties by generation order
-// (collision.cpp:290-295), places it in the env's contact slabs. A list longer
-// than its capacity (>= max_contacts) only occurs with a contact overflow, which
-// is reported as an error; the contacts kept then come from the stored prefix.
-template <class R> __global__ void __launch_bounds__(128, 4) k_batch_collide(BatchArgs<R> A) {
+// Step setup of one rigid body for the warp path, body lane b (step_world's torque
+// hook + newton_setup, scene.cpp:709-732, newton.cpp:327-338): the arithmetic of
+// env_setup / nsd::newton_setup for a rigid body. Needs the rotation cache of
+// every body at q- (the torque hook rotates the joint axis by body a's frame).
+// Writes u~ (also to the shared-memory view of the narrow phase), I_w and I_w^-1.
+template <class R>
+__device__ __forceinline__ void rigid_setup(const BatchArgs<R>& A, int env, int b, const R* q0, const R* u0,
+                                            const R* rot, R* ut_view, R* ut, R* iw6, R* iwi6) {
+  const nsd::Topo<R>& T = A.T;
+  const int d = T.bdof[b], cd = T.bcoord[b];
+  const R m = T.bmass[b], h = A.h;
+  nsd::V3<R> f = nsd::v3(m * A.grav[0], m * A.grav[1], m * A.grav[2]);
+  nsd::V3<R> tx = nsd::v3(R(0), R(0), R(0));  // joint torques about revolute axes at q- (extension hook)
+  if (A.torque) {
+    for (int j = 0; j < T.nj; ++j) {
+      if (T.jkind[j] != 1) continue;
+      const int ja = T.jbody[2 * j], jb = T.jbody[2 * j + 1];
+      if (ja != b && jb != b) continue;
+      const R tau = A.torque_double ? R(static_cast<const double*>(A.torque)[(size_t)env * T.nj + j])
+                                    : R(static_cast<const float*>(A.torque)[(size_t)env * T.nj + j]);
+      const nsd::V3<R> axl = nsd::ld3(A.jframe + 21 * j + 6);
+      nsd::M3<R> Rj;
+      if (ja >= 0)
+        for (int i = 0; i < 9; ++i) Rj.a[i] = rot[9 * ja + i];
+      const nsd::V3<R> ax = ja < 0 ? axl : nsd::mul(Rj, axl);
+      if (ja == b) tx = tx + tau * ax;
+      if (jb == b) tx = tx - tau * ax;
+    }
+    f = f + nsd::v3(R(0), R(0), R(0));  // the hook's zero linear part, added as newton_setup adds f_extra
+  }
+  const nsd::V3<R> ul = nsd::ld3(u0 + d) + h * (f / m);
+  const nsd::M3<R> Rm = nsd::quat_rot(q0[cd + 3], q0[cd + 4], q0[cd + 5], q0[cd + 6]);
+  nsd::M3<R> I;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) I.a[i] = T.binertia[9 * b + i];
+  const nsd::M3<R> Iw = nsd::mul(nsd::mul(Rm, I), nsd::transpose(Rm));
+  const nsd::M3<R> Ii = nsd::inverse3(Iw);
+  const nsd::V3<R> w = nsd::ld3(u0 + d + 3);
+  nsd::V3<R> tq = -nsd::cross(w, nsd::mul(Iw, w));
+  if (A.torque) tq = tq + tx;
+  const nsd::V3<R> ua = w + h * nsd::mul(Ii, tq);
+  nsd::st3(ut + d, ul);
+  nsd::st3(ut + d + 3, ua);
+  nsd::st3(ut_view + d, ul);
+  nsd::st3(ut_view + d + 3, ua);
+  const int ab3 = 6 * (d / 3 + 1);
+  const R s6[6] = {Iw(0, 0), Iw(1, 1), Iw(2, 2), Iw(0, 1), Iw(0, 2), Iw(1, 2)};
+  const R i6[6] = {Ii(0, 0), Ii(1, 1), Ii(2, 2), Ii(0, 1), Ii(0, 2), Ii(1, 2)};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    iw6[ab3 + k] = s6[k];
+    iwi6[ab3 + k] = i6[k];
+  }
+}
+
+// Narrow phase + step setup, one warp per rigid environment (the rigid path's
+// first launch). Body lanes stage q-, the rotation cache and u~ in shared memory
+// (rigid_setup), then the shape pairs run 32 per round, one per lane
+// (pair_contacts, collision.cpp:253-287) against that view, writing their candidates
+// to per-pair slots in global memory. Each round's candidate keys are appended to
+// the env's compact shared-memory list in (pair, k) generation order by a warp
+// prefix sum; each candidate's rank under the canonical
+// (a.body, b.body, feature) order, ties by generation order (collision.cpp:290-295),
+// places it in the env's contact slabs. Only what k_batch_warp reads is written:
+// u~, I_w, I_w^-1 (compact per env) and the contact set; the large-env launch
+// recomputes its own setup. A candidate list longer than its capacity
+// (>= max_contacts) only occurs with a contact overflow, which is an error; the
+// contacts kept then come from the stored prefix.
+#ifndef NSD_COLLIDE_MINB
+#define NSD_COLLIDE_MINB 4
+#endif
+template <class R> __global__ void __launch_bounds__(128, NSD_COLLIDE_MINB) k_batch_collide(BatchArgs<R> A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int env = blockIdx.x * (blockDim.x >> 5) + wib;
@@ -83,30 +146,37 @@ template <class R> __global__ void __launch_bounds__(128, 4) k_batch_collide(Bat
   const nsd::Topo<R>& T = A.T;
   const WorkPlan& P = A.plan;
   const int cap = A.collide_cap;
-  nsd::CandD<R>* cand = reinterpret_cast<nsd::CandD<R>*>(smem) + (size_t)wib * cap;
-  R* hr = reinterpret_cast<R*>(A.hot_global + (size_t)env * A.hot_bytes);
-  int* hi = P.hot_ints(hr);
-  R* cr = A.cold_r + (size_t)env * P.coldR;
-  int* ci = A.cold_i + (size_t)env * P.coldI;
-  nsd::Work<R> W = P.template bind<R>(hr, hi, cr, ci);
-  W.jframe = A.jframe;
-  W.h = A.h;
-  W.grav[0] = A.grav[0];
-  W.grav[1] = A.grav[1];
-  W.grav[2] = A.grav[2];
-  R* qrot = hr + P.qrot;
-  nsd::WarpTeam t(lane);
-  env_setup(t, A, env, W, A.qs + (size_t)env * T.ncoord, A.us + (size_t)env * T.ndof, cr, qrot);
-  const nsd::BodyView<R> view{T.btype, T.bdof, T.bcoord, W.q0, W.ut, qrot};
+  const int nview = (T.ncoord + T.ndof + 9 * T.nb + 1) & ~1;  // q-, u~, rotations (R elements)
+  R* view_r = reinterpret_cast<R*>(smem) + (size_t)wib * nview;
+  int4* key = reinterpret_cast<int4*>(reinterpret_cast<R*>(smem) + 4 * nview) + (size_t)wib * cap;
+  R* vq = view_r;
+  R* vu = vq + T.ncoord;
+  R* vrot = vu + T.ndof;
+  const R* qs = A.qs + (size_t)env * T.ncoord;
+  const R* us = A.us + (size_t)env * T.ndof;
+  for (int i = lane; i < T.ncoord; i += 32) vq[i] = qs[i];
+  __syncwarp();
+  if (lane < T.nb) {
+    const nsd::M3<R> m = nsd::body_rot(T, vq, lane);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) vrot[9 * lane + i] = m.a[i];
+  }
+  __syncwarp();
+  R* ws = A.wsetup + (size_t)env * A.wsetup_stride;
+  if (lane < T.nb) rigid_setup(A, env, lane, vq, us, vrot, vu, ws, ws + T.ndof, ws + T.ndof + 6 * T.nd3);
+  __syncwarp();
+  // candidates are generated in the env's per-pair global slots (4 per pair, L2),
+  // their keys appended to the compact shared-memory list in generation order
+  const nsd::BodyView<R> view{T.btype, T.bdof, T.bcoord, vq, vu, vrot};
+  nsd::CandD<R>* gc = A.cand + (size_t)env * A.npairs * 4;
   int total = 0;
   for (int p0 = 0; p0 < A.npairs; p0 += 32) {
     const int p = p0 + lane;
-    nsd::CandD<R> loc[4];
     int n = 0;
     if (p < A.npairs) {
       const int2 ij = A.pairs[p];
       R th, mu;
-      n = nsd::pair_contacts(view, A.shapes[ij.x], A.shapes[ij.y], A.h, A.margin, A.mu_default, loc, &th, &mu);
+      n = nsd::pair_contacts(view, A.shapes[ij.x], A.shapes[ij.y], A.h, A.margin, A.mu_default, gc + 4 * p, &th, &mu);
     }
     int incl = n;  // inclusive prefix sum of the counts over the lanes
 #pragma unroll
@@ -116,39 +186,42 @@ template <class R> __global__ void __launch_bounds__(128, 4) k_batch_collide(Bat
     }
     const int base = total + incl - n;
     for (int k = 0; k < n; ++k)
-      if (base + k < cap) cand[base + k] = loc[k];
+      if (base + k < cap) key[base + k] = make_int4(gc[4 * p + k].a, gc[4 * p + k].b, gc[4 * p + k].feature, 4 * p + k);
     total += __shfl_sync(0xffffffffu, incl, 31);
   }
   __syncwarp();
   const int stored = total < cap ? total : cap;
   const int nc = total < A.maxc ? total : A.maxc;
-  int* cbody = hi + P.cbody;
-  int* cfeat = ci + P.cfeat;
+  R* hr = reinterpret_cast<R*>(A.hot_global + (size_t)env * A.hot_bytes);
+  int* cbody = P.hot_ints(hr) + P.cbody;
+  R* cr = A.cold_r + (size_t)env * P.coldR;
+  int* cfeat = A.cold_i + (size_t)env * P.coldI + P.cfeat;
   R* cgeo = cr + P.cgeo;
   for (int i = lane; i < stored; i += 32) {
-    const nsd::CandD<R> c = cand[i];
+    const int4 c = key[i];
     int rank = 0;
     for (int j = 0; j < stored; ++j) {
-      const int oa = cand[j].a, ob = cand[j].b, of = cand[j].feature;
-      if (nsd::canonical_less(oa, ob, of, c.a, c.b, c.feature) || (oa == c.a && ob == c.b && of == c.feature && j < i))
+      const int4 o = key[j];
+      if (nsd::canonical_less(o.x, o.y, o.z, c.x, c.y, c.z) || (o.x == c.x && o.y == c.y && o.z == c.z && j < i))
         ++rank;
     }
     if (rank >= nc) continue;
-    cbody[2 * rank] = c.a;
-    cbody[2 * rank + 1] = c.b;
-    cfeat[rank] = c.feature;
+    const nsd::CandD<R>& cd = gc[c.w];
+    cbody[2 * rank] = c.x;
+    cbody[2 * rank + 1] = c.y;
+    cfeat[rank] = c.z;
     R* g = cgeo + 17 * rank;
-    nsd::V3<R> nn = nsd::get3(c.n), d1, d2;
+    nsd::V3<R> nn = nsd::get3(cd.n), d1, d2;
     nsd::tangent_basis(nn, d1, d2);
     for (int k = 0; k < 3; ++k) {
-      g[k] = c.la[k];
-      g[3 + k] = c.lb[k];
-      g[6 + k] = c.n[k];
+      g[k] = cd.la[k];
+      g[3 + k] = cd.lb[k];
+      g[6 + k] = cd.n[k];
     }
     nsd::st3(g + 9, d1);
     nsd::st3(g + 12, d2);
-    g[15] = c.thick;
-    g[16] = c.mu;
+    g[15] = cd.thick;
+    g[16] = cd.mu;
   }
   if (lane == 0) {  // contact count; overflow is sticky until nsd_batch_results
     A.nc_out[env] = nc;

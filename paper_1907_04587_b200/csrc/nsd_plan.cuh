@@ -213,6 +213,8 @@ template <class R> struct BatchArgs {
   unsigned long long* wptime;  // k_batch_warp phase cycles (NSD_PHASE_TIMING) or null
   R* wlam;                    // k_batch_warp: per env 5 x 32 multipliers ([row][lane])
   int collide_cap;            // k_batch_collide: candidates kept per env in shared memory
+  R* wsetup;                  // rigid path: per env u~ (ndof), I_w and I_w^-1 (6 per dof3 block each)
+  int wsetup_stride;
   int warp_max_obj;           // k_batch_warp solves envs with nj + nc <= this (<= 32); mode 2 the rest
   int profile;                // k_batch_warp: clock64 cycles inside the PCR loops / per env into counters[1..2]
 };
