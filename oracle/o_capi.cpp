@@ -636,4 +636,235 @@ int orc_run(const char* name, unsigned seed, int steps, const char* out_dir) {
   }
 }
 
+
+// ---------------- KAT entry points (tests/test_oracle_kats.py) --------------------
+// A state of nb bodies from arrays: type (0 particle / 1 rigid), mass, inertia
+// (9 per body, body frame), q (num_coord) and u (num_dof, may be null).
+static State make_state(int nb, const int* type, const double* mass, const double* inertia, const double* q,
+                        const double* u) {
+  State s;
+  for (int b = 0; b < nb; ++b) {
+    Body bd;
+    bd.type = static_cast<BodyType>(type[b]);
+    bd.mass = mass ? mass[b] : 1.0;
+    if (inertia) bd.inertia = m3_from(inertia + 9 * b);
+    s.bodies.push_back(bd);
+  }
+  s.finalize_layout();
+  if (q)
+    for (int k = 0; k < s.num_coord; ++k) s.q[k] = q[k];
+  if (u)
+    for (int k = 0; k < s.num_dof; ++k) s.u[k] = u[k];
+  return s;
+}
+
+// bodies.cpp:7-22 layout: dof/coord offsets, totals[2] = {num_dof, num_coord}.
+void orc_layout(int nb, const int* type, int* dof_off, int* coord_off, int* totals) {
+  const State s = make_state(nb, type, nullptr, nullptr, nullptr, nullptr);
+  for (int b = 0; b < nb; ++b) {
+    dof_off[b] = s.dof_off[b];
+    coord_off[b] = s.coord_off[b];
+  }
+  totals[0] = s.num_dof;
+  totals[1] = s.num_coord;
+}
+
+// 0.5 * quaternion_rate_matrix(t) * w (bodies.cpp:39-46).
+void orc_quat_rate(const double* t, const double* w, double* out) {
+  const V4 r = quat_rate(V4(t[0], t[1], t[2], t[3]), V3(w[0], w[1], w[2]));
+  for (int k = 0; k < 4; ++k) out[k] = r[k];
+}
+
+// integrate_coordinates (bodies.cpp:78-86) on a state; q in-out. 0 ok, 1 invalid.
+int orc_integrate_state(int nb, const int* type, double* q, const double* u, double h) {
+  try {
+    State s = make_state(nb, type, nullptr, nullptr, q, nullptr);
+    integrate(s, VecX(u, u + s.num_dof), h);
+    for (int k = 0; k < s.num_coord; ++k) q[k] = s.q[k];
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// BlockDiagMass at q (bodies.cpp:88-198): M v, M^-1 (M v), and the sparse-row
+// quadratic form inverse_quadratic(idx, val).
+void orc_mass_kat(int nb, const int* type, const double* mass, const double* inertia, const double* q,
+                  const double* v, double* mv, double* minv_mv, int nnz, const int* idx, const double* val,
+                  double* quad) {
+  const State s = make_state(nb, type, mass, inertia, q, nullptr);
+  const BlockMass m = mass_matrix(s);
+  const VecX a = m.apply(VecX(v, v + s.num_dof));
+  const VecX b = m.apply_inverse(a);
+  for (int k = 0; k < s.num_dof; ++k) {
+    mv[k] = a[k];
+    minv_mv[k] = b[k];
+  }
+  *quad = m.inverse_quadratic(idx, val, nnz);
+}
+
+// detect (collision.cpp:239-297) on a fixture: shapes' dparam = normal 3, offset,
+// radius, half_extents 3, thickness, mu (11 each). Returns the contact count
+// (export layout of orc_world_contacts, at most cap written) or -1.
+int orc_detect(int nb, const int* type, const double* mass, const double* inertia, const double* q,
+               const double* u_predict, int ns, const int* sbody, const int* skind, const double* sparam, double h,
+               double margin, double mu_default, int cap, int* ib, double* db) {
+  try {
+    const State s = make_state(nb, type, mass, inertia, q, nullptr);
+    std::vector<AttachedShape> shapes(ns);
+    for (int i = 0; i < ns; ++i) {
+      const double* d = sparam + 11 * i;
+      shapes[i].body = sbody[i];
+      shapes[i].shape.kind = static_cast<ShapeKind>(skind[i]);
+      shapes[i].shape.normal = V3(d[0], d[1], d[2]);
+      shapes[i].shape.offset = d[3];
+      shapes[i].shape.radius = d[4];
+      shapes[i].shape.half_extents = V3(d[5], d[6], d[7]);
+      shapes[i].shape.thickness = d[8];
+      shapes[i].shape.mu = d[9];
+    }
+    ContactParams p;
+    p.margin = margin;
+    p.mu_default = mu_default;
+    const VecX up = u_predict ? VecX(u_predict, u_predict + s.num_dof) : VecX(s.num_dof, 0.0);
+    const std::vector<Contact> cs = detect(s, shapes, up, h, p);
+    std::vector<Contact> head(cs.begin(), cs.begin() + std::min<size_t>(cs.size(), static_cast<size_t>(cap)));
+    export_contacts(head, ib, db);
+    return static_cast<int>(cs.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// contact_gap and contact_normal_row (constraints.cpp:56-91) at q; row dense over the dofs.
+double orc_contact_gap_row(int nb, const int* type, const double* q, int a_body, const double* a_local, int b_body,
+                           const double* b_local, const double* normal, double thickness, double* row) {
+  const State s = make_state(nb, type, nullptr, nullptr, q, nullptr);
+  Contact c;
+  c.a = {a_body, V3(a_local[0], a_local[1], a_local[2])};
+  c.b = {b_body, V3(b_local[0], b_local[1], b_local[2])};
+  c.normal = V3(normal[0], normal[1], normal[2]);
+  c.thickness = thickness;
+  const Row r = contact_normal_row(c, s);
+  for (int k = 0; k < s.num_dof; ++k) row[k] = 0.0;
+  for (size_t k = 0; k < r.idx.size(); ++k) row[r.idx[k]] += r.val[k];
+  return contact_gap(c, s);
+}
+
+// bind_joint at q_bind (world anchor, axis; constraints.cpp:222-263), then
+// joint_rows at q_eval (:141-220): values, compliances, dense Jacobian rows.
+int orc_joint_rows(int kind, double compliance, double stiffness, int nb, const int* type, int body_a, int body_b,
+                   const double* q_bind, const double* anchor, const double* axis, const double* q_eval,
+                   double* values, double* comp, double* jac) {
+  try {
+    const State sb = make_state(nb, type, nullptr, nullptr, q_bind, nullptr);
+    Joint j;
+    j.kind = static_cast<JointKind>(kind);
+    j.body_a = body_a;
+    j.body_b = body_b;
+    j.compliance = compliance;
+    j.stiffness = stiffness;
+    bind_joint(j, sb, V3(anchor[0], anchor[1], anchor[2]), V3(axis[0], axis[1], axis[2]));
+    const State se = make_state(nb, type, nullptr, nullptr, q_eval, nullptr);
+    const std::vector<BRow> rows = joint_rows(j, se);
+    for (size_t i = 0; i < rows.size(); ++i) {
+      values[i] = rows[i].value;
+      comp[i] = rows[i].compliance;
+      for (int k = 0; k < se.num_dof; ++k) jac[i * se.num_dof + k] = 0.0;
+      for (size_t k = 0; k < rows[i].jac.idx.size(); ++k) jac[i * se.num_dof + rows[i].jac.idx[k]] += rows[i].jac.val[k];
+    }
+    return static_cast<int>(rows.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// SparseMatrix::from_triplets (linalg.cpp:9-40): off[rows+1], idx/val[nnz]. Returns
+// nnz, or -1 (invalid_argument).
+int orc_csr(int rows, int cols, int nt, const int* r, const int* c, const double* v, int* off, int* idx, double* val,
+            int* valid) {
+  try {
+    std::vector<Trip> t(nt);
+    for (int i = 0; i < nt; ++i) t[i] = {r[i], c[i], v[i]};
+    const Csr a = Csr::from_triplets(rows, cols, t);
+    for (int i = 0; i <= rows; ++i) off[i] = a.off[i];
+    for (int i = 0; i < a.nnz(); ++i) {
+      idx[i] = a.idx[i];
+      val[i] = a.val[i];
+    }
+    *valid = a.valid() ? 1 : 0;
+    return a.nnz();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// y = A x (mode 0: spmv, OpenMP rows; 1: spmv_serial; 2: spmv_transpose) on the
+// CSR of the triplets; x has nx entries (a mismatch throws, returns 1).
+int orc_spmv(int rows, int cols, int nt, const int* r, const int* c, const double* v, int mode, const double* x,
+             int nx, double* y) {
+  try {
+    std::vector<Trip> t(nt);
+    for (int i = 0; i < nt; ++i) t[i] = {r[i], c[i], v[i]};
+    const Csr a = Csr::from_triplets(rows, cols, t);
+    const VecX xv(x, x + nx);
+    const VecX out = mode == 0 ? spmv(a, xv) : (mode == 1 ? spmv_serial(a, xv) : spmv_transpose(a, xv));
+    for (size_t i = 0; i < out.size(); ++i) y[i] = out[i];
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// diagonal_preconditioner (solvers.cpp:178-184) of the square CSR of the triplets.
+void orc_diag_precond(int n, int nt, const int* r, const int* c, const double* v, double* out) {
+  std::vector<Trip> t(nt);
+  for (int i = 0; i < nt; ++i) t[i] = {r[i], c[i], v[i]};
+  const VecX d = diag_precond(Csr::from_triplets(n, n, t));
+  for (int i = 0; i < n; ++i) out[i] = d[i];
+}
+
+// deformation_gradient (materials.cpp:23-30) of a tet with rest / current vertices (12 each).
+void orc_deformation_gradient(const double* rest12, const double* pos12, double* f9) {
+  V3 r[4], p[4];
+  for (int k = 0; k < 4; ++k) {
+    r[k] = V3(rest12[3 * k], rest12[3 * k + 1], rest12[3 * k + 2]);
+    p[k] = V3(pos12[3 * k], pos12[3 * k + 1], pos12[3 * k + 2]);
+  }
+  const Tet e = make_tet({0, 1, 2, 3}, r[0], r[1], r[2], r[3]);
+  m3_to(deformation_gradient(p[0], p[1], p[2], p[3], e), f9);
+}
+
+// compute_material_rows (materials.cpp:217-223) over ne disjoint Neo-Hookean tets
+// (vertex 4e..4e+3), OpenMP (parallel = 1) or serial: c (3), jac (36), comp (9) per tet.
+void orc_material_rows_many(int ne, double young, double poisson, const double* rest, const double* pos,
+                            int parallel, double* c, double* jac, double* comp) {
+  TetMesh m;
+  m.material.model = MatModel::NeoHookean;
+  m.material.young = young;
+  m.material.poisson = poisson;
+  std::vector<V3> p(4 * ne);
+  for (int e = 0; e < ne; ++e) {
+    V3 r[4];
+    for (int k = 0; k < 4; ++k) {
+      r[k] = V3(rest[12 * e + 3 * k], rest[12 * e + 3 * k + 1], rest[12 * e + 3 * k + 2]);
+      p[4 * e + k] = V3(pos[12 * e + 3 * k], pos[12 * e + 3 * k + 1], pos[12 * e + 3 * k + 2]);
+    }
+    m.elements.push_back(make_tet({4 * e, 4 * e + 1, 4 * e + 2, 4 * e + 3}, r[0], r[1], r[2], r[3]));
+  }
+  m.prepare();
+  std::vector<MatRows> out;
+  compute_material_rows(m, p, out, parallel != 0);
+  for (int e = 0; e < ne; ++e)
+    for (int i = 0; i < 3; ++i) {
+      c[3 * e + i] = out[e].c[i];
+      for (int k = 0; k < 12; ++k) jac[36 * e + 12 * i + k] = out[e].jac[i][k];
+      for (int k = 0; k < 3; ++k) comp[9 * e + 3 * i + k] = out[e].comp[i][k];
+    }
+}
 }  // extern "C"

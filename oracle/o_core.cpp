@@ -391,7 +391,6 @@ V4 normalized_quat(const V4& t) {
   return V4(t[0] / n, t[1] / n, t[2] / n, t[3] / n);
 }
 
-namespace {
 // 0.5 * Q(theta) * omega with Q from src/bodies.cpp:39-46.
 V4 quat_rate(const V4& t, const V3& w) {
   const double q[4][3] = {{-t[1], -t[2], -t[3]},
@@ -402,7 +401,6 @@ V4 quat_rate(const V4& t, const V3& w) {
   for (int i = 0; i < 4; ++i) r[i] = 0.5 * (q[i][0] * w[0] + q[i][1] * w[1] + q[i][2] * w[2]);
   return r;
 }
-}  // namespace
 
 // src/bodies.cpp:58-86: rates from the state's current coordinates, then
 // q = q_from + h*rates, then renormalise the quaternions.

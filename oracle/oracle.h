@@ -92,6 +92,7 @@ struct State {
   M3 world_inertia(int b) const;
 };
 V4 normalized_quat(const V4& t);                                          // bodies.cpp:52-56
+V4 quat_rate(const V4& t, const V3& w);  // 0.5 * quaternion_rate_matrix(t) * w, bodies.cpp:39-46
 void integrate_from(State& s, const VecX& q_from, const VecX& u_new, double h);  // :78-86
 void integrate(State& s, const VecX& u_new, double h);
 

@@ -47,6 +47,7 @@ def lib():
         _lib.orc_world_h.restype = C.c_double
         _lib.orc_c5_bench.restype = C.c_double
         _lib.orc_action_torque.restype = C.c_double
+        _lib.orc_contact_gap_row.restype = C.c_double
     return _lib
 
 
@@ -60,6 +61,143 @@ def ip(a):
 
 def m3(a):
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(3, 3))
+
+
+def _f64(a, n=None):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1))
+    assert n is None or a.size == n
+    return a
+
+
+def _i32(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32).reshape(-1))
+
+
+# ---------------------------------------------------------------- state-level KAT helpers
+def layout(types):
+    t = _i32(types)
+    do, co, tot = np.zeros(len(t), np.int32), np.zeros(len(t), np.int32), np.zeros(2, np.int32)
+    lib().orc_layout(C.c_int(len(t)), ip(t), ip(do), ip(co), ip(tot))
+    return do, co, int(tot[0]), int(tot[1])
+
+
+def quat_rate(theta, omega):
+    out = np.zeros(4)
+    lib().orc_quat_rate(dp(_f64(theta, 4)), dp(_f64(omega, 3)), dp(out))
+    return out
+
+
+def integrate_state(types, q, u, h):
+    """integrate_coordinates (bodies.cpp:78-86); raises ValueError on invalid input."""
+    t, q = _i32(types), _f64(q).copy()
+    if lib().orc_integrate_state(C.c_int(len(t)), ip(t), dp(q), dp(_f64(u)), C.c_double(h)):
+        raise ValueError(lib().orc_last_error().decode())
+    return q
+
+
+def mass_kat(types, masses, inertias, q, v, idx=(), val=()):
+    t = _i32(types)
+    v = _f64(v)
+    mv, mi = np.zeros(v.size), np.zeros(v.size)
+    quad = C.c_double()
+    ii, vv = _i32(idx), _f64(val)
+    lib().orc_mass_kat(C.c_int(len(t)), ip(t), dp(_f64(masses)), dp(_f64(inertias)), dp(_f64(q)), dp(v), dp(mv),
+                       dp(mi), C.c_int(ii.size), ip(ii), dp(vv), C.byref(quad))
+    return mv, mi, quad.value
+
+
+def detect(types, masses, inertias, q, shapes, u_predict=None, h=0.0083, margin=0.01, mu_default=0.5, cap=256):
+    """detect (collision.cpp:239-297) on a fixture. shapes: list of dicts with body,
+    kind (0 half-space, 1 sphere, 2 box), normal, offset, radius, half_extents,
+    thickness, mu. Returns (ib, db) in orc_world_contacts' layout."""
+    t = _i32(types)
+    ns = len(shapes)
+    sb = _i32([sh["body"] for sh in shapes])
+    sk = _i32([sh["kind"] for sh in shapes])
+    sp = _f64([list(sh.get("normal", (0, 0, 1))) + [sh.get("offset", 0.0), sh.get("radius", 0.5)]
+               + list(sh.get("half_extents", (0.5, 0.5, 0.5))) + [sh.get("thickness", 0.0), sh.get("mu", -1.0), 0.0]
+               for sh in shapes])
+    ib, db = np.zeros((cap, 4), np.int32), np.zeros((cap, 22))
+    up = _f64(u_predict) if u_predict is not None else None
+    n = lib().orc_detect(C.c_int(len(t)), ip(t), dp(_f64(masses)), dp(_f64(inertias)), dp(_f64(q)),
+                         dp(up) if up is not None else None, C.c_int(ns), ip(sb), ip(sk), dp(sp), C.c_double(h),
+                         C.c_double(margin), C.c_double(mu_default), C.c_int(cap), ip(ib), dp(db))
+    if n < 0:
+        raise ValueError(lib().orc_last_error().decode())
+    return ib[:n], db[:n]
+
+
+def contact_gap_row(types, q, a_body, a_local, b_body, b_local, normal, thickness=0.0):
+    t = _i32(types)
+    _, _, ndof, _ = layout(t)
+    row = np.zeros(ndof)
+    g = lib().orc_contact_gap_row(C.c_int(len(t)), ip(t), dp(_f64(q)), C.c_int(a_body), dp(_f64(a_local, 3)),
+                                  C.c_int(b_body), dp(_f64(b_local, 3)), dp(_f64(normal, 3)), C.c_double(thickness),
+                                  dp(row))
+    return g, row
+
+
+def joint_rows(kind, types, body_a, body_b, q_bind, anchor, axis, q_eval, compliance=0.0, stiffness=0.0):
+    """bind_joint at q_bind, joint_rows at q_eval: (values, compliances, dense Jacobian)."""
+    t = _i32(types)
+    _, _, ndof, _ = layout(t)
+    vals, comp, jac = np.zeros(5), np.zeros(5), np.zeros(5 * ndof)
+    n = lib().orc_joint_rows(C.c_int(kind), C.c_double(compliance), C.c_double(stiffness), C.c_int(len(t)), ip(t),
+                             C.c_int(body_a), C.c_int(body_b), dp(_f64(q_bind)), dp(_f64(anchor, 3)),
+                             dp(_f64(axis, 3)), dp(_f64(q_eval)), dp(vals), dp(comp), dp(jac))
+    if n < 0:
+        raise ValueError(lib().orc_last_error().decode())
+    return vals[:n], comp[:n], jac[:n * ndof].reshape(n, ndof)
+
+
+def csr(rows, cols, trips):
+    r = _i32([x[0] for x in trips])
+    c = _i32([x[1] for x in trips])
+    v = _f64([x[2] for x in trips])
+    off, idx, val, valid = np.zeros(rows + 1, np.int32), np.zeros(max(len(trips), 1), np.int32), \
+        np.zeros(max(len(trips), 1)), C.c_int()
+    n = lib().orc_csr(C.c_int(rows), C.c_int(cols), C.c_int(len(trips)), ip(r), ip(c), dp(v), ip(off), ip(idx),
+                      dp(val), C.byref(valid))
+    if n < 0:
+        raise ValueError(lib().orc_last_error().decode())
+    return off, idx[:n], val[:n], bool(valid.value)
+
+
+def spmv(rows, cols, trips, x, mode=0):
+    """mode 0 spmv (OpenMP rows), 1 spmv_serial, 2 spmv_transpose; ValueError on a dimension mismatch."""
+    r = _i32([t[0] for t in trips]) if trips else np.zeros(1, np.int32)
+    c = _i32([t[1] for t in trips]) if trips else np.zeros(1, np.int32)
+    v = _f64([t[2] for t in trips]) if trips else np.zeros(1)
+    x = _f64(x)
+    y = np.zeros(cols if mode == 2 else rows)
+    if lib().orc_spmv(C.c_int(rows), C.c_int(cols), C.c_int(len(trips)), ip(r), ip(c), dp(v), C.c_int(mode), dp(x),
+                      C.c_int(x.size), dp(y)):
+        raise ValueError(lib().orc_last_error().decode())
+    return y
+
+
+def diag_precond(dense):
+    a = np.asarray(dense, dtype=np.float64)
+    n = a.shape[0]
+    ii, jj = np.nonzero(a)
+    out = np.zeros(n)
+    lib().orc_diag_precond(C.c_int(n), C.c_int(len(ii)), ip(_i32(ii)), ip(_i32(jj)), dp(_f64(a[ii, jj])), dp(out))
+    return out
+
+
+def deformation_gradient(rest, pos):
+    f = np.zeros(9)
+    lib().orc_deformation_gradient(dp(_f64(rest, 12)), dp(_f64(pos, 12)), dp(f))
+    return f.reshape(3, 3)
+
+
+def material_rows_many(young, poisson, rest, pos, parallel):
+    rest, pos = _f64(rest), _f64(pos)
+    ne = rest.size // 12
+    c, jac, comp = np.zeros(3 * ne), np.zeros(36 * ne), np.zeros(9 * ne)
+    lib().orc_material_rows_many(C.c_int(ne), C.c_double(young), C.c_double(poisson), dp(rest), dp(pos),
+                                 C.c_int(1 if parallel else 0), dp(c), dp(jac), dp(comp))
+    return c.reshape(ne, 3), jac.reshape(ne, 3, 12), comp.reshape(ne, 3, 3)
 
 
 # ---------------------------------------------------------------- KAT helpers
