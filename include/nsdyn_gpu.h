@@ -119,6 +119,14 @@ typedef struct nsd_step_out {
   int32_t n_iterations, n_rows;
   double final_residual_inf, final_comp_error, final_cone_violation, min_gap, min_diag_shift;
   int32_t aborted, converged;
+  /* optional: newton_iterations x (n_contacts + n_tets + num_dof + 1) decision bytes
+   * per Newton iteration: per contact bit0 normal J row kept, bit1
+   * friction active, bit2 W capped at 1e12, bit3 min-map stick branch (W = 0), bit4 NCP branch (FB origin /
+   * min-map c <= r lambda); per tet bit0 PSD projection, bit1 diagonal compliance
+   * fallback; per dof bit0 GS secant skipped, bit1 GS clamp, bit2 rigid dof zeroed
+   * (GS active iterations); last byte the PCR exit: 0 budget, 1 tolerance, 2 monotone
+   * guard, 3 breakdown, 4 no rows. */
+  uint8_t* decisions;
 } nsd_step_out;
 
 typedef struct nsd_solver nsd_solver;

@@ -381,6 +381,17 @@ static void export_contacts(const std::vector<Contact>& cs, int* ib, double* db)
     d[20] = d[21] = 0.0;
   }
 }
+// Decision vectors of the last newton step (Report::decisions): up to max_rows rows of
+// `stride` bytes; returns the number of rows (Newton iterations run).
+int orc_world_decisions(void* hd, unsigned char* out, int stride, int max_rows) {
+  OWorld* w = static_cast<OWorld*>(hd);
+  const auto& d = w->last.decisions;
+  const int n = std::min<int>(static_cast<int>(d.size()), max_rows);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < stride; ++k) out[i * stride + k] = k < static_cast<int>(d[i].size()) ? d[i][k] : 0xff;
+  return n;
+}
+
 int orc_world_n_contacts(void* h) { return static_cast<int>(static_cast<OWorld*>(h)->w.contacts.size()); }
 void orc_world_contacts(void* h, int* ib, double* db) { export_contacts(static_cast<OWorld*>(h)->w.contacts, ib, db); }
 

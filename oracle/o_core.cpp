@@ -283,7 +283,10 @@ LinResult run_pcr(const Csr& a, const VecX& b, const VecX& x0, const LinCfg& cfg
       rn[i] = r[i] - alpha * ap[i];
     }
     const double pn = pnorm(inv, rn);
-    if (pn > out.phist.back()) break;
+    if (pn > out.phist.back()) {
+      out.exit_reason = 2;
+      break;
+    }
     x = xn;
     r = rn;
     out.hist.push_back(vnorm(r));
@@ -304,6 +307,10 @@ LinResult run_pcr(const Csr& a, const VecX& b, const VecX& x0, const LinCfg& cfg
     }
     zaz = zaz_new;
   }
+  if (out.breakdown)
+    out.exit_reason = 3;
+  else if (out.exit_reason != 2)
+    out.exit_reason = out.hist.back() <= cfg.tolerance ? 1 : 0;
   out.solution = best.x;
   return out;
 }
@@ -324,10 +331,14 @@ LinResult solve_linear(const Csr& a, const VecX& b, const VecX& x0, const LinCfg
   if (cfg.max_iterations < 1) throw std::invalid_argument("solve_linear: max_iterations < 1");
   VecX inv;
   if (cfg.precond == Precond::Diagonal) inv = diag_precond(a);
+  const auto classify = [&](LinResult r) {  // decision vector exit reason (no monotone guard)
+    r.exit_reason = r.breakdown ? 3 : (!r.hist.empty() && r.hist.back() <= cfg.tolerance ? 1 : 0);
+    return r;
+  };
   switch (cfg.method) {
-    case LinMethod::Jacobi: return run_jacobi(a, b, x0, cfg);
-    case LinMethod::GaussSeidel: return run_gs(a, b, x0, cfg);
-    case LinMethod::PCG: return run_pcg(a, b, x0, cfg, inv);
+    case LinMethod::Jacobi: return classify(run_jacobi(a, b, x0, cfg));
+    case LinMethod::GaussSeidel: return classify(run_gs(a, b, x0, cfg));
+    case LinMethod::PCG: return classify(run_pcg(a, b, x0, cfg, inv));
     case LinMethod::PCR: return run_pcr(a, b, x0, cfg, inv);
   }
   throw std::logic_error("solve_linear: unknown method");
@@ -912,12 +923,16 @@ double nh_energy(const V3& s, const NH& m) {
   return m.c1 * (ic - 3.0) + m.d1 * (j - m.alpha) * (j - m.alpha);
 }
 
-M3 compliance_block(double vol, const M3& hess, bool project, bool diag) {  // :82-102
+M3 compliance_block(double vol, const M3& hess, bool project, bool diag, unsigned char* flags) {  // :82-102
   M3 h = hess;
+  unsigned char f = 0;
   if (project) {
     const Eig3 e = sym_eig3(h, false);
     const double mn = std::min(e.val[0], std::min(e.val[1], e.val[2]));
-    if (mn <= 0.0) h = project_psd3(h);
+    if (mn <= 0.0) {
+      h = project_psd3(h);
+      f |= 1;
+    }
   }
   const M3 n = vol * h;
   const auto diagonal = [&]() {
@@ -925,9 +940,16 @@ M3 compliance_block(double vol, const M3& hess, bool project, bool diag) {  // :
     for (int i = 0; i < 3; ++i) e(i, i) = n(i, i) > 0.0 ? 1.0 / n(i, i) : 0.0;
     return e;
   };
-  if (diag) return diagonal();
+  if (flags) *flags = f;
+  if (diag) {
+    if (flags) *flags |= 2;
+    return diagonal();
+  }
   const double d = det3(n);
-  if (!std::isfinite(d) || std::abs(d) < 1e-300) return diagonal();
+  if (!std::isfinite(d) || std::abs(d) < 1e-300) {
+    if (flags) *flags |= 2;
+    return diagonal();
+  }
   return inverse3(n);
 }
 
@@ -1026,7 +1048,7 @@ MatRows neo_hookean_rows(const Tet& e, const TetMesh& mesh, const V3& p0, const 
   for (int i = 0; i < 3; ++i)
     for (int k = 0; k < 12; ++k) o.jac[i][k] = j[i][k];
   const M3 h = nh_hessian(svd.S, mesh.nh);
-  const M3 cb = compliance_block(e.vol, h, true, mesh.material.diagonal_compliance);
+  const M3 cb = compliance_block(e.vol, h, true, mesh.material.diagonal_compliance, &o.flags);
   for (int i = 0; i < 3; ++i)
     for (int k = 0; k < 3; ++k) o.comp[i][k] = cb(i, k);
   return o;

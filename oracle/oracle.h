@@ -62,6 +62,7 @@ struct LinResult {
   std::vector<double> phist;  // precond_residual_history
   int iterations_used = 0;
   bool breakdown = false;
+  int exit_reason = 0;  // decision vector: 0 budget, 1 tolerance, 2 monotone guard, 3 breakdown
 };
 VecX diag_precond(const Csr& a);                                                  // solvers.cpp:178-184
 LinResult solve_linear(const Csr& a, const VecX& b, const VecX& x0, const LinCfg& c);  // :186-206
@@ -198,7 +199,8 @@ M6 inverse6(const M6& a);
 V3 nh_gradient(const V3& s, const NH& m);
 M3 nh_hessian(const V3& s, const NH& m);
 double nh_energy(const V3& s, const NH& m);
-M3 compliance_block(double vol, const M3& hess, bool project = true, bool diag = false);  // :82-102
+M3 compliance_block(double vol, const M3& hess, bool project = true, bool diag = false,
+                    unsigned char* flags = nullptr);  // :82-102; flags: 1 PSD projected, 2 diagonal fallback
 using J312 = std::array<std::array<double, 12>, 3>;
 J312 strain_jacobian(const Tet& e, const Svd3& svd);  // :104-114
 enum class MatModel { Linear = 0, NeoHookean = 1 };
@@ -209,6 +211,7 @@ struct MatSpec {
 };
 struct MatRows {
   int dim = 3;
+  unsigned char flags = 0;  // decision vector: compliance_block's PSD projection / diagonal fallback
   double c[6] = {0, 0, 0, 0, 0, 0};
   double jac[6][12] = {};
   double comp[6][6] = {};
@@ -253,6 +256,7 @@ struct NSystem {
   BlockMass h_mass;
   int num_rows = 0;
   double comp_error_max = 0.0, cone_violation_max = 0.0, min_gap = 0.0;
+  std::vector<unsigned char> cflags, tflags;  // decision vectors (nsd_step_out::decisions layout)
 };
 struct IterStats {
   double residual_inf = 0, merit_l2 = 0, comp_error_max = 0, cone_violation_max = 0, step_size = 0;
@@ -272,6 +276,9 @@ struct Report {
          min_diag_shift = 0;
   bool aborted = false, converged = false;
   VecX lambda;  // oracle extra: the step's final multipliers in row layout
+  // oracle extra: per Newton iteration [contacts][tets][dofs][PCR exit] decision bytes,
+  // the layout of nsd_step_out::decisions (include/nsdyn_gpu.h)
+  std::vector<std::vector<unsigned char>> decisions;
 };
 struct StepCtx {
   State* state = nullptr;

@@ -453,6 +453,17 @@ class OracleWorld:
             raise RuntimeError(lib().orc_last_error().decode())
         return rc
 
+    def decisions(self):
+        """Decision vectors of the last newton step (N x (nc + nt + ndof + 1) bytes, the
+        layout of nsd_step_out::decisions)."""
+        d = self.dims()
+        cfg = self.get_config()
+        stride = d["n_contacts"] + d["n_tets"] + d["num_dof"] + 1
+        out = np.zeros(cfg["newton_iterations"] * stride, np.uint8)
+        n = lib().orc_world_decisions(self._hp, out.ctypes.data_as(C.POINTER(C.c_uint8)), C.c_int(stride),
+                                      C.c_int(cfg["newton_iterations"]))
+        return out.reshape(-1, stride)[:n]
+
     def report(self, n_rows=None):
         d = self.dims()
         cfg = self.get_config()

@@ -197,12 +197,15 @@ class NewtonSolver:
         hist = np.zeros(max(N, 1) * (ml + 1))
         hlen = np.zeros(max(N, 1), np.int32)
         tel = np.zeros(6 * max(nc, 1))
+        dec_stride = nc + T.n_tets + T.num_dof + 1
+        dec = np.zeros(max(N, 1) * dec_stride, np.uint8)
         cout = (nsd_contact * max(nc, 1))()
         so = nsd_step_out()
         so.q, so.u, so.lambda_ = _dp(qo), _dp(uo), _dp(lam)
         so.contacts = C.cast(cout, C.POINTER(nsd_contact))
         so.iters = C.cast(iters, C.POINTER(nsd_iter_stats))
         so.linear_history, so.linear_history_len, so.contact_telemetry = _dp(hist), _ip(hlen), _dp(tel)
+        so.decisions = dec.ctypes.data_as(C.POINTER(C.c_uint8))
         rc = lib().nsd_step(self._h, C.byref(sin), C.byref(so))
         check(rc, allow_abort=True)
         n = so.n_iterations
@@ -213,7 +216,7 @@ class NewtonSolver:
                     final=np.array([so.final_residual_inf, so.final_comp_error, so.final_cone_violation,
                                     so.min_gap, so.min_diag_shift, so.aborted, so.converged]),
                     contacts=contacts_to_arrays(cout, nc), n_rows=so.n_rows, aborted=bool(so.aborted),
-                    ms=self.last_step_ms)
+                    ms=self.last_step_ms, decisions=dec.reshape(max(N, 1), dec_stride)[:n].copy())
 
 
 def _open_scene(name, seed, json_text):

@@ -58,7 +58,7 @@ class nsd_step_out(C.Structure):
                 ("contact_telemetry", D), ("n_iterations", C.c_int32), ("n_rows", C.c_int32),
                 ("final_residual_inf", C.c_double), ("final_comp_error", C.c_double),
                 ("final_cone_violation", C.c_double), ("min_gap", C.c_double), ("min_diag_shift", C.c_double),
-                ("aborted", C.c_int32), ("converged", C.c_int32)]
+                ("aborted", C.c_int32), ("converged", C.c_int32), ("decisions", C.POINTER(C.c_uint8))]
 
 
 class nsd_shape(C.Structure):

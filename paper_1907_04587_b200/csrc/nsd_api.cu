@@ -494,8 +494,10 @@ template <class R> struct Solver final : SolverBase {
       NSD_CK(cudaMemcpyAsync(hi + plan.cinc_ent, sent, sizeof(int) * cnt[H.nd3], cudaMemcpyHostToDevice, stream));
     // ---- outputs
     Layout L;
+    const int dec_stride = nc + H.nt + H.ndof + 1;
     const size_t o_it = L.add<nsd::IterOut>(N), o_hist = L.add<double>((size_t)N * (ml + 1)),
-                 o_hl = L.add<int>(N), o_tel = L.add<double>(6 * (size_t)nc), o_fin = L.add<double>(8);
+                 o_hl = L.add<int>(N), o_tel = L.add<double>(6 * (size_t)nc), o_fin = L.add<double>(8),
+                 o_dec = L.add<unsigned char>((size_t)N * dec_stride);
     outbuf.alloc(L.bytes);
     char* ob = outbuf.as<char>();
     NSD_CK(cudaMemsetAsync(ob, 0, L.bytes, stream));
@@ -505,6 +507,8 @@ template <class R> struct Solver final : SolverBase {
     so.hist_len = reinterpret_cast<int*>(ob + o_hl);
     so.tel = reinterpret_cast<double*>(ob + o_tel);
     so.fin = reinterpret_cast<double*>(ob + o_fin);
+    so.dec = out->decisions ? reinterpret_cast<unsigned char*>(ob + o_dec) : nullptr;
+    so.dec_stride = dec_stride;
     nsd::Work<R> W = plan.bind<R>(hr, hi, cr, ci);
     W.jframe = topo.jframe;
     W.f_extra = in->f_extra ? cr + plan.fx : nullptr;
@@ -578,6 +582,7 @@ template <class R> struct Solver final : SolverBase {
       std::memcpy(out->linear_history, hh, sizeof(double) * (size_t)N * (ml + 1));
     }
     if (out->linear_history_len) std::memcpy(out->linear_history_len, ho + o_hl, sizeof(int) * N);
+    if (out->decisions) std::memcpy(out->decisions, ho + o_dec, (size_t)N * dec_stride);
     if (out->contact_telemetry && nc && !aborted)
       std::memcpy(out->contact_telemetry, ho + o_tel, sizeof(double) * 6 * nc);
     if (out->contacts && !aborted) {

@@ -128,7 +128,25 @@ template <class R> struct Work {
   // dof3 block data
   R* iw6;   // 6 per block (sym: xx yy zz xy xz yz), angular blocks
   R* iwi6;  // inverse
+  // per-iteration decision row (decision vectors, see StepOut::dec) or null
+  unsigned char* dec;
 };
+
+// Decision-vector flags, one byte per contact / tet / dof per Newton
+// iteration, plus the PCR exit reason; the oracle writes the same layout.
+enum DecFlags : unsigned char {
+  kDecNormalKept = 1,     // contact: dphi/dC != 0, the normal J row exists (newton.cpp:187)
+  kDecFrictionOn = 2,     // contact: mu lambda_n > 0 (newton.cpp:200)
+  kDecWCap = 4,           // contact: friction W hit the 1e12 cap (ncp.cpp:37-48)
+  kDecWZero = 8,          // contact: min-map friction on its stick branch, W = 0 (ncp.cpp:37-41)
+  kDecNcpBranch = 16,     // contact: FB origin root == 0 / min-map branch c <= r lambda (ncp.cpp:11,24)
+  kDecPsd = 1,            // tet: Hessian projected to PSD (materials.cpp:85-88)
+  kDecDiagFallback = 2,   // tet: diagonal compliance fallback (materials.cpp:96-100)
+  kDecGsSkip = 1,         // dof: |du_k| < 1e-10, no secant (newton.cpp:306)
+  kDecGsClamp = 2,        // dof: c_k >= 0 clamped to a zero shift (newton.cpp:308)
+  kDecRigidDof = 4,       // dof: rigid, shift zeroed by the policy (newton.cpp:316-317)
+};
+enum PcrExit : unsigned char { kExitBudget = 0, kExitTol = 1, kExitMonotone = 2, kExitBreakdown = 3, kExitNone = 4 };
 
 struct IterOut {
   double residual_inf, merit_l2, comp_error_max, cone_violation_max, step_size, linear_residual;
@@ -136,6 +154,9 @@ struct IterOut {
 };
 
 struct StepOut {
+  unsigned char* dec;  // newton_iterations x dec_stride decision bytes (may be null):
+                       // [nc contacts][nt tets][ndof dofs][PCR exit reason]
+  int dec_stride;
   IterOut* iters;  // newton_iterations (may be null)
   double* hist;    // newton_iterations * (max_lin + 1) (may be null)
   int* hist_len;   // newton_iterations (may be null)
@@ -659,6 +680,7 @@ __device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R 
   const Svd<R> sv = svd3_signed(F);
   const R vol = T.tvol[e];
   if (T.tdim == 6) {
+    if (W.dec) W.dec[W.nc + e] = 0;  // the linear model has no compliance decisions
     assemble_tet_linear(T, W, e, h, dm, sv, vol, st);
     return;
   }
@@ -679,11 +701,15 @@ __device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R 
   H(0, 1) = H(1, 0) = R(2) * k1;
   H(0, 2) = H(2, 0) = R(2) * k2;
   H(1, 2) = H(2, 1) = R(2) * k3;
+  unsigned char tflags = 0;
   {  // compliance_block (materials.cpp:82-102): PSD check with the restated eigensolver
     V3<R> ev;
     M3<R> dummy;
     sym_eig3<R, false>(H, ev, dummy);
-    if (mn(ev.x, mn(ev.y, ev.z)) <= R(0)) H = project_psd3(H);
+    if (mn(ev.x, mn(ev.y, ev.z)) <= R(0)) {
+      H = project_psd3(H);
+      tflags |= kDecPsd;
+    }
   }
   M3<R> N;
 #pragma unroll
@@ -694,6 +720,8 @@ __device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R 
     const R det = det3(N);
     if (!isfinite(det) || fabs((double)det) < 1e-300) use_diag = true;
   }
+  if (use_diag) tflags |= kDecDiagFallback;
+  if (W.dec) W.dec[W.nc + e] = tflags;
   if (use_diag) {
     E = m3_zero<R>();
     E(0, 0) = N(0, 0) > R(0) ? R(1) / N(0, 0) : R(0);
@@ -793,13 +821,14 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
   const R mu_ln = mu * lam_n;
   const R lfn = sqrt(lf0 * lf0 + lf1 * lf1);
   st.cone = fmax(st.cone, (double)mx(R(0), lfn - mu_ln));
-  R h1, h2;
+  R h1, h2, wdec = R(-1);
   if (mu_ln > R(0)) {
     const V3<R> dv = contact_dv(cv, u);
     const R v0 = dot(cv.d1, dv), v1 = dot(cv.d2, dv);
     const R df = R(0.5) * (contact_quad(T, W, cv, cv.d1, false) + contact_quad(T, W, cv, cv.d2, false));
     const R rf = r_factor(df, h, false, cfg.r_strategy);
     const R wv = friction_W(sqrt(v0 * v0 + v1 * v1), lfn, mu_ln, rf, cfg.ncp_kind);
+    wdec = wv;
     h1 = v0 + wv * lf0;
     h2 = v1 + wv * lf1;
     W.cd[f0] = W.cd[f0 + 1] = wv / h;
@@ -820,6 +849,18 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
   W.hv[f0 + 1] = h2;
   st.hmax = fmax(st.hmax, fmax((double)ab(hn), fmax((double)ab(h1), (double)ab(h2))));
   st.hsq += (double)hn * hn + (double)h1 * h1 + (double)h2 * h2;
+  if (W.dec) {
+    unsigned char f = 0;
+    if (phi.dc != R(0)) f |= kDecNormalKept;
+    if (mu_ln > R(0)) {
+      f |= kDecFrictionOn;
+      if (wdec == R(1e12)) f |= kDecWCap;
+      if (cfg.ncp_kind == 0 && wdec == R(0)) f |= kDecWZero;  // FB's W has no stick branch
+    }
+    const R rl = rn * lam_n;
+    if (cfg.ncp_kind == 1 ? (gap * gap + rl * rl == R(0)) : (gap <= rl)) f |= kDecNcpBranch;
+    W.dec[c] = f;
+  }
 }
 
 template <class R, bool kTets, class Team>
@@ -1077,7 +1118,9 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
   int n_done = 0;
   int aborted = 0;
 
+  const int dec_dof = W.nc + (kTets ? T.nt : 0), dec_exit = dec_dof + T.ndof;
   for (int it = 0; it < cfg.newton_iterations; ++it) {
+    W.dec = out.dec ? out.dec + (size_t)it * out.dec_stride : nullptr;
     // ---- assemble
     AsmStats as{0.0, 0.0, 0.0, 0.0};
     assemble<R, kTets>(t, T, W, W.q, W.u, cfg, as);
@@ -1104,19 +1147,27 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
         const R m = mdiag.x;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
+          unsigned char df = 0;
           if (gs) {
             const R dd = W.u[d + k] - W.up[d + k];
             R sh = R(0);
             if (!(ab(dd) < R(1e-10))) {
               const R ck = -((gv[k] - W.gp[d + k] + m * dd) / dd);
               sh = -mn(R(0), ck);
+              if (!(ck < R(0))) df = kDecGsClamp;
+            } else {
+              df = kDecGsSkip;
             }
             W.shift[d + k] = sh;
             smin = fmin(smin, (double)sh);
           }
+          if (W.dec) W.dec[dec_dof + d + k] = df;
           W.gp[d + k] = gv[k];
           W.up[d + k] = W.u[d + k];
         }
+      } else if (W.dec) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) W.dec[dec_dof + d + k] = gs ? kDecRigidDof : 0;
       }
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
@@ -1161,7 +1212,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
       rr += (double)b * b;
       rzr += (double)b * (double)(inv * b);
     }
-    int lin_used = 0, breakdown = 0, hist_n = 0;
+    int lin_used = 0, breakdown = 0, hist_n = 0, mono = 0;
     double hist_last = 0.0;
     if (nr > 0) {
       double s1[2] = {rr, rzr};
@@ -1354,7 +1405,10 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
             rn2 = s[1];
           }
           const double pn = sqrt(pn2);
-          if (pn > phist_last) break;  // monotone guard
+          if (pn > phist_last) {  // monotone guard
+            mono = 1;
+            break;
+          }
 #pragma unroll
           for (int k = 0; k < RPT; ++k) {  // commit
             xr[k] = xnr[k];
@@ -1485,7 +1539,10 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
           rn2 = s[1];
         }
         const double pn = sqrt(pn2);
-        if (pn > phist_last) break;  // monotone guard: stop at the numerical floor
+        if (pn > phist_last) {  // monotone guard: stop at the numerical floor
+          mono = 1;
+          break;
+        }
         if (kInPlace) {
           pend = ra;  // commit deferred to the next row pass
         } else {
@@ -1561,6 +1618,11 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
     io.linear_iterations = lin_used;
     io.linear_breakdown = breakdown;
     io.linear_residual = hist_n > 0 ? hist_last : 0.0;
+    if (W.dec && t.rank() == 0)  // PCR exit: breakdown > monotone guard > tolerance > budget
+      W.dec[dec_exit] = !(nr > 0) ? kExitNone
+                                  : (breakdown ? kExitBreakdown
+                                               : (mono ? kExitMonotone
+                                                       : (hist_last <= cfg.linear_tolerance ? kExitTol : kExitBudget)));
     t.sync();
     // ---- du = H^-1 (J^T dlambda - g); NaN check (newton.cpp:295,362-369)
     double dl2 = 0.0, du2 = 0.0, bad = 0.0;
@@ -1594,6 +1656,8 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
     // ---- optional merit line search (newton.cpp:371-391)
     R tstep = tfrac;
     if (line_search) {
+      unsigned char* const dec_row = W.dec;  // the probes' assemblies record no decisions
+      W.dec = nullptr;
       const R trials[4] = {R(1), R(0.5), R(0.25), R(0.125)};
       for (int k = 0; k < 4; ++k) {
         const R tr = trials[k];
@@ -1629,6 +1693,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
           break;
         }
       }
+      W.dec = dec_row;
     }
     // ---- damped update + integration (newton.cpp:393-396). Each body owns its
     // dofs, so u += t du and q = q- + h G(q) u run in one pass.
@@ -1657,6 +1722,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
     return 1;
   }
   // ---- final assembly for classification and telemetry (newton.cpp:409-416)
+  W.dec = nullptr;
   AsmStats fs{0.0, 0.0, 0.0, 0.0};
   assemble<R, kTets>(t, T, W, W.q, W.u, cfg, fs);
   t.sync();

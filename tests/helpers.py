@@ -45,7 +45,7 @@ def run_oracle(case):
     rc = w.newton()
     q, u = w.state()
     rep = w.report()
-    return dict(q=q, u=u, rc=rc, **rep)
+    return dict(q=q, u=u, rc=rc, decisions=w.decisions(), **rep)
 
 
 def rel_err(a, b, floor=1e-12):

@@ -424,9 +424,16 @@ def test_gyroscopic_torque():  # :157-170
 
 # ---------------------------------------------------------------- SPEC newton examples
 def test_spec_zero_rows_free_fall():
-    """no constraints, 1 Newton iteration: u equals u~ exactly."""
-    w = O.OracleWorld("c3:1", 0)  # single link hanging from its joint; remove the joint effect by config
-    w.set_config(newton_iterations=1)
-    w.step(1)
+    """no constraints, 1 Newton iteration (undamped, t = 1): u equals u~ exactly."""
+    w = O.OracleWorld("box_on_plane", 0)
+    w.set_config(newton_iterations=1, step_fraction=1.0)
+    q, u = w.state()
+    q = q.copy()
+    q[2] += 10.0  # far above the margin: no contacts, no rows
+    w.set_state(q, u)
+    assert w.step(1) == 0
     r = w.report()
-    assert r["n_iterations"] == 1
+    assert r["n_iterations"] == 1 and len(r["tel"]) == 0
+    ut = u.copy()
+    ut[2] += w.h * w.gravity()[2]  # unit mass, zero spin: u~ = u- + h g
+    assert np.array_equal(w.state()[1], ut)
