@@ -754,6 +754,21 @@ __device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R 
 
 // Contact rows (newton.cpp:166-218; constraints.cpp:67-91, 103-115) in the
 // structured form: lever arms, NCP scale and friction flag per contact.
+// contact_gap (constraints.cpp:67-71) uncontracted: n . (p_a - p_b) - thickness with
+// p = position + R(quaternion) local (State::world_point), the oracle's roundings.
+template <class R>
+__device__ __forceinline__ R contact_gap_strict(const Topo<R>& T, const R* q, int ba, int bb, V3<R> la, V3<R> lb,
+                                                V3<R> n, R thick) {
+  auto wp = [&](int b, V3<R> l) {
+    if (b < 0) return l;
+    const R* p = q + T.bcoord[b];
+    if (T.btype[b] == 0) return v3(p[0], p[1], p[2]);
+    return sworld(quat_rot_strict(p[3], p[4], p[5], p[6]), l, v3(p[0], p[1], p[2]));
+  };
+  const V3<R> pa = wp(ba, la), pb = wp(bb, lb);
+  return ssub(sdot(n, v3(ssub(pa.x, pb.x), ssub(pa.y, pb.y), ssub(pa.z, pb.z))), thick);
+}
+
 template <class R>
 __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const R* u, int c, R h, const Cfg& cfg,
                                  AsmStats& st) {
@@ -805,7 +820,9 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
     W.cblk[c] = make_int4(cv.al, cv.aa, cv.bl, cv.bA);
   }
   const int nr = W.normal_begin + c, f0 = W.friction_begin + 2 * c;
-  const R gap = dot(cv.n, pa - pb) - thick;
+  // the gap decides the Fischer-Burmeister branch at the origin (ncp.cpp:24): computed
+  // without contraction, as contact_gap (constraints.cpp:67-71) rounds on the CPU
+  const R gap = contact_gap_strict(T, q, ba, bb, la, lb, cv.n, thick);
   const R lam_n = W.lam[nr] / h;
   const R rn = r_factor(contact_quad(T, W, cv, cv.n, false), h, true, cfg.r_strategy);
   const PhiV<R> phi = phi_n(gap, lam_n, rn, cfg.ncp_kind);

@@ -131,6 +131,85 @@ template <class R> NSD_HD M3<R> inverse3(const M3<R>& m) {
 }
 
 // Quaternion (w, x, y, z) -> rotation, normalising first (Quaterniond::normalized().toRotationMatrix()).
+// Uncontracted arithmetic (no FMA) for values that feed a data-dependent decision
+// exactly at its boundary (the contact gap at the Fischer-Burmeister origin): the
+// same roundings as the CPU oracle, which is compiled with -ffp-contract=off.
+NSD_HD double smul(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+NSD_HD double sadd(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+NSD_HD double ssub(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dsub_rn(a, b);
+#else
+  return a - b;
+#endif
+}
+NSD_HD float smul(float a, float b) {
+#if defined(__CUDA_ARCH__)
+  return __fmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+NSD_HD float sadd(float a, float b) {
+#if defined(__CUDA_ARCH__)
+  return __fadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+NSD_HD float ssub(float a, float b) {
+#if defined(__CUDA_ARCH__)
+  return __fsub_rn(a, b);
+#else
+  return a - b;
+#endif
+}
+template <class R> NSD_HD R sdot(V3<R> a, V3<R> b) { return sadd(sadd(smul(a.x, b.x), smul(a.y, b.y)), smul(a.z, b.z)); }
+// R local + pos, uncontracted (State::world_point: position + rotation * local).
+template <class R> NSD_HD V3<R> sworld(const M3<R>& m, V3<R> l, V3<R> p) {
+  return v3(sadd(p.x, sadd(sadd(smul(m.a[0], l.x), smul(m.a[1], l.y)), smul(m.a[2], l.z))),
+            sadd(p.y, sadd(sadd(smul(m.a[3], l.x), smul(m.a[4], l.y)), smul(m.a[5], l.z))),
+            sadd(p.z, sadd(sadd(smul(m.a[6], l.x), smul(m.a[7], l.y)), smul(m.a[8], l.z))));
+}
+// quat_rot (below) uncontracted.
+template <class R> NSD_HD M3<R> quat_rot_strict(R w, R x, R y, R z) {
+  const R n2 = sadd(sadd(sadd(smul(w, w), smul(x, x)), smul(y, y)), smul(z, z));
+  if (n2 > R(0)) {
+    const R n = sqrt(n2);
+    w = w / n;
+    x = x / n;
+    y = y / n;
+    z = z / n;
+  }
+  const R tx = smul(R(2), x), ty = smul(R(2), y), tz = smul(R(2), z);
+  const R twx = smul(tx, w), twy = smul(ty, w), twz = smul(tz, w);
+  const R txx = smul(tx, x), txy = smul(ty, x), txz = smul(tz, x);
+  const R tyy = smul(ty, y), tyz = smul(tz, y), tzz = smul(tz, z);
+  M3<R> r;
+  r(0, 0) = ssub(R(1), sadd(tyy, tzz));
+  r(0, 1) = ssub(txy, twz);
+  r(0, 2) = sadd(txz, twy);
+  r(1, 0) = sadd(txy, twz);
+  r(1, 1) = ssub(R(1), sadd(txx, tzz));
+  r(1, 2) = ssub(tyz, twx);
+  r(2, 0) = ssub(txz, twy);
+  r(2, 1) = sadd(tyz, twx);
+  r(2, 2) = ssub(R(1), sadd(txx, tyy));
+  return r;
+}
+
 template <class R> NSD_HD M3<R> quat_rot(R w, R x, R y, R z) {
   const R n2 = w * w + x * x + y * y + z * z;
   if (n2 > R(0)) {

@@ -4,7 +4,10 @@ state, bit for bit: per contact the normal-row-kept, friction-active, W-cap,
 W-zero and NCP-branch flags; per tet the PSD projection and diagonal
 fallback; per dof the geometric-stiffness skip / clamp / rigid-zeroing; and
 the PCR exit reason (budget, tolerance, monotone guard, breakdown). Layout:
-nsd_step_out::decisions (include/nsdyn_gpu.h)."""
+nsd_step_out::decisions (include/nsdyn_gpu.h). The incline cases at step 0
+start exactly touching (gap 0, lambda 0): the Fischer-Burmeister origin, where
+the branch depends on the gap's last bit; the device computes that gap without
+FMA contraction, as the oracle does, so they agree there too."""
 import numpy as np
 import pytest
 
@@ -14,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 RIGID = [("c1", 0, 0), ("c1", 0, 5), ("c1", 0, 20), ("c3", 0, 0), ("c3", 0, 6), ("c5", 3, 0), ("c5", 3, 10),
          ("heavy_stack", 0, 0), ("heavy_stack", 0, 12), ("box_pile", 1, 10), ("box_pile", 1, 30),
-         ("incline:35:0.5", 0, 5), ("incline:20:0.5", 0, 5), ("arch", 0, 0), ("arch", 0, 2), ("box_on_plane", 0, 8)]
+         ("incline:35:0.5", 0, 0), ("incline:35:0.5", 0, 5), ("incline:20:0.5", 0, 0), ("incline:20:0.5", 0, 5), ("arch", 0, 0), ("arch", 0, 2), ("box_on_plane", 0, 8)]
 FEM = [("c2:6", 0, 0), ("c2:6", 0, 2), ("c2:6", 0, 4)]
 
 
@@ -46,17 +49,3 @@ def test_decision_vectors_exercise_every_flag():
         seen[2] += int(np.any(gd[:, -1] == 0)) + int(np.any(gd[:, -1] == 2))
     assert seen[0] >= 2 and seen[1] >= 1 and seen[2] >= 1
 
-
-def test_touching_start_differs_only_at_the_fb_origin():
-    """The incline box starts exactly touching (gap 0, lambda 0): the Fischer-Burmeister
-    origin (ncp.cpp:22-31). The device's FMA-contracted gap is ~1e-17, the oracle's 0,
-    so in the first Newton iteration the two take different subgradient branches. The
-    differences are confined to that iteration and to the normal-row / NCP-branch flags;
-    from the next iteration on every decision agrees again."""
-    gd, od, dims = _compare("incline:35:0.5", 0, 0)
-    nc = dims["n_contacts"]
-    diff = np.argwhere(gd != od)
-    assert diff.size > 0  # the documented case: not silently equal
-    assert set(diff[:, 0].tolist()) == {0}
-    assert all(k < nc for _, k in diff)
-    assert all(((int(gd[i, k]) ^ int(od[i, k])) & ~(1 | 16)) == 0 for i, k in diff)
