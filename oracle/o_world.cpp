@@ -699,6 +699,29 @@ SceneDesc build_c3_chain(int links) {
   return s;
 }
 
+// Cantilever with FixedPoint hinges and BendSpring joints (constraints.cpp:209-216);
+// the product's bend_chain builder (csrc/nsd_scene.cpp) builds the same scene.
+SceneDesc build_bend_chain(int links, double k) {
+  SceneDesc s;
+  const double pitch = 0.12, half = 0.05, z = 2.0;
+  for (int i = 0; i < links; ++i)
+    s.bodies.push_back(rigid_box(V3(0.06 + pitch * i, 0, z), V3(half, 0.01, 0.01), 0.1));
+  for (int i = 0; i < links; ++i) {
+    JointDesc j;
+    j.kind = JointKind::FixedPoint;
+    j.a.body = i - 1;
+    j.b.body = i;
+    j.anchor = V3(pitch * i, 0, z);
+    s.joints.push_back(j);
+    JointDesc b = j;
+    b.kind = JointKind::BendSpring;
+    b.axis = V3(1, 0, 0);
+    b.stiffness = k;
+    s.joints.push_back(b);
+  }
+  return s;
+}
+
 SceneDesc build_c4_hand_ball(int n, double speed, double scale) {
   SceneDesc s;
   s.bodies.push_back(static_ground());  // palm surface
@@ -851,6 +874,8 @@ bool build_scene_by_name(const std::string& name, unsigned seed, SceneDesc& out)
   else if (base == "c1") out = build_c1_box_stack();
   else if (base == "c2") out = build_c2_fem_block(args.size() > 0 ? static_cast<int>(args[0]) : 12);
   else if (base == "c3") out = build_c3_chain(args.size() > 0 ? static_cast<int>(args[0]) : 100);
+  else if (base == "bend_chain")
+    out = build_bend_chain(args.size() > 0 ? static_cast<int>(args[0]) : 10, args.size() > 1 ? args[1] : 50.0);
   else if (base == "c4")
     out = build_c4_hand_ball(args.size() > 0 ? static_cast<int>(args[0]) : 12, args.size() > 1 ? args[1] : kC4Speed,
                              args.size() > 2 ? args[2] : kC4Scale);

@@ -542,18 +542,6 @@ template <class R> struct Solver final : SolverBase {
     NSD_CK(cudaMemcpyAsync(hu, hr + plan.u, sizeof(R) * H.ndof, cudaMemcpyDeviceToHost, stream));
     if (nrows) NSD_CK(cudaMemcpyAsync(hl, hr + plan.lam, sizeof(R) * nrows, cudaMemcpyDeviceToHost, stream));
     NSD_CK(cudaStreamSynchronize(stream));
-    if (std::getenv("NSD_DUMP_COEFF") && H.nt > 0) {  // diagnostics: the first tet's row coefficients and blocks
-      std::vector<R> co(12 * H.tdim);
-      std::vector<int> bk(4 * H.tdim);
-      NSD_CK(cudaMemcpy(co.data(), hr + plan.coeff + 12 * H.rows_joint, sizeof(R) * co.size(), cudaMemcpyDeviceToHost));
-      NSD_CK(cudaMemcpy(bk.data(), plan.hot_ints(hr) + plan.blk + 4 * H.rows_joint, sizeof(int) * bk.size(),
-                        cudaMemcpyDeviceToHost));
-      for (int i = 0; i < H.tdim; ++i) {
-        std::fprintf(stderr, "row %d blk %d %d %d %d :", i, bk[4 * i], bk[4 * i + 1], bk[4 * i + 2], bk[4 * i + 3]);
-        for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %.9g", double(co[12 * i + k]));
-        std::fprintf(stderr, "\n");
-      }
-    }
     float ms = 0.f;
     NSD_CK(cudaEventElapsedTime(&ms, ev0, ev1));
     last_ms = ms;

@@ -14,6 +14,7 @@
 #include <limits>
 #include <memory>
 #include <random>
+#include <atomic>
 #include <thread>
 #include <sstream>
 #include <stdexcept>
@@ -248,6 +249,29 @@ Scene s_c3(int links) {
   s.solver.linear_max_iterations = 40;
   return s;
 }
+// A cantilever of `links` boxes along +x from a world anchor: a FixedPoint joint at
+// every hinge and a BendSpring of stiffness k about the link axis (constraints.cpp:
+// 209-216, compliance 1/k), sagging under gravity.
+Scene s_bend_chain(int links, double k) {
+  Scene s;
+  s.solver = defaults();
+  const double pitch = 0.12, half = 0.05, z = 2.0;
+  for (int i = 0; i < links; ++i) s.bodies.push_back(box(Vec3{0.06 + pitch * i, 0, z}, Vec3{half, 0.01, 0.01}, 0.1));
+  for (int i = 0; i < links; ++i) {
+    JointSpecDesc j;
+    j.kind = 0;
+    j.a.body = i - 1;
+    j.b.body = i;
+    j.anchor = Vec3{pitch * i, 0, z};
+    s.joints.push_back(j);
+    JointSpecDesc bs = j;
+    bs.kind = 3;
+    bs.axis = Vec3{1, 0, 0};
+    bs.stiffness = k;
+    s.joints.push_back(bs);
+  }
+  return s;
+}
 Scene s_c4(int n, double speed, double L) {
   Scene s;
   s.solver = defaults();
@@ -424,6 +448,8 @@ Scene build(const std::string& name, unsigned seed, bool* ok) {
   if (base == "c1") return s_c1();
   if (base == "c2") return s_c2(args.size() > 0 ? static_cast<int>(args[0]) : 12);
   if (base == "c3") return s_c3(args.size() > 0 ? static_cast<int>(args[0]) : 100);
+  if (base == "bend_chain")
+    return s_bend_chain(args.size() > 0 ? static_cast<int>(args[0]) : 10, args.size() > 1 ? args[1] : 50.0);
   // C4 drop speed 0.2 m/s: at 1.0 m/s the 8 mm Neo-Hookean elements blow up at step 4
   // under the 6 x 50 budget (the reference then throws in spmv_transpose)
   if (base == "c4")
@@ -777,9 +803,57 @@ int nsd_scene_advance_anchors(nsd_scene* s) {
 // particle generators with the predicted-gap rule, in canonical
 // (a.body, b.body, feature) order (collision.cpp:239-297). The Newton step
 // that consumes the contacts runs on the GPU (nsd_step).
+static int scene_detect(const nsd_scene* s, const double* q, const double* u, const double* f_extra,
+                        int32_t capacity, nsd_contact* out, int32_t* n);
+
 int nsd_scene_detect(const nsd_scene* s, const double* q, const double* u, const double* f_extra, int32_t capacity,
                      nsd_contact* out, int32_t* n) {
   if (!s || !q || !u || !n || capacity < 0 || (capacity > 0 && !out)) return NSD_INVALID;
+  try {
+    return scene_detect(s, q, u, f_extra, capacity, out, n);
+  } catch (const std::exception&) {  // allocation or thread failure: an error code, never std::terminate
+    return NSD_INVALID;
+  }
+}
+
+}  // extern "C"
+
+namespace {
+
+// Runs work(0 .. nth-1): the calling thread takes index 0 and every index whose
+// thread could not be started. Each index is a fixed strided set of rows written
+// to its own slots, so the result does not depend on which thread ran it. All
+// started threads are joined before any exception propagates.
+template <class F> void run_strided(unsigned nth, F&& work) {
+  std::vector<std::thread> pool;
+  std::atomic<bool> failed{false};
+  auto guarded = [&](unsigned t) {
+    try {
+      work(t);
+    } catch (...) {
+      failed = true;
+    }
+  };
+  unsigned started = 1;
+  try {
+    for (unsigned t = 1; t < nth; ++t) {
+      pool.emplace_back(guarded, t);
+      started = t + 1;
+    }
+  } catch (...) {  // e.g. std::system_error under a pids limit: run the rest here
+  }
+  guarded(0);
+  for (unsigned t = started; t < nth; ++t) guarded(t);
+  for (auto& th : pool) th.join();
+  if (failed) throw std::runtime_error("nsd_scene_detect: worker failed");
+}
+
+}  // namespace
+
+extern "C" {
+
+static int scene_detect(const nsd_scene* s, const double* q, const double* u, const double* f_extra, int32_t capacity,
+                        nsd_contact* out, int32_t* n) {
   using V = nsd::V3<double>;
   using M = nsd::M3<double>;
   const nsdw::World& w = s->w;
@@ -843,10 +917,7 @@ int nsd_scene_detect(const nsd_scene* s, const double* q, const double* u, const
           rows[i].insert(rows[i].end(), b4, b4 + k);
         }
     };
-    std::vector<std::thread> pool;
-    for (unsigned t = 1; t < nth; ++t) pool.emplace_back(work, t);
-    work(0);
-    for (auto& th_ : pool) th_.join();
+    run_strided(nth, work);
     for (const auto& r : rows) cands.insert(cands.end(), r.begin(), r.end());
   } else {
     for (size_t i = 0; i < ns; ++i)
@@ -874,10 +945,7 @@ int nsd_scene_detect(const nsd_scene* s, const double* q, const double* u, const
           rows[r].insert(rows[r].end(), b4, b4 + k);
         }
     };
-    std::vector<std::thread> pool;
-    for (unsigned t = 1; t < pth; ++t) pool.emplace_back(work, t);
-    work(0);
-    for (auto& th_ : pool) th_.join();
+    run_strided(pth, work);
     for (const auto& r : rows) cands.insert(cands.end(), r.begin(), r.end());
   } else {
     for (const int b : pbodies)

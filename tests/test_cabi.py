@@ -44,7 +44,7 @@ def test_config_defaults_match_reference():
 
 @pytest.mark.parametrize("name,seed", [("c1", 0), ("c2:4", 0), ("c3:20", 0), ("c4:6", 0), ("c5", 0), ("c5", 17),
                                        ("c5", 4095), ("heavy_stack", 0), ("arch", 0), ("stretch_sheet", 0), ("stretch_sheet_linear", 0),
-                                       ("incline:35:0.5", 0), ("box_on_plane", 0)])
+                                       ("incline:35:0.5", 0), ("box_on_plane", 0), ("bend_chain", 0), ("bend_chain:6:5", 0)])
 def test_product_builders_match_oracle_bitwise(name, seed):
     from paper_1907_04587_b200 import Scene
 

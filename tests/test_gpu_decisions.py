@@ -17,7 +17,8 @@ pytestmark = pytest.mark.gpu
 
 RIGID = [("c1", 0, 0), ("c1", 0, 5), ("c1", 0, 20), ("c3", 0, 0), ("c3", 0, 6), ("c5", 3, 0), ("c5", 3, 10),
          ("heavy_stack", 0, 0), ("heavy_stack", 0, 12), ("box_pile", 1, 10), ("box_pile", 1, 30),
-         ("incline:35:0.5", 0, 0), ("incline:35:0.5", 0, 5), ("incline:20:0.5", 0, 0), ("incline:20:0.5", 0, 5), ("arch", 0, 0), ("arch", 0, 2), ("box_on_plane", 0, 8)]
+         ("incline:35:0.5", 0, 0), ("incline:35:0.5", 0, 5), ("incline:20:0.5", 0, 0), ("incline:20:0.5", 0, 5), ("arch", 0, 0), ("arch", 0, 2), ("box_on_plane", 0, 8),
+         ("bend_chain", 0, 0), ("bend_chain", 0, 12)]
 FEM = [("c2:6", 0, 0), ("c2:6", 0, 2), ("c2:6", 0, 4)]
 
 

@@ -29,7 +29,8 @@ from tests.helpers import decision_mismatches, oracle_case, oracle_self_divergen
 pytestmark = pytest.mark.gpu
 
 RIGID = [("c1", 0, 0), ("c1", 0, 20), ("c3", 0, 0), ("c3", 0, 15), ("c5", 0, 0), ("c5", 3, 12),
-         ("heavy_stack", 0, 0), ("box_pile", 1, 30), ("incline:35:0.5", 0, 5), ("arch", 0, 0)]
+         ("heavy_stack", 0, 0), ("box_pile", 1, 30), ("incline:35:0.5", 0, 0), ("incline:35:0.5", 0, 5), ("arch", 0, 0),
+         ("bend_chain", 0, 0), ("bend_chain", 0, 12)]
 FEM = [("c2:6", 0, 0)]
 TOL64_RIGID = (1e-9, 1e-8, 1e-6)
 TOL64_FEM = (1e-6, 1e-4, 1e-2)

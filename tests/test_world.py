@@ -75,7 +75,8 @@ def test_driven_anchor_frames_advance():
 # and the incline box starts at gap 0 / lambda 0, the Fischer-Burmeister origin
 # where dphi switches branch (ncp.cpp:22-31) on a rounding-level gap.
 STEP_CASES = [("c1", 0, 12, 1e-9), ("c3:30", 0, 6, 1e-9), ("c5", 1, 15, 1e-8), ("box_pile", 2, 10, 1e-8),
-              ("incline:35:0.5", 0, 10, None), ("c4:6", 0, 4, None), ("c2:6", 0, 3, None)]
+              ("incline:35:0.5", 0, 10, 1e-9), ("bend_chain", 0, 30, 1e-9), ("bend_chain:6:5", 0, 30, 1e-9),
+              ("c4:6", 0, 4, None), ("c2:6", 0, 3, None)]
 
 
 @pytest.mark.gpu
