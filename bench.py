@@ -330,7 +330,7 @@ def measure(args, prec, T, tmpl, E, env0, ws, rank, local, sample_clocks):
     # ---- e2e: host actions -> H2D, step, D2H of the state, through the C ABI,
     # replaying the timed steps from the same post-warmup state with the same actions
     b.set_state(q_w, u_w)
-    dt = torch.float32 if prec == "fp32" else torch.float64
+    dt = torch.float64  # the batch state is fp64 in both precisions (fp32 = mixed: fp32 PCR operator)
     h_tq = torch.empty((K, E, nj), dtype=tdt, pin_memory=True)
     h_tq.copy_(torques[W:W + K].cpu())
     d_tq = torch.empty((E, nj), dtype=tdt, device="cuda")
@@ -368,7 +368,7 @@ def measure(args, prec, T, tmpl, E, env0, ws, rank, local, sample_clocks):
     b.results()
     b.close()
     h2d = 0 if args.passive else E * nj * h_tq.element_size()
-    d2h = E * (T.num_coord + T.num_dof) * (4 if prec == "fp32" else 8)
+    d2h = E * (T.num_coord + T.num_dof) * 8
     if ws > 1:
         t = torch.tensor([dev_ms, e2e_ms, e2e_copy_ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -577,8 +577,10 @@ def main():
         a = measure(args, alt, T, tmpl, E, env0, ws, rank, local, False)
         other = {"dtype": "f32" if alt == "fp32" else "f64", "value": a["value"], "ms_per_step": a["dev_ms"] / K,
                  "e2e": a["e2e"], "e2e_copy_path": a["e2e_copy"], "roofline_frac": roofline(a, alt, K)["frac"],
-                 "parity": ("tracks the oracle to 1e-4 until the first ground impact, O(1e-3) after "
-                            "(DESIGN.md Parity)") if alt == "fp32" else "oracle parity 1e-8 over 25 steps"}
+                 "mode": ("mixed precision: fp64 state, assembly, Newton update and reductions; fp32 PCR operator "
+                          "and row vectors") if alt == "fp32" else "fp64",
+                 "parity": ("oracle parity 1e-4 over 25 steps (tests/test_gpu_batch.py)") if alt == "fp32"
+                 else "oracle parity 1e-8 over 25 steps"}
     if rank != 0:
         if ws > 1:
             torch.distributed.destroy_process_group()

@@ -364,7 +364,8 @@ template <class R> struct Solver final : SolverBase {
   int ccap = 0;
   WorkPlan plan;
   DBuf hotr, hoti, coldr, coldi, outbuf, gpart;
-  HBuf stage_r, stage_i, stage_o;
+  HBuf stage_in, stage_o;
+  DBuf upbuf;  // the step's inputs, one H2D copy
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int grid_blocks = 0;
@@ -425,10 +426,28 @@ template <class R> struct Solver final : SolverBase {
     ensure(nc);
     const int N = cfg.newton_iterations, ml = cfg.linear_max_iterations;
     const int nrows = H.rows_static + 3 * nc;
-    // ---- stage inputs: q0, u0, f_extra (cold); cgeo (hot); joint frames (topology)
+    // ---- stage inputs in ONE pinned buffer and ONE H2D copy: q-, u-, f_extra, contact
+    // geometry, joint frames (R part); contact bodies and the contact incidence (int
+    // part). The kernel reads them in place (Work's const input pointers).
     const size_t nR = (size_t)H.ncoord + H.ndof + H.ndof + 17 * (size_t)nc + 21 * (size_t)H.nj;
-    stage_r.alloc(sizeof(R) * nR);
-    R* sr = static_cast<R*>(stage_r.p);
+    // contact incidence (contact*4 + slot), contacts ascending within a block
+    std::vector<int> cnt(H.nd3 + 1, 0);
+    std::vector<int> b4all(4 * (size_t)nc);
+    for (int c = 0; c < nc; ++c) {
+      int* b4 = &b4all[4 * c];
+      body_blocks_h(H, in->contacts[c].body_a, b4[0], b4[1]);
+      body_blocks_h(H, in->contacts[c].body_b, b4[2], b4[3]);
+      for (int s = 0; s < 4; ++s)
+        if (b4[s] >= 0) cnt[b4[s] + 1]++;
+    }
+    for (int b = 0; b < H.nd3; ++b) cnt[b + 1] += cnt[b];
+    const size_t nI = 2 * (size_t)nc + (H.nd3 + 1) + 4 * (size_t)nc;
+    Layout U;
+    const size_t u_r = U.add<R>(nR), u_i = U.add<int>(nI);
+    stage_in.alloc(U.bytes);
+    upbuf.alloc(U.bytes);
+    R* sr = reinterpret_cast<R*>(static_cast<char*>(stage_in.p) + u_r);
+    int* si = reinterpret_cast<int*>(static_cast<char*>(stage_in.p) + u_i);
     size_t o = 0;
     for (int i = 0; i < H.ncoord; ++i) sr[o++] = R(in->q[i]);
     for (int i = 0; i < H.ndof; ++i) sr[o++] = R(in->u[i]);
@@ -446,20 +465,6 @@ template <class R> struct Solver final : SolverBase {
     }
     const double* jf = in->joint_frame ? in->joint_frame : H.jframe.data();
     for (int i = 0; i < 21 * H.nj; ++i) sr[o++] = R(jf[i]);
-    // contact incidence (contact*4 + slot), contacts ascending within a block
-    std::vector<int> cnt(H.nd3 + 1, 0);
-    std::vector<int> b4all(4 * (size_t)nc);
-    for (int c = 0; c < nc; ++c) {
-      int* b4 = &b4all[4 * c];
-      body_blocks_h(H, in->contacts[c].body_a, b4[0], b4[1]);
-      body_blocks_h(H, in->contacts[c].body_b, b4[2], b4[3]);
-      for (int s = 0; s < 4; ++s)
-        if (b4[s] >= 0) cnt[b4[s] + 1]++;
-    }
-    for (int b = 0; b < H.nd3; ++b) cnt[b + 1] += cnt[b];
-    const size_t nI = 2 * (size_t)nc + (H.nd3 + 1) + 4 * (size_t)nc;
-    stage_i.alloc(sizeof(int) * nI);
-    int* si = static_cast<int*>(stage_i.p);
     for (int c = 0; c < nc; ++c) {
       si[2 * c] = in->contacts[c].body_a;
       si[2 * c + 1] = in->contacts[c].body_b;
@@ -479,25 +484,16 @@ template <class R> struct Solver final : SolverBase {
     int* hi = plan.hot_ints(hr);
     R* cr = coldr.as<R>();
     int* ci = coldi.as<int>();
-    NSD_CK(cudaMemcpyAsync(cr + plan.q0, sr, sizeof(R) * H.ncoord, cudaMemcpyHostToDevice, stream));
-    NSD_CK(cudaMemcpyAsync(cr + plan.u0, sr + H.ncoord, sizeof(R) * H.ndof, cudaMemcpyHostToDevice, stream));
-    NSD_CK(cudaMemcpyAsync(cr + plan.fx, sr + H.ncoord + H.ndof, sizeof(R) * H.ndof, cudaMemcpyHostToDevice, stream));
-    if (nc)
-      NSD_CK(cudaMemcpyAsync(cr + plan.cgeo, sr + H.ncoord + 2 * H.ndof, sizeof(R) * 17 * nc, cudaMemcpyHostToDevice,
-                             stream));
-    if (H.nj)
-      NSD_CK(cudaMemcpyAsync(topo.jframe, sr + H.ncoord + 2 * H.ndof + 17 * nc, sizeof(R) * 21 * H.nj,
-                             cudaMemcpyHostToDevice, stream));
-    if (nc) NSD_CK(cudaMemcpyAsync(hi + plan.cbody, si, sizeof(int) * 2 * nc, cudaMemcpyHostToDevice, stream));
-    NSD_CK(cudaMemcpyAsync(hi + plan.cinc_off, soff, sizeof(int) * (H.nd3 + 1), cudaMemcpyHostToDevice, stream));
-    if (nc)
-      NSD_CK(cudaMemcpyAsync(hi + plan.cinc_ent, sent, sizeof(int) * cnt[H.nd3], cudaMemcpyHostToDevice, stream));
+    NSD_CK(cudaMemcpyAsync(upbuf.p, stage_in.p, U.bytes, cudaMemcpyHostToDevice, stream));
+    const R* dr = reinterpret_cast<const R*>(upbuf.as<char>() + u_r);
+    const int* di = reinterpret_cast<const int*>(upbuf.as<char>() + u_i);
     // ---- outputs
     Layout L;
     const int dec_stride = nc + H.nt + H.ndof + 1;
     const size_t o_it = L.add<nsd::IterOut>(N), o_hist = L.add<double>((size_t)N * (ml + 1)),
                  o_hl = L.add<int>(N), o_tel = L.add<double>(6 * (size_t)nc), o_fin = L.add<double>(8),
-                 o_dec = L.add<unsigned char>((size_t)N * dec_stride);
+                 o_dec = L.add<unsigned char>((size_t)N * dec_stride), o_q = L.add<R>(H.ncoord),
+                 o_u = L.add<R>(H.ndof), o_lam = L.add<R>(nrows);
     outbuf.alloc(L.bytes);
     char* ob = outbuf.as<char>();
     NSD_CK(cudaMemsetAsync(ob, 0, L.bytes, stream));
@@ -510,8 +506,18 @@ template <class R> struct Solver final : SolverBase {
     so.dec = out->decisions ? reinterpret_cast<unsigned char*>(ob + o_dec) : nullptr;
     so.dec_stride = dec_stride;
     nsd::Work<R> W = plan.bind<R>(hr, hi, cr, ci);
-    W.jframe = topo.jframe;
-    W.f_extra = in->f_extra ? cr + plan.fx : nullptr;
+    // inputs in place in the upload buffer; q, u, lambda in the output buffer (one D2H)
+    W.q0 = dr;
+    W.u0 = dr + H.ncoord;
+    W.f_extra = in->f_extra ? dr + H.ncoord + H.ndof : nullptr;
+    W.cgeo = dr + H.ncoord + 2 * H.ndof;
+    W.jframe = dr + H.ncoord + 2 * H.ndof + 17 * (size_t)nc;
+    W.cbody = di;
+    W.cinc_off = di + 2 * nc;
+    W.cinc_ent = di + 2 * nc + H.nd3 + 1;
+    W.q = reinterpret_cast<R*>(ob + o_q);
+    W.u = reinterpret_cast<R*>(ob + o_u);
+    W.lam = reinterpret_cast<R*>(ob + o_lam);
     W.h = R(in->h);
     for (int k = 0; k < 3; ++k) W.grav[k] = R(in->gravity[k]);
     W.nc = nc;
@@ -531,16 +537,13 @@ template <class R> struct Solver final : SolverBase {
       NSD_CK(launch_single_grid<R>(tets, regs, grid_blocks, stream, topo.t, W, kc, so, gp));
     }
     NSD_CK(cudaEventRecord(ev1, stream));
-    // ---- download
-    stage_o.alloc(L.bytes + sizeof(R) * ((size_t)H.ncoord + H.ndof + nrows));
+    // ---- download: one D2H of the output buffer (reports, q, u, lambda)
+    stage_o.alloc(L.bytes);
     char* ho = static_cast<char*>(stage_o.p);
     NSD_CK(cudaMemcpyAsync(ho, ob, L.bytes, cudaMemcpyDeviceToHost, stream));
-    R* hq = reinterpret_cast<R*>(ho + L.bytes);
-    R* hu = hq + H.ncoord;
-    R* hl = hu + H.ndof;
-    NSD_CK(cudaMemcpyAsync(hq, hr + plan.q, sizeof(R) * H.ncoord, cudaMemcpyDeviceToHost, stream));
-    NSD_CK(cudaMemcpyAsync(hu, hr + plan.u, sizeof(R) * H.ndof, cudaMemcpyDeviceToHost, stream));
-    if (nrows) NSD_CK(cudaMemcpyAsync(hl, hr + plan.lam, sizeof(R) * nrows, cudaMemcpyDeviceToHost, stream));
+    const R* hq = reinterpret_cast<const R*>(ho + o_q);
+    const R* hu = reinterpret_cast<const R*>(ho + o_u);
+    const R* hl = reinterpret_cast<const R*>(ho + o_lam);
     NSD_CK(cudaStreamSynchronize(stream));
     float ms = 0.f;
     NSD_CK(cudaEventElapsedTime(&ms, ev0, ev1));
@@ -644,9 +647,10 @@ template <class R> struct Batch final : BatchBase {
   DBuf ptime;        // NSD_PHASE_TIMING counters
   std::vector<nsd::ShapeD<R>> hshapes;
 
+  bool mixed = false;  // precision fp32 on the warp path: fp64 state, fp32 PCR operator
   Batch(const nsd_topology& tp, int n_shapes, const nsd_shape* sh, double mg, double mud, const nsd_config& c,
-        int nenv, int mc, int device)
-      : cfg(c), n_env(nenv), maxc(mc), ns(n_shapes), margin(mg), mu_default(mud) {
+        int nenv, int mc, int device, bool mixed_precision = false)
+      : cfg(c), n_env(nenv), maxc(mc), ns(n_shapes), margin(mg), mu_default(mud), mixed(mixed_precision) {
     NSD_CK(cudaSetDevice(device));
     if (nenv < 1 || mc < 1 || n_shapes < 0) throw NsdError(NSD_INVALID, "bad batch sizes");
     H = preprocess(tp);
@@ -830,7 +834,7 @@ template <class R> struct Batch final : BatchBase {
       for (int b = 0; b < H.nb; ++b) flat.insert(flat.end(), per[b].begin(), per[b].end());
       wjinc.alloc(sizeof(int) * flat.size());
       NSD_CK(cudaMemcpy(wjinc.p, flat.data(), sizeof(int) * flat.size(), cudaMemcpyHostToDevice));
-      wplan = nsd::wp::Plan::make<R>(H.nb);
+      wplan = mixed ? nsd::wp::Plan::make<R, float>(H.nb) : nsd::wp::Plan::make<R, R>(H.nb);
       wlam.alloc(sizeof(R) * nsd::wp::kRows * 32 * (size_t)n_env);
       if (std::getenv("NSD_PHASE_TIMING")) {
         wptime.alloc(sizeof(unsigned long long) * nsd::wp::kWPhases);
@@ -844,7 +848,7 @@ template <class R> struct Batch final : BatchBase {
       wsetup.alloc(sizeof(R) * (size_t)(H.ndof + 12 * H.nd3) * n_env);
       warp_smem = static_cast<size_t>(wplan.bytes) * warp_epb;
       int per_sm = 0;
-      NSD_CK(batch_warp_setup<R>(max_optin, 32 * warp_epb, warp_smem, &per_sm));
+      NSD_CK(batch_warp_setup<R>(mixed, max_optin, 32 * warp_epb, warp_smem, &per_sm));
       if (per_sm < 1) warp_path = false;
       if (std::getenv("NSD_VERBOSE"))
         std::fprintf(stderr, "nsd batch warp path: %d B/env, %d envs/block, %d blocks/SM\n", wplan.bytes, warp_epb,
@@ -1017,7 +1021,7 @@ template <class R> struct Batch final : BatchBase {
       if (ev) NSD_CK(cudaEventRecord(ev[0], stream));
       NSD_CK(launch_batch_collide<R>((n_env + 3) / 4, 128, collide_smem, stream, A1));
       if (ev) NSD_CK(cudaEventRecord(ev[1], stream));
-      NSD_CK(launch_batch_warp<R>((n_env + warp_epb - 1) / warp_epb, 32 * warp_epb, warp_smem, stream, A));
+      NSD_CK(launch_batch_warp<R>(mixed, (n_env + warp_epb - 1) / warp_epb, 32 * warp_epb, warp_smem, stream, A));
       if (ev) NSD_CK(cudaEventRecord(ev[2], stream));
       A.mode = 2;
       NSD_CK(launch_batch_sub<R>(16, nblk, 16 * epb, smem_bytes, stream, A));
@@ -1223,10 +1227,10 @@ int nsd_batch_create(const nsd_topology* topo, int32_t n_shapes, const nsd_shape
     check_cfg(*cfg);
     auto* b = new nsd_batch();
     try {
-      if (cfg->precision == NSD_FP64)
-        b->impl.reset(new Batch<double>(*topo, n_shapes, shapes, margin, mu_default, *cfg, n_env, max_contacts, device));
-      else
-        b->impl.reset(new Batch<float>(*topo, n_shapes, shapes, margin, mu_default, *cfg, n_env, max_contacts, device));
+      // fp32 is the mixed-precision mode: fp64 state, assembly, Newton update and
+      // reductions; the PCR operator's data and row vectors in fp32 (warp path)
+      b->impl.reset(new Batch<double>(*topo, n_shapes, shapes, margin, mu_default, *cfg, n_env, max_contacts, device,
+                                      cfg->precision == NSD_FP32));
     } catch (...) {
       delete b;
       throw;

@@ -15,8 +15,10 @@ using namespace nsdi;
 #ifndef NSD_WARP_MINB_D
 #define NSD_WARP_MINB_D 7
 #endif
-template <class R> constexpr int warp_minb() { return sizeof(R) == 8 ? NSD_WARP_MINB_D : 8; }
-template <class R> __global__ void __launch_bounds__(64, warp_minb<R>()) k_batch_warp(BatchArgs<R> A) {
+template <class S> constexpr int warp_minb() { return sizeof(S) == 8 ? NSD_WARP_MINB_D : 8; }
+// R: the batch's state precision (double); S: the PCR operator's (double, or float
+// in the mixed-precision mode).
+template <class R, class S> __global__ void __launch_bounds__(64, warp_minb<S>()) k_batch_warp(BatchArgs<R> A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int env = blockIdx.x * (blockDim.x >> 5) + wib;
@@ -27,11 +29,12 @@ template <class R> __global__ void __launch_bounds__(64, warp_minb<R>()) k_batch
   const WorkPlan& P = A.plan;
   const nsd::wp::Plan& L = A.wplan;
   unsigned char* base = smem + (size_t)wib * L.bytes;
-  R* sr = reinterpret_cast<R*>(base);
-  int* si = reinterpret_cast<int*>(base + ((L.nR * sizeof(R) + 15) & ~size_t(15)));
-  nsd::wp::Env<R> E{T,          sr + L.bq,  sr + L.brot, sr + L.bu, sr + L.biwi,     sr + L.bhi,  sr + L.bw,
-                    sr + L.stg, sr + L.rec, sr + L.x,    sr + L.bx, si + L.gent_off, si + L.gent, T.nj,
-                    nc,         T.nb};
+  auto rp = [&](int off) { return reinterpret_cast<R*>(base + off); };
+  auto sp = [&](int off) { return reinterpret_cast<S*>(base + off); };
+  auto ip = [&](int off) { return reinterpret_cast<int*>(base + off); };
+  nsd::wp::Env<R, S> E{T,           rp(L.bq),   rp(L.brot), rp(L.bu), rp(L.biwi),   rp(L.bhi),
+                       sp(L.bw),    base + L.stg, sp(L.rec), rp(L.x),  rp(L.bx),     ip(L.gent_off),
+                       ip(L.gent),  T.nj,       nc,         T.nb};
   R* hr = reinterpret_cast<R*>(A.hot_global + (size_t)env * A.hot_bytes);
   const int* hi = P.hot_ints(hr);
   R* cr = A.cold_r + (size_t)env * P.coldR;
@@ -236,26 +239,28 @@ cudaError_t launch_batch_collide(int nblk, int threads, size_t smem, cudaStream_
   k_batch_collide<R><<<nblk, threads, smem, s>>>(A);
   return cudaGetLastError();
 }
-template cudaError_t launch_batch_collide<float>(int, int, size_t, cudaStream_t, const BatchArgs<float>&);
 template cudaError_t launch_batch_collide<double>(int, int, size_t, cudaStream_t, const BatchArgs<double>&);
 
-template <class R> cudaError_t batch_warp_setup(int max_optin, int threads, size_t smem, int* blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(k_batch_warp<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
+template <class R>
+cudaError_t batch_warp_setup(bool mixed, int max_optin, int threads, size_t smem, int* blocks_per_sm) {
+  const void* kw = mixed ? (const void*)k_batch_warp<R, float> : (const void*)k_batch_warp<R, R>;
+  cudaError_t e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_batch_collide<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_batch_warp<R>, threads, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kw, threads, smem);
 }
 
 template <class R>
-cudaError_t launch_batch_warp(int nblk, int threads, size_t smem, cudaStream_t s, const BatchArgs<R>& A) {
-  k_batch_warp<R><<<nblk, threads, smem, s>>>(A);
+cudaError_t launch_batch_warp(bool mixed, int nblk, int threads, size_t smem, cudaStream_t s, const BatchArgs<R>& A) {
+  if (mixed)
+    k_batch_warp<R, float><<<nblk, threads, smem, s>>>(A);
+  else
+    k_batch_warp<R, R><<<nblk, threads, smem, s>>>(A);
   return cudaGetLastError();
 }
 
-template cudaError_t batch_warp_setup<float>(int, int, size_t, int*);
-template cudaError_t batch_warp_setup<double>(int, int, size_t, int*);
-template cudaError_t launch_batch_warp<float>(int, int, size_t, cudaStream_t, const BatchArgs<float>&);
-template cudaError_t launch_batch_warp<double>(int, int, size_t, cudaStream_t, const BatchArgs<double>&);
+template cudaError_t batch_warp_setup<double>(bool, int, int, size_t, int*);
+template cudaError_t launch_batch_warp<double>(bool, int, int, size_t, cudaStream_t, const BatchArgs<double>&);
 
 }  // namespace nsdi

@@ -266,9 +266,11 @@ template <class R>
 cudaError_t launch_batch_sub(int tpe, int nblk, int threads, size_t smem, cudaStream_t s, const BatchArgs<R>& A);
 template <class R>
 cudaError_t launch_batch_block(int nblk, int threads, size_t smem, cudaStream_t s, const BatchArgs<R>& A);
-template <class R> cudaError_t batch_warp_setup(int max_optin, int threads, size_t smem, int* blocks_per_sm);
+// rigid warp path (double state; mixed = fp32 PCR operator)
 template <class R>
-cudaError_t launch_batch_warp(int nblk, int threads, size_t smem, cudaStream_t s, const BatchArgs<R>& A);
+cudaError_t batch_warp_setup(bool mixed, int max_optin, int threads, size_t smem, int* blocks_per_sm);
+template <class R>
+cudaError_t launch_batch_warp(bool mixed, int nblk, int threads, size_t smem, cudaStream_t s, const BatchArgs<R>& A);
 template <class R>
 cudaError_t launch_batch_collide(int nblk, int threads, size_t smem, cudaStream_t s, const BatchArgs<R>& A);
 

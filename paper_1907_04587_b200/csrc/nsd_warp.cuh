@@ -112,12 +112,13 @@ template <class R> __device__ __forceinline__ Rec<R> rec_load(const R* rec, int 
   o.d[4] = rec_v3<18>(rec, lane);
   return o;
 }
-template <class R> __device__ __forceinline__ void rec3_put(R* rec, int v, int lane, V3<R> x) {
-  R* p = rec + rec_stride<R>() * lane + v;
-  p[0] = x.x;
-  p[1] = x.y;
-  p[2] = x.z;
+template <class S, class R> __device__ __forceinline__ void rec3_put(S* rec, int v, int lane, V3<R> x) {
+  S* p = rec + rec_stride<S>() * lane + v;
+  p[0] = S(x.x);
+  p[1] = S(x.y);
+  p[2] = S(x.z);
 }
+template <class T, class S> __device__ __forceinline__ V3<T> cv3(V3<S> v) { return v3(T(v.x), T(v.y), T(v.z)); }
 
 // This lane's constraint object.
 struct Obj {
@@ -136,16 +137,18 @@ template <class R> __device__ __forceinline__ R lin_quad_shifted(V3<R> c, R hi) 
   return c.x * c.x * hi + c.y * c.y * hi + c.z * c.z * hi;
 }
 
-template <class R> struct Env {
+// R: state, assembly, Newton update (double); S: the PCR operator's data and row
+// vectors (double, or float in the mixed-precision mode).
+template <class R, class S> struct Env {
   const Topo<R>& T;
   R* bq;
   R* brot;
   R* bu;
   R* biwi;
   R* bhi;
-  R* bw;
-  R* stg;
-  R* rec;
+  S* bw;     // w = H^-1 J^T y of the operator
+  void* stg;  // staging: R (momentum, du) or S (operator) values
+  S* rec;
   R* x;  // [row][lane]
   R* bx;
   int* gent_off;  // per body: its staged wrenches (joints, then contacts ascending)
@@ -157,59 +160,70 @@ template <class R> struct Env {
 // in the reference's order a.lin + a.ang + b.lin + b.ang (contact_quad /
 // object_quad). shifted: H^-1 = 1/(m + 0) per linear dof; else the unshifted
 // c^2/m of BlockDiagMass::inverse_quadratic (bodies.cpp:149-177).
-template <class R>
-__device__ __forceinline__ R point_quad(const Topo<R>& T, const R* biwi, int a, int b, V3<R> d, V3<R> arm_a, V3<R> arm_b,
+// sym_mul / sym_quad (nsd_engine.cuh) with the symmetric matrix held in R and the
+// vector in S (the same expressions when R == S).
+template <class S, class R> __device__ __forceinline__ V3<S> sym_mul_t(const R* s6, V3<S> v) {
+  const S a = S(s6[0]), b = S(s6[1]), c = S(s6[2]), d = S(s6[3]), e = S(s6[4]), f = S(s6[5]);
+  return v3(a * v.x + d * v.y + e * v.z, d * v.x + b * v.y + f * v.z, e * v.x + f * v.y + c * v.z);
+}
+template <class S, class R> __device__ __forceinline__ S sym_quad_t(const R* s6, V3<S> v) { return dot(v, sym_mul_t(s6, v)); }
+
+template <class S, class R>
+__device__ __forceinline__ S point_quad(const Topo<R>& T, const R* biwi, int a, int b, V3<S> d, V3<S> arm_a, V3<S> arm_b,
                                         bool shifted) {
-  R s = R(0);
+  S s = S(0);
   if (a >= 0) {
-    const R m = T.bmass[a];
-    s += shifted ? lin_quad_shifted(d, R(1) / (m + R(0))) : lin_quad_unshifted(d, m);
-    s += sym_quad(biwi + 6 * a, cross(arm_a, d));
+    const S m = S(T.bmass[a]);
+    s += shifted ? lin_quad_shifted(d, S(1) / (m + S(0))) : lin_quad_unshifted(d, m);
+    s += sym_quad_t(biwi + 6 * a, cross(arm_a, d));
   }
   if (b >= 0) {
-    const R m = T.bmass[b];
-    s += shifted ? lin_quad_shifted(d, R(1) / (m + R(0))) : lin_quad_unshifted(d, m);
-    s += sym_quad(biwi + 6 * b, cross(arm_b, d));
+    const S m = S(T.bmass[b]);
+    s += shifted ? lin_quad_shifted(d, S(1) / (m + S(0))) : lin_quad_unshifted(d, m);
+    s += sym_quad_t(biwi + 6 * b, cross(arm_b, d));
   }
   return s;
 }
 
 // J^T y of this lane's object into its staging slot: a side (f, r_a x f + tau),
 // b side (-f, -(r_b x f + tau)); f = sum_i (s_i y_i) D_i, tau = sum_i y_i C_i.
-template <class R, class YF>
-__device__ __forceinline__ void stage_f(const Env<R>& E, const Obj& o, int lane, const R (&s)[3], const YF& y) {
+// T: the precision of the staged values (S for the operator, R for the momentum
+// and Newton-update gathers); the records are read in S and widened.
+template <class T, class R, class S, class YF>
+__device__ __forceinline__ void stage_f(const Env<R, S>& E, const Obj& o, int lane, const T (&s)[3], const YF& y) {
   if (o.kind < 0) return;
-  V3<R> f = v3(R(0), R(0), R(0)), ta = f;
-  if (0 < o.np) f = f + (s[0] * y(0)) * rec_v3<6>(E.rec, lane);
-  if (1 < o.np) f = f + (s[1] * y(1)) * rec_v3<9>(E.rec, lane);
-  if (2 < o.np) f = f + (s[2] * y(2)) * rec_v3<12>(E.rec, lane);
-  if (0 >= o.np && 0 < o.nr) ta = ta + y(0) * rec_v3<6>(E.rec, lane);
-  if (1 >= o.np && 1 < o.nr) ta = ta + y(1) * rec_v3<9>(E.rec, lane);
-  if (2 >= o.np && 2 < o.nr) ta = ta + y(2) * rec_v3<12>(E.rec, lane);
-  if (3 < o.nr) ta = ta + y(3) * rec_v3<15>(E.rec, lane);
-  if (4 < o.nr) ta = ta + y(4) * rec_v3<18>(E.rec, lane);
-  R* d = E.stg + kStg * lane;
+  V3<T> f = v3(T(0), T(0), T(0)), ta = f;
+  if (0 < o.np) f = f + (s[0] * y(0)) * cv3<T>(rec_v3<6>(E.rec, lane));
+  if (1 < o.np) f = f + (s[1] * y(1)) * cv3<T>(rec_v3<9>(E.rec, lane));
+  if (2 < o.np) f = f + (s[2] * y(2)) * cv3<T>(rec_v3<12>(E.rec, lane));
+  if (0 >= o.np && 0 < o.nr) ta = ta + y(0) * cv3<T>(rec_v3<6>(E.rec, lane));
+  if (1 >= o.np && 1 < o.nr) ta = ta + y(1) * cv3<T>(rec_v3<9>(E.rec, lane));
+  if (2 >= o.np && 2 < o.nr) ta = ta + y(2) * cv3<T>(rec_v3<12>(E.rec, lane));
+  if (3 < o.nr) ta = ta + y(3) * cv3<T>(rec_v3<15>(E.rec, lane));
+  if (4 < o.nr) ta = ta + y(4) * cv3<T>(rec_v3<18>(E.rec, lane));
+  T* d = static_cast<T*>(E.stg) + kStg * lane;
   if (o.a >= 0) {
     sts3(d, f);
-    sts3(d + 3, cross(rec_v3<0>(E.rec, lane), f) + ta);
+    sts3(d + 3, cross(cv3<T>(rec_v3<0>(E.rec, lane)), f) + ta);
   }
   if (o.b >= 0) {
     sts3(d + 6, -f);
-    sts3(d + 9, -(cross(rec_v3<3>(E.rec, lane), f) + ta));
+    sts3(d + 9, -(cross(cv3<T>(rec_v3<3>(E.rec, lane)), f) + ta));
   }
 }
 
-template <class R>
-__device__ __forceinline__ void stage(const Env<R>& E, const Obj& o, int lane, const R (&s)[3], const R (&y)[kRows]) {
+template <class T, class R, class S>
+__device__ __forceinline__ void stage(const Env<R, S>& E, const Obj& o, int lane, const T (&s)[3], const T (&y)[kRows]) {
   stage_f(E, o, lane, s, [&](int i) { return y[i]; });
 }
 
 // Body gather of the staged wrenches (joints first, then contacts ascending).
-template <class R> __device__ __forceinline__ void gather(const Env<R>& E, int b, V3<R>& lin, V3<R>& ang) {
-  lin = v3(R(0), R(0), R(0));
+template <class T, class R, class S>
+__device__ __forceinline__ void gather(const Env<R, S>& E, int b, V3<T>& lin, V3<T>& ang) {
+  lin = v3(T(0), T(0), T(0));
   ang = lin;
   for (int e = E.gent_off[b]; e < E.gent_off[b + 1]; ++e) {
-    const R* s = E.stg + E.gent[e];
+    const T* s = static_cast<const T*>(E.stg) + E.gent[e];
     lin = lin + lds3(s);
     ang = ang + lds3(s + 3);
   }
@@ -218,15 +232,15 @@ template <class R> __device__ __forceinline__ void gather(const Env<R>& E, int b
 // One component k of body b's gathered J^T y: the body's staged wrenches summed in
 // entry order (the order of gather()); the offsets and values of four entries are
 // loaded before their ordered adds.
-template <class R> __device__ __forceinline__ R gather_comp(const Env<R>& E, int b, int k) {
+template <class R, class S> __device__ __forceinline__ S gather_comp(const Env<R, S>& E, int b, int k) {
   const int e0 = E.gent_off[b], n = E.gent_off[b + 1] - e0;
   const int* ge = E.gent + e0;
-  const R* sk = E.stg + k;
-  R acc = R(0);
+  const S* sk = static_cast<const S*>(E.stg) + k;
+  S acc = S(0);
   int e = 0;
   for (; e + 4 <= n; e += 4) {
     const int o0 = ge[e], o1 = ge[e + 1], o2 = ge[e + 2], o3 = ge[e + 3];
-    const R v0 = sk[o0], v1 = sk[o1], v2 = sk[o2], v3 = sk[o3];
+    const S v0 = sk[o0], v1 = sk[o1], v2 = sk[o2], v3 = sk[o3];
     acc = acc + v0;
     acc = acc + v1;
     acc = acc + v2;
@@ -240,26 +254,26 @@ template <class R> __device__ __forceinline__ R gather_comp(const Env<R>& E, int
 // 6 g + k owns component k of body 5 r + g. Linear rows scale by 1/m; angular row
 // k - 3 applies I_w^-1 (sym_mul's expression) to the torque held by the group's
 // lanes 3..5, exchanged by shuffles. Needs __syncwarp() before (staging) and after.
-template <class R> __device__ __forceinline__ void bodies_w(const Env<R>& E, int lane) {
+template <class R, class S> __device__ __forceinline__ void bodies_w(const Env<R, S>& E, int lane) {
   const int g = lane / 6, k = lane - 6 * g;
   const int g3 = 6 * g + 3;
   for (int b0 = 0; b0 < E.nb; b0 += 5) {
     const int b = b0 + g;
     const bool on = g < 5 && b < E.nb;
-    const R t = on ? gather_comp(E, b, k) : R(0);
-    const R tx = __shfl_sync(0xffffffffu, t, g3 < 32 ? g3 : 0);
-    const R ty = __shfl_sync(0xffffffffu, t, g3 + 1 < 32 ? g3 + 1 : 0);
-    const R tz = __shfl_sync(0xffffffffu, t, g3 + 2 < 32 ? g3 + 2 : 0);
+    const S t = on ? gather_comp(E, b, k) : S(0);
+    const S tx = __shfl_sync(0xffffffffu, t, g3 < 32 ? g3 : 0);
+    const S ty = __shfl_sync(0xffffffffu, t, g3 + 1 < 32 ? g3 + 1 : 0);
+    const S tz = __shfl_sync(0xffffffffu, t, g3 + 2 < 32 ? g3 + 2 : 0);
     if (on) {
-      R w;
+      S w;
       if (k < 3) {
-        w = t * E.bhi[b];
+        w = t * S(E.bhi[b]);
       } else {
         const R* s6 = E.biwi + 6 * b;  // xx yy zz xy xz yz; row k - 3 of sym_mul
         const int r = k - 3;
-        const R c0 = r == 0 ? s6[0] : (r == 1 ? s6[3] : s6[4]);
-        const R c1 = r == 0 ? s6[3] : (r == 1 ? s6[1] : s6[5]);
-        const R c2 = r == 0 ? s6[4] : (r == 1 ? s6[5] : s6[2]);
+        const S c0 = S(r == 0 ? s6[0] : (r == 1 ? s6[3] : s6[4]));
+        const S c1 = S(r == 0 ? s6[3] : (r == 1 ? s6[1] : s6[5]));
+        const S c2 = S(r == 0 ? s6[4] : (r == 1 ? s6[5] : s6[2]));
         w = c0 * tx + c1 * ty + c2 * tz;
       }
       E.bw[6 * b + k] = w;
@@ -267,47 +281,48 @@ template <class R> __device__ __forceinline__ void bodies_w(const Env<R>& E, int
   }
 }
 
-template <class R>
-__device__ __forceinline__ void jw(const Env<R>& E, const Obj& o, int lane, const R (&s)[3], R (&out)[kRows]) {
-  V3<R> dv = v3(R(0), R(0), R(0)), wr = dv;
+template <class R, class S>
+__device__ __forceinline__ void jw(const Env<R, S>& E, const Obj& o, int lane, const S (&s)[3], S (&out)[kRows]) {
+  V3<S> dv = v3(S(0), S(0), S(0)), wr = dv;
   if (o.a >= 0) {
-    const R* w = E.bw + 6 * o.a;
+    const S* w = E.bw + 6 * o.a;
     wr = lds3(w + 3);
     dv = lds3(w) + cross(wr, rec_v3<0>(E.rec, lane));
   }
   if (o.b >= 0) {
-    const R* w = E.bw + 6 * o.b;
-    const V3<R> wb = lds3(w + 3);
+    const S* w = E.bw + 6 * o.b;
+    const V3<S> wb = lds3(w + 3);
     dv = dv - lds3(w);
     dv = dv - cross(wb, rec_v3<3>(E.rec, lane));
     wr = wr - wb;
   }
-  auto row = [&](int i, V3<R> d) {
+  auto row = [&](int i, V3<S> d) {
     if (i < o.np) {
-      const R t = dot(d, dv);
-      return s[i] == R(0) ? R(0) : s[i] * t;
+      const S t = dot(d, dv);
+      return s[i] == S(0) ? S(0) : s[i] * t;
     }
-    return i < o.nr ? dot(d, wr) : R(0);
+    return i < o.nr ? dot(d, wr) : S(0);
   };
   out[0] = row(0, rec_v3<6>(E.rec, lane));
   out[1] = row(1, rec_v3<9>(E.rec, lane));
   out[2] = row(2, rec_v3<12>(E.rec, lane));
-  out[3] = 3 < o.nr ? dot(rec_v3<15>(E.rec, lane), wr) : R(0);
-  out[4] = 4 < o.nr ? dot(rec_v3<18>(E.rec, lane), wr) : R(0);
+  out[3] = 3 < o.nr ? dot(rec_v3<15>(E.rec, lane), wr) : S(0);
+  out[4] = 4 < o.nr ? dot(rec_v3<18>(E.rec, lane), wr) : S(0);
 }
 
 // J_i H^-1 J_i^T (shifted H; rigid bodies carry no shift) for this lane's rows.
-template <class R> __device__ __forceinline__ void quads(const Env<R>& E, const Obj& o, int lane, const R (&s)[3], R (&q)[kRows]) {
-  const Rec<R> rc = rec_load(E.rec, lane);
+template <class R, class S>
+__device__ __forceinline__ void quads(const Env<R, S>& E, const Obj& o, int lane, const S (&s)[3], S (&q)[kRows]) {
+  const Rec<S> rc = rec_load(E.rec, lane);
 #pragma unroll
   for (int i = 0; i < kRows; ++i) {
-    q[i] = R(0);
+    q[i] = S(0);
     if (i < o.np) {
-      if (s[i] != R(0)) q[i] = point_quad(E.T, E.biwi, o.a, o.b, s[i] * rc.d[i], rc.arm_a, rc.arm_b, true);
+      if (s[i] != S(0)) q[i] = point_quad(E.T, E.biwi, o.a, o.b, s[i] * rc.d[i], rc.arm_a, rc.arm_b, true);
     } else if (i < o.nr) {
-      R t = R(0);
-      if (o.a >= 0) t += sym_quad(E.biwi + 6 * o.a, rc.d[i]);
-      if (o.b >= 0) t += sym_quad(E.biwi + 6 * o.b, rc.d[i]);
+      S t = S(0);
+      if (o.a >= 0) t += sym_quad_t(E.biwi + 6 * o.a, rc.d[i]);
+      if (o.b >= 0) t += sym_quad_t(E.biwi + 6 * o.b, rc.d[i]);
       q[i] = t;
     }
   }
@@ -316,8 +331,8 @@ template <class R> __device__ __forceinline__ void quads(const Env<R>& E, const 
 // Assembly of this lane's object at the current iterate (newton.cpp:100-231):
 // writes the record (arms, row directions), the row scales s, h and the C
 // diagonal per row, and accumulates the telemetry maxima / |h|^2.
-template <class R>
-__device__ __forceinline__ void assemble_obj(const Env<R>& E, const Obj& o, int lane, const R* jframe, const R* jparam,
+template <class R, class S>
+__device__ __forceinline__ void assemble_obj(const Env<R, S>& E, const Obj& o, int lane, const R* jframe, const R* jparam,
                                              const R* cgeo, R h, const Cfg& cfg, const R (&lam)[kRows], R (&s)[3],
                                              R (&hv)[kRows], R (&cd)[kRows], AsmStats& st) {
   s[0] = s[1] = s[2] = R(1);
@@ -458,7 +473,7 @@ __device__ __forceinline__ void assemble_obj(const Env<R>& E, const Obj& o, int 
 }
 
 // Refresh the rotation cache of body b from its quaternion.
-template <class R> __device__ __forceinline__ void refresh_rot(const Env<R>& E, int b) {
+template <class R, class S> __device__ __forceinline__ void refresh_rot(const Env<R, S>& E, int b) {
   const R* t = E.bq + 8 * b + 3;
   const M3<R> m = quat_rot(t[0], t[1], t[2], t[3]);
 #pragma unroll
@@ -517,8 +532,8 @@ template <class R> __device__ __forceinline__ void rows_load(const R* v, int lan
 
 // Body b's gradient block g = M~(u - u~) - J^T lambda (after staging lambda);
 // accumulates residual_inf / |g|^2 in the reference's order (bodies rigid).
-template <class R>
-__device__ __forceinline__ void body_grad(const Topo<R>& T, const Env<R>& E, const EnvIO<R>& io, int b, V3<R>& gl,
+template <class R, class S>
+__device__ __forceinline__ void body_grad(const Topo<R>& T, const Env<R, S>& E, const EnvIO<R>& io, int b, V3<R>& gl,
                                           V3<R>& ga, double& gmax, double& gsq) {
   const int d = T.bdof[b];
   V3<R> jl, ja;
@@ -538,8 +553,8 @@ __device__ __forceinline__ void body_grad(const Topo<R>& T, const Env<R>& E, con
   gsq += (double)ga.x * ga.x + (double)ga.y * ga.y + (double)ga.z * ga.z;
 }
 
-template <class R>
-__device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h, Env<R>& E, const EnvIO<R>& io,
+template <class R, class S>
+__device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h, Env<R, S>& E, const EnvIO<R>& io,
                           int lane) {
   const int nb = T.nb, nj = T.nj, nc = E.nc;
   const long long t_env0 = io.env_cycles ? clock64() : 0;
@@ -613,7 +628,7 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
     row0 = T.rows_static + c;
     row1 = T.rows_static + nc + 2 * c;
   }
-  const R eps = R(cfg.epsilon_reg), tfrac = R(cfg.step_fraction);
+  const R tfrac = R(cfg.step_fraction);
   const int maxlin = cfg.linear_max_iterations;
   R s[3], cd[kRows], lam[kRows];
   long long cr_cyc = 0;
@@ -639,9 +654,9 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
       sts3(io.g + d, gl);
       sts3(io.g + d + 3, ga);
       const R hi = E.bhi[b];
-      R* w = E.bw + 6 * b;
-      sts3(w, v3(gl.x * hi, gl.y * hi, gl.z * hi));
-      sts3(w + 3, sym_mul(E.biwi + 6 * b, ga));
+      S* w = E.bw + 6 * b;
+      sts3(w, cv3<S>(v3(gl.x * hi, gl.y * hi, gl.z * hi)));
+      sts3(w + 3, cv3<S>(sym_mul(E.biwi + 6 * b, ga)));
     }
     double s_g = gsq, s_h = as.hsq;
     wsum2(s_g, s_h);
@@ -656,12 +671,20 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
     st.step_size = 0.0;
     __syncwarp();
     pc.mark(2);
-    // ---- Schur rhs b = J H^-1 g - h, diagonal preconditioner, r = b, x = 0, z = M^-1 r
+    // ---- Schur rhs b = J H^-1 g - h, diagonal preconditioner, r = b, x = 0, z = M^-1 r.
+    // The PCR recurrence (row vectors, preconditioner, C diagonal) runs in R; the
+    // operator's products J^T y, H^-1, J w in S (the scales cast once): with S = float
+    // the operator is rounded at 1e-7 while the recurrence keeps its fp64 floor, so
+    // its exits (monotone guard, tolerance) stay those of the fp64 solve.
     R r[kRows], z[kRows], p[kRows], ap[kRows], az[kRows], inv[kRows];
+    S ss[3];
+    const R eps = R(cfg.epsilon_reg);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) ss[i] = S(s[i]);
     {
-      R jwv[kRows], qd[kRows];
-      jw(E, o, lane, s, jwv);
-      quads(E, o, lane, s, qd);
+      S jwv[kRows], qd[kRows];
+      jw(E, o, lane, ss, jwv);
+      quads(E, o, lane, ss, qd);
       double rr = 0.0, rzr = 0.0;
 #pragma unroll
       for (int i = 0; i < kRows; ++i) {
@@ -670,10 +693,10 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
         E.x[32 * i + lane] = R(0);
         E.bx[32 * i + lane] = R(0);
         if (i < o.nr) {
-          const R bi = jwv[i] - hv[i];
+          const R bi = R(jwv[i]) - hv[i];
           R iv = R(1);
           if (cfg.preconditioner == 1) {
-            const R sd = qd[i] + cd[i] + eps;
+            const R sd = R(qd[i]) + cd[i] + eps;
             iv = sd > R(0) ? R(1) / sd : R(1);
           }
           inv[i] = iv;
@@ -690,17 +713,17 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
       const long long tc0 = io.cr_cycles ? clock64() : 0;
       if (maxlin > 0 && hist_last > cfg.linear_tolerance) {
         // az = A z, zaz = z . az (solvers.cpp PCR setup)
-        stage(E, o, lane, s, z);
+        stage_f(E, o, lane, ss, [&](int i) { return S(z[i]); });
         __syncwarp();
         bodies_w(E, lane);
         __syncwarp();
-        R jz[kRows];
-        jw(E, o, lane, s, jz);
+        S jz[kRows];
+        jw(E, o, lane, ss, jz);
         double za = 0.0;
 #pragma unroll
         for (int i = 0; i < kRows; ++i)
           if (i < o.nr) {
-            az[i] = jz[i] + cd[i] * z[i] + eps * z[i];
+            az[i] = R(jz[i]) + cd[i] * z[i] + eps * z[i];
             za += (double)z[i] * az[i];
           }
         double zaz = wsum(za), beta = 0.0;
@@ -727,7 +750,8 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
             breakdown = 1;
             break;
           }
-          const R ra = R(zaz / den);
+          const double alpha = zaz / den;
+          const R ra = R(alpha);
           // trial r' = r - a ap, z' = z - a M^-1 ap and its norms; J^T z' staged
           // speculatively in the same pass (a rejected trial discards it)
           double pn2 = 0.0, rn2 = 0.0;
@@ -739,7 +763,7 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
               rn2 += (double)rv * rv;
             }
           const bool zaz_ok = fabs(zaz) >= 1e-300;
-          if (zaz_ok) stage_f(E, o, lane, s, [&](int i) { return z[i] - ra * (inv[i] * ap[i]); });
+          if (zaz_ok) stage_f(E, o, lane, ss, [&](int i) { return S(z[i] - ra * (inv[i] * ap[i])); });
           wsum2(pn2, rn2);
           pc.mark(6);
           const double pn = sqrt(pn2);
@@ -766,13 +790,13 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
           bodies_w(E, lane);
           __syncwarp();
           pc.mark(8);
-          R jz2[kRows];
-          jw(E, o, lane, s, jz2);
+          S jz2[kRows];
+          jw(E, o, lane, ss, jz2);
           double za2 = 0.0;
 #pragma unroll
           for (int i = 0; i < kRows; ++i)
             if (i < o.nr) {
-              az[i] = jz2[i] + cd[i] * z[i] + eps * z[i];
+              az[i] = R(jz2[i]) + cd[i] * z[i] + eps * z[i];
               za2 += (double)z[i] * az[i];
             }
           za2 = wsum(za2);
@@ -891,9 +915,14 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
     double mgap = __builtin_huge_val();
     if (o.kind == 4) {
       const R* g = io.cgeo + 17 * o.idx;
-      const Rec<R> rc = rec_load(E.rec, lane);
-      const V3<R> pa = o.a < 0 ? lds3(g) : lds3(E.bq + 8 * o.a) + rc.arm_a;
-      const V3<R> pb = o.b < 0 ? lds3(g + 3) : lds3(E.bq + 8 * o.b) + rc.arm_b;
+      auto arm = [&](int b, V3<R> l) {  // the arm of the final assembly, in R
+        M3<R> m;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) m.a[i] = E.brot[9 * b + i];
+        return mul(m, l);
+      };
+      const V3<R> pa = o.a < 0 ? lds3(g) : lds3(E.bq + 8 * o.a) + arm(o.a, lds3(g));
+      const V3<R> pb = o.b < 0 ? lds3(g + 3) : lds3(E.bq + 8 * o.b) + arm(o.b, lds3(g + 3));
       mgap = (double)(dot(lds3(g + 6), pa - pb) - g[15]);
     }
     const double fr = wmax(fmax(gmax, fs.hmax)), fcomp = wmax(fs.comp), fcone = wmax(fs.cone);

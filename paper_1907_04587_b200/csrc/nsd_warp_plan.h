@@ -16,34 +16,34 @@ constexpr int kWPhases = 14;  // NSD_PHASE_TIMING counters of the warp solver
 // fp32 28 words = 28 mod 32).
 template <class R> __host__ __device__ constexpr int rec_stride() { return sizeof(R) == 8 ? 22 : 28; }
 
-// Per-env shared-memory layout (element offsets; R part then int part).
+// Per-env shared-memory layout, byte offsets: R (state/assembly) arrays, S (PCR
+// operator) arrays, the staging area sized for R values (it holds R or S values),
+// then the int lists.
 struct Plan {
-  int bq, brot, bu, biwi, bhi, bw, stg, rec, x, bx, nR;  // R elements
-  int gent_off, gent, nI;                                      // int elements after the R part
-  int bytes;                                                   // per env, 16-byte multiple
-  template <class R> static Plan make(int nb) {
+  int bq, brot, bu, biwi, bhi, bw, stg, rec, x, bx, gent_off, gent;
+  int bytes;  // per env, 16-byte multiple
+  template <class R, class S> static Plan make(int nb) {
     Plan p{};
     int o = 0;
-    auto a = [&](int n) {
+    auto a = [&](int bytes) {
       const int off = o;
-      o += (n + 3) & ~3;  // 16-byte aligned sub-arrays (fp32 and fp64)
+      o += (bytes + 15) & ~15;  // 16-byte aligned sub-arrays
       return off;
     };
-    p.bq = a(8 * nb);  // pos 3, quat 4, pad
-    p.brot = a(9 * nb);
-    p.bu = a(6 * nb);
-    p.biwi = a(6 * nb);
-    p.bhi = a(nb);     // 1 / (m + 0): H^-1 of the linear block (rigid dofs carry no shift)
-    p.bw = a(6 * nb);  // w = H^-1 J^T y
-    p.stg = a(kStg * 32);
-    p.rec = a(rec_stride<R>() * 32);
-    p.x = a(kRows * 32);  // lane-private row vectors, [row][lane]
-    p.bx = a(kRows * 32);
-    p.nR = o;
-    p.gent_off = 0;  // per body: first entry; entries are staging offsets (object * kStg + 6 * side)
-    p.gent = (nb + 1 + 3) & ~3;
-    p.nI = p.gent + 64;
-    p.bytes = ((o * (int)sizeof(R) + 15) & ~15) + ((p.nI * 4 + 15) & ~15);
+    const int r = sizeof(R), sz = sizeof(S);
+    p.bq = a(8 * nb * r);  // pos 3, quat 4, pad
+    p.brot = a(9 * nb * r);
+    p.bu = a(6 * nb * r);
+    p.biwi = a(6 * nb * r);
+    p.bhi = a(nb * r);     // 1 / (m + 0): H^-1 of the linear block (rigid dofs carry no shift)
+    p.bw = a(6 * nb * sz);  // w = H^-1 J^T y of the operator
+    p.stg = a(kStg * 32 * r);
+    p.rec = a(rec_stride<S>() * 32 * sz);
+    p.x = a(kRows * 32 * r);  // lane-private row vectors, [row][lane]
+    p.bx = a(kRows * 32 * r);
+    p.gent_off = a((nb + 1) * 4);  // per body: first entry; entries are staging offsets
+    p.gent = a(64 * 4);            // (object * kStg + 6 * side)
+    p.bytes = o;
     return p;
   }
 };
