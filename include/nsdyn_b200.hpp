@@ -20,8 +20,8 @@
 // std::invalid_argument (bodies.cpp:80, constraints.cpp:142-144,
 // solvers.cpp:188-190); a NaN in the Newton update rolls q, u back and returns
 // a report with aborted = true (newton.cpp:362-369). A CUDA failure or an
-// option that is not on the GPU path (Gauss-Seidel, record_iterates, mixed
-// material models in one scene) throws std::runtime_error — there is no CPU fallback.
+// option that is not on the GPU path (record_iterates, mixed material models in
+// one scene) throws std::runtime_error — there is no CPU fallback.
 //
 // Device state: newton_step keeps one device solver per thread, keyed by the
 // StepContext's state/joints/meshes addresses and sizes and by the config;
@@ -366,8 +366,6 @@ struct FlatTopology {
 
 inline nsd_config to_c(const NewtonConfig& c) {
   if (c.record_iterates) throw std::runtime_error("nsdyn_b200: record_iterates is not on the GPU path");
-  if (c.linear.method == LinearMethod::GaussSeidel)
-    throw std::runtime_error("nsdyn_b200: Gauss-Seidel's sequential row sweep is not on the GPU path");
   nsd_config k{};
   nsd_config_default(&k, c.precision == Precision::FP64 ? NSD_FP64 : NSD_FP32);
   k.newton_iterations = c.newton_iterations;
@@ -376,7 +374,7 @@ inline nsd_config to_c(const NewtonConfig& c) {
   k.geometric_stiffness = c.geometric_stiffness ? 1 : 0;
   k.r_strategy = static_cast<int32_t>(c.r_strategy);
   k.ncp_kind = static_cast<int32_t>(c.ncp_kind);
-  k.linear_method = static_cast<int32_t>(c.linear.method);  // 0 Jacobi, 2 PCG, 3 PCR
+  k.linear_method = static_cast<int32_t>(c.linear.method);  // 0 Jacobi, 1 Gauss-Seidel, 2 PCG, 3 PCR
   k.linear_max_iterations = c.linear.max_iterations;
   k.linear_tolerance = c.linear.tolerance;
   k.preconditioner = static_cast<int32_t>(c.linear.preconditioner);
@@ -756,9 +754,10 @@ inline void write_atomic(const std::filesystem::path& path, const std::string& c
 inline void apply_overrides(const RunOptions& o, NewtonConfig& c) {
   if (o.solver_method) {
     const std::string& m = *o.solver_method;
-    if (m == "gs") throw std::runtime_error("solver \"gs\" (Gauss-Seidel) is not on the GPU Newton path");
     if (m == "jacobi")
       c.linear.method = LinearMethod::Jacobi;
+    else if (m == "gs")
+      c.linear.method = LinearMethod::GaussSeidel;
     else if (m == "pcg")
       c.linear.method = LinearMethod::PCG;
     else if (m == "pcr")
@@ -887,13 +886,13 @@ inline int run(const RunOptions& o, std::string* error = nullptr) {
 }
 
 // sweep (runner.cpp:182-218): one run per axis value, merged sweep.csv. The
-// "solver" axis runs jacobi, pcg and pcr (Gauss-Seidel is not on the GPU path).
+// "solver" axis runs jacobi, gs, pcg and pcr (runner.cpp:187).
 inline int sweep(const RunOptions& o, const std::string& axis, std::string* error = nullptr) {
   try {
     if (o.steps < 1) throw std::runtime_error("--steps must be >= 1");
     std::vector<std::string> values;
     if (axis == "solver")
-      values = {"jacobi", "pcg", "pcr"};
+      values = {"jacobi", "gs", "pcg", "pcr"};
     else if (axis == "r_strategy")
       values = {"identity", "h2", "effmass"};
     else if (axis == "ncp")

@@ -46,7 +46,7 @@ typedef struct nsd_config {
   int32_t geometric_stiffness;   /* default 1 */
   int32_t r_strategy;            /* 0 Identity, 1 TimestepSquared, 2 EffectiveMass (default) */
   int32_t ncp_kind;              /* 0 MinimumMap, 1 FischerBurmeister (default) */
-  int32_t linear_method;         /* 0 Jacobi, 2 PCG, 3 PCR (default); 1 Gauss-Seidel -> NSD_UNSUPPORTED */
+  int32_t linear_method;         /* 0 Jacobi, 1 Gauss-Seidel, 2 PCG, 3 PCR (default); batches: PCR only */
   int32_t linear_max_iterations; /* default 40 */
   double linear_tolerance;       /* absolute residual 2-norm, default 1e-10 */
   int32_t preconditioner;        /* 0 None, 1 Diagonal (default) */

@@ -121,10 +121,8 @@ nsd::Cfg to_cfg(const nsd_config& c) {
 
 void check_cfg(const nsd_config& c) {
   if (c.precision != NSD_FP32 && c.precision != NSD_FP64) throw NsdError(NSD_INVALID, "precision must be 0 or 1");
-  if (c.linear_method == 1)
-    throw NsdError(NSD_UNSUPPORTED, "Gauss-Seidel's ascending-row sweep is sequential: not on the device path");
-  if (c.linear_method != 0 && c.linear_method != 2 && c.linear_method != 3)
-    throw NsdError(NSD_INVALID, "linear_method must be 0 (Jacobi), 2 (PCG) or 3 (PCR)");
+  if (c.linear_method < 0 || c.linear_method > 3)
+    throw NsdError(NSD_INVALID, "linear_method must be 0 (Jacobi), 1 (Gauss-Seidel), 2 (PCG) or 3 (PCR)");
   if (c.linear_max_iterations < 1) throw NsdError(NSD_INVALID, "solve_linear: max_iterations < 1");
   if (c.newton_iterations < 0) throw NsdError(NSD_INVALID, "newton_iterations < 0");
   if (c.r_strategy < 0 || c.r_strategy > 2 || c.ncp_kind < 0 || c.ncp_kind > 1 || c.preconditioner < 0 ||

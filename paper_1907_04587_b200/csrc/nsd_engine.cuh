@@ -394,6 +394,35 @@ template <class R> __device__ __forceinline__ R row_quad(const Topo<R>& T, const
   return contact_quad(T, W, c, (k & 1) ? c.d2 : c.d1, true);
 }
 
+// J_i^T d as (dof3 block, 3-vector) pairs, f(block, v): the transpose of row_J for one
+// row (Gauss-Seidel's incremental w = H^-1 J^T x update).
+template <class R, class F>
+__device__ __forceinline__ void row_JT(const Topo<R>& T, const Work<R>& W, int i, R d, F&& f) {
+  if (i < T.rows_static) {
+    const R* c = W.coeff + 12 * i;
+    const int* b4 = W.blk + 4 * i;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (b4[k] >= 0) f(b4[k], v3(c[3 * k] * d, c[3 * k + 1] * d, c[3 * k + 2] * d));
+    return;
+  }
+  const bool normal = i < W.friction_begin;
+  const int k = i - W.friction_begin, c0 = normal ? i - W.normal_begin : (k >> 1);
+  const CView<R> c = contact_view(T, W, c0);
+  const R sc = normal ? c.dc : c.act;
+  if (sc == R(0)) return;
+  const V3<R> dir = normal ? c.n : ((k & 1) ? c.d2 : c.d1);
+  const V3<R> fv = (sc * d) * dir;
+  if (c.al >= 0) {
+    f(c.al, fv);
+    if (c.aa >= 0) f(c.aa, cross(c.ra, fv));
+  }
+  if (c.bl >= 0) {
+    f(c.bl, -fv);
+    if (c.bA >= 0) f(c.bA, -cross(c.rb, fv));
+  }
+}
+
 // ------------------------------------------------------------------ static row blocks (once per step)
 template <class R, bool kTets, class Team> __device__ void setup_row_blocks(Team& t, const Topo<R>& T, Work<R>& W) {
   const int ng = T.nj + (kTets ? T.nt : 0);
@@ -1217,7 +1246,7 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
     for (int i = t.rank(); i < nr; i += t.size()) {
       const R b = row_J(T, W, i, W.w) - W.hv[i];
       R inv = R(1);
-      if (cfg.preconditioner == 1 || cfg.linear_method == 0) {  // Jacobi always uses the diagonal (solvers.cpp:35)
+      if (cfg.preconditioner == 1 || cfg.linear_method == 0 || cfg.linear_method == 1) {  // Jacobi / GS use the diagonal
         const R sd = row_quad(T, W, i) + row_Cdiag<R, kTets>(T, W, i) + eps;
         inv = sd > R(0) ? R(1) / sd : R(1);
       }
@@ -1242,7 +1271,60 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
       // kTets == false (diagonal C): the accepted update x+=a p, r-=a ap, z-=a M^-1 ap
       // is committed in place during the next row pass (the operator reads the
       // pending z' on the fly), so no trial buffers xn/rn/zn are needed.
-      if (cfg.linear_method == 0 || cfg.linear_method == 2) {
+      if (cfg.linear_method == 1) {
+        // Gauss-Seidel (solvers.cpp:52-81): forward sweeps in ascending row order, one
+        // thread, on the matrix-free operator. (S x)_row = J_row w + (C x)_row + eps x_row
+        // with w = H^-1 J^T x kept current: each row's change d adds H^-1 J_row^T d to the
+        // <= 4 dof3 blocks the row touches. x0 = 0, so w starts at 0. The diagonal
+        // S_rr = J_row H^-1 J_row^T + C_rr + eps is the preconditioner's (1 / inv).
+        // After each sweep r = b - S x is re-evaluated in parallel for the history.
+        R *x = W.x, *bb = W.zn;
+        for (int i = t.rank(); i < nr; i += t.size()) {
+          bb[i] = W.r[i];
+          x[i] = R(0);
+        }
+        for (int b = t.rank(); b < T.nd3; b += t.size()) st3(W.w + 3 * b, v3(R(0), R(0), R(0)));
+        t.sync();
+        for (int itl = 0; itl < maxlin && hist_last > cfg.linear_tolerance; ++itl) {
+          if (t.rank() == 0) {
+            for (int i = 0; i < nr; ++i) {
+              const R diag = row_quad(T, W, i) + row_Cdiag<R, kTets>(T, W, i) + eps;  // S_ii
+              if (!(fabs((double)diag) > 1e-300)) continue;  // solvers.cpp:73
+              const R sx = row_J(T, W, i, W.w) + row_C<R, kTets>(T, W, i, x) + eps * x[i];
+              const R xn = (bb[i] - (sx - diag * x[i])) / diag;
+              const R d = xn - x[i];
+              x[i] = xn;
+              row_JT(T, W, i, d, [&](int b, V3<R> v) {
+                const V3<R> hv = hinv_apply(T, W, b, v);
+                R* wb = W.w + 3 * b;
+                wb[0] += hv.x;
+                wb[1] += hv.y;
+                wb[2] += hv.z;
+              });
+            }
+          }
+          t.sync();
+          op_pull(t, T, W, RowArr<R>{x});  // w = H^-1 J^T x afresh for the residual
+          t.sync();
+          double rr2 = 0.0;
+          for (int i = t.rank(); i < nr; i += t.size()) {
+            const R ri = bb[i] - (row_J(T, W, i, W.w) + row_C<R, kTets>(T, W, i, x) + eps * x[i]);
+            W.r[i] = ri;
+            rr2 += (double)ri * ri;
+          }
+          double s[1] = {rr2};
+          t.reduce_sum(s);
+          hist_last = sqrt(s[0]);
+          if (t.rank() == 0 && out.hist && hist_n <= maxlin) out.hist[(size_t)it * (maxlin + 1) + hist_n] = hist_last;
+          ++hist_n;
+          lin_used = itl + 1;
+          if (hist_last < best_res) {
+            best_res = hist_last;
+            for (int i = t.rank(); i < nr; i += t.size()) W.bx[i] = x[i];
+          }
+          t.sync();
+        }
+      } else if (cfg.linear_method == 0 || cfg.linear_method == 2) {
         // Jacobi (solvers.cpp:32-50) and PCG (solvers.cpp:83-121) on the same
         // matrix-free operator S v = J H^-1 J^T v + C v + eps v, x0 = 0, best iterate
         // by residual 2-norm, breakdown tests at 1e-300 in double.

@@ -229,10 +229,12 @@ def test_nan_input_rolls_back_and_reports_abort():
 
 
 @pytest.mark.parametrize("name,seed,warm", [("c1", 0, 10), ("c3:20", 0, 3), ("c5", 3, 12), ("box_pile", 1, 20)])
-@pytest.mark.parametrize("method,precond", [(0, 1), (2, 1), (2, 0)])
-def test_linear_methods_jacobi_pcg_fp64(name, seed, warm, method, precond):
-    """Jacobi (solvers.cpp:32-50) and PCG (solvers.cpp:83-121) on
-    the same matrix-free Schur operator, against the oracle's explicit-S solvers."""
+@pytest.mark.parametrize("method,precond", [(0, 1), (1, 1), (2, 1), (2, 0)])
+def test_linear_methods_jacobi_gs_pcg_fp64(name, seed, warm, method, precond):
+    """Jacobi (solvers.cpp:32-50), Gauss-Seidel (solvers.cpp:52-81,
+    ascending-row sweeps with w = H^-1 J^T x updated row by row) and PCG
+    (solvers.cpp:83-121) on the same matrix-free Schur operator, against the
+    oracle's explicit-S solvers."""
     case = oracle_case(name, seed, warm, overrides=dict(linear_method=method, preconditioner=precond))
     g = run_gpu(case, "fp64")
     o = run_oracle(case)
@@ -241,12 +243,27 @@ def test_linear_methods_jacobi_pcg_fp64(name, seed, warm, method, precond):
     assert rel_err(g["u"], o["u"], floor=1e-6) < 1e-6
 
 
-def test_gauss_seidel_unsupported_on_device():
-    from paper_1907_04587_b200 import NsdError
+def test_gauss_seidel_histories_and_counts_fp64():
+    """Gauss-Seidel's residual history (b - S x after every sweep) and iteration counts
+    against the oracle, and the FEM path (tet C blocks inside the sweep)."""
+    for name, seed, warm in (("c1", 0, 10), ("c2:4", 0, 1)):
+        case = oracle_case(name, seed, warm, overrides=dict(linear_method=1))
+        g = run_gpu(case, "fp64")
+        o = run_oracle(case)
+        assert np.array_equal(g["stats"][:, 5], o["stats"][:, 5]), name
+        n = int(g["hist_len"][0])
+        assert rel_err(g["hist"][0, :n], o["hist"][0, :n], floor=1e-12) < 1e-6, name
+        assert rel_err(g["q"], o["q"]) < 1e-8, name
 
-    case = oracle_case("c1", 0, 0, overrides=dict(linear_method=1))
+
+def test_batch_rejects_non_pcr():
+    from paper_1907_04587_b200 import BatchSolver, NsdError, Scene
+
+    s0 = Scene("c5", 0)
+    cfg = s0.config
+    cfg.linear_method = 1
     with pytest.raises(NsdError) as e:
-        run_gpu(case, "fp64")
+        BatchSolver(s0.topology, s0.shapes, s0.n_shapes, s0.margin, s0.mu_default, cfg, 4, 48)
     assert e.value.code == 4
 
 
