@@ -9,6 +9,8 @@
 
 #include "nsd_plan.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -24,6 +26,28 @@ namespace {
 using namespace nsdi;
 
 thread_local std::string g_err;
+
+// NVTX range (nsys / ncu --nvtx): the host phases of a step around its launches. The
+// Newton phases run inside one persistent launch; their device time comes from the
+// in-kernel clock64 counters (NSD_PHASE_TIMING, nsd_batch_profile).
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
+// Consecutive sub-ranges of one scope (each start() closes the previous one).
+struct NvtxPhase {
+  bool open = false;
+  void start(const char* name) {
+    if (open) nvtxRangePop();
+    nvtxRangePushA(name);
+    open = true;
+  }
+  ~NvtxPhase() {
+    if (open) nvtxRangePop();
+  }
+};
 
 struct NsdError : std::runtime_error {
   int code;
@@ -424,6 +448,9 @@ template <class R> struct Solver final : SolverBase {
     ensure(nc);
     const int N = cfg.newton_iterations, ml = cfg.linear_max_iterations;
     const int nrows = H.rows_static + 3 * nc;
+    Nvtx range_step("nsd_step");
+    NvtxPhase phase;
+    phase.start("nsd_step: stage inputs (one H2D)");
     // ---- stage inputs in ONE pinned buffer and ONE H2D copy: q-, u-, f_extra, contact
     // geometry, joint frames (R part); contact bodies and the contact incidence (int
     // part). The kernel reads them in place (Work's const input pointers).
@@ -523,6 +550,7 @@ template <class R> struct Solver final : SolverBase {
     W.normal_begin = H.rows_static;
     W.friction_begin = H.rows_static + nc;
     nsd::Cfg kc = to_cfg(cfg);
+    phase.start(use_grid ? "nsd_step: newton_step (persistent cooperative grid)" : "nsd_step: newton_step (one CTA)");
     NSD_CK(cudaEventRecord(ev0, stream));
     if (!use_grid) {
       NSD_CK(launch_single_block<R>(tets, block_threads, stream, topo.t, W, kc, so));
@@ -535,6 +563,7 @@ template <class R> struct Solver final : SolverBase {
       NSD_CK(launch_single_grid<R>(tets, regs, grid_blocks, stream, topo.t, W, kc, so, gp));
     }
     NSD_CK(cudaEventRecord(ev1, stream));
+    phase.start("nsd_step: download (one D2H) + unpack");
     // ---- download: one D2H of the output buffer (reports, q, u, lambda)
     stage_o.alloc(L.bytes);
     char* ho = static_cast<char*>(stage_o.p);
@@ -1017,12 +1046,21 @@ template <class R> struct Batch final : BatchBase {
       A1.row_pool = 0;
       A1.ptime = nullptr;
       if (ev) NSD_CK(cudaEventRecord(ev[0], stream));
-      NSD_CK(launch_batch_collide<R>((n_env + 3) / 4, 128, collide_smem, stream, A1));
+      {
+        Nvtx r("nsd_batch_step: narrow phase + setup (k_batch_collide)");
+        NSD_CK(launch_batch_collide<R>((n_env + 3) / 4, 128, collide_smem, stream, A1));
+      }
       if (ev) NSD_CK(cudaEventRecord(ev[1], stream));
-      NSD_CK(launch_batch_warp<R>(mixed, (n_env + warp_epb - 1) / warp_epb, 32 * warp_epb, warp_smem, stream, A));
+      {
+        Nvtx r("nsd_batch_step: newton_step, warp per env (k_batch_warp)");
+        NSD_CK(launch_batch_warp<R>(mixed, (n_env + warp_epb - 1) / warp_epb, 32 * warp_epb, warp_smem, stream, A));
+      }
       if (ev) NSD_CK(cudaEventRecord(ev[2], stream));
       A.mode = 2;
-      NSD_CK(launch_batch_sub<R>(16, nblk, 16 * epb, smem_bytes, stream, A));
+      {
+        Nvtx r("nsd_batch_step: newton_step, large envs (k_batch_sub mode 2)");
+        NSD_CK(launch_batch_sub<R>(16, nblk, 16 * epb, smem_bytes, stream, A));
+      }
       if (ev) NSD_CK(cudaEventRecord(ev[3], stream));
       return;
     }

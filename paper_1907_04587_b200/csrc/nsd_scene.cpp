@@ -8,6 +8,8 @@
 #include "nsd_collide.cuh"
 #include "nsd_math.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -809,6 +811,10 @@ static int scene_detect(const nsd_scene* s, const double* q, const double* u, co
 int nsd_scene_detect(const nsd_scene* s, const double* q, const double* u, const double* f_extra, int32_t capacity,
                      nsd_contact* out, int32_t* n) {
   if (!s || !q || !u || !n || capacity < 0 || (capacity > 0 && !out)) return NSD_INVALID;
+  nvtxRangePushA("nsd_scene_detect (host narrow phase)");
+  struct Pop {
+    ~Pop() { nvtxRangePop(); }
+  } pop;
   try {
     return scene_detect(s, q, u, f_extra, capacity, out, n);
   } catch (const std::exception&) {  // allocation or thread failure: an error code, never std::terminate
