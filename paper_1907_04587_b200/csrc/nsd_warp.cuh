@@ -630,7 +630,7 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
   }
   const R tfrac = R(cfg.step_fraction);
   const int maxlin = cfg.linear_max_iterations;
-  R s[3], cd[kRows], lam[kRows];
+  R s[3], cd[kRows];
   long long cr_cyc = 0;
   unsigned cr_it = 0;
   int n_done = 0, aborted = 0;
@@ -640,11 +640,14 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
     R hv[kRows];
     AsmStats as{0.0, 0.0, 0.0, 0.0};
     pc.mark(0);
-    rows_load(io.lam, lane, lam);
-    assemble_obj(E, o, lane, jframe, T.jparam, io.cgeo, h, cfg, lam, s, hv, cd, as);
-    pc.mark(1);
-    // ---- g = M~(u - u~) - J^T lambda; H^-1 = M~^-1 (no shift on rigid dofs); w = H^-1 g
-    stage(E, o, lane, s, lam);
+    {  // lambda is re-read for the update: not kept in registers across the PCR loop
+      R lam[kRows];
+      rows_load(io.lam, lane, lam);
+      assemble_obj(E, o, lane, jframe, T.jparam, io.cgeo, h, cfg, lam, s, hv, cd, as);
+      pc.mark(1);
+      // ---- g = M~(u - u~) - J^T lambda; H^-1 = M~^-1 (no shift on rigid dofs); w = H^-1 g
+      stage(E, o, lane, s, lam);
+    }
     __syncwarp();
     double gmax = 0.0, gsq = 0.0;
     if (lane < nb) {
@@ -852,7 +855,7 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
     }
     // ---- damped update + integration (newton.cpp:393-396; bodies.cpp:58-86)
 #pragma unroll
-    for (int i = 0; i < kRows; ++i) io.lam[32 * i + lane] = lam[i] + tfrac * bx[i];
+    for (int i = 0; i < kRows; ++i) io.lam[32 * i + lane] = io.lam[32 * i + lane] + tfrac * bx[i];
     if (lane < nb) {
       const int b = lane, d = T.bdof[b], cdd = T.bcoord[b];
       R* u = E.bu + 6 * b;
@@ -901,7 +904,7 @@ __device__ void solve_env(const Topo<R>& T, const Cfg& cfg, const R* jframe, R h
     }
   } else {
     // ---- final assembly for classification and telemetry (newton.cpp:409-416)
-    R hv[kRows];
+    R hv[kRows], lam[kRows];
     AsmStats fs{0.0, 0.0, 0.0, 0.0};
     rows_load(io.lam, lane, lam);
     assemble_obj(E, o, lane, jframe, T.jparam, io.cgeo, h, cfg, lam, s, hv, cd, fs);
