@@ -232,51 +232,61 @@ __device__ __forceinline__ void gather(const Env<R, S>& E, int b, V3<T>& lin, V3
 // One component k of body b's gathered J^T y: the body's staged wrenches summed in
 // entry order (the order of gather()); the offsets and values of four entries are
 // loaded before their ordered adds.
-template <class R, class S> __device__ __forceinline__ S gather_comp(const Env<R, S>& E, int b, int k) {
+// Components k and k + 3 (linear, angular) of body b's gathered J^T y: the body's
+// staged wrenches summed in entry order (the order of gather()); up to 8 entries'
+// offsets and values are loaded before the ordered adds.
+template <class R, class S>
+__device__ __forceinline__ void gather_pair(const Env<R, S>& E, int b, int k, S& lin, S& ang) {
   const int e0 = E.gent_off[b], n = E.gent_off[b + 1] - e0;
   const int* ge = E.gent + e0;
   const S* sk = static_cast<const S*>(E.stg) + k;
-  S acc = S(0);
-  int e = 0;
-  for (; e + 4 <= n; e += 4) {
-    const int o0 = ge[e], o1 = ge[e + 1], o2 = ge[e + 2], o3 = ge[e + 3];
-    const S v0 = sk[o0], v1 = sk[o1], v2 = sk[o2], v3 = sk[o3];
-    acc = acc + v0;
-    acc = acc + v1;
-    acc = acc + v2;
-    acc = acc + v3;
+  constexpr int kU = 8;
+  int off[kU];
+  S vl[kU], va[kU];
+#pragma unroll
+  for (int e = 0; e < kU; ++e) off[e] = e < n ? ge[e] : 0;
+#pragma unroll
+  for (int e = 0; e < kU; ++e) {
+    vl[e] = e < n ? sk[off[e]] : S(0);
+    va[e] = e < n ? sk[off[e] + 3] : S(0);
   }
-  for (; e < n; ++e) acc = acc + sk[ge[e]];
-  return acc;
+  lin = S(0);
+  ang = S(0);
+#pragma unroll
+  for (int e = 0; e < kU; ++e)
+    if (e < n) {
+      lin = lin + vl[e];
+      ang = ang + va[e];
+    }
+  for (int e = kU; e < n; ++e) {
+    lin = lin + sk[ge[e]];
+    ang = ang + sk[ge[e] + 3];
+  }
 }
 
-// w = H^-1 J^T y for every body with the whole warp: 5 bodies per round, lane
-// 6 g + k owns component k of body 5 r + g. Linear rows scale by 1/m; angular row
-// k - 3 applies I_w^-1 (sym_mul's expression) to the torque held by the group's
-// lanes 3..5, exchanged by shuffles. Needs __syncwarp() before (staging) and after.
+// w = H^-1 J^T y for every body with the whole warp: 10 bodies per round (one round
+// for an ant), lane 3 g + k owns components k (linear) and k + 3 (angular) of body
+// 10 r + g. The linear part scales by 1/m; the angular row k applies I_w^-1
+// (sym_mul's expression) to the torque held by the group's three lanes, exchanged by
+// shuffles. Needs __syncwarp() before (staging) and after.
 template <class R, class S> __device__ __forceinline__ void bodies_w(const Env<R, S>& E, int lane) {
-  const int g = lane / 6, k = lane - 6 * g;
-  const int g3 = 6 * g + 3;
-  for (int b0 = 0; b0 < E.nb; b0 += 5) {
+  const int g = lane / 3, k = lane - 3 * g;
+  const int g0 = 3 * g;
+  for (int b0 = 0; b0 < E.nb; b0 += 10) {
     const int b = b0 + g;
-    const bool on = g < 5 && b < E.nb;
-    const S t = on ? gather_comp(E, b, k) : S(0);
-    const S tx = __shfl_sync(0xffffffffu, t, g3 < 32 ? g3 : 0);
-    const S ty = __shfl_sync(0xffffffffu, t, g3 + 1 < 32 ? g3 + 1 : 0);
-    const S tz = __shfl_sync(0xffffffffu, t, g3 + 2 < 32 ? g3 + 2 : 0);
+    const bool on = g < 10 && b < E.nb;
+    S tl = S(0), ta = S(0);
+    if (on) gather_pair(E, b, k, tl, ta);
+    const S tx = __shfl_sync(0xffffffffu, ta, g0 < 32 ? g0 : 0);
+    const S ty = __shfl_sync(0xffffffffu, ta, g0 + 1 < 32 ? g0 + 1 : 0);
+    const S tz = __shfl_sync(0xffffffffu, ta, g0 + 2 < 32 ? g0 + 2 : 0);
     if (on) {
-      S w;
-      if (k < 3) {
-        w = t * S(E.bhi[b]);
-      } else {
-        const R* s6 = E.biwi + 6 * b;  // xx yy zz xy xz yz; row k - 3 of sym_mul
-        const int r = k - 3;
-        const S c0 = S(r == 0 ? s6[0] : (r == 1 ? s6[3] : s6[4]));
-        const S c1 = S(r == 0 ? s6[3] : (r == 1 ? s6[1] : s6[5]));
-        const S c2 = S(r == 0 ? s6[4] : (r == 1 ? s6[5] : s6[2]));
-        w = c0 * tx + c1 * ty + c2 * tz;
-      }
-      E.bw[6 * b + k] = w;
+      const R* s6 = E.biwi + 6 * b;  // xx yy zz xy xz yz; row k of sym_mul
+      const S c0 = S(k == 0 ? s6[0] : (k == 1 ? s6[3] : s6[4]));
+      const S c1 = S(k == 0 ? s6[3] : (k == 1 ? s6[1] : s6[5]));
+      const S c2 = S(k == 0 ? s6[4] : (k == 1 ? s6[5] : s6[2]));
+      E.bw[6 * b + k] = tl * S(E.bhi[b]);
+      E.bw[6 * b + 3 + k] = c0 * tx + c1 * ty + c2 * tz;
     }
   }
 }
