@@ -170,23 +170,22 @@ template <class S, class R> __device__ __forceinline__ S sym_quad_t(const R* s6,
 
 template <class S, class R>
 __device__ __forceinline__ S point_quad(const Topo<R>& T, const R* biwi, int a, int b, V3<S> d, V3<S> arm_a, V3<S> arm_b,
-                                        bool shifted) {
+                                        bool shifted, const R* bhi = nullptr) {
+  // shifted: H^-1 = 1 / (m + 0) per linear dof, the value batch setup stores in bhi
   S s = S(0);
   if (a >= 0) {
     const S m = S(T.bmass[a]);
-    s += shifted ? lin_quad_shifted(d, S(1) / (m + S(0))) : lin_quad_unshifted(d, m);
+    s += shifted ? lin_quad_shifted(d, bhi ? S(bhi[a]) : S(1) / (m + S(0))) : lin_quad_unshifted(d, m);
     s += sym_quad_t(biwi + 6 * a, cross(arm_a, d));
   }
   if (b >= 0) {
     const S m = S(T.bmass[b]);
-    s += shifted ? lin_quad_shifted(d, S(1) / (m + S(0))) : lin_quad_unshifted(d, m);
+    s += shifted ? lin_quad_shifted(d, bhi ? S(bhi[b]) : S(1) / (m + S(0))) : lin_quad_unshifted(d, m);
     s += sym_quad_t(biwi + 6 * b, cross(arm_b, d));
   }
   return s;
 }
 
-// J^T y of this lane's object into its staging slot: a side (f, r_a x f + tau),
-// b side (-f, -(r_b x f + tau)); f = sum_i (s_i y_i) D_i, tau = sum_i y_i C_i.
 // T: the precision of the staged values (S for the operator, R for the momentum
 // and Newton-update gathers); the records are read in S and widened.
 template <class T, class R, class S, class YF>
@@ -222,16 +221,25 @@ template <class T, class R, class S>
 __device__ __forceinline__ void gather(const Env<R, S>& E, int b, V3<T>& lin, V3<T>& ang) {
   lin = v3(T(0), T(0), T(0));
   ang = lin;
-  for (int e = E.gent_off[b]; e < E.gent_off[b + 1]; ++e) {
-    const T* s = static_cast<const T*>(E.stg) + E.gent[e];
-    lin = lin + lds3(s);
-    ang = ang + lds3(s + 3);
+  const int e0 = E.gent_off[b], n = E.gent_off[b + 1] - e0;
+  const int* ge = E.gent + e0;
+  const T* st = static_cast<const T*>(E.stg);
+  constexpr int kU = 8;  // up to 8 entries' offsets loaded before their ordered adds
+  int off[kU];
+#pragma unroll
+  for (int e = 0; e < kU; ++e) off[e] = e < n ? ge[e] : 0;
+#pragma unroll
+  for (int e = 0; e < kU; ++e)
+    if (e < n) {
+      lin = lin + lds3(st + off[e]);
+      ang = ang + lds3(st + off[e] + 3);
+    }
+  for (int e = kU; e < n; ++e) {
+    lin = lin + lds3(st + ge[e]);
+    ang = ang + lds3(st + ge[e] + 3);
   }
 }
 
-// One component k of body b's gathered J^T y: the body's staged wrenches summed in
-// entry order (the order of gather()); the offsets and values of four entries are
-// loaded before their ordered adds.
 // Components k and k + 3 (linear, angular) of body b's gathered J^T y: the body's
 // staged wrenches summed in entry order (the order of gather()); up to 8 entries'
 // offsets and values are loaded before the ordered adds.
@@ -328,7 +336,7 @@ __device__ __forceinline__ void quads(const Env<R, S>& E, const Obj& o, int lane
   for (int i = 0; i < kRows; ++i) {
     q[i] = S(0);
     if (i < o.np) {
-      if (s[i] != S(0)) q[i] = point_quad(E.T, E.biwi, o.a, o.b, s[i] * rc.d[i], rc.arm_a, rc.arm_b, true);
+      if (s[i] != S(0)) q[i] = point_quad(E.T, E.biwi, o.a, o.b, s[i] * rc.d[i], rc.arm_a, rc.arm_b, true, E.bhi);
     } else if (i < o.nr) {
       S t = S(0);
       if (o.a >= 0) t += sym_quad_t(E.biwi + 6 * o.a, rc.d[i]);
