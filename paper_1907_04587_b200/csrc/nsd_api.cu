@@ -649,7 +649,7 @@ template <class R> struct Batch final : BatchBase {
   int n_env, maxc, ns, npairs;
   WorkPlan plan;
   DBuf hotg, coldr, coldi, shapes, pairs, cand, paircnt, ncout, ovf, fin, iters, qs, us, torque, jbinc, jblk;
-  DBuf abany, ctr, wjinc, wlam, wptime;  // sticky abort flags; counters; k_batch_warp's joint incidence (both sides)
+  DBuf abany, ctr, wjinc, wlam, wptime, porder;  // sticky abort flags; counters; k_batch_warp's joint incidence (both sides)
   bool warp_path = false;  // k_batch_warp for rigid scenes (narrow-phase launch + warp solver + large-env launch)
   nsd::wp::Plan wplan{};
   int warp_epb = 2;        // environments (warps) per block of k_batch_warp (64 threads, 7 blocks/SM)
@@ -702,6 +702,18 @@ template <class R> struct Batch final : BatchBase {
     for (int i = 0; i < ns; ++i)
       for (int j = i + 1; j < ns; ++j) hp.push_back(make_int2(i, j));
     npairs = static_cast<int>(hp.size());
+    {  // the warp narrow phase runs the pairs grouped by kind pair, most expensive first
+      std::vector<int> order(npairs);
+      for (int k = 0; k < npairs; ++k) order[k] = k;
+      auto cls = [&](int k) {
+        const int a = sh[hp[k].x].kind, b = sh[hp[k].y].kind;
+        const int lo = std::min(a, b), hi = std::max(a, b);  // 0 half-space, 1 sphere, 2 box
+        return lo == 2 ? 0 : (hi == 2 && lo == 1 ? 1 : (hi == 2 ? 2 : (lo == 1 ? 3 : 4)));
+      };
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cls(x) < cls(y); });
+      porder.alloc(sizeof(int) * std::max(npairs, 1));
+      if (npairs) NSD_CK(cudaMemcpy(porder.p, order.data(), sizeof(int) * npairs, cudaMemcpyHostToDevice));
+    }
     shapes.alloc(sizeof(nsd::ShapeD<R>) * std::max(ns, 1));
     pairs.alloc(sizeof(int2) * std::max(npairs, 1));
     if (ns) NSD_CK(cudaMemcpy(shapes.p, hshapes.data(), sizeof(nsd::ShapeD<R>) * ns, cudaMemcpyHostToDevice));
@@ -971,6 +983,7 @@ template <class R> struct Batch final : BatchBase {
     A.row_pool = row_pool;
     A.ptime = ptime.as<unsigned long long>();
     A.pairs = pairs.as<int2>();
+    A.pair_order = porder.as<int>();
     A.shapes = shapes.as<nsd::ShapeD<R>>();
     A.jframe = topo.jframe;
     A.margin = R(margin);

@@ -206,8 +206,18 @@ template <class R>
 NSD_HD int box_box(const BodyView<R>& v, const ShapeD<R>& sa, const ShapeD<R>& sb, R margin, CandD<R>* out) {
   // (the two boxes' frames are selected by value, never through a runtime index,
   // so they stay in registers)
-  const M3<R> rot0 = shape_rot(v, sa), rot1 = shape_rot(v, sb);
   const V3<R> pos0 = shape_pos(v, sa), pos1 = shape_pos(v, sb);
+  {  // Exact early-out (results unchanged): the face axis of box a nearest the centre
+     // line makes an angle with it of cos >= 1/sqrt(3), so its separation is at least
+     // |dc|/sqrt(3) - r_a - r_b (circumradii); beyond sqrt(3)(r_a + r_b + margin) every
+     // face-axis separation, hence best_sep below, exceeds the margin -> no candidates.
+    const V3<R> dc = pos1 - pos0;
+    const R ra = sqrt(sa.he[0] * sa.he[0] + sa.he[1] * sa.he[1] + sa.he[2] * sa.he[2]);
+    const R rb = sqrt(sb.he[0] * sb.he[0] + sb.he[1] * sb.he[1] + sb.he[2] * sb.he[2]);
+    const R lim = ra + rb + margin;
+    if (dot(dc, dc) > R(3.0001) * lim * lim) return 0;
+  }
+  const M3<R> rot0 = shape_rot(v, sa), rot1 = shape_rot(v, sb);
   int best_ref = -1, best_axis = -1;
   R best_dir = R(1), best_sep = -Lim<R>::inf();
 #pragma unroll

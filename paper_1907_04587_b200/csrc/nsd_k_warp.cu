@@ -174,9 +174,11 @@ template <class R> __global__ void __launch_bounds__(128, NSD_COLLIDE_MINB) k_ba
   nsd::CandD<R>* gc = A.cand + (size_t)env * A.npairs * 4;
   int total = 0;
   for (int p0 = 0; p0 < A.npairs; p0 += 32) {
-    const int p = p0 + lane;
+    // pairs run grouped by shape kinds (less divergence in a round); slots and the
+    // tie-break use each pair's original index p, so the order does not matter
+    const int p = p0 + lane < A.npairs ? A.pair_order[p0 + lane] : 0;
     int n = 0;
-    if (p < A.npairs) {
+    if (p0 + lane < A.npairs) {
       const int2 ij = A.pairs[p];
       R th, mu;
       n = nsd::pair_contacts(view, A.shapes[ij.x], A.shapes[ij.y], A.h, A.margin, A.mu_default, gc + 4 * p, &th, &mu);
@@ -205,7 +207,7 @@ template <class R> __global__ void __launch_bounds__(128, NSD_COLLIDE_MINB) k_ba
     int rank = 0;
     for (int j = 0; j < stored; ++j) {
       const int4 o = key[j];
-      if (nsd::canonical_less(o.x, o.y, o.z, c.x, c.y, c.z) || (o.x == c.x && o.y == c.y && o.z == c.z && j < i))
+      if (nsd::canonical_less(o.x, o.y, o.z, c.x, c.y, c.z) || (o.x == c.x && o.y == c.y && o.z == c.z && o.w < c.w))
         ++rank;
     }
     if (rank >= nc) continue;

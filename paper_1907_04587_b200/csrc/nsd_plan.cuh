@@ -180,6 +180,7 @@ template <class R> struct BatchArgs {
   int n_env, ns, npairs, maxc, envs_per_block, hot_in_smem;
   int row_pool;  // per-env shared-memory region (elements of R) for the PCR row state; 0 = off
   const int2* pairs;
+  const int* pair_order;  // k_batch_collide's processing order of the pairs (grouped by shape kinds)
   const nsd::ShapeD<R>* shapes;
   const R* jframe;
   R margin, mu_default, h, grav[3];
