@@ -3,8 +3,16 @@
 key raw metrics (duration, DRAM bytes, L1/L2 traffic, occupancy, issue, stall
 reasons) and the source-line hotspots (warp-stall samples, instructions).
 
-    python profiles/summarize_ncu.py <report.ncu-rep> <out_prefix>
+    python profiles/summarize_ncu.py <report.ncu-rep> <out_prefix> [--traffic KEY TU.cu]
+
+--traffic also records the capture's dram__bytes_read.sum + dram__bytes_write.sum as
+profiles/dram_traffic.json[KEY], with the sha256 of the TU and every header it
+includes: bench.py reports it as roofline.traffic only while those sources are
+unchanged (a stale capture reads as null).
 """
+import hashlib
+import os
+import re
 import collections
 import csv
 import io
@@ -90,6 +98,38 @@ def main():
                 for r in rows[:60]:
                     f.write(" | ".join(c.strip()[:90] for c in r) + "\n")
     print(json.dumps({"duration_ms": dur_ns / 1e6, "dram_traffic_bytes": traffic_mb * 1e6}))
+    if "--traffic" in sys.argv:
+        i = sys.argv.index("--traffic")
+        record_traffic(sys.argv[i + 1], sys.argv[i + 2], int(round(traffic_mb * 1e6)), rep)
+
+
+def tu_sources(tu):
+    """The TU and its transitive quoted includes, in first-visit order, repo-relative."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    seen, todo = [], [os.path.relpath(os.path.abspath(tu), root)]
+    while todo:
+        f = todo.pop(0)
+        if f in seen:
+            continue
+        seen.append(f)
+        for inc in re.findall(r'#include "([^"]+)"', open(os.path.join(root, f)).read()):
+            todo.append(os.path.join(os.path.dirname(f), inc))
+    return root, seen
+
+
+def record_traffic(key, tu, nbytes, rep):
+    root, srcs = tu_sources(tu)
+    h = hashlib.sha256()
+    for f in srcs:
+        h.update(open(os.path.join(root, f), "rb").read())
+    path = os.path.join(root, "profiles", "dram_traffic.json")
+    try:
+        d = json.load(open(path))
+    except Exception:
+        d = {}
+    d[key] = {"bytes": nbytes, "sources": srcs, "sha256": h.hexdigest(),
+              "capture": os.path.basename(rep) + " (ncu --set full, cache control all: cold L2)"}
+    json.dump(d, open(path, "w"), indent=1)
 
 
 if __name__ == "__main__":
