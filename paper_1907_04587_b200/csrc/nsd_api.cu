@@ -394,6 +394,12 @@ template <class R> struct Solver final : SolverBase {
   bool use_grid = false;
   bool tets = false;
   int block_threads = 256;
+  // partitioned grid PCR (nsd_part.cuh): static objects (joints, tets) split over the
+  // CTAs once, contacts added per step (PartPlanH)
+  std::vector<int> ps_row_begin;         // CTA p owns static rows [ps_row_begin[p], ps_row_begin[p + 1])
+  std::vector<std::vector<int>> ps_blk;  // per CTA: its static rows' dof3 blocks, ascending
+  std::vector<int> first_cta;            // per dof3 block: the lowest CTA whose static rows touch it, or -1
+  DBuf partbuf;                          // shared-block partials, 3 per flat local block
 
   Solver(const nsd_topology& tp, const nsd_config& c, int device) : cfg(c) {
     NSD_CK(cudaSetDevice(device));
@@ -418,7 +424,43 @@ template <class R> struct Solver final : SolverBase {
       grid_blocks = dev_sms * std::min(per_sm, bps ? std::max(1, std::atoi(bps)) : 1);
       // partials (+ 2 x kRedMax spare slots) and the arrival count of the grid barrier (nsd_team.cuh)
       gpart.alloc(sizeof(double) * (2 * grid_blocks * nsd::kRedMax + 2 * nsd::kRedMax + 2));
+      part_static();
+      int optin = 0;
+      NSD_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+      part_smem_max = optin > 8192 ? (size_t)optin - 8192 : 0;  // the team's static reduction buffer stays below
     }
+  }
+  size_t part_smem_max = 0;
+  // partitioned grid PCR unless NSD_GRID_PART=0
+  static bool part_enabled() {
+    const char* e = std::getenv("NSD_GRID_PART");
+    return !(e && std::atoi(e) == 0);
+  }
+  // Static objects (joints, then tets; all rows of an object together) over the grid's
+  // CTAs in row order, balanced by rows; each CTA's blocks from the static incidence.
+  void part_static() {
+    const int P = grid_blocks;
+    std::vector<int> starts;  // object starts in row order
+    for (int j = 0; j < H.nj; ++j) starts.push_back(H.jrow[j]);
+    for (int e = 0; e < H.nt; ++e) starts.push_back(H.rows_joint + H.tdim * e);
+    starts.push_back(H.rows_static);
+    ps_row_begin.assign(P + 1, H.rows_static);
+    ps_row_begin[0] = 0;
+    for (int p = 1; p < P; ++p) {
+      const long target = (long)H.rows_static * p / P;
+      ps_row_begin[p] = *std::lower_bound(starts.begin(), starts.end(), (int)target);
+    }
+    std::vector<int> owner(H.rows_static);
+    for (int p = 0; p < P; ++p)
+      for (int i = ps_row_begin[p]; i < ps_row_begin[p + 1]; ++i) owner[i] = p;
+    ps_blk.assign(P, {});
+    first_cta.assign(H.nd3, -1);
+    for (int b = 0; b < H.nd3; ++b)
+      for (int e = H.sinc_off[b]; e < H.sinc_off[b + 1]; ++e) {
+        const int p = owner[H.sinc_ent[e] >> 2];
+        if (ps_blk[p].empty() || ps_blk[p].back() != b) ps_blk[p].push_back(b);
+        if (first_cta[b] < 0 || p < first_cta[b]) first_cta[b] = p;
+      }
   }
   ~Solver() override {
     if (ev0) cudaEventDestroy(ev0);
@@ -466,7 +508,84 @@ template <class R> struct Solver final : SolverBase {
         if (b4[s] >= 0) cnt[b4[s] + 1]++;
     }
     for (int b = 0; b < H.nd3; ++b) cnt[b + 1] += cnt[b];
-    const size_t nI = 2 * (size_t)nc + (H.nd3 + 1) + 4 * (size_t)nc;
+    // ---- partitioned grid PCR plan (nsd_part.cuh): the CTA of each contact is the
+    // lowest CTA whose static rows touch one of its blocks (else contact % P); its three
+    // rows follow the CTA's static rows; local blocks = static blocks + contact blocks;
+    // per dof3 block the flat local-block indices of all CTAs touching it, CTA order.
+    std::vector<int> p_row_off, p_rows, p_lb_off, p_lb_blk, p_gb_off, p_gb_ent;
+    int p_mr = 0, p_ml = 0, p_mx = 0;
+    size_t p_smem = 0;
+    bool use_part = false;
+    if (use_grid && cfg.linear_method == 3 && part_enabled()) {
+      const int P = grid_blocks;
+      std::vector<int> cstart(P + 1, 0), cown(nc), clist(nc);
+      for (int c = 0; c < nc; ++c) {
+        const int* b4 = &b4all[4 * c];
+        int o = -1;
+        for (int s : {0, 2, 1, 3})
+          if (b4[s] >= 0 && first_cta[b4[s]] >= 0) {
+            o = first_cta[b4[s]];
+            break;
+          }
+        cown[c] = o >= 0 ? o : c % P;
+        cstart[cown[c] + 1]++;
+      }
+      for (int p = 0; p < P; ++p) cstart[p + 1] += cstart[p];
+      {
+        std::vector<int> fp(cstart.begin(), cstart.end() - 1);
+        for (int c = 0; c < nc; ++c) clist[fp[cown[c]]++] = c;
+      }
+      p_row_off.assign(P + 1, 0);
+      p_rows.reserve(nrows);
+      p_lb_off.assign(P + 1, 0);
+      std::vector<int> extra, merged;
+      for (int p = 0; p < P; ++p) {
+        for (int i = ps_row_begin[p]; i < ps_row_begin[p + 1]; ++i) p_rows.push_back(i);
+        extra.clear();
+        for (int k = cstart[p]; k < cstart[p + 1]; ++k) {
+          const int c = clist[k];
+          p_rows.push_back(H.rows_static + c);
+          p_rows.push_back(H.rows_static + nc + 2 * c);
+          p_rows.push_back(H.rows_static + nc + 2 * c + 1);
+          for (int s = 0; s < 4; ++s)
+            if (b4all[4 * c + s] >= 0) extra.push_back(b4all[4 * c + s]);
+        }
+        p_row_off[p + 1] = (int)p_rows.size();
+        p_mr = std::max(p_mr, p_row_off[p + 1] - p_row_off[p]);
+        if (extra.empty()) {
+          p_lb_blk.insert(p_lb_blk.end(), ps_blk[p].begin(), ps_blk[p].end());
+        } else {
+          std::sort(extra.begin(), extra.end());
+          extra.erase(std::unique(extra.begin(), extra.end()), extra.end());
+          merged.clear();
+          std::set_union(ps_blk[p].begin(), ps_blk[p].end(), extra.begin(), extra.end(), std::back_inserter(merged));
+          p_lb_blk.insert(p_lb_blk.end(), merged.begin(), merged.end());
+        }
+        p_lb_off[p + 1] = (int)p_lb_blk.size();
+        p_ml = std::max(p_ml, p_lb_off[p + 1] - p_lb_off[p]);
+      }
+      const int nlb = (int)p_lb_blk.size();
+      p_gb_off.assign(H.nd3 + 1, 0);
+      for (int f = 0; f < nlb; ++f) p_gb_off[p_lb_blk[f] + 1]++;
+      for (int b = 0; b < H.nd3; ++b) p_gb_off[b + 1] += p_gb_off[b];
+      p_gb_ent.resize(std::max(nlb, 1));
+      {
+        std::vector<int> fp(p_gb_off.begin(), p_gb_off.end() - 1);
+        for (int f = 0; f < nlb; ++f) p_gb_ent[fp[p_lb_blk[f]]++] = f;  // f ascending = CTA order
+      }
+      for (int p = 0; p < P; ++p) {
+        int x = 0;
+        for (int f = p_lb_off[p]; f < p_lb_off[p + 1]; ++f) x += p_gb_off[p_lb_blk[f] + 1] - p_gb_off[p_lb_blk[f]];
+        p_mx = std::max(p_mx, x);
+      }
+      p_smem = nsd::part_smem<R>(std::max(p_mr, 1), std::max(p_ml, 1), std::max(p_mx, 1)).bytes;
+      use_part = (int)p_rows.size() == nrows && p_smem <= part_smem_max;
+      if (use_part) partbuf.alloc(sizeof(R) * 3 * (size_t)std::max(nlb, 1));
+    }
+    const size_t n_part = use_part ? p_row_off.size() + p_rows.size() + p_lb_off.size() + p_lb_blk.size() +
+                                         p_gb_off.size() + p_gb_ent.size()
+                                   : 0;
+    const size_t nI = 2 * (size_t)nc + (H.nd3 + 1) + 4 * (size_t)nc + n_part;
     Layout U;
     const size_t u_r = U.add<R>(nR), u_i = U.add<int>(nI);
     stage_in.alloc(U.bytes);
@@ -505,6 +624,14 @@ template <class R> struct Solver final : SolverBase {
           if (b >= 0) sent[fillp[b]++] = 4 * c + s;
         }
     }
+    {
+      int* pi = sent + 4 * (size_t)nc;
+      for (const std::vector<int>* v : {&p_row_off, &p_rows, &p_lb_off, &p_lb_blk, &p_gb_off, &p_gb_ent})
+        if (use_part) {
+          std::memcpy(pi, v->data(), v->size() * sizeof(int));
+          pi += v->size();
+        }
+    }
     R* hr = hotr.as<R>();
     int* hi = plan.hot_ints(hr);
     R* cr = coldr.as<R>();
@@ -540,6 +667,22 @@ template <class R> struct Solver final : SolverBase {
     W.cbody = di;
     W.cinc_off = di + 2 * nc;
     W.cinc_ent = di + 2 * nc + H.nd3 + 1;
+    W.part_row_off = W.part_rows = W.part_lb_off = W.part_lb_blk = W.part_gb_off = W.part_gb_ent = nullptr;
+    W.part_partial = nullptr;
+    W.part_mr = W.part_ml = W.part_mx = 0;
+    if (use_part) {
+      const int* pi = di + 2 * nc + (H.nd3 + 1) + 4 * (size_t)nc;
+      W.part_row_off = pi;
+      W.part_rows = (pi += p_row_off.size());
+      W.part_lb_off = (pi += p_rows.size());
+      W.part_lb_blk = (pi += p_lb_off.size());
+      W.part_gb_off = (pi += p_lb_blk.size());
+      W.part_gb_ent = (pi += p_gb_off.size());
+      W.part_partial = partbuf.p;
+      W.part_mr = std::max(p_mr, 1);
+      W.part_ml = std::max(p_ml, 1);
+      W.part_mx = std::max(p_mx, 1);
+    }
     W.q = reinterpret_cast<R*>(ob + o_q);
     W.u = reinterpret_cast<R*>(ob + o_u);
     W.lam = reinterpret_cast<R*>(ob + o_lam);
@@ -560,7 +703,8 @@ template <class R> struct Solver final : SolverBase {
       // register-resident PCR rows when every thread owns <= 2 rows (NSD_GRID_REGS=0 disables)
       const bool regs = cfg.linear_method == 3 && nrows <= 2 * grid_blocks * kGridThreads && !(std::getenv("NSD_GRID_REGS") &&
                                                                        std::atoi(std::getenv("NSD_GRID_REGS")) == 0);
-      NSD_CK(launch_single_grid<R>(tets, regs, grid_blocks, stream, topo.t, W, kc, so, gp));
+      NSD_CK(launch_single_grid<R>(tets, use_part ? -1 : (regs ? 2 : 0), p_smem, grid_blocks, stream, topo.t, W, kc,
+                                   so, gp));
     }
     NSD_CK(cudaEventRecord(ev1, stream));
     phase.start("nsd_step: download (one D2H) + unpack");

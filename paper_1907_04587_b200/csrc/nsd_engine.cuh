@@ -130,6 +130,11 @@ template <class R> struct Work {
   R* iwi6;  // inverse
   // per-iteration decision row (decision vectors, see StepOut::dec) or null
   unsigned char* dec;
+  // partitioned grid PCR (nsd_part.cuh): per-CTA rows and local dof3 blocks, the
+  // CTAs touching each dof3 block (flat local-block indices), shared-block partials
+  const int *part_row_off, *part_rows, *part_lb_off, *part_lb_blk, *part_gb_off, *part_gb_ent;
+  void* part_partial;
+  int part_mr, part_ml, part_mx;  // per-CTA maxima: rows, local blocks, exchange entries
 };
 
 // Decision-vector flags, one byte per contact / tet / dof per Newton
@@ -1065,6 +1070,10 @@ template <class R, bool kTets> __device__ __forceinline__ R row_Cdiag(const Topo
   return W.cd[i];
 }
 
+}  // namespace nsd
+#include "nsd_part.cuh"
+namespace nsd {
+
 // ------------------------------------------------------------------ Newton step
 // Step setup (newton.cpp:327-338): q = q-, M~ at q- (world inertia and its
 // inverse per rigid body), f_ext = gravity + gyroscopic (+ extension force),
@@ -1160,6 +1169,10 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
     t.sync();
   }
   const bool line_search = cfg.line_search && has_fric == 0.0;
+  // partitioned PCR (RPT < 0, grid kernel): per-step tables in dynamic shared memory
+  extern __shared__ __align__(16) char nsd_dyn_smem[];
+  PartView<R> PV(nsd_dyn_smem, W, RPT < 0);
+  if constexpr (RPT < 0) part_setup<R, kTets>(T, W, PV);
   double min_shift = 0.0;
   int n_done = 0;
   int aborted = 0;
@@ -1415,6 +1428,121 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
         }
         if (pending_best)
           for (int i = t.rank(); i < nr; i += t.size()) W.bx[i] = x[i];
+      } else if constexpr (RPT < 0) {
+        // Partitioned PCR (nsd_part.cuh): the same recurrence, exits and reductions as
+        // the register path below (den expanded from the previous J w pass's sums),
+        // with every CTA's rows, coefficients and local dof3 blocks in shared memory
+        // and only the shared blocks' J^T partials exchanged through global memory.
+        part_load<R, kTets>(T, W, PV);
+        const int td = kTets ? T.tdim : 0;
+        const int tid = threadIdx.x, ntd = blockDim.x;
+        R *xs = PV.x, *rs = PV.r, *zs = PV.z, *zns = PV.zn, *xns = PV.xn, *rns = PV.rn;
+        double zaz = 0.0, den_next = 0.0;
+        if (maxlin > 0 && hist_last > cfg.linear_tolerance) {
+          part_scatter(W, PV, zs);
+          t.sync();
+          part_gather(W, PV, tid, ntd);
+          __syncthreads();
+          double za = 0.0, aa = 0.0;
+          for (int li = tid; li < PV.nrow; li += ntd) {
+            const R a = part_row(PV, li, zs, td, eps);
+            PV.az[li] = a;
+            za += (double)zs[li] * a;
+            aa += (double)a * (double)(PV.inv[li] * a);
+          }
+          double s[2] = {za, aa};
+          t.reduce_sum(s);
+          zaz = s[0];
+          den_next = s[1];  // ap' = az on the first iteration
+        }
+        double beta = 0.0;
+        for (int itl = 0; itl < maxlin && hist_last > cfg.linear_tolerance; ++itl) {
+          const double den = den_next;
+          if (fabs(den) < 1e-300) {
+            breakdown = 1;
+            break;
+          }
+          const double alpha = zaz / den;
+          const R ra = R(alpha), rb = R(beta);
+          double pn2 = 0.0, rn2 = 0.0;
+          for (int li = tid; li < PV.nrow; li += ntd) {
+            R pv, apv;
+            if (itl == 0) {
+              pv = zs[li];
+              apv = PV.az[li];
+            } else {
+              pv = zs[li] + rb * PV.p[li];
+              apv = PV.az[li] + rb * PV.ap[li];
+            }
+            PV.p[li] = pv;
+            PV.ap[li] = apv;
+            const R rv = rs[li] - ra * apv;
+            xns[li] = xs[li] + ra * pv;
+            rns[li] = rv;
+            zns[li] = zs[li] - ra * (PV.inv[li] * apv);
+            pn2 += (double)rv * (double)(PV.inv[li] * rv);
+            rn2 += (double)rv * rv;
+          }
+          const bool pull = fabs(zaz) >= 1e-300;  // w = H^-1 J^T z'
+          if (pull) {
+            __syncthreads();
+            part_scatter(W, PV, zns);
+          }
+          {
+            double s[2] = {pn2, rn2};
+            t.reduce_sum_side(s, [&](int first, int n) {
+              if (pull) part_gather(W, PV, first, n);
+            });
+            pn2 = s[0];
+            rn2 = s[1];
+          }
+          const double pn = sqrt(pn2);
+          if (pn > phist_last) {  // monotone guard
+            mono = 1;
+            break;
+          }
+          R* tmp = xs;  // commit
+          xs = xns;
+          xns = tmp;
+          tmp = rs;
+          rs = rns;
+          rns = tmp;
+          tmp = zs;
+          zs = zns;
+          zns = tmp;
+          hist_last = sqrt(rn2);
+          phist_last = pn;
+          if (t.rank() == 0 && out.hist && hist_n <= maxlin) out.hist[(size_t)it * (maxlin + 1) + hist_n] = hist_last;
+          ++hist_n;
+          if (hist_last < best_res) {
+            best_res = hist_last;
+            for (int li = tid; li < PV.nrow; li += ntd) PV.bx[li] = xs[li];
+          }
+          lin_used = itl + 1;
+          if (fabs(zaz) < 1e-300) {
+            breakdown = 1;
+            break;
+          }
+          double za = 0.0, aa = 0.0, ab = 0.0, bb = 0.0;
+          for (int li = tid; li < PV.nrow; li += ntd) {
+            const R a = part_row(PV, li, zs, td, eps);
+            PV.az[li] = a;
+            za += (double)zs[li] * a;
+            const double ia = (double)(PV.inv[li] * a);
+            aa += (double)a * ia;
+            const R apv = PV.ap[li];
+            ab += (double)apv * ia;
+            bb += (double)apv * (double)(PV.inv[li] * apv);
+          }
+          {
+            double s[4] = {za, aa, ab, bb};
+            t.reduce_sum(s);
+            beta = s[0] / zaz;
+            zaz = s[0];
+            den_next = s[1] + 2.0 * beta * s[2] + beta * beta * s[3];
+          }
+        }
+        for (int li = tid; li < PV.nrow; li += ntd) W.bx[PV.gid[li]] = PV.bx[li];
       } else if constexpr (RPT > 0) {
         // Register-resident PCR (grid kernel, nr <= RPT * team size): each thread's
         // own rows keep x, r, z, p, ap, az, inv, bx in registers across all phases.

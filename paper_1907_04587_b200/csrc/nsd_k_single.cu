@@ -45,24 +45,36 @@ cudaError_t launch_single_block(bool tets, int threads, cudaStream_t s, const ns
   return cudaGetLastError();
 }
 
+// mode: 0 memory-path PCR, 2 register-resident rows, -1 partitioned (smem bytes of
+// dynamic shared memory per CTA, nsd_part.cuh)
 template <class R>
-cudaError_t launch_single_grid(bool tets, bool regs, int blocks, cudaStream_t s, const nsd::Topo<R>& T,
+cudaError_t launch_single_grid(bool tets, int mode, size_t smem, int blocks, cudaStream_t s, const nsd::Topo<R>& T,
                                const nsd::Work<R>& W, const nsd::Cfg& c, const nsd::StepOut& o, double* gpart) {
   nsd::Topo<R> t = T;
   nsd::Work<R> w = W;
   nsd::Cfg cf = c;
   nsd::StepOut so = o;
   void* args[] = {&t, &w, &cf, &so, &gpart};
-  void* fn = tets ? (regs ? (void*)k_single_grid<R, true, 2> : (void*)k_single_grid<R, true, 0>)
-                  : (regs ? (void*)k_single_grid<R, false, 2> : (void*)k_single_grid<R, false, 0>);
-  return cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kGridThreads), args, 0, s);
+  void* fn;
+  if (mode < 0) {
+    fn = tets ? (void*)k_single_grid<R, true, -1> : (void*)k_single_grid<R, false, -1>;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  } else if (mode == 2) {
+    fn = tets ? (void*)k_single_grid<R, true, 2> : (void*)k_single_grid<R, false, 2>;
+    smem = 0;
+  } else {
+    fn = tets ? (void*)k_single_grid<R, true, 0> : (void*)k_single_grid<R, false, 0>;
+    smem = 0;
+  }
+  return cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kGridThreads), args, smem, s);
 }
 
 #define NSD_INST(R)                                                                                                \
   template int single_grid_blocks_per_sm<R>(bool);                                                                 \
   template cudaError_t launch_single_block<R>(bool, int, cudaStream_t, const nsd::Topo<R>&, const nsd::Work<R>&,   \
                                               const nsd::Cfg&, const nsd::StepOut&);                               \
-  template cudaError_t launch_single_grid<R>(bool, bool, int, cudaStream_t, const nsd::Topo<R>&,                   \
+  template cudaError_t launch_single_grid<R>(bool, int, size_t, int, cudaStream_t, const nsd::Topo<R>&,          \
                                              const nsd::Work<R>&, const nsd::Cfg&, const nsd::StepOut&, double*);
 NSD_INST(float)
 NSD_INST(double)

@@ -258,7 +258,7 @@ template <class R>
 cudaError_t launch_single_block(bool tets, int threads, cudaStream_t s, const nsd::Topo<R>& T, const nsd::Work<R>& W,
                                 const nsd::Cfg& c, const nsd::StepOut& o);
 template <class R>
-cudaError_t launch_single_grid(bool tets, bool regs, int blocks, cudaStream_t s, const nsd::Topo<R>& T,
+cudaError_t launch_single_grid(bool tets, int mode, size_t smem, int blocks, cudaStream_t s, const nsd::Topo<R>& T,
                                const nsd::Work<R>& W, const nsd::Cfg& c, const nsd::StepOut& o, double* gpart);
 // k_batch_sub<R, 4/8/16/32> and k_batch_block<R> attributes (a negative value leaves one unset)
 template <class R> cudaError_t batch_sub_attrs(int max_dyn_smem, int carveout);

@@ -204,8 +204,23 @@ struct GridTeam {
     double m[1] = {0.0};
     reduce(s, m);
   }
+  struct NoSide {
+    __device__ __forceinline__ void operator()(int, int) const {}
+  };
   template <int NS, int NM>
   __device__ __forceinline__ void reduce(double (&s)[NS], double (&m)[NM]) {
+    reduce(s, m, NoSide{});
+  }
+  // side(first, n): work for the threads of the warps that do not sum partials, run
+  // after the barrier concurrently with the partial sums (threads first, first + 1,
+  // ... of n); its shared-memory writes are visible when reduce returns.
+  template <int NS, class F>
+  __device__ __forceinline__ void reduce_sum_side(double (&s)[NS], F&& side) {
+    double m[1] = {0.0};
+    reduce(s, m, side);
+  }
+  template <int NS, int NM, class F>
+  __device__ __forceinline__ void reduce(double (&s)[NS], double (&m)[NM], F&& side) {
     constexpr int K = NS + NM;
     static_assert(K <= kRedMax, "too many values in one reduction");
     double* buf = red + parity * (33 * kRedMax);
@@ -234,6 +249,7 @@ struct GridTeam {
         for (int k = 0; k < K; ++k) gp[part_idx(blockIdx.x, k)] = v[k];
     }
     sync();
+    if (warp >= K) side(threadIdx.x - 32 * K, static_cast<int>(blockDim.x) - 32 * K);
     if (warp < K) {  // one warp per value, all values in parallel, CTA order fixed
       const int k = warp;
       const bool is_sum = k < NS;
