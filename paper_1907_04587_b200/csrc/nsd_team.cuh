@@ -201,26 +201,25 @@ struct GridTeam {
     __syncthreads();
   }
   template <int NS> __device__ __forceinline__ void reduce_sum(double (&s)[NS]) {
-    double m[1] = {0.0};
-    reduce(s, m);
+    red_impl<NS, 0>(s, nullptr, NoSide{});
   }
   struct NoSide {
     __device__ __forceinline__ void operator()(int, int) const {}
   };
   template <int NS, int NM>
   __device__ __forceinline__ void reduce(double (&s)[NS], double (&m)[NM]) {
-    reduce(s, m, NoSide{});
+    red_impl<NS, NM>(s, m, NoSide{});
   }
   // side(first, n): work for the threads of the warps that do not sum partials, run
   // after the barrier concurrently with the partial sums (threads first, first + 1,
   // ... of n); its shared-memory writes are visible when reduce returns.
   template <int NS, class F>
   __device__ __forceinline__ void reduce_sum_side(double (&s)[NS], F&& side) {
-    double m[1] = {0.0};
-    reduce(s, m, side);
+    red_impl<NS, 0>(s, nullptr, side);
   }
+  // sums s[0..NS), maxima m[0..NM) (m may be null when NM == 0)
   template <int NS, int NM, class F>
-  __device__ __forceinline__ void reduce(double (&s)[NS], double (&m)[NM], F&& side) {
+  __device__ __forceinline__ void red_impl(double* s, double* m, F&& side) {
     constexpr int K = NS + NM;
     static_assert(K <= kRedMax, "too many values in one reduction");
     double* buf = red + parity * (33 * kRedMax);
@@ -239,7 +238,7 @@ struct GridTeam {
     }
     __syncthreads();
     if (warp == 0) {  // CTA partials
-      double v[K];
+      double v[K > 0 ? K : 1];
 #pragma unroll
       for (int k = 0; k < NS; ++k) v[k] = warp_sum_down(lane < nw ? buf[lane * kRedMax + k] : 0.0);
 #pragma unroll
