@@ -69,6 +69,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU baseline sample length")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-alt", action="store_true", help="skip the secondary-precision measurement")
+    p.add_argument("--no-parity-sample", action="store_true", help="skip the end-of-run oracle check of 64 envs")
     p.add_argument("--no-scenes", action="store_true", help="skip the C1-C4 single-scene summary")
     p.add_argument("--workload", default="c5",
                    help="c5 (default: batched ants, the headline) or one single scene (c1, c2, c3, c4, c2:6, ...) "
@@ -374,9 +375,38 @@ def measure(args, prec, T, tmpl, E, env0, ws, rank, local, sample_clocks):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         dev_ms, e2e_ms, e2e_copy_ms = float(t[0]), float(t[1]), float(t[2])
     total_envs = E * ws
-    return dict(dev_ms=dev_ms, e2e_ms=e2e_ms, value=total_envs * K / (dev_ms / 1000.0),
+    ns = min(E, PARITY_SAMPLE_ENVS)  # the first envs' final state, for the oracle parity sample
+    q_fin = h_q[K - 1][: ns * T.num_coord].numpy().reshape(ns, T.num_coord).copy()
+    u_fin = h_u[K - 1][: ns * T.num_dof].numpy().reshape(ns, T.num_dof).copy()
+    return dict(dev_ms=dev_ms, e2e_ms=e2e_ms, value=total_envs * K / (dev_ms / 1000.0), q_fin=q_fin, u_fin=u_fin,
                 e2e=total_envs * K / (e2e_ms / 1000.0), e2e_copy=total_envs * K / (e2e_copy_ms / 1000.0), nc=nc,
                 aborted=aborted, clocks=clocks, h2d=h2d, d2h=d2h, cfg=cfg, ctr=ctr, cr_share=cr_share, E=E)
+
+
+PARITY_SAMPLE_ENVS = 64
+
+
+def parity_sample(args, m, env0, T, prec):
+    """The bench run itself against the oracle: the first PARITY_SAMPLE_ENVS envs of
+    the shard after all W + K steps (same initial states and action stream, oracle
+    step_world on the host cores), max relative error of q and u over the sample.
+    Stated tolerance: fp64 1e-6 (C5 tracks the oracle to ~1e-14 over 25 steps,
+    tests/test_gpu_batch.py; rounding grows over 200+ contact-rich steps), fp32
+    mixed mode 1e-2."""
+    from oracle import oracle_py as O
+
+    n = m["q_fin"].shape[0]
+    steps = args.warmup + args.steps
+    t0 = time.perf_counter()
+    oq, ou, onc = O.c5_states(env0, n, steps, T.num_coord, T.num_dof, actuated=not args.passive)
+    eq = float(np.max(np.abs(m["q_fin"] - oq)) / max(np.max(np.abs(oq)), 1e-12))
+    eu = float(np.max(np.abs(m["u_fin"] - ou)) / max(np.max(np.abs(ou)), 1e-3))
+    tol = 1e-6 if prec == "fp64" else 1e-2
+    return {"envs": n, "env_ids": f"{env0}..{env0 + n - 1}", "steps": steps, "max_rel_err_q": eq,
+            "max_rel_err_u": eu, "tolerance_q": tol, "pass": bool(eq <= tol),
+            "oracle_seconds": time.perf_counter() - t0,
+            "note": "final (q, u) of the timed run (e2e replay) vs the oracle's step_world from the same initial "
+                    "states and actions"}
 
 
 def traffic_record(kernel_key):
@@ -603,6 +633,11 @@ def main():
             "gpu_launches": 3 * K, "clocks": m["clocks"]}
     if other:
         line["other_precision"] = other
+    if not args.no_parity_sample:
+        try:
+            line["parity_sample"] = parity_sample(args, m, env0, T, prec)
+        except Exception as e:  # reported, never fatal for the headline
+            line["parity_sample"] = {"error": str(e)}
     if ws == 1 and not args.no_scenes:
         # the other BASELINE configs (single scenes, replicas only), fp64, 20 steps each
         line["single_scenes"] = {}

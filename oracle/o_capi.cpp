@@ -578,6 +578,38 @@ double orc_c5_bench(int env0, int n_env, int n_warm, int n_steps, int actuated, 
   return std::chrono::duration<double>(t1 - t0).count();
 }
 
+// The same C5 ants stepped n_steps times (actions as orc_c5_bench), returning each
+// env's final q, u (env-major) and contact count: bench.py's end-of-run parity sample.
+int orc_c5_states(int env0, int n_env, int n_steps, int actuated, int threads, double* q_out, double* u_out,
+                  int* nc_out) {
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#else
+  (void)threads;
+#endif
+  std::vector<World> worlds(n_env);
+  for (int e = 0; e < n_env; ++e) worlds[e] = build_world(build_c5_ant(static_cast<unsigned>(env0 + e)));
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int e = 0; e < n_env; ++e) {
+    World& w = worlds[e];
+    for (int s = 0; s < n_steps; ++s) {
+      if (actuated) {
+        std::vector<double> tau(w.joints.size());
+        for (size_t j = 0; j < tau.size(); ++j) tau[j] = action_torque(env0 + e, s, static_cast<int>(j));
+        w.f_extra = joint_torque_forces(w, tau.data());
+      }
+      (void)step_world(w);
+    }
+  }
+  for (int e = 0; e < n_env; ++e) {
+    const World& w = worlds[e];
+    std::copy(w.state.q.begin(), w.state.q.end(), q_out + e * w.state.q.size());
+    std::copy(w.state.u.begin(), w.state.u.end(), u_out + e * w.state.u.size());
+    nc_out[e] = static_cast<int>(w.contacts.size());
+  }
+  return 0;
+}
+
 
 // Runner CSV output (restates src/runner.cpp:13-27, 80-126, 148-180 for the
 // GPU-vs-oracle file diff): trajectory.csv + convergence.csv, %.17g. Returns

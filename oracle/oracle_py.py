@@ -488,6 +488,16 @@ def action_torque(env, step, joint):
     return lib().orc_action_torque(C.c_int(env), C.c_int(step), C.c_int(joint))
 
 
+def c5_states(env0, n_env, n_steps, ncoord, ndof, actuated=True, threads=0):
+    """Final (q, u, n_contacts) of C5 ants env0.. after n_steps oracle step_world calls."""
+    q = np.zeros((n_env, ncoord))
+    u = np.zeros((n_env, ndof))
+    nc = np.zeros(n_env, dtype=np.int32)
+    lib().orc_c5_states(C.c_int(env0), C.c_int(n_env), C.c_int(n_steps), C.c_int(int(actuated)), C.c_int(threads),
+                        dp(q), dp(u), ip(nc))
+    return q, u, nc
+
+
 def c5_bench(env0, n_env, n_steps, actuated=False, threads=0, warm=0):
     """Times steps [warm, warm + n_steps) of n_env C5 ants (OpenMP over envs)."""
     used, cs = C.c_int(), C.c_double()

@@ -421,9 +421,10 @@ template <class R> struct Solver final : SolverBase {
       per_sm = single_grid_blocks_per_sm<R>(tets);
       if (per_sm < 1) throw NsdError(NSD_CUDA_ERROR, "grid kernel cannot be resident");
       const char* bps = std::getenv("NSD_GRID_BLOCKS_PER_SM");
-      grid_blocks = dev_sms * std::min(per_sm, bps ? std::max(1, std::atoi(bps)) : 1);
-      // partials (+ 2 x kRedMax spare slots) and the arrival count of the grid barrier (nsd_team.cuh)
-      gpart.alloc(sizeof(double) * (2 * grid_blocks * nsd::kRedMax + 2 * nsd::kRedMax + 2));
+      grid_blocks = std::min(nsd::kGridMaxCtas, dev_sms * std::min(per_sm, bps ? std::max(1, std::atoi(bps)) : 1));
+      if (const char* gc = std::getenv("NSD_GRID_CTAS")) grid_blocks = std::max(1, std::min(grid_blocks, std::atoi(gc)));
+      // partials, arrival count and flag-in-data words of the grid reductions (nsd_team.cuh)
+      gpart.alloc(sizeof(double) * nsd::grid_scratch_doubles(grid_blocks));
       part_static();
       int optin = 0;
       NSD_CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
@@ -688,6 +689,7 @@ template <class R> struct Solver final : SolverBase {
     W.lam = reinterpret_cast<R*>(ob + o_lam);
     W.h = R(in->h);
     for (int k = 0; k < 3; ++k) W.grav[k] = R(in->gravity[k]);
+    W.op32 = cfg.precision == NSD_FP32 ? 1 : 0;  // fp32 J/C coefficient storage (nsd_engine.cuh opg)
     W.nc = nc;
     W.nrows = nrows;
     W.normal_begin = H.rows_static;
@@ -699,7 +701,9 @@ template <class R> struct Solver final : SolverBase {
       NSD_CK(launch_single_block<R>(tets, block_threads, stream, topo.t, W, kc, so));
     } else {
       double* gp = gpart.as<double>();
-      NSD_CK(cudaMemsetAsync(gp + 2 * grid_blocks * nsd::kRedMax + 2 * nsd::kRedMax, 0, 2 * sizeof(unsigned), stream));
+      NSD_CK(cudaMemsetAsync(gp + nsd::grid_scratch_reset_off(grid_blocks), 0,
+                             sizeof(double) * (nsd::grid_scratch_doubles(grid_blocks) - nsd::grid_scratch_reset_off(grid_blocks)),
+                             stream));  // arrival count and flag words: epochs restart every launch
       // register-resident PCR rows when every thread owns <= 2 rows (NSD_GRID_REGS=0 disables)
       const bool regs = cfg.linear_method == 3 && nrows <= 2 * grid_blocks * kGridThreads && !(std::getenv("NSD_GRID_REGS") &&
                                                                        std::atoi(std::getenv("NSD_GRID_REGS")) == 0);
@@ -1376,10 +1380,9 @@ int nsd_create(const nsd_topology* topo, const nsd_config* cfg, int32_t device, 
     check_cfg(*cfg);
     auto* s = new nsd_solver();
     try {
-      if (cfg->precision == NSD_FP64)
-        s->impl.reset(new Solver<double>(*topo, *cfg, device));
-      else
-        s->impl.reset(new Solver<float>(*topo, *cfg, device));
+      // one fp64 engine for both precisions: fp32 stores the operator's J/C
+      // coefficients in fp32 (Work::op32), state and arithmetic stay fp64
+      s->impl.reset(new Solver<double>(*topo, *cfg, device));
     } catch (...) {
       delete s;
       throw;

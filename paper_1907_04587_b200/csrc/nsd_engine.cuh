@@ -37,6 +37,16 @@
 #include "nsd_math.cuh"
 #include "nsd_team.cuh"
 
+// Element assembly (SVD, eigensolver, 3x3 inverses) is called once per Newton
+// iteration; a TU whose kernel runs a register-resident PCR loop around it can keep
+// it out of line (NSD_ASM_NOINLINE, nsd_k_single.cu) so the loop is not allocated
+// for the assembly's register pressure.
+#ifdef NSD_ASM_NOINLINE
+#define NSD_ASM __device__ __noinline__
+#else
+#define NSD_ASM __device__
+#endif
+
 namespace nsd {
 
 using std::isfinite;
@@ -111,6 +121,7 @@ template <class R> struct Work {
   // rows
   int nrows, normal_begin, friction_begin;
   R* coeff;  // 12 per static row
+  int op32;  // fp32 mode: coeff, ctet, cdir, carm hold floats (see opg/ops)
   int* blk;  // 4 per static row
   R* jstr;   // batched path: 24 per joint (structured rows, see assemble_joint) or null
   R* crec;   // batched path: 20 per contact (n d1 d2 r_a r_b dc act, 16-byte aligned) or null
@@ -192,6 +203,27 @@ template <class R> __device__ __forceinline__ void st3(R* p, V3<R> v) {
   p[0] = v.x;
   p[1] = v.y;
   p[2] = v.z;
+}
+// Operator coefficient arrays (coeff, ctet, cdir, carm): element i of array a, stored in
+// R, or — single-scene fp32 mode, W.op32 — as float in the same buffer. State, row
+// and dof vectors and all arithmetic stay in R (fp64): the fp32 mode halves the
+// operator's coefficient stream only (the batch warp solver's mixed mode likewise).
+template <class R> __device__ __forceinline__ R opg(const Work<R>& W, const R* a, size_t i) {
+  return W.op32 ? R(reinterpret_cast<const float*>(a)[i]) : a[i];
+}
+template <class R> __device__ __forceinline__ void ops(const Work<R>& W, R* a, size_t i, R v) {
+  if (W.op32)
+    reinterpret_cast<float*>(a)[i] = static_cast<float>(v);
+  else
+    a[i] = v;
+}
+template <class R> __device__ __forceinline__ V3<R> opg3(const Work<R>& W, const R* a, size_t i) {
+  return v3(opg(W, a, i), opg(W, a, i + 1), opg(W, a, i + 2));
+}
+template <class R> __device__ __forceinline__ void ops3(const Work<R>& W, R* a, size_t i, V3<R> v) {
+  ops(W, a, i, v.x);
+  ops(W, a, i + 1, v.y);
+  ops(W, a, i + 2, v.z);
 }
 template <class R> __device__ __forceinline__ V3<R> sym_mul(const R* s6, V3<R> v) {
   // s6 = xx yy zz xy xz yz
@@ -310,13 +342,11 @@ template <class R> __device__ __forceinline__ CView<R> contact_view(const Topo<R
   v.bb = W.cbody[2 * c + 1];
   body_blocks(T, v.ba, v.al, v.aa);
   body_blocks(T, v.bb, v.bl, v.bA);
-  const R* g = W.cdir + 9 * c;
-  v.n = ld3(g);
-  v.d1 = ld3(g + 3);
-  v.d2 = ld3(g + 6);
-  const R* a = W.carm + 6 * c;
-  v.ra = ld3(a);
-  v.rb = ld3(a + 3);
+  v.n = opg3(W, W.cdir, 9 * c);
+  v.d1 = opg3(W, W.cdir, 9 * c + 3);
+  v.d2 = opg3(W, W.cdir, 9 * c + 6);
+  v.ra = opg3(W, W.carm, 6 * c);
+  v.rb = opg3(W, W.carm, 6 * c + 3);
   v.dc = W.cscale[2 * c];
   v.act = W.cscale[2 * c + 1];
   return v;
@@ -351,32 +381,35 @@ __device__ __forceinline__ R contact_quad(const Topo<R>& T, const Work<R>& W, co
 }
 
 // ------------------------------------------------------------------ row-level J and diag
-// J_i . v for static rows (4 slots x 3).
-template <class R> __device__ __forceinline__ R slot_dot(const R* c12, const int* b4, const R* v) {
+// J_i . v for static row i (4 slots x 3).
+template <class R> __device__ __forceinline__ R slot_dot(const Work<R>& W, int i, const R* v) {
+  const int* b4 = W.blk + 4 * i;
   R s = R(0);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int b = b4[k];
     if (b < 0) continue;
     const R* vb = v + 3 * b;
-    s += c12[3 * k] * vb[0] + c12[3 * k + 1] * vb[1] + c12[3 * k + 2] * vb[2];
+    const V3<R> c = opg3(W, W.coeff, 12 * (size_t)i + 3 * k);
+    s += c.x * vb[0] + c.y * vb[1] + c.z * vb[2];
   }
   return s;
 }
 template <class R>
-__device__ __forceinline__ R slot_quad(const Topo<R>& T, const Work<R>& W, const R* c12, const int* b4, bool shifted) {
+__device__ __forceinline__ R slot_quad(const Topo<R>& T, const Work<R>& W, int i, bool shifted) {
+  const int* b4 = W.blk + 4 * i;
   R s = R(0);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int b = b4[k];
     if (b < 0) continue;
-    s += block_quad(T, W, b, v3(c12[3 * k], c12[3 * k + 1], c12[3 * k + 2]), shifted);
+    s += block_quad(T, W, b, opg3(W, W.coeff, 12 * (size_t)i + 3 * k), shifted);
   }
   return s;
 }
 // J_i . v for any row.
 template <class R> __device__ __forceinline__ R row_J(const Topo<R>& T, const Work<R>& W, int i, const R* v) {
-  if (i < T.rows_static) return slot_dot(W.coeff + 12 * i, W.blk + 4 * i, v);
+  if (i < T.rows_static) return slot_dot(W, i, v);
   if (i < W.friction_begin) {
     const CView<R> c = contact_view(T, W, i - W.normal_begin);
     return c.dc == R(0) ? R(0) : c.dc * dot(c.n, contact_dv(c, v));
@@ -388,7 +421,7 @@ template <class R> __device__ __forceinline__ R row_J(const Topo<R>& T, const Wo
 }
 // J_i H^-1 J_i^T (shifted) for any row.
 template <class R> __device__ __forceinline__ R row_quad(const Topo<R>& T, const Work<R>& W, int i) {
-  if (i < T.rows_static) return slot_quad(T, W, W.coeff + 12 * i, W.blk + 4 * i, true);
+  if (i < T.rows_static) return slot_quad(T, W, i, true);
   if (i < W.friction_begin) {
     const CView<R> c = contact_view(T, W, i - W.normal_begin);
     return c.dc == R(0) ? R(0) : contact_quad(T, W, c, c.dc * c.n, true);
@@ -404,11 +437,10 @@ template <class R> __device__ __forceinline__ R row_quad(const Topo<R>& T, const
 template <class R, class F>
 __device__ __forceinline__ void row_JT(const Topo<R>& T, const Work<R>& W, int i, R d, F&& f) {
   if (i < T.rows_static) {
-    const R* c = W.coeff + 12 * i;
     const int* b4 = W.blk + 4 * i;
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (b4[k] >= 0) f(b4[k], v3(c[3 * k] * d, c[3 * k + 1] * d, c[3 * k + 2] * d));
+      if (b4[k] >= 0) f(b4[k], d * opg3(W, W.coeff, 12 * (size_t)i + 3 * k));
     return;
   }
   const bool normal = i < W.friction_begin;
@@ -479,7 +511,7 @@ struct AsmStats {
 };
 
 template <class R>
-__device__ void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, R h, AsmStats& st) {
+NSD_ASM void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, R h, AsmStats& st) {
   const int kind = T.jkind[j], ba = T.jbody[2 * j], bb = T.jbody[2 * j + 1];
   const R* fr = W.jframe + 21 * j;
   const V3<R> anc_a = ld3(fr), anc_b = ld3(fr + 3), ax_a = ld3(fr + 6), ax_a2 = ld3(fr + 9), ax_b1 = ld3(fr + 12),
@@ -531,7 +563,7 @@ __device__ void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, 
       emit(k, value, comp);
       return;
     }
-    R* c = W.coeff + 12 * (r0 + k);
+    R c[12];
     const int* b = W.blk + 4 * (r0 + k);
 #pragma unroll
     for (int i = 0; i < 12; ++i) c[i] = R(0);
@@ -540,6 +572,8 @@ __device__ void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, 
     slot_add(c, b, 2, bl, -d);
     if (rig_b) slot_add(c, b, 3, bA, -cross(rb, d));
     if (prism && rig_a) slot_add(c, b, 1, aa, cross(d, wa - wb));  // t x d (constraints.cpp:195-196)
+#pragma unroll
+    for (int i = 0; i < 12; ++i) ops(W, W.coeff, 12 * (size_t)(r0 + k) + i, c[i]);
     emit(k, value, comp);
   };
   const int n_point = (kind == 0 || kind == 1) ? 3 : (kind == 2 ? 2 : 0);
@@ -549,13 +583,15 @@ __device__ void assemble_joint(const Topo<R>& T, Work<R>& W, const R* q, int j, 
       emit(k, dot(xa, xb) - restv, e);
       return;
     }
-    R* c = W.coeff + 12 * (r0 + k);
+    R c[12];
     const int* b = W.blk + 4 * (r0 + k);
 #pragma unroll
     for (int i = 0; i < 12; ++i) c[i] = R(0);
     const V3<R> cr = cross(xa, xb);
     if (rig_a) slot_add(c, b, 1, aa, cr);
     if (rig_b) slot_add(c, b, 3, bA, -cr);
+#pragma unroll
+    for (int i = 0; i < 12; ++i) ops(W, W.coeff, 12 * (size_t)(r0 + k) + i, c[i]);
     emit(k, dot(xa, xb) - restv, e);
   };
   const V3<R> e0 = v3(R(1), R(0), R(0)), e1 = v3(R(0), R(1), R(0)), e2 = v3(R(0), R(0), R(1));
@@ -642,7 +678,7 @@ __device__ void assemble_tet_linear(const Topo<R>& T, Work<R>& W, int e, R h, co
     st.hsq += (double)hv * (double)hv;
   }
 #pragma unroll
-  for (int i = 0; i < 36; ++i) W.ctet[36 * e + i] = E[i] / (h * h);
+  for (int i = 0; i < 36; ++i) ops(W, W.ctet, 36 * (size_t)e + i, E[i] / (h * h));
   // G = tr(S) I - S and its inverse (frozen frame when |det G| <= 1e-12)
   const R tr = S(0, 0) + S(1, 1) + S(2, 2);
   M3<R> G;
@@ -687,14 +723,14 @@ __device__ void assemble_tet_linear(const Topo<R>& T, Work<R>& W, int e, R h, co
       const R sym[6] = {A(0, 0), A(1, 1), A(2, 2), R(2) * (R(0.5) * (A(1, 2) + A(2, 1))),
                         R(2) * (R(0.5) * (A(0, 2) + A(2, 0))), R(2) * (R(0.5) * (A(0, 1) + A(1, 0)))};
 #pragma unroll
-      for (int i = 0; i < 6; ++i) W.coeff[12 * (r0 + i) + 3 * k + d] = sym[i];
+      for (int i = 0; i < 6; ++i) ops(W, W.coeff, 12 * (size_t)(r0 + i) + 3 * k + d, sym[i]);
     }
   }
 }
 
 // Neo-Hookean element rows (materials.cpp:180-193, 57-114).
 template <class R>
-__device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R h, AsmStats& st) {
+NSD_ASM void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R h, AsmStats& st) {
   const int* tb = T.tbody + 4 * e;
   V3<R> p[4];
 #pragma unroll
@@ -775,15 +811,15 @@ __device__ void assemble_tet(const Topo<R>& T, Work<R>& W, const R* q, int e, R 
     st.hsq += (double)hv * (double)hv;
     const V3<R> ui = col(sv.U, i);
     const V3<R> wi = mul(dm, col(sv.V, i));
-    R* c = W.coeff + 12 * (r0 + i);
+    const size_t c = 12 * (size_t)(r0 + i);
     const R w0 = -(wi.x + wi.y + wi.z);
-    st3(c, w0 * ui);
-    st3(c + 3, wi.x * ui);
-    st3(c + 6, wi.y * ui);
-    st3(c + 9, wi.z * ui);
+    ops3(W, W.coeff, c, w0 * ui);
+    ops3(W, W.coeff, c + 3, wi.x * ui);
+    ops3(W, W.coeff, c + 6, wi.y * ui);
+    ops3(W, W.coeff, c + 9, wi.z * ui);
   }
 #pragma unroll
-  for (int i = 0; i < 9; ++i) W.ctet[9 * e + i] = E.a[i] / (h * h);
+  for (int i = 0; i < 9; ++i) ops(W, W.ctet, 9 * (size_t)e + i, E.a[i] / (h * h));
 }
 
 // Contact rows (newton.cpp:166-218; constraints.cpp:67-91, 103-115) in the
@@ -804,7 +840,7 @@ __device__ __forceinline__ R contact_gap_strict(const Topo<R>& T, const R* q, in
 }
 
 template <class R>
-__device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const R* u, int c, R h, const Cfg& cfg,
+NSD_ASM void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const R* u, int c, R h, const Cfg& cfg,
                                  AsmStats& st) {
   const int ba = W.cbody[2 * c], bb = W.cbody[2 * c + 1];
   const R* g = W.cgeo + 17 * c;
@@ -825,8 +861,8 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
     pb = body_pos(T, q, bb) + rb;
   }
   if (!W.crec) {  // the batched path keeps the same data in its contact record only
-    st3(W.carm + 6 * c, ra);
-    st3(W.carm + 6 * c + 3, rb);
+    ops3(W, W.carm, 6 * (size_t)c, ra);
+    ops3(W, W.carm, 6 * (size_t)c + 3, rb);
   }
   CView<R> cv;
   cv.ba = ba;
@@ -837,10 +873,9 @@ __device__ void assemble_contact(const Topo<R>& T, Work<R>& W, const R* q, const
   cv.d1 = ld3(g + 9);
   cv.d2 = ld3(g + 12);
   if (!W.crec) {
-    R* cdir = W.cdir + 9 * c;
-    st3(cdir, cv.n);
-    st3(cdir + 3, cv.d1);
-    st3(cdir + 6, cv.d2);
+    ops3(W, W.cdir, 9 * (size_t)c, cv.n);
+    ops3(W, W.cdir, 9 * (size_t)c + 3, cv.d1);
+    ops3(W, W.cdir, 9 * (size_t)c + 6, cv.d2);
   }
   cv.ra = ra;
   cv.rb = rb;
@@ -974,24 +1009,25 @@ __device__ __forceinline__ V3<R> pull_part(const Topo<R>& T, const Work<R>& W, i
     const int ent = T.sinc_ent[e];
     const int row = ent >> 2, slot = ent & 3;
     const R yr = y(row);
-    const R* c = W.coeff + 12 * row + 3 * slot;
-    sx += c[0] * yr;
-    sy += c[1] * yr;
-    sz += c[2] * yr;
+    const V3<R> c = opg3(W, W.coeff, 12 * (size_t)row + 3 * slot);
+    sx += c.x * yr;
+    sy += c.y * yr;
+    sz += c.z * yr;
   }
   if (W.nc > 0) {
     const int c0 = W.cinc_off[b], c1 = W.cinc_off[b + 1];
     for (int e = c0 + first; e < c1; e += stride) {
       const int ent = W.cinc_ent[e];
       const int c = ent >> 2, slot = ent & 3;
-      const R* g = W.cdir + 9 * c;
+      const V3<R> gn = opg3(W, W.cdir, 9 * (size_t)c), g1 = opg3(W, W.cdir, 9 * (size_t)c + 3),
+                  g2 = opg3(W, W.cdir, 9 * (size_t)c + 6);
       const R dc = W.cscale[2 * c], act = W.cscale[2 * c + 1];
       const int f0 = W.friction_begin + 2 * c;
       const R yn = dc * y(W.normal_begin + c), y1 = act * y(f0), y2 = act * y(f0 + 1);
       // contact force f = dc z_n n + z_1 d1 + z_2 d2
-      V3<R> f = v3(yn * g[0] + y1 * g[3] + y2 * g[6], yn * g[1] + y1 * g[4] + y2 * g[7],
-                   yn * g[2] + y1 * g[5] + y2 * g[8]);
-      if (slot & 1) f = cross(ld3(W.carm + 6 * c + ((slot & 2) ? 3 : 0)), f);
+      V3<R> f = v3(yn * gn.x + y1 * g1.x + y2 * g2.x, yn * gn.y + y1 * g1.y + y2 * g2.y,
+                   yn * gn.z + y1 * g1.z + y2 * g2.z);
+      if (slot & 1) f = cross(opg3(W, W.carm, 6 * (size_t)c + ((slot & 2) ? 3 : 0)), f);
       if (slot & 2) f = -f;
       sx += f.x;
       sy += f.y;
@@ -1053,11 +1089,11 @@ template <class R, bool kTets>
 __device__ __forceinline__ R row_C(const Topo<R>& T, const Work<R>& W, int i, const R* z) {
   if (kTets && i >= T.rows_joint && i < T.rows_static) {
     const int td = T.tdim, e = (i - T.rows_joint) / td, k = (i - T.rows_joint) - td * e;
-    const R* cb = W.ctet + td * td * e + td * k;
+    const size_t cb = (size_t)td * td * e + td * k;
     const int r0 = T.rows_joint + td * e;
-    if (td == 3) return cb[0] * z[r0] + cb[1] * z[r0 + 1] + cb[2] * z[r0 + 2];
+    if (td == 3) return opg(W, W.ctet, cb) * z[r0] + opg(W, W.ctet, cb + 1) * z[r0 + 1] + opg(W, W.ctet, cb + 2) * z[r0 + 2];
     R acc = R(0);
-    for (int j = 0; j < 6; ++j) acc += cb[j] * z[r0 + j];
+    for (int j = 0; j < 6; ++j) acc += opg(W, W.ctet, cb + j) * z[r0 + j];
     return acc;
   }
   return W.cd[i] * z[i];
@@ -1065,7 +1101,7 @@ __device__ __forceinline__ R row_C(const Topo<R>& T, const Work<R>& W, int i, co
 template <class R, bool kTets> __device__ __forceinline__ R row_Cdiag(const Topo<R>& T, const Work<R>& W, int i) {
   if (kTets && i >= T.rows_joint && i < T.rows_static) {
     const int td = T.tdim, e = (i - T.rows_joint) / td, k = (i - T.rows_joint) - td * e;
-    return W.ctet[td * td * e + (td + 1) * k];
+    return opg(W, W.ctet, (size_t)td * td * e + (td + 1) * k);
   }
   return W.cd[i];
 }

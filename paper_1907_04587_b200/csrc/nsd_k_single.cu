@@ -1,5 +1,6 @@
 // Single-scene kernels (nsd_step, the newton_step boundary): one CTA for small
 // scenes, a persistent cooperative grid for the FEM configs.
+#define NSD_ASM_NOINLINE 1
 #include "nsd_plan.cuh"
 
 using namespace nsdi;
@@ -76,7 +77,6 @@ cudaError_t launch_single_grid(bool tets, int mode, size_t smem, int blocks, cud
                                               const nsd::Cfg&, const nsd::StepOut&);                               \
   template cudaError_t launch_single_grid<R>(bool, int, size_t, int, cudaStream_t, const nsd::Topo<R>&,          \
                                              const nsd::Work<R>&, const nsd::Cfg&, const nsd::StepOut&, double*);
-NSD_INST(float)
 NSD_INST(double)
 #undef NSD_INST
 

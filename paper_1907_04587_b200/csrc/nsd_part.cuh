@@ -61,6 +61,7 @@ template <class R> struct PartView {
   R *x, *r, *z, *zn, *p, *ap, *az, *inv, *bx, *xn, *rn;
   int *gid, *slot, *cb, *lbg, *lbk, *incoff, *inc, *xoff, *xent;
   int nrow, nlb, f0;  // own rows, local blocks, flat index of local block 0
+  int sg;             // lanes per local block in part_scatter (power of two <= 32)
   __device__ PartView(char* s, const Work<R>& W, bool on) {
     if (!on) return;
     const PartSmem L = part_smem<R>(W.part_mr, W.part_ml, W.part_mx);
@@ -94,6 +95,8 @@ template <class R> struct PartView {
     nrow = W.part_row_off[b + 1] - W.part_row_off[b];
     nlb = W.part_lb_off[b + 1] - W.part_lb_off[b];
     f0 = W.part_lb_off[b];
+    sg = 1;
+    while (sg < 32 && 2 * sg * nlb <= (int)blockDim.x) sg *= 2;
   }
 };
 
@@ -182,7 +185,7 @@ __device__ void part_load(const Topo<R>& T, const Work<R>& W, PartView<R>& V) {
     R* cc = V.cc + 6 * li;
     if (i < T.rows_static) {
 #pragma unroll
-      for (int k = 0; k < 12; ++k) c[k] = W.coeff[12 * i + k];
+      for (int k = 0; k < 12; ++k) c[k] = opg(W, W.coeff, 12 * (size_t)i + k);
     } else {
       const bool normal = i < W.friction_begin;
       const int k = i - W.friction_begin, c0 = normal ? i - W.normal_begin : (k >> 1);
@@ -196,7 +199,7 @@ __device__ void part_load(const Topo<R>& T, const Work<R>& W, PartView<R>& V) {
     }
     if (kTets && i >= T.rows_joint && i < T.rows_static) {
       const int td = T.tdim, e = (i - T.rows_joint) / td, k = (i - T.rows_joint) - td * e;
-      for (int j = 0; j < td; ++j) cc[j] = W.ctet[td * td * e + td * k + j];
+      for (int j = 0; j < td; ++j) cc[j] = opg(W, W.ctet, (size_t)td * td * e + td * k + j);
     } else {
       cc[0] = W.cd[i];
     }
@@ -228,20 +231,34 @@ template <class R> __device__ __forceinline__ V3<R> part_hinv(const PartView<R>&
 
 // J^T y per local block from shared memory; blocks of this CTA alone get w, shared
 // blocks publish their partial (read back by part_gather after a grid barrier).
+// V.sg lanes of one warp share a block: each sums every sg-th incidence entry, then a
+// fixed shuffle tree combines them (deterministic). A FEM vertex block gathers up to
+// ~60 (row, slot) entries inside one CTA, so one lane per block made this serial
+// chain the CTA's critical path while most threads idled (nlb << blockDim).
 template <class R>
 __device__ __forceinline__ void part_scatter(const Work<R>& W, PartView<R>& V, const R* y) {
   R* gp = static_cast<R*>(W.part_partial);
-  for (int l = threadIdx.x; l < V.nlb; l += blockDim.x) {
+  const int G = V.sg, gl = threadIdx.x & (G - 1), ng = blockDim.x / G;
+  for (int base = 0; base < V.nlb; base += ng) {  // uniform trip count: every lane joins the shuffles
+    const int l = base + threadIdx.x / G;
     R sx = R(0), sy = R(0), sz = R(0);
-    for (int e = V.incoff[l]; e < V.incoff[l + 1]; ++e) {
-      const int ent = V.inc[e];
-      const int li = ent >> 2, k = ent & 3;
-      const R yr = y[li];
-      const R* c = V.coeff + 12 * li + 3 * k;
-      sx += c[0] * yr;
-      sy += c[1] * yr;
-      sz += c[2] * yr;
+    if (l < V.nlb) {
+      for (int e = V.incoff[l] + gl; e < V.incoff[l + 1]; e += G) {
+        const int ent = V.inc[e];
+        const int li = ent >> 2, k = ent & 3;
+        const R yr = y[li];
+        const R* c = V.coeff + 12 * li + 3 * k;
+        sx += c[0] * yr;
+        sy += c[1] * yr;
+        sz += c[2] * yr;
+      }
     }
+    for (int off = G >> 1; off > 0; off >>= 1) {
+      sx += __shfl_down_sync(0xffffffffu, sx, off, G);
+      sy += __shfl_down_sync(0xffffffffu, sy, off, G);
+      sz += __shfl_down_sync(0xffffffffu, sz, off, G);
+    }
+    if (l >= V.nlb || gl != 0) continue;
     if (V.xoff[l + 1] - V.xoff[l] > 1) {
       R* o = gp + 3 * (V.f0 + l);
       o[0] = sx;

@@ -132,6 +132,7 @@ struct WorkPlan {
     W.iw6 = cr + iw6;
     W.iwi6 = hr + iwi6;
     W.coeff = hr + coeff;
+    W.op32 = 0;
     W.hv = hr + hv;
     W.cd = hr + cd;
     W.lam = hr + lam;

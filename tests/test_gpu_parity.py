@@ -16,10 +16,11 @@ in DESIGN.md "Parity":
     Decisions (PCR iterations used per Newton iteration, breakdown, abort) are
     identical except at borderline exits (residual within 10x of tolerance or
     at the rounding floor), which are counted; non-borderline mismatches: 0.
-  fp32 performance mode — rigid configs: q 1e-4, u 0.2 (redundant resting
-    contact sets make u/lambda ill-posed at fp32), lambda not compared.
-    Tetrahedral (stiff Neo-Hookean) scenes are not claimed in fp32: they run,
-    stay finite, and use fp64 by default in bench/production.
+  fp32 mode — fp64 state, assembly, PCR recurrence and arithmetic; the operator's
+    J and C coefficients (joint/tet rows, tet compliance blocks, contact frames and
+    lever arms) stored in fp32 (nsd_engine.cuh opg/ops). Rigid configs: q 1e-6,
+    u 1e-4, lambda 1e-2 per step; the C2 FEM block at step 0 as fp64's FEM bound.
+    Trajectories: tests/test_world.py (1e-4 after 25 steps).
 """
 import numpy as np
 import pytest
@@ -92,15 +93,12 @@ def test_newton_step_fp64_degenerate_svd():
 
 @pytest.mark.parametrize("name,seed,warm", RIGID)
 def test_newton_step_fp32_rigid(name, seed, warm):
-    _check(name, seed, warm, "fp32", (1e-4, 0.2, None), False)
+    _check(name, seed, warm, "fp32", (1e-6, 1e-4, 1e-2), False)
 
 
 @pytest.mark.parametrize("name,seed,warm", FEM)
-def test_newton_step_fp32_fem_runs(name, seed, warm):
-    case = oracle_case(name, seed, warm)
-    g = run_gpu(case, "fp32")
-    assert not g["aborted"]
-    assert np.all(np.isfinite(g["q"])) and np.all(np.isfinite(g["u"]))
+def test_newton_step_fp32_fem(name, seed, warm):
+    _check(name, seed, warm, "fp32", TOL64_FEM, False)
 
 
 @pytest.mark.slow
