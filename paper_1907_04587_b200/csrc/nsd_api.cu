@@ -398,7 +398,7 @@ template <class R> struct Solver final : SolverBase {
   // CTAs once, contacts added per step (PartPlanH)
   std::vector<int> ps_row_begin;         // CTA p owns static rows [ps_row_begin[p], ps_row_begin[p + 1])
   std::vector<std::vector<int>> ps_blk;  // per CTA: its static rows' dof3 blocks, ascending
-  std::vector<int> first_cta;            // per dof3 block: the lowest CTA whose static rows touch it, or -1
+  std::vector<std::vector<int>> blk_ctas;  // per dof3 block: the CTAs whose static rows touch it, ascending
   DBuf partbuf;                          // shared-block partials, 3 per flat local block
 
   Solver(const nsd_topology& tp, const nsd_config& c, int device) : cfg(c) {
@@ -455,15 +455,49 @@ template <class R> struct Solver final : SolverBase {
     for (int p = 0; p < P; ++p)
       for (int i = ps_row_begin[p]; i < ps_row_begin[p + 1]; ++i) owner[i] = p;
     ps_blk.assign(P, {});
-    first_cta.assign(H.nd3, -1);
-    for (int b = 0; b < H.nd3; ++b)
+    blk_ctas.assign(H.nd3, {});
+    for (int b = 0; b < H.nd3; ++b) {
       for (int e = H.sinc_off[b]; e < H.sinc_off[b + 1]; ++e) {
         const int p = owner[H.sinc_ent[e] >> 2];
         if (ps_blk[p].empty() || ps_blk[p].back() != b) ps_blk[p].push_back(b);
-        if (first_cta[b] < 0 || p < first_cta[b]) first_cta[b] = p;
+        blk_ctas[b].push_back(p);
       }
+      std::sort(blk_ctas[b].begin(), blk_ctas[b].end());
+      blk_ctas[b].erase(std::unique(blk_ctas[b].begin(), blk_ctas[b].end()), blk_ctas[b].end());
+    }
   }
+  DBuf ptime;  // NSD_PHASE_TIMING: CTA 0's clock64 cycles per partitioned-PCR phase
+  long n_steps = 0;
   ~Solver() override {
+    if (ptime.p && n_steps > 0) {  // diagnostics: cycles per phase, summed over the solver's steps
+      unsigned long long h[16] = {};
+      if (cudaMemcpy(h, ptime.p, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess) {
+        static const char* names[] = {"trial pass", "scatter", "reduce+gather", "row pass", "reduce"};
+        std::fprintf(stderr, "nsd_step phase cycles (CTA 0, thread 0, %ld steps):", n_steps);
+        for (int k = 0; k < 5; ++k) std::fprintf(stderr, " %s %llu", names[k], h[k]);
+        std::fprintf(stderr, "\n");
+        static const char* rn[] = {"local sums + partial store", "arrival atomic", "spin", "partial sums (+side)", "tail"};
+        std::fprintf(stderr, "nsd_step grid reductions (CTA 0, thread 0, all launches' reductions and syncs):");
+        for (int k = 1; k < 6; ++k) std::fprintf(stderr, " %s %llu", rn[k - 1], h[8 + k]);
+        std::fprintf(stderr, "\n");
+        std::vector<unsigned long long> pc(2 * (size_t)grid_blocks);
+        if (cudaMemcpy(pc.data(), static_cast<unsigned long long*>(ptime.p) + 16, pc.size() * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost) == cudaSuccess) {
+          for (int k = 0; k < 2; ++k) {
+            unsigned long long mn = ~0ull, mx = 0, sum = 0;
+            int amx = 0;
+            for (int b = 0; b < grid_blocks; ++b) {
+              const unsigned long long v = pc[2 * b + k];
+              mn = std::min(mn, v);
+              if (v > mx) { mx = v; amx = b; }
+              sum += v;
+            }
+            std::fprintf(stderr, "nsd_step per-CTA %s cycles: min %llu mean %llu max %llu (CTA %d)\n",
+                         k ? "reduction" : "compute", mn, sum / grid_blocks, mx, amx);
+          }
+        }
+      }
+    }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -509,26 +543,31 @@ template <class R> struct Solver final : SolverBase {
         if (b4[s] >= 0) cnt[b4[s] + 1]++;
     }
     for (int b = 0; b < H.nd3; ++b) cnt[b + 1] += cnt[b];
-    // ---- partitioned grid PCR plan (nsd_part.cuh): the CTA of each contact is the
-    // lowest CTA whose static rows touch one of its blocks (else contact % P); its three
-    // rows follow the CTA's static rows; local blocks = static blocks + contact blocks;
-    // per dof3 block the flat local-block indices of all CTAs touching it, CTA order.
+    // ---- partitioned grid PCR plan (nsd_part.cuh): each contact goes to the least
+    // loaded (fewest rows so far; ties: lowest) CTA among those whose static rows touch
+    // one of its blocks (else the least loaded CTA), so its blocks stay local there
+    // and ground-contact CTAs do not pile up rows; its three rows follow the CTA's
+    // static rows; local blocks = static blocks + contact blocks; per dof3 block the
+    // flat local-block indices of all CTAs touching it, CTA order.
     std::vector<int> p_row_off, p_rows, p_lb_off, p_lb_blk, p_gb_off, p_gb_ent;
     int p_mr = 0, p_ml = 0, p_mx = 0;
     size_t p_smem = 0;
     bool use_part = false;
     if (use_grid && cfg.linear_method == 3 && part_enabled()) {
       const int P = grid_blocks;
-      std::vector<int> cstart(P + 1, 0), cown(nc), clist(nc);
+      std::vector<int> cstart(P + 1, 0), cown(nc), clist(nc), load(P);
+      for (int p = 0; p < P; ++p) load[p] = ps_row_begin[p + 1] - ps_row_begin[p];
       for (int c = 0; c < nc; ++c) {
         const int* b4 = &b4all[4 * c];
         int o = -1;
-        for (int s : {0, 2, 1, 3})
-          if (b4[s] >= 0 && first_cta[b4[s]] >= 0) {
-            o = first_cta[b4[s]];
-            break;
-          }
-        cown[c] = o >= 0 ? o : c % P;
+        for (int s = 0; s < 4; ++s)
+          if (b4[s] >= 0)
+            for (int p : blk_ctas[b4[s]])
+              if (o < 0 || load[p] < load[o] || (load[p] == load[o] && p < o)) o = p;
+        if (o < 0)
+          o = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+        cown[c] = o;
+        load[o] += 3;
         cstart[cown[c] + 1]++;
       }
       for (int p = 0; p < P; ++p) cstart[p + 1] += cstart[p];
@@ -658,6 +697,14 @@ template <class R> struct Solver final : SolverBase {
     so.fin = reinterpret_cast<double*>(ob + o_fin);
     so.dec = out->decisions ? reinterpret_cast<unsigned char*>(ob + o_dec) : nullptr;
     so.dec_stride = dec_stride;
+    if (std::getenv("NSD_PHASE_TIMING") && use_grid) {
+      if (!ptime.p) {
+        ptime.alloc(sizeof(unsigned long long) * (16 + 2 * (size_t)grid_blocks));
+        NSD_CK(cudaMemset(ptime.p, 0, sizeof(unsigned long long) * (16 + 2 * (size_t)grid_blocks)));
+      }
+      so.ptime = ptime.as<unsigned long long>();
+    }
+    ++n_steps;
     nsd::Work<R> W = plan.bind<R>(hr, hi, cr, ci);
     // inputs in place in the upload buffer; q, u, lambda in the output buffer (one D2H)
     W.q0 = dr;

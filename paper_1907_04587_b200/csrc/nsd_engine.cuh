@@ -1470,6 +1470,9 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
         // with every CTA's rows, coefficients and local dof3 blocks in shared memory
         // and only the shared blocks' J^T partials exchanged through global memory.
         part_load<R, kTets>(T, W, PV);
+        PhaseClock pcl(out.ptime, blockIdx.x == 0 && threadIdx.x == 0);  // NSD_PHASE_TIMING diagnostics
+        // per CTA: [compute, reduction incl. waiting] cycles (load-balance diagnostics)
+        PhaseClock pcb(out.ptime ? out.ptime + 16 + 2 * blockIdx.x : nullptr, threadIdx.x == 0);
         const int td = kTets ? T.tdim : 0;
         const int tid = threadIdx.x, ntd = blockDim.x;
         R *xs = PV.x, *rs = PV.r, *zs = PV.z, *zns = PV.zn, *xns = PV.xn, *rns = PV.rn;
@@ -1519,11 +1522,14 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
             pn2 += (double)rv * (double)(PV.inv[li] * rv);
             rn2 += (double)rv * rv;
           }
+          pcl.mark(0);
           const bool pull = fabs(zaz) >= 1e-300;  // w = H^-1 J^T z'
           if (pull) {
             __syncthreads();
             part_scatter(W, PV, zns);
           }
+          pcl.mark(1);
+          pcb.mark(0);
           {
             double s[2] = {pn2, rn2};
             t.reduce_sum_side(s, [&](int first, int n) {
@@ -1532,6 +1538,8 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
             pn2 = s[0];
             rn2 = s[1];
           }
+          pcl.mark(2);
+          pcb.mark(1);
           const double pn = sqrt(pn2);
           if (pn > phist_last) {  // monotone guard
             mono = 1;
@@ -1571,12 +1579,16 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
             bb += (double)apv * (double)(PV.inv[li] * apv);
           }
           {
+            pcl.mark(3);
+            pcb.mark(0);
             double s[4] = {za, aa, ab, bb};
             t.reduce_sum(s);
             beta = s[0] / zaz;
             zaz = s[0];
             den_next = s[1] + 2.0 * beta * s[2] + beta * beta * s[3];
           }
+          pcl.mark(4);
+          pcb.mark(1);
         }
         for (int li = tid; li < PV.nrow; li += ntd) W.bx[PV.gid[li]] = PV.bx[li];
       } else if constexpr (RPT > 0) {

@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(kGridThreads) k_single_grid(nsd::Topo<R> T, ns
                                                      double* gpart) {
   __shared__ double red[2 * 33 * nsd::kRedMax];
   nsd::GridTeam t(red, gpart);
+  if (out.ptime) t.prof = out.ptime + 8;
   nsd::newton_setup(t, T, W);
   t.sync();
   nsd::newton_solve<R, kTets, nsd::GridTeam, RPT>(t, T, W, cfg, out);

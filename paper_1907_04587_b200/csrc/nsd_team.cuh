@@ -149,108 +149,74 @@ struct BlockTeam {
   }
 };
 
-// Grid team: one cooperative launch, one CTA per SM (<= 320 CTAs). Every CTA
-// sums all CTAs' partials itself, in CTA order, with the same code in every CTA —
-// so every member gets the identical bits (deterministic, team-uniform branches).
-//
-// Arrival is flag-in-data (NSD_GRID_LL, default): a CTA publishes each partial as
-// one 16-byte store of two 8-byte words, (epoch << 32 | low 32 bits) and
-// (epoch << 32 | high 32 bits), after a release fence. Readers poll the words of
-// all CTAs until every word carries the current epoch; the data arrive with the
-// flags, so one L2 round trip after the last writer ends the reduction. There is
-// no arrival counter: no 148-way atomic serialisation at one L2 slice and no
-// separate read of the partials after the count completes. Each 8-byte word is
-// single-copy atomic, so a word with the current epoch holds the current bits.
-// Plain barriers (sync) publish one epoch word per CTA; warp 0 polls all of them.
-//   Partials are double-buffered by parity. A CTA can write reduction n + 2's
-// words (same parity as n) only after passing reduction n + 1, which every CTA
-// reaches only after it finished reading reduction n's words; stale words carry
-// older epochs and are never accepted. Epochs restart at 1 every launch: the host
-// zeroes the flag words before each launch (grid_scratch_reset).
-//   NSD_GRID_LL=0 builds the previous scheme (one acq_rel arrival on a monotonic
-// count, then the value-major partials are read): C2 8.9 us per CR iteration.
+// Grid team: one cooperative launch, one CTA per SM (<= 320 CTAs). Barrier: every
+// CTA arrives on a global count that only grows within a launch and spins until it
+// reaches this barrier's target. All-reduce: each CTA publishes its partials, passes
+// the barrier, then sums every CTA's partials itself, in CTA order, with the same
+// code in every CTA — so every member gets the identical bits (deterministic,
+// team-uniform branches). Partials are stored value-major (one value's partials of
+// all CTAs contiguous: 37 sectors per value for 148 CTAs), double-buffered by parity.
 // Measured history (C2 FEM): CG grid sync + value-by-value re-read
-// 18.0 ms/step; "last CTA reduces and releases a generation flag" 11.1 ms; count
-// + every CTA reduces 8.0 ms; partitioned PCR 5.4 ms.
-#ifndef NSD_GRID_LL
-#define NSD_GRID_LL 0
-#endif
+// 18.0 ms/step; "last CTA reduces and releases a generation flag" 11.1 ms; this
+// scheme 8.0 ms (two L2 round trips fewer per reduction); partitioned PCR 5.0 ms.
+// Tried and slower (profiles/r2_grid_barrier_ab.txt): flag-in-data partials (each
+// partial carries its epoch, no count; every CTA polling every CTA's words hammers
+// the same L2 lines: 15.4 vs 9.0 us per CR iteration), and 16 arrival counts 1 KB
+// apart polled by the lanes of warp 0 with one acquire fence (6.0 vs 5.0 ms/step).
+// The partitioned PCR also tried ONE grid reduction per CR iteration, with the
+// shared blocks' partials exchanged point to point (release flag per CTA, acquire
+// polls of the neighbour CTAs only): 5.5 vs 5.0 ms/step — a neighbour handshake
+// costs as much as the grid barrier (release, flag, poll and acquire are ~3 L2
+// round trips either way; measured ~4,600 cycles per grid reduction on C2 with the
+// CTAs' compute balanced to 4 %).
+// Double buffering suffices: a CTA can write reduction n + 2's partials (same
+// parity as n) only after passing reduction n + 1's barrier, which every CTA
+// reaches only after it finished reading reduction n's partials.
 constexpr int kGridMaxCtas = 320;
-// Global scratch (doubles): [2 x nb x kRedMax partials][2 x kRedMax unused][count, unused]
-// then, 16-byte aligned, the flag-in-data words [2 parity][kRedMax][nb][2] and the
-// barrier words [nb].
+// Global scratch (doubles): [2 x nb x kRedMax partials][2 x kRedMax unused][count, unused].
 __host__ __device__ constexpr size_t grid_scratch_count_off(int nb) { return 2 * (size_t)nb * kRedMax + 2 * kRedMax; }
-__host__ __device__ constexpr size_t grid_scratch_ll_off(int nb) { return (grid_scratch_count_off(nb) + 2 + 1) & ~size_t(1); }
-__host__ __device__ constexpr size_t grid_scratch_doubles(int nb) {
-  return grid_scratch_ll_off(nb) + 4 * (size_t)kRedMax * nb + nb;
-}
-// what the host zeroes before every launch: [count .. end)
+__host__ __device__ constexpr size_t grid_scratch_doubles(int nb) { return grid_scratch_count_off(nb) + 2; }
+// what the host zeroes before every launch: the count
 __host__ __device__ constexpr size_t grid_scratch_reset_off(int nb) { return grid_scratch_count_off(nb); }
-
-__device__ __forceinline__ void ll_fence() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-__device__ __forceinline__ void ll_put(unsigned long long* p, double v, unsigned e) {
-  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
-  const unsigned long long hi = static_cast<unsigned long long>(e) << 32;
-  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(hi | (b & 0xffffffffull)), "l"(hi | (b >> 32))
-               : "memory");
-}
-__device__ __forceinline__ void ll_get(const unsigned long long* p, unsigned long long& w0, unsigned long long& w1) {
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
-}
 
 struct GridTeam {
   double* red;    // shared: 2 * (33 * kRedMax)
   double* gpart;  // global partials
   unsigned* bar;  // [0] arrival count
-  unsigned long long* ll;     // flag-in-data partials [2][kRedMax][nb][2]
-  unsigned long long* lflag;  // barrier words [nb]
   int parity;
   unsigned epoch;
+  // NSD_PHASE_TIMING diagnostics: CTA 0 thread 0's cycles per reduction stage
+  // (local sums, partial store, arrival atomic, spin, partial sums, tail), or null
+  unsigned long long* prof = nullptr;
+  long long pt = 0;
+  __device__ __forceinline__ void pmark(int k) {
+    if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
+      const long long t = clock64();
+      if (k >= 0) prof[k] += static_cast<unsigned long long>(t - pt);
+      pt = t;
+    }
+  }
   __device__ GridTeam(double* smem_red, double* global_part)
       : red(smem_red), gpart(global_part),
-        bar(reinterpret_cast<unsigned*>(global_part + grid_scratch_count_off(gridDim.x))),
-        ll(reinterpret_cast<unsigned long long*>(global_part + grid_scratch_ll_off(gridDim.x))),
-        lflag(ll + 4 * (size_t)kRedMax * gridDim.x), parity(0), epoch(0) {}
+        bar(reinterpret_cast<unsigned*>(global_part + grid_scratch_count_off(gridDim.x))), parity(0), epoch(0) {}
   __device__ __forceinline__ int rank() const { return blockIdx.x * blockDim.x + threadIdx.x; }
   __device__ __forceinline__ int size() const { return gridDim.x * blockDim.x; }
   static __device__ __forceinline__ int part_idx(int b, int k) { return k * gridDim.x + b; }
 
-  // Arrive and wait for every CTA. The release (fence + flag store by thread 0 after
-  // the __syncthreads) publishes the CTA's writes; warp 0's acquire (fence after
-  // the polls) sees every other CTA's, and the closing __syncthreads extends that
-  // to the whole CTA. CTAs already past this barrier may publish the next epoch
-  // before a slow poller reads the word, hence the signed-distance test.
+  // Arrive and wait for every CTA. Thread 0's acq_rel atomic publishes the CTA's
+  // writes (ordered before it by the __syncthreads) and its acquire loads see
+  // every other CTA's; the closing __syncthreads extends that to the whole CTA.
+  // CTAs already past this barrier may arrive at the next one before a slow
+  // spinner reads the count, hence the signed-distance test.
   __device__ __forceinline__ void sync() {
     __syncthreads();
     ++epoch;
-#if NSD_GRID_LL
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x, nb = gridDim.x;
-      if (lane == 0) {
-        ll_fence();
-        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(lflag + blockIdx.x),
-                     "l"(static_cast<unsigned long long>(epoch))
-                     : "memory");
-      }
-      bool ok;
-      do {
-        ok = true;
-#pragma unroll
-        for (int u = 0; u < kGridMaxCtas / 32; ++u) {
-          const int b = lane + 32 * u;
-          if (b < nb) {
-            unsigned long long f;
-            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(lflag + b) : "memory");
-            ok &= static_cast<int>(static_cast<unsigned>(f) - epoch) >= 0;
-          }
-        }
-      } while (!__all_sync(0xffffffffu, ok));
-      ll_fence();
-    }
-#else
     if (threadIdx.x == 0) {
+      const bool timed = pt != 0;  // inside a reduction (plain barriers are not profiled)
+      if (timed) pmark(1);
       unsigned prev;
       asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(bar) : "memory");
+      if (timed) pmark(2);
       const unsigned target = epoch * gridDim.x;
       if (prev + 1u != target) {
         unsigned c;
@@ -258,8 +224,8 @@ struct GridTeam {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(bar) : "memory");
         } while (static_cast<int>(c - target) < 0);
       }
+      if (timed) pmark(3);
     }
-#endif
     __syncthreads();
   }
   template <int NS> __device__ __forceinline__ void reduce_sum(double (&s)[NS]) {
@@ -284,6 +250,7 @@ struct GridTeam {
   __device__ __forceinline__ void red_impl(double* s, double* m, F&& side) {
     constexpr int K = NS + NM;
     static_assert(K <= kRedMax && K > 0, "1..kRedMax values per reduction");
+    pmark(-1);
     double* buf = red + parity * (33 * kRedMax);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
@@ -298,58 +265,6 @@ struct GridTeam {
     }
     __syncthreads();
     const int nb = gridDim.x;
-#if NSD_GRID_LL
-    ++epoch;
-    unsigned long long* lp = ll + (size_t)parity * kRedMax * nb * 2;
-    parity ^= 1;
-    if (warp == 0) {  // CTA partials, published with the epoch after a release fence
-      double v[K > 0 ? K : 1];
-#pragma unroll
-      for (int k = 0; k < NS; ++k) v[k] = warp_sum_down(lane < nw ? buf[lane * kRedMax + k] : 0.0);
-#pragma unroll
-      for (int k = 0; k < NM; ++k) v[NS + k] = warp_max_down(lane < nw ? buf[lane * kRedMax + NS + k] : -__builtin_huge_val());
-      if (lane == 0) {
-        ll_fence();
-#pragma unroll
-        for (int k = 0; k < K; ++k) ll_put(lp + 2 * ((size_t)k * nb + blockIdx.x), v[k], epoch);
-      }
-    }
-    // warps < K poll (and then sum) value k of every CTA; the side warps wait on
-    // named barrier 1 for warp 0's acquire
-    constexpr int kU = kGridMaxCtas / 32;
-    if (warp < K) {
-      const int k = warp;
-      const bool is_sum = k < NS;
-      const unsigned long long* src = lp + 2 * (size_t)k * nb;
-      double part[kU];
-      bool ok;
-      do {
-        ok = true;
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const int b = lane + 32 * u;
-          if (b < nb) {
-            unsigned long long w0, w1;
-            ll_get(src + 2 * b, w0, w1);
-            ok &= (static_cast<unsigned>(w0 >> 32) == epoch) & (static_cast<unsigned>(w1 >> 32) == epoch);
-            part[u] = __longlong_as_double(static_cast<long long>((w1 << 32) | (w0 & 0xffffffffull)));
-          } else {
-            part[u] = is_sum ? 0.0 : -__builtin_huge_val();
-          }
-        }
-      } while (!__all_sync(0xffffffffu, ok));
-      ll_fence();
-      if (warp == 0 && nw > K) asm volatile("bar.arrive 1, %0;" ::"r"(32 * (nw - K + 1)) : "memory");
-      double acc = is_sum ? 0.0 : -__builtin_huge_val();
-#pragma unroll
-      for (int u = 0; u < kU; ++u) acc = is_sum ? acc + part[u] : fmax(acc, part[u]);
-      acc = is_sum ? warp_sum_down(acc) : warp_max_down(acc);
-      if (lane == 0) buf[32 * kRedMax + k] = acc;
-    } else {
-      asm volatile("bar.sync 1, %0;" ::"r"(32 * (nw - K + 1)) : "memory");
-      side(threadIdx.x - 32 * K, static_cast<int>(blockDim.x) - 32 * K);
-    }
-#else
     double* gp = gpart + parity * (nb * kRedMax);
     parity ^= 1;
     if (warp == 0) {  // CTA partials
@@ -383,8 +298,10 @@ struct GridTeam {
       acc = is_sum ? warp_sum_down(acc) : warp_max_down(acc);
       if (lane == 0) buf[32 * kRedMax + k] = acc;
     }
-#endif
+    pmark(4);
     __syncthreads();
+    pmark(5);
+    pt = 0;
 #pragma unroll
     for (int k = 0; k < NS; ++k) s[k] = buf[32 * kRedMax + k];
 #pragma unroll
