@@ -197,6 +197,10 @@ struct PhaseClock {
   }
 };
 
+struct NoClock {
+  __device__ __forceinline__ void mark(int) const {}
+};
+
 // ------------------------------------------------------------------ helpers
 template <class R> __device__ __forceinline__ V3<R> ld3(const R* p) { return v3(p[0], p[1], p[2]); }
 template <class R> __device__ __forceinline__ void st3(R* p, V3<R> v) {
@@ -1470,9 +1474,13 @@ __device__ int newton_solve(Team& t, const Topo<R>& T, Work<R>& W, const Cfg& cf
         // with every CTA's rows, coefficients and local dof3 blocks in shared memory
         // and only the shared blocks' J^T partials exchanged through global memory.
         part_load<R, kTets>(T, W, PV);
-        PhaseClock pcl(out.ptime, blockIdx.x == 0 && threadIdx.x == 0);  // NSD_PHASE_TIMING diagnostics
+#ifdef NSD_PROFILE_GRID  // NSD_PHASE_TIMING diagnostics (a -DNSD_PROFILE_GRID build; they cost registers)
+        PhaseClock pcl(out.ptime, blockIdx.x == 0 && threadIdx.x == 0);
         // per CTA: [compute, reduction incl. waiting] cycles (load-balance diagnostics)
         PhaseClock pcb(out.ptime ? out.ptime + 16 + 2 * blockIdx.x : nullptr, threadIdx.x == 0);
+#else
+        NoClock pcl, pcb;
+#endif
         const int td = kTets ? T.tdim : 0;
         const int tid = threadIdx.x, ntd = blockDim.x;
         R *xs = PV.x, *rs = PV.r, *zs = PV.z, *zns = PV.zn, *xns = PV.xn, *rns = PV.rn;

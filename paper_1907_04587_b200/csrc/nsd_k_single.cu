@@ -19,7 +19,9 @@ __global__ void __launch_bounds__(kGridThreads) k_single_grid(nsd::Topo<R> T, ns
                                                      double* gpart) {
   __shared__ double red[2 * 33 * nsd::kRedMax];
   nsd::GridTeam t(red, gpart);
+#ifdef NSD_PROFILE_GRID
   if (out.ptime) t.prof = out.ptime + 8;
+#endif
   nsd::newton_setup(t, T, W);
   t.sync();
   nsd::newton_solve<R, kTets, nsd::GridTeam, RPT>(t, T, W, cfg, out);

@@ -190,11 +190,15 @@ struct GridTeam {
   unsigned long long* prof = nullptr;
   long long pt = 0;
   __device__ __forceinline__ void pmark(int k) {
+#ifdef NSD_PROFILE_GRID  // compile-time: the counters' register and branch cost is not free in the PCR loop
     if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
       const long long t = clock64();
       if (k >= 0) prof[k] += static_cast<unsigned long long>(t - pt);
       pt = t;
     }
+#else
+    (void)k;
+#endif
   }
   __device__ GridTeam(double* smem_red, double* global_part)
       : red(smem_red), gpart(global_part),
@@ -301,7 +305,9 @@ struct GridTeam {
     pmark(4);
     __syncthreads();
     pmark(5);
+#ifdef NSD_PROFILE_GRID
     pt = 0;
+#endif
 #pragma unroll
     for (int k = 0; k < NS; ++k) s[k] = buf[32 * kRedMax + k];
 #pragma unroll

@@ -17,7 +17,7 @@ for pass in 1 2; do
   cp /tmp/default.so $L; echo "default $(run)"
   for v in $(ls -d tools/_var*/ 2>/dev/null); do cp $v/libnsdyn_b200.so $L; echo "$v $(run)"; done
 done
-for v in $(ls -d tools/_var*/ 2>/dev/null); do
+[ "${AB_TESTS:-1}" = 1 ] && for v in $(ls -d tools/_var*/ 2>/dev/null); do
   cp $v/libnsdyn_b200.so $L
   echo "$v tests: $(timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_world.py -m gpu -q -x 2>&1 | tail -1)"
 done
