@@ -52,7 +52,7 @@ typedef struct nsd_config {
   int32_t preconditioner;        /* 0 None, 1 Diagonal (default) */
   double newton_tolerance;       /* convergence classification only, default 1e-6 */
   int32_t line_search;           /* merit backtracking, frictionless scenes only */
-  int32_t precision;             /* NSD_FP32 (performance) or NSD_FP64 (parity) */
+  int32_t precision;             /* NSD_FP64, or NSD_FP32: mixed mode (fp64 state and arithmetic, fp32 operator coefficients) */
 } nsd_config;
 
 /* Fills the reference defaults (newton.h:12-23) with the given precision. */

@@ -18,13 +18,16 @@ def main(path, command):
     for r in rows[1:]:
         agg.setdefault(r[ki], []).append(float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0))
     total = sum(sum(v) for v in agg.values())
-    step = sum(sum(v) for k, v in agg.items() if "k_batch_sub" in k)
+    ours = {k: sum(v) for k, v in agg.items() if "nsdi::" in k or "nsd::" in k or k.startswith("void k_")}
+    step = sum(ours.values())
     print(f"# ncu --metrics gpu__time_duration.sum --clock-control none -c 400: {command}")
     print("# per-launch times are cold-cache and serialised; the shares, not the absolutes, compare with bench.py")
     print("launches  mean_us  total_us  kernel")
     for k, v in agg.items():
         print(f"{len(v):8d} {sum(v) / len(v):8.1f} {sum(v):9.1f}  {k[:70]}")
-    print(f"# share of GPU time in k_batch_sub: {100 * step / total:.1f}% "
+    for k, t in ours.items():
+        print(f"# {k.split('(')[0][5:]}: {100 * t / step:.1f}% of the step's kernel time")
+    print(f"# share of GPU time in the library's kernels: {100 * step / total:.1f}% "
           "(the rest: the 256 MiB L2-flush memsets between timed steps, outside the timed events)")
 
 
