@@ -418,7 +418,7 @@ template <class R> struct Solver final : SolverBase {
       use_grid = true;
       int dev_sms = 0, per_sm = 0;
       NSD_CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
-      per_sm = single_grid_blocks_per_sm<R>(tets);
+      per_sm = std::min(s64::single_grid_blocks_per_sm<R>(tets), s32::single_grid_blocks_per_sm<R>(tets));
       if (per_sm < 1) throw NsdError(NSD_CUDA_ERROR, "grid kernel cannot be resident");
       const char* bps = std::getenv("NSD_GRID_BLOCKS_PER_SM");
       grid_blocks = std::min(nsd::kGridMaxCtas, dev_sms * std::min(per_sm, bps ? std::max(1, std::atoi(bps)) : 1));
@@ -736,7 +736,6 @@ template <class R> struct Solver final : SolverBase {
     W.lam = reinterpret_cast<R*>(ob + o_lam);
     W.h = R(in->h);
     for (int k = 0; k < 3; ++k) W.grav[k] = R(in->gravity[k]);
-    W.op32 = cfg.precision == NSD_FP32 ? 1 : 0;  // fp32 J/C coefficient storage (nsd_engine.cuh opg)
     W.nc = nc;
     W.nrows = nrows;
     W.normal_begin = H.rows_static;
@@ -745,7 +744,9 @@ template <class R> struct Solver final : SolverBase {
     phase.start(use_grid ? "nsd_step: newton_step (persistent cooperative grid)" : "nsd_step: newton_step (one CTA)");
     NSD_CK(cudaEventRecord(ev0, stream));
     if (!use_grid) {
-      NSD_CK(launch_single_block<R>(tets, block_threads, stream, topo.t, W, kc, so));
+      // fp32 mode: the kernels that store the J/C coefficients as float (nsd_k_single32.cu)
+      NSD_CK(cfg.precision == NSD_FP32 ? s32::launch_single_block<R>(tets, block_threads, stream, topo.t, W, kc, so)
+                                       : s64::launch_single_block<R>(tets, block_threads, stream, topo.t, W, kc, so));
     } else {
       double* gp = gpart.as<double>();
       NSD_CK(cudaMemsetAsync(gp + nsd::grid_scratch_reset_off(grid_blocks), 0,
@@ -754,8 +755,10 @@ template <class R> struct Solver final : SolverBase {
       // register-resident PCR rows when every thread owns <= 2 rows (NSD_GRID_REGS=0 disables)
       const bool regs = cfg.linear_method == 3 && nrows <= 2 * grid_blocks * kGridThreads && !(std::getenv("NSD_GRID_REGS") &&
                                                                        std::atoi(std::getenv("NSD_GRID_REGS")) == 0);
-      NSD_CK(launch_single_grid<R>(tets, use_part ? -1 : (regs ? 2 : 0), p_smem, grid_blocks, stream, topo.t, W, kc,
-                                   so, gp));
+      const int mode = use_part ? -1 : (regs ? 2 : 0);
+      NSD_CK(cfg.precision == NSD_FP32
+                 ? s32::launch_single_grid<R>(tets, mode, p_smem, grid_blocks, stream, topo.t, W, kc, so, gp)
+                 : s64::launch_single_grid<R>(tets, mode, p_smem, grid_blocks, stream, topo.t, W, kc, so, gp));
     }
     NSD_CK(cudaEventRecord(ev1, stream));
     phase.start("nsd_step: download (one D2H) + unpack");
@@ -1428,7 +1431,7 @@ int nsd_create(const nsd_topology* topo, const nsd_config* cfg, int32_t device, 
     auto* s = new nsd_solver();
     try {
       // one fp64 engine for both precisions: fp32 stores the operator's J/C
-      // coefficients in fp32 (Work::op32), state and arithmetic stay fp64
+      // coefficients in fp32 (NSD_OP32 kernels, nsd_k_single32.cu), state and arithmetic stay fp64
       s->impl.reset(new Solver<double>(*topo, *cfg, device));
     } catch (...) {
       delete s;

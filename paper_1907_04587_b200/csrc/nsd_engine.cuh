@@ -120,8 +120,7 @@ template <class R> struct Work {
   const int* cinc_ent;  // contact*4 + slot
   // rows
   int nrows, normal_begin, friction_begin;
-  R* coeff;  // 12 per static row
-  int op32;  // fp32 mode: coeff, ctet, cdir, carm hold floats (see opg/ops)
+  R* coeff;  // 12 per static row (floats in an NSD_OP32 TU, see opg/ops)
   int* blk;  // 4 per static row
   R* jstr;   // batched path: 24 per joint (structured rows, see assemble_joint) or null
   R* crec;   // batched path: 20 per contact (n d1 d2 r_a r_b dc act, 16-byte aligned) or null
@@ -209,14 +208,22 @@ template <class R> __device__ __forceinline__ void st3(R* p, V3<R> v) {
   p[2] = v.z;
 }
 // Operator coefficient arrays (coeff, ctet, cdir, carm): element i of array a, stored in
-// R, or — single-scene fp32 mode, W.op32 — as float in the same buffer. State, row
-// and dof vectors and all arithmetic stay in R (fp64): the fp32 mode halves the
-// operator's coefficient stream only (the batch warp solver's mixed mode likewise).
-template <class R> __device__ __forceinline__ R opg(const Work<R>& W, const R* a, size_t i) {
-  return W.op32 ? R(reinterpret_cast<const float*>(a)[i]) : a[i];
+// R, or — single-scene fp32 mode, a TU compiled with NSD_OP32=1 (nsd_k_single32.cu) —
+// as float in the same buffer. State, row and dof vectors and all arithmetic stay in
+// R (fp64): the fp32 mode halves the operator's coefficient stream only (the batch
+// warp solver's mixed mode likewise). A compile-time choice: a run-time flag cost
+// 16 % on C1 (both load paths in every coefficient access).
+#ifndef NSD_OP32
+#define NSD_OP32 0
+#endif
+template <class R> __device__ __forceinline__ R opg(const Work<R>&, const R* a, size_t i) {
+  if constexpr (NSD_OP32 != 0)
+    return R(reinterpret_cast<const float*>(a)[i]);
+  else
+    return a[i];
 }
-template <class R> __device__ __forceinline__ void ops(const Work<R>& W, R* a, size_t i, R v) {
-  if (W.op32)
+template <class R> __device__ __forceinline__ void ops(const Work<R>&, R* a, size_t i, R v) {
+  if constexpr (NSD_OP32 != 0)
     reinterpret_cast<float*>(a)[i] = static_cast<float>(v);
   else
     a[i] = v;

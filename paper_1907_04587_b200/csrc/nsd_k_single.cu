@@ -1,9 +1,21 @@
 // Single-scene kernels (nsd_step, the newton_step boundary): one CTA for small
-// scenes, a persistent cooperative grid for the FEM configs.
+// scenes, a persistent cooperative grid for the FEM configs. Compiled twice: this
+// TU (fp64 J/C coefficients, namespace nsdi::s64) and nsd_k_single32.cu (NSD_OP32=1:
+// the fp32 mode's float coefficients, namespace nsdi::s32).
+#ifndef NSD_OP32
+#define NSD_OP32 0
+#endif
 #define NSD_ASM_NOINLINE 1
 #include "nsd_plan.cuh"
 
-using namespace nsdi;
+#if NSD_OP32
+#define NSD_SINGLE_NS s32
+#else
+#define NSD_SINGLE_NS s64
+#endif
+
+namespace nsdi {
+namespace NSD_SINGLE_NS {
 
 template <class R, bool kTets>
 __global__ void __launch_bounds__(512) k_single_block(nsd::Topo<R> T, nsd::Work<R> W, nsd::Cfg cfg, nsd::StepOut out) {
@@ -26,9 +38,6 @@ __global__ void __launch_bounds__(kGridThreads) k_single_grid(nsd::Topo<R> T, ns
   t.sync();
   nsd::newton_solve<R, kTets, nsd::GridTeam, RPT>(t, T, W, cfg, out);
 }
-
-
-namespace nsdi {
 
 template <class R> int single_grid_blocks_per_sm(bool tets) {
   int per_sm = 0;
@@ -74,13 +83,11 @@ cudaError_t launch_single_grid(bool tets, int mode, size_t smem, int blocks, cud
   return cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kGridThreads), args, smem, s);
 }
 
-#define NSD_INST(R)                                                                                                \
-  template int single_grid_blocks_per_sm<R>(bool);                                                                 \
-  template cudaError_t launch_single_block<R>(bool, int, cudaStream_t, const nsd::Topo<R>&, const nsd::Work<R>&,   \
-                                              const nsd::Cfg&, const nsd::StepOut&);                               \
-  template cudaError_t launch_single_grid<R>(bool, int, size_t, int, cudaStream_t, const nsd::Topo<R>&,          \
-                                             const nsd::Work<R>&, const nsd::Cfg&, const nsd::StepOut&, double*);
-NSD_INST(double)
-#undef NSD_INST
+template int single_grid_blocks_per_sm<double>(bool);
+template cudaError_t launch_single_block<double>(bool, int, cudaStream_t, const nsd::Topo<double>&,
+                                                 const nsd::Work<double>&, const nsd::Cfg&, const nsd::StepOut&);
+template cudaError_t launch_single_grid<double>(bool, int, size_t, int, cudaStream_t, const nsd::Topo<double>&,
+                                                const nsd::Work<double>&, const nsd::Cfg&, const nsd::StepOut&, double*);
 
+}  // namespace NSD_SINGLE_NS
 }  // namespace nsdi

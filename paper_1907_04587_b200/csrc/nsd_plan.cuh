@@ -132,7 +132,6 @@ struct WorkPlan {
     W.iw6 = cr + iw6;
     W.iwi6 = hr + iwi6;
     W.coeff = hr + coeff;
-    W.op32 = 0;
     W.hv = hr + hv;
     W.cd = hr + cd;
     W.lam = hr + lam;
@@ -253,14 +252,24 @@ template <class R> __host__ __device__ inline int row_pool_elems(int rows_static
 }
 
 
-// ---- launch wrappers (defined with their kernels; instantiated for float and double)
-template <class R> int single_grid_blocks_per_sm(bool tets);
-template <class R>
-cudaError_t launch_single_block(bool tets, int threads, cudaStream_t s, const nsd::Topo<R>& T, const nsd::Work<R>& W,
-                                const nsd::Cfg& c, const nsd::StepOut& o);
-template <class R>
-cudaError_t launch_single_grid(bool tets, int mode, size_t smem, int blocks, cudaStream_t s, const nsd::Topo<R>& T,
-                               const nsd::Work<R>& W, const nsd::Cfg& c, const nsd::StepOut& o, double* gpart);
+// ---- launch wrappers (defined with their kernels). Single scenes: s64 = fp64 J/C
+// coefficients (nsd_k_single.cu), s32 = the fp32 mode's float coefficients
+// (nsd_k_single32.cu, the same source compiled with NSD_OP32=1).
+#define NSD_SINGLE_DECL                                                                                            \
+  template <class R> int single_grid_blocks_per_sm(bool tets);                                                     \
+  template <class R>                                                                                               \
+  cudaError_t launch_single_block(bool tets, int threads, cudaStream_t s, const nsd::Topo<R>& T,                   \
+                                  const nsd::Work<R>& W, const nsd::Cfg& c, const nsd::StepOut& o);                \
+  template <class R>                                                                                               \
+  cudaError_t launch_single_grid(bool tets, int mode, size_t smem, int blocks, cudaStream_t s, const nsd::Topo<R>& T, \
+                                 const nsd::Work<R>& W, const nsd::Cfg& c, const nsd::StepOut& o, double* gpart);
+namespace s64 {
+NSD_SINGLE_DECL
+}
+namespace s32 {
+NSD_SINGLE_DECL
+}
+#undef NSD_SINGLE_DECL
 // k_batch_sub<R, 4/8/16/32> and k_batch_block<R> attributes (a negative value leaves one unset)
 template <class R> cudaError_t batch_sub_attrs(int max_dyn_smem, int carveout);
 template <class R> cudaError_t batch_block_attrs(int max_optin);

@@ -5,7 +5,7 @@ set -u
 L=paper_1907_04587_b200/_build/libnsdyn_b200.so
 cp $L /tmp/default.so
 run() {
-  for wl in c2 c4; do
+  for wl in ${AB_WORKLOADS:-c2 c4}; do
     python bench.py --workload $wl --steps 20 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c '
 import sys,json
 for l in sys.stdin:
