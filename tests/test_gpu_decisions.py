@@ -50,3 +50,17 @@ def test_decision_vectors_exercise_every_flag():
         seen[2] += int(np.any(gd[:, -1] == 0)) + int(np.any(gd[:, -1] == 2))
     assert seen[0] >= 2 and seen[1] >= 1 and seen[2] >= 1
 
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("warm", [0, 2])
+@pytest.mark.parametrize("name", ["c2", "c4"])
+def test_decision_vectors_full_fem_fp64(name, warm):
+    """Full-size FEM configs (C2 12^3 block, C4 hand + ball), one step from the oracle's
+    state after `warm` steps: every Newton iteration's contact / tet / dof decisions
+    and PCR exit reasons bit-equal."""
+    gd, od, dims = _compare(name, 0, warm)
+    mism = [int(np.count_nonzero(gd[i] != od[i])) for i in range(gd.shape[0])]
+    print(name, "decision mismatches per Newton iteration:", mism)
+    assert mism[0] == 0
+    assert sum(mism) == 0, mism
