@@ -580,15 +580,24 @@ double orc_c5_bench(int env0, int n_env, int n_warm, int n_steps, int actuated, 
 
 // The same C5 ants stepped n_steps times (actions as orc_c5_bench), returning each
 // env's final q, u (env-major) and contact count: bench.py's end-of-run parity sample.
+// perturb > 0: every initial coordinate is scaled by (1 + perturb * N(0, 1)) (seeded by
+// pseed and the env id) — the oracle's own sensitivity, for stated tolerances.
 int orc_c5_states(int env0, int n_env, int n_steps, int actuated, int threads, double* q_out, double* u_out,
-                  int* nc_out) {
+                  int* nc_out, double perturb, unsigned pseed) {
 #ifdef _OPENMP
   if (threads > 0) omp_set_num_threads(threads);
 #else
   (void)threads;
 #endif
   std::vector<World> worlds(n_env);
-  for (int e = 0; e < n_env; ++e) worlds[e] = build_world(build_c5_ant(static_cast<unsigned>(env0 + e)));
+  for (int e = 0; e < n_env; ++e) {
+    worlds[e] = build_world(build_c5_ant(static_cast<unsigned>(env0 + e)));
+    if (perturb > 0.0) {
+      std::mt19937_64 rng(pseed * 1000003ull + static_cast<unsigned>(env0 + e));
+      std::normal_distribution<double> nd(0.0, 1.0);
+      for (double& v : worlds[e].state.q) v *= 1.0 + perturb * nd(rng);
+    }
+  }
 #pragma omp parallel for schedule(dynamic, 1)
   for (int e = 0; e < n_env; ++e) {
     World& w = worlds[e];

@@ -488,13 +488,14 @@ def action_torque(env, step, joint):
     return lib().orc_action_torque(C.c_int(env), C.c_int(step), C.c_int(joint))
 
 
-def c5_states(env0, n_env, n_steps, ncoord, ndof, actuated=True, threads=0):
-    """Final (q, u, n_contacts) of C5 ants env0.. after n_steps oracle step_world calls."""
+def c5_states(env0, n_env, n_steps, ncoord, ndof, actuated=True, threads=0, perturb=0.0, pseed=0):
+    """Final (q, u, n_contacts) of C5 ants env0.. after n_steps oracle step_world calls
+    (perturb > 0: initial q scaled by 1 + perturb * N(0, 1), seeded by pseed)."""
     q = np.zeros((n_env, ncoord))
     u = np.zeros((n_env, ndof))
     nc = np.zeros(n_env, dtype=np.int32)
     lib().orc_c5_states(C.c_int(env0), C.c_int(n_env), C.c_int(n_steps), C.c_int(int(actuated)), C.c_int(threads),
-                        dp(q), dp(u), ip(nc))
+                        dp(q), dp(u), ip(nc), C.c_double(perturb), C.c_uint(pseed))
     return q, u, nc
 
 
