@@ -413,7 +413,7 @@ template <class R> struct Solver final : SolverBase {
     const size_t work = std::max<size_t>({(size_t)H.rows_static + 48, (size_t)H.nd3, (size_t)H.nb});
     if (work <= 1536) {  // small scenes: one CTA (block barriers); larger: cooperative grid
       use_grid = false;
-      block_threads = work <= 256 ? 128 : (work <= 1024 ? 256 : 512);
+      block_threads = work <= 256 ? 128 : 256;  // k_single_block's launch bound
     } else {
       use_grid = true;
       int dev_sms = 0, per_sm = 0;
