@@ -4,7 +4,7 @@ set -u
 L=paper_1907_04587_b200/_build/libnsdyn_b200.so
 cp $L /tmp/default.so
 run() {
-  python bench.py --steps 100 --warmup 5 --no-alt --no-scenes --no-cpu-baseline --no-parity-sample 2>/dev/null |
+  python bench.py --precision ${AB_PREC:-fp64} --steps 100 --warmup 5 --no-alt --no-scenes --no-cpu-baseline --no-parity-sample 2>/dev/null |
     python -c '
 import sys,json
 for l in sys.stdin:
