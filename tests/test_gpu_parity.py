@@ -34,7 +34,7 @@ RIGID = [("c1", 0, 0), ("c1", 0, 20), ("c3", 0, 0), ("c3", 0, 15), ("c5", 0, 0),
          ("bend_chain", 0, 0), ("bend_chain", 0, 12)]
 FEM = [("c2:6", 0, 0)]
 TOL64_RIGID = (1e-9, 1e-8, 1e-6)
-TOL64_FEM = (1e-6, 1e-4, 1e-2)
+TOL64_FEM = (1e-7, 1e-5, 1e-5)  # c2:6 at step 0, measured 1.7e-8 / 5.9e-7 / 1.1e-6
 
 
 def _errs(g, o):
@@ -98,21 +98,25 @@ def test_newton_step_fp32_rigid(name, seed, warm):
 
 @pytest.mark.parametrize("name,seed,warm", FEM)
 def test_newton_step_fp32_fem(name, seed, warm):
-    _check(name, seed, warm, "fp32", TOL64_FEM, False)
+    _check(name, seed, warm, "fp32", (1e-6, 1e-4, 1e-3), False)  # measured 1.9e-7 / 6.5e-6 / 2.2e-5
 
 
 @pytest.mark.slow
 def test_newton_step_full_fem_fp64():
-    _check("c2", 0, 0, "fp64", TOL64_FEM, True)
+    # full-size C2 (10,368 tets) at step 0: measured q 1.4e-8, u 4.8e-7, lambda 2.1e-5
+    _check("c2", 0, 0, "fp64", (1e-7, 1e-5, 1e-3), True)
 
 
 @pytest.mark.slow
 def test_newton_step_full_c4_fp64():
-    sq, su = oracle_self_divergence("c4", 0, 0)
-    case = oracle_case("c4", 0, 0)
-    g, o = run_gpu(case, "fp64"), run_oracle(case)
-    assert rel_err(g["q"], o["q"]) <= 10 * sq + 1e-8
-    assert rel_err(g["u"], o["u"], floor=1e-6) <= 10 * su + 1e-6
+    # full-size C4 (hand + 5,520-tet ball) at step 0: measured q 1.2e-14, u 3.2e-12, lambda 1.6e-14
+    _check("c4", 0, 0, "fp64", TOL64_RIGID, True)
+
+
+@pytest.mark.slow
+def test_newton_step_full_c4_fp32():
+    # fp32 mode at full-size C4 step 0: measured q 2.6e-8, u 7.3e-6, lambda 7.2e-9
+    _check("c4", 0, 0, "fp32", (1e-6, 1e-4, 1e-6), False)
 
 
 def test_report_fields_fp64():
