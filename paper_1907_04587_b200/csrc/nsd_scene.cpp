@@ -17,7 +17,11 @@
 #include <memory>
 #include <random>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
+#include <unistd.h>
 #include <sstream>
 #include <stdexcept>
 
@@ -826,32 +830,101 @@ int nsd_scene_detect(const nsd_scene* s, const double* q, const double* u, const
 
 namespace {
 
-// Runs work(0 .. nth-1): the calling thread takes index 0 and every index whose
-// thread could not be started. Each index is a fixed strided set of rows written
-// to its own slots, so the result does not depend on which thread ran it. All
-// started threads are joined before any exception propagates.
-template <class F> void run_strided(unsigned nth, F&& work) {
-  std::vector<std::thread> pool;
-  std::atomic<bool> failed{false};
-  auto guarded = [&](unsigned t) {
-    try {
-      work(t);
-    } catch (...) {
-      failed = true;
+// Persistent host workers for the threaded narrow phase: created once per process
+// (lazily, up to 7) and parked on a condition variable between World.step calls.
+// Creating and joining threads on every call cost more than the C3/C4 rows they ran.
+// The pool is per process: a forked child (whose copy has no threads behind it)
+// gets a fresh one. It is never destroyed; parked workers end with the process.
+class DetectPool {
+ public:
+  static DetectPool& get() {
+    static std::mutex gm;
+    static DetectPool* pool = nullptr;
+    static pid_t owner = 0;
+    std::lock_guard<std::mutex> g(gm);
+    if (!pool || owner != getpid()) {
+      pool = new DetectPool();  // a stale parent pool in a forked child is left untouched
+      owner = getpid();
     }
-  };
-  unsigned started = 1;
-  try {
-    for (unsigned t = 1; t < nth; ++t) {
-      pool.emplace_back(guarded, t);
-      started = t + 1;
-    }
-  } catch (...) {  // e.g. std::system_error under a pids limit: run the rest here
+    return *pool;
   }
-  guarded(0);
-  for (unsigned t = started; t < nth; ++t) guarded(t);
-  for (auto& th : pool) th.join();
-  if (failed) throw std::runtime_error("nsd_scene_detect: worker failed");
+  // Runs work(0 .. nth-1): the caller takes index 0 and every index without a worker.
+  // Each index is a fixed strided set of rows written to its own slots, so the result
+  // does not depend on which thread ran it. Returns false if any index threw.
+  bool run(unsigned nth, const std::function<void(unsigned)>& work) {
+    std::lock_guard<std::mutex> serial(run_mu_);  // one job at a time (several Worlds may call)
+    ensure(nth > 0 ? nth - 1 : 0);
+    const unsigned nw = std::min<unsigned>(static_cast<unsigned>(threads_.size()), nth > 0 ? nth - 1 : 0);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = &work;
+      njob_ = nw;
+      pending_ = nw;
+      failed_ = false;
+      ++generation_;
+    }
+    cv_.notify_all();
+    bool ok = true;
+    auto guarded = [&](unsigned t) {
+      try {
+        work(t);
+      } catch (...) {
+        ok = false;
+      }
+    };
+    guarded(0);
+    for (unsigned t = nw + 1; t < nth; ++t) guarded(t);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+    return ok && !failed_;
+  }
+ private:
+  void ensure(unsigned n) {
+    while (threads_.size() < n && threads_.size() < 7) {
+      const unsigned idx = static_cast<unsigned>(threads_.size()) + 1;  // work index this worker runs
+      try {
+        threads_.emplace_back([this, idx] { loop(idx); });
+      } catch (...) {  // e.g. std::system_error under a pids limit: the caller runs the rest
+        return;
+      }
+    }
+  }
+  void loop(unsigned idx) {
+    unsigned seen = 0;
+    for (;;) {
+      const std::function<void(unsigned)>* job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return generation_ != seen; });
+        seen = generation_;
+        if (idx > njob_) continue;  // not needed for this job
+        job = job_;
+      }
+      bool threw = false;
+      try {
+        (*job)(idx);
+      } catch (...) {
+        threw = true;
+      }
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (threw) failed_ = true;
+        if (--pending_ == 0) done_.notify_all();
+      }
+    }
+  }
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> threads_;
+  const std::function<void(unsigned)>* job_ = nullptr;
+  unsigned njob_ = 0, pending_ = 0, generation_ = 0;
+  bool failed_ = false;
+};
+
+template <class F> void run_strided(unsigned nth, F&& work) {
+  const std::function<void(unsigned)> fn = std::forward<F>(work);
+  if (!DetectPool::get().run(nth, fn)) throw std::runtime_error("nsd_scene_detect: worker failed");
 }
 
 }  // namespace
