@@ -1011,6 +1011,37 @@ static int scene_detect(const nsd_scene* s, const double* q, const double* u, co
   for (const auto& pr : w.particle_ranges)
     for (int b = pr.first; b < pr.first + pr.second; ++b) pbodies.push_back(b);
   const size_t nprow = pbodies.size();
+  // Conservative cull of particle-vs-box tests that cannot pass the predicted-gap
+  // rule (gap - thickness - h closing > margin): gap >= |x - c| - R (R the box's
+  // half-diagonal) and closing <= |u~_particle| + |v_box| + |w_box| R. Culled tests
+  // produce no candidate either way, so the contact set is unchanged bit for bit.
+  struct BoxBound {
+    V c;
+    double reach;  // R + thickness + h (|v| + |w| R) + margin, with slack
+  };
+  std::vector<BoxBound> bbound(ns);
+  for (size_t i = 0; i < ns; ++i) {
+    if (sh[i].kind != 2) continue;
+    const double R = std::sqrt(sh[i].he[0] * sh[i].he[0] + sh[i].he[1] * sh[i].he[1] + sh[i].he[2] * sh[i].he[2]);
+    const int b = sh[i].body;
+    V c = nsd::v3(0.0, 0.0, 0.0);
+    double vb = 0.0;
+    if (b >= 0) {
+      c = nsd::bv_pos(view, b);
+      const double* ub = ut.data() + w.dof_off[b];
+      vb = std::sqrt(ub[0] * ub[0] + ub[1] * ub[1] + ub[2] * ub[2]);
+      if (w.body_type[b] == 1) vb += std::sqrt(ub[3] * ub[3] + ub[4] * ub[4] + ub[5] * ub[5]) * R;
+    }
+    bbound[i] = {c, (R + sh[i].thick + h * vb + w.margin) * (1.0 + 1e-9) + 1e-12};
+  }
+  auto culled = [&](int body, size_t i) {
+    if (sh[i].kind != 2) return false;
+    const V x = nsd::bv_pos(view, body);
+    const double* up = ut.data() + w.dof_off[body];
+    const double reach = bbound[i].reach + h * std::sqrt(up[0] * up[0] + up[1] * up[1] + up[2] * up[2]) * (1.0 + 1e-9);
+    const V d = x - bbound[i].c;
+    return d.x * d.x + d.y * d.y + d.z * d.z > reach * reach;
+  };
   const unsigned pth = nprow * ns >= 4096 ? std::min<unsigned>(hw, 8u) : 1u;
   if (pth > 1) {
     std::vector<std::vector<nsd::CandD<double>>> rows(nprow);
@@ -1018,8 +1049,9 @@ static int scene_detect(const nsd_scene* s, const double* q, const double* u, co
       nsd::CandD<double> b4[4];
       double tth = 0.0, tmu = 0.0;
       for (size_t r = t; r < nprow; r += pth)
-        for (const auto& shape : sh) {
-          const int k = nsd::particle_shape_contact(view, pbodies[r], shape, h, w.margin, w.mu_default, 0.0, -1.0,
+        for (size_t i = 0; i < ns; ++i) {
+          if (culled(pbodies[r], i)) continue;
+          const int k = nsd::particle_shape_contact(view, pbodies[r], sh[i], h, w.margin, w.mu_default, 0.0, -1.0,
                                                     b4, &tth, &tmu);
           rows[r].insert(rows[r].end(), b4, b4 + k);
         }
@@ -1028,8 +1060,9 @@ static int scene_detect(const nsd_scene* s, const double* q, const double* u, co
     for (const auto& r : rows) cands.insert(cands.end(), r.begin(), r.end());
   } else {
     for (const int b : pbodies)
-      for (const auto& shape : sh) {
-        const int k = nsd::particle_shape_contact(view, b, shape, h, w.margin, w.mu_default, 0.0, -1.0, c4, &th, &mu);
+      for (size_t i = 0; i < ns; ++i) {
+        if (culled(b, i)) continue;
+        const int k = nsd::particle_shape_contact(view, b, sh[i], h, w.margin, w.mu_default, 0.0, -1.0, c4, &th, &mu);
         cands.insert(cands.end(), c4, c4 + k);
       }
   }

@@ -15,7 +15,8 @@ from oracle import oracle_py as O
 from tests.helpers import oracle_trajectory, rel_err
 
 DETECT_CASES = [("c1", 0, 0), ("c1", 0, 20), ("c5", 3, 12), ("c2:6", 0, 3), ("c4:6", 0, 4), ("box_pile", 1, 30),
-                ("arch", 0, 2), ("c3", 0, 5), ("heavy_stack", 0, 10), ("incline:35:0.5", 0, 5)]
+                ("arch", 0, 2), ("c3", 0, 5), ("heavy_stack", 0, 10), ("incline:35:0.5", 0, 5),
+                ("c4", 0, 3)]
 
 
 @pytest.mark.parametrize("name,seed,warm", DETECT_CASES)
