@@ -168,8 +168,10 @@ class NewtonSolver:
         return lib().nsd_last_step_ms(self._h)
 
     def newton_step(self, q, u, contacts=None, h=0.0083, gravity=(0.0, 0.0, -9.81), f_extra=None,
-                    joint_frame=None):
-        """newton_step (newton.cpp:321-418). contacts: (ib, db) arrays or (nsd_contact array, n)."""
+                    joint_frame=None, decisions=True):
+        """newton_step (newton.cpp:321-418). contacts: (ib, db) arrays or (nsd_contact array, n).
+        decisions: also return the per-iteration decision vectors (a diagnostic; World.step
+        skips them)."""
         T, cfg = self.topology, self.config
         q = np.ascontiguousarray(q, np.float64)
         u = np.ascontiguousarray(u, np.float64)
@@ -198,14 +200,14 @@ class NewtonSolver:
         hlen = np.zeros(max(N, 1), np.int32)
         tel = np.zeros(6 * max(nc, 1))
         dec_stride = nc + T.n_tets + T.num_dof + 1
-        dec = np.zeros(max(N, 1) * dec_stride, np.uint8)
+        dec = np.zeros(max(N, 1) * dec_stride if decisions else 1, np.uint8)
         cout = (nsd_contact * max(nc, 1))()
         so = nsd_step_out()
         so.q, so.u, so.lambda_ = _dp(qo), _dp(uo), _dp(lam)
         so.contacts = C.cast(cout, C.POINTER(nsd_contact))
         so.iters = C.cast(iters, C.POINTER(nsd_iter_stats))
         so.linear_history, so.linear_history_len, so.contact_telemetry = _dp(hist), _ip(hlen), _dp(tel)
-        so.decisions = dec.ctypes.data_as(C.POINTER(C.c_uint8))
+        so.decisions = dec.ctypes.data_as(C.POINTER(C.c_uint8)) if decisions else None
         rc = lib().nsd_step(self._h, C.byref(sin), C.byref(so))
         check(rc, allow_abort=True)
         n = so.n_iterations
@@ -216,7 +218,8 @@ class NewtonSolver:
                     final=np.array([so.final_residual_inf, so.final_comp_error, so.final_cone_violation,
                                     so.min_gap, so.min_diag_shift, so.aborted, so.converged]),
                     contacts=contacts_to_arrays(cout, nc), n_rows=so.n_rows, aborted=bool(so.aborted),
-                    ms=self.last_step_ms, decisions=dec.reshape(max(N, 1), dec_stride)[:n].copy())
+                    ms=self.last_step_ms,
+                    decisions=dec.reshape(max(N, 1), dec_stride)[:n].copy() if decisions else None)
 
 
 def _open_scene(name, seed, json_text):
@@ -348,7 +351,7 @@ class World:
             self.contacts = self.detect()
             self.report = self.solver.newton_step(self.q, self.u, self.contacts, h=self.h,
                                                   gravity=tuple(self.gravity), f_extra=self.f_extra,
-                                                  joint_frame=self.joint_frames())
+                                                  joint_frame=self.joint_frames(), decisions=False)
             self.q, self.u = self.report["q"], self.report["u"]
             self.contacts = self.report.get("contacts", self.contacts)
             self.time += self.h

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -37,15 +38,27 @@ struct Nvtx {
   Nvtx& operator=(const Nvtx&) = delete;
 };
 // Consecutive sub-ranges of one scope (each start() closes the previous one).
+// NVTX range per host phase of a step; with acc set (NSD_HOST_TIMING) it also sums
+// each phase's wall time (ms) into acc[k], k = the phase's ordinal.
 struct NvtxPhase {
   bool open = false;
+  double* acc = nullptr;
+  int k = -1;
+  std::chrono::steady_clock::time_point t0;
+  void stamp() {
+    if (acc && k >= 0) acc[k] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (acc) t0 = std::chrono::steady_clock::now();
+    ++k;
+  }
   void start(const char* name) {
     if (open) nvtxRangePop();
+    stamp();
     nvtxRangePushA(name);
     open = true;
   }
   ~NvtxPhase() {
     if (open) nvtxRangePop();
+    stamp();
   }
 };
 
@@ -468,7 +481,11 @@ template <class R> struct Solver final : SolverBase {
   }
   DBuf ptime;  // NSD_PHASE_TIMING: CTA 0's clock64 cycles per partitioned-PCR phase
   long n_steps = 0;
+  double host_ms[4] = {0, 0, 0, 0};  // NSD_HOST_TIMING: wall ms per nsd_step host phase
   ~Solver() override {
+    if (std::getenv("NSD_HOST_TIMING") && n_steps > 0)
+      std::fprintf(stderr, "nsd_step host wall ms per step: stage %.4f launch %.4f download+sync+unpack %.4f (%ld steps)\n",
+                   host_ms[0] / n_steps, host_ms[1] / n_steps, host_ms[2] / n_steps, n_steps);
     if (ptime.p && n_steps > 0) {  // diagnostics: cycles per phase, summed over the solver's steps
       unsigned long long h[16] = {};
       if (cudaMemcpy(h, ptime.p, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess) {
@@ -527,6 +544,7 @@ template <class R> struct Solver final : SolverBase {
     const int nrows = H.rows_static + 3 * nc;
     Nvtx range_step("nsd_step");
     NvtxPhase phase;
+    if (std::getenv("NSD_HOST_TIMING")) phase.acc = host_ms;
     phase.start("nsd_step: stage inputs (one H2D)");
     // ---- stage inputs in ONE pinned buffer and ONE H2D copy: q-, u-, f_extra, contact
     // geometry, joint frames (R part); contact bodies and the contact incidence (int
