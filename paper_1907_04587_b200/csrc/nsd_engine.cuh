@@ -348,6 +348,7 @@ template <class R> struct CView {
   R dc, act;
 };
 template <class R> __device__ __forceinline__ CView<R> contact_view(const Topo<R>& T, const Work<R>& W, int c) {
+  NSD_CHECK(c >= 0 && c < W.nc);
   CView<R> v;
   v.ba = W.cbody[2 * c];
   v.bb = W.cbody[2 * c + 1];
@@ -420,6 +421,7 @@ __device__ __forceinline__ R slot_quad(const Topo<R>& T, const Work<R>& W, int i
 }
 // J_i . v for any row.
 template <class R> __device__ __forceinline__ R row_J(const Topo<R>& T, const Work<R>& W, int i, const R* v) {
+  NSD_CHECK(i >= 0 && i < W.nrows);
   if (i < T.rows_static) return slot_dot(W, i, v);
   if (i < W.friction_begin) {
     const CView<R> c = contact_view(T, W, i - W.normal_begin);
@@ -500,7 +502,10 @@ template <class R, bool kTets, class Team> __device__ void setup_row_blocks(Team
       for (int i = 0; i < T.tdim; ++i) {
         int* b = W.blk + 4 * (r0 + i);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) b[k] = vb[k];
+        for (int k = 0; k < 4; ++k) {
+          NSD_CHECK(vb[k] >= 0 && vb[k] < T.nd3);
+          b[k] = vb[k];
+        }
       }
     }
   }

@@ -26,6 +26,7 @@ template <class R, class S> __global__ void __launch_bounds__(64, warp_minb<S>()
   const nsd::Topo<R>& T = A.T;
   const int nc = A.nc_out[env];
   if (T.nj + nc > A.warp_max_obj) return;  // warp-uniform
+  NSD_CHECK(nc >= 0 && nc <= A.maxc && T.nj + nc <= 32);
   const WorkPlan& P = A.plan;
   const nsd::wp::Plan& L = A.wplan;
   unsigned char* base = smem + (size_t)wib * L.bytes;
@@ -197,6 +198,7 @@ template <class R> __global__ void __launch_bounds__(128, NSD_COLLIDE_MINB) k_ba
   __syncwarp();
   const int stored = total < cap ? total : cap;
   const int nc = total < A.maxc ? total : A.maxc;
+  NSD_CHECK(A.maxc <= cap);  // every kept contact is among the stored keys
   R* hr = reinterpret_cast<R*>(A.hot_global + (size_t)env * A.hot_bytes);
   int* cbody = P.hot_ints(hr) + P.cbody;
   R* cr = A.cold_r + (size_t)env * P.coldR;

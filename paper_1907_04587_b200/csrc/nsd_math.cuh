@@ -19,6 +19,36 @@
 #define NSD_HD inline
 #endif
 
+// Bounds and invariant checks of the checked build (make checks: -DNSD_CHECKS,
+// tools/run_checked.sh), compiled out otherwise. compute-sanitizer is closed on the
+// GPU pool (profiles/r2_sanitizer_attempt.txt); these take its place for the
+// index arithmetic of the hot kernels. A failed check traps the kernel.
+#ifdef NSD_CHECKS
+#include <cstdio>
+#include <cstdlib>
+#ifdef __CUDA_ARCH__
+#define NSD_CHECK(c)                                                               \
+  do {                                                                             \
+    if (!(c)) {                                                                    \
+      printf("NSD_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);              \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define NSD_CHECK(c)                                                               \
+  do {                                                                             \
+    if (!(c)) {                                                                    \
+      std::fprintf(stderr, "NSD_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c); \
+      std::abort();                                                                \
+    }                                                                              \
+  } while (0)
+#endif
+#else
+#define NSD_CHECK(c) \
+  do {               \
+  } while (0)
+#endif
+
 namespace nsd {
 
 template <class R> struct Lim;

@@ -95,6 +95,7 @@ template <class R> struct PartView {
     nrow = W.part_row_off[b + 1] - W.part_row_off[b];
     nlb = W.part_lb_off[b + 1] - W.part_lb_off[b];
     f0 = W.part_lb_off[b];
+    NSD_CHECK(nrow >= 0 && nrow <= W.part_mr && nlb >= 0 && nlb <= W.part_ml);
     sg = 1;
     while (sg < 32 && 2 * sg * nlb <= (int)blockDim.x) sg *= 2;
   }
@@ -139,7 +140,10 @@ __device__ void part_setup(const Topo<R>& T, const Work<R>& W, PartView<R>& V) {
       body_blocks(T, W.cbody[2 * c + 1], g4[2], g4[3]);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) V.slot[4 * li + k] = part_find(V.lbg, V.nlb, g4[k]);
+    for (int k = 0; k < 4; ++k) {
+      V.slot[4 * li + k] = part_find(V.lbg, V.nlb, g4[k]);
+      NSD_CHECK(g4[k] < 0 || V.slot[4 * li + k] >= 0);  // every block a row touches is local
+    }
     // C block base (a tet's rows are consecutive among the CTA's rows) or -1 (diagonal C)
     V.cb[li] = (kTets && i >= T.rows_joint && i < T.rows_static) ? li - (i - T.rows_joint) % T.tdim : -1;
   }
@@ -160,6 +164,7 @@ __device__ void part_setup(const Topo<R>& T, const Work<R>& W, PartView<R>& V) {
       V.incoff[l + 1] += V.incoff[l];
       V.xoff[l + 1] += V.xoff[l];
     }
+    NSD_CHECK(V.incoff[V.nlb] <= 4 * V.nrow && V.xoff[V.nlb] <= W.part_mx);
   }
   __syncthreads();
   for (int l = tid; l < V.nlb; l += nt) {
@@ -168,6 +173,7 @@ __device__ void part_setup(const Topo<R>& T, const Work<R>& W, PartView<R>& V) {
       if (V.slot[e] == l) V.inc[o++] = e;
     const int g = V.lbg[l];
     const int g0 = W.part_gb_off[g], n = W.part_gb_off[g + 1] - g0;
+    NSD_CHECK(o == V.incoff[l + 1] && V.xoff[l] + n == V.xoff[l + 1]);
     for (int k = 0; k < n; ++k) V.xent[V.xoff[l] + k] = W.part_gb_ent[g0 + k];
   }
   __syncthreads();

@@ -17,6 +17,8 @@
 
 #include <cooperative_groups.h>
 
+#include "nsd_math.cuh"  // NSD_CHECK
+
 namespace nsd {
 
 constexpr int kRedMax = 8;  // max values per fused reduction
@@ -220,6 +222,8 @@ struct GridTeam {
       if (timed) pmark(1);
       unsigned prev;
       asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(bar) : "memory");
+      // no CTA can arrive at the next barrier before this one completes
+      NSD_CHECK(static_cast<int>(prev + 1u - epoch * gridDim.x) <= 0);
       if (timed) pmark(2);
       const unsigned target = epoch * gridDim.x;
       if (prev + 1u != target) {
